@@ -1,0 +1,154 @@
+/*
+ * podecm_cuda.h — C-ABI drop-in boundary of the B200-native (sm_100a) hot
+ * path of the POD + ECM reduced-order model (arXiv 2307.16894).
+ *
+ * Plain pointers and sizes only; no C++, Eigen or torch types cross it.  Each
+ * entry point replaces one reference interface from /root/reference/proj
+ * (cited per declaration).  INTEGRATION.md shows the binding the reference
+ * side would add.
+ *
+ * Conventions
+ *   - Device pointers unless stated "host".  The ABI never frees caller
+ *     memory.  Calls are stream-ordered on the caller's cudaStream_t (passed
+ *     as void*; NULL = legacy default stream) and return once launched.
+ *   - Return codes: 0 OK, 2 configuration/shape error (reference
+ *     ConfigError), 3 solve error (reference SolveError), 4 CUDA error.
+ *     Per-item failures (a material point that hits a non-positive elastic
+ *     stretch, an instance whose Newton/bisection gives up) are reported in
+ *     the nullable per-item status[] arrays (0 ok / 3 SolveError) and in a
+ *     context-wide flag that podecm_check() collects (it synchronises the
+ *     stream and returns 3 with the reference's message when any item
+ *     failed).  podecm_last_error() returns the last message.
+ *   - Tensor layout follows the reference (types.hpp:21-48): a 2x2 tensor is
+ *     flattened column-stacked (A00, A10, A01, A11); a 4x4 tangent is the
+ *     Eigen::Matrix4d storage, entry (r, c) at r + 4c with r = i + 2j,
+ *     c = k + 2l.  Batched arrays are structure-of-arrays: component-major
+ *     planes of length n ("[4][n]").
+ *   - Material history ("state") is 6 planes: Fp00, Fp10, Fp01, Fp11, Fp_zz,
+ *     xi (PlasticState, material.hpp:55-59).
+ */
+#ifndef PODECM_CUDA_H
+#define PODECM_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PODECM_OK 0
+#define PODECM_ECONFIG 2
+#define PODECM_ESOLVE 3
+#define PODECM_ECUDA 4
+
+typedef struct podecm_ctx podecm_ctx;
+typedef struct podecm_rve podecm_rve;
+typedef struct podecm_rom podecm_rom;
+
+/* PlasticityParams, material.hpp:9-17 (lambda/mu derived as in :15-16). */
+typedef struct podecm_params {
+  double E, nu, sigma_y0, H;
+} podecm_params;
+
+/* NewtonOpts, microfem.hpp:45-56. */
+typedef struct podecm_newton {
+  double eps_rel, eps_abs, force_ref;
+  int32_t max_iter;
+  int32_t max_bisect; /* rom_solve_step_adaptive default 5, rom.hpp:66-73 */
+} podecm_newton;
+
+/* ---- context ------------------------------------------------------------ */
+int podecm_ctx_create(int device, podecm_ctx** out);
+void podecm_ctx_destroy(podecm_ctx* ctx);
+const char* podecm_last_error(const podecm_ctx* ctx);
+/* Synchronise `stream`, collect per-item failures flagged since the last
+ * check; returns 0 or 3 (SolveError). */
+int podecm_check(podecm_ctx* ctx, void* stream);
+/* Number of kernels this context has launched (for bench accounting). */
+int64_t podecm_launch_count(const podecm_ctx* ctx);
+
+/* ---- (i) material point -------------------------------------------------
+ * Replaces large_strain_update + large_strain_tangent per point
+ * (material.hpp:69-75; material.cpp:120-181), batched over n points.
+ *   mats (host)  : n_mats parameter sets; region (device, nullable) picks one
+ *                  per point (default 0).
+ *   F [4][n], st_in [6][n]  -> P [4][n], A [16][n] (nullable), st_out [6][n]
+ *   (nullable), status [n] (nullable).  h_rel: FD step (reference 1e-7). */
+int podecm_material_batch(podecm_ctx* ctx, void* stream, int64_t n, const podecm_params* mats,
+                          int n_mats, const int32_t* region, const double* F, const double* st_in,
+                          double* P, double* A, double* st_out, int32_t* status, double h_rel);
+
+/* ---- RVE tables (mesh, quadrature cache, periodic dof map, CSR pattern,
+ * deterministic scatter map) ----------------------------------------------
+ * Replaces RveProblem::build (microfem.cpp:9-23) with build_quad_cache
+ * (mesh.cpp:412-451), periodic_pairs/periodic_dof_map (mesh.cpp:307-374) and
+ * the setFromTriplets pattern (microfem.cpp:125-128) for the structured
+ * n_cells x n_cells bilinear Q4 unit cell of BASELINE configs 0/2/3
+ * (region 1 = element centroid within r0 of the centre). */
+int podecm_rve_create_q4(podecm_ctx* ctx, int n_cells, double r0, const podecm_params* mats,
+                         int n_mats, podecm_rve** out);
+void podecm_rve_destroy(podecm_rve* rve);
+/* out[0..5] = n_nodes, n_elems, n_qp, n_red, nnz, anchor node. */
+int podecm_rve_info(const podecm_rve* rve, int64_t out[6]);
+/* Copy the host-side tables out (all host pointers, each nullable):
+ * nodes [n_nodes][2], elems [n_elems][4], regions [n_elems],
+ * grad [n_qp][4][2], w [n_qp], node_dof [n_nodes], row_ptr [n_red+1],
+ * col_idx [nnz], slot_ptr [nnz+1] and slot_terms [n_triplets]: for CSR slot
+ * s the triplets (qp*64 + (a*4+b)*4 + i*2 + j) that sum into it, in
+ * reference triplet order. */
+int podecm_rve_export(const podecm_rve* rve, double* nodes, int32_t* elems, int32_t* regions,
+                      double* grad, double* w, int32_t* node_dof, int32_t* row_ptr,
+                      int32_t* col_idx, int32_t* slot_ptr, int32_t* slot_terms);
+int64_t podecm_rve_n_triplets(const podecm_rve* rve);
+
+/* Analytic morph (BASELINE configs 0/2/3) of one geometry (a, b):
+ * fmu_inv [4][n_qp], det [n_qp] (device) — MorphOperator::derive semantics
+ * (morph.cpp:97-126) with nodal d(X) from the circle->ellipse map. */
+int podecm_rve_morph(podecm_ctx* ctx, void* stream, podecm_rve* rve, int64_t n_inst,
+                     const double* geom, double* fmu_inv, double* det, int32_t* status);
+
+/* ---- (ii) batched assembly ----------------------------------------------
+ * Replaces assemble (microfem.hpp:74-77; microfem.cpp:56-130) for n_inst
+ * independent instances sharing the RVE tables.  Instance-major arrays:
+ *   geom [n_inst][2] (a, b) of the analytic morph, or morph (nullable,
+ *   overrides geom) [n_inst][5][n_qp] = fmu_inv planes + det plane;
+ *   fbar [n_inst][4]; w_red [n_inst][n_red]; st0 [n_inst][6][n_qp];
+ *   outputs st1 [n_inst][6][n_qp] (nullable), f [n_inst][n_red],
+ *   kvals [n_inst][nnz] (nullable => no tangent, AssemblyOpts.tangent=false),
+ *   p_field [n_inst][4][n_qp] (nullable), status [n_inst] (nullable).
+ * The CSR values are summed per slot in the reference triplet order (no
+ * atomics; bitwise reproducible). */
+int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* rve, int64_t n_inst,
+                          const double* geom, const double* morph, const double* fbar,
+                          const double* w_red, const double* st0, double* st1, double* f,
+                          double* kvals, double* p_field, int32_t* status);
+
+/* ---- (iii) hyper-reduced online stage ------------------------------------
+ * RomModel (rom.hpp:15-30) restricted to what the online solve reads:
+ * host arrays ids [Q] ascending, weights [Q], mode_grads [Q][N][4]
+ * (build_rom, rom.cpp:80-109). */
+int podecm_rom_create(podecm_ctx* ctx, podecm_rve* rve, int N, int Q, const int32_t* ids,
+                      const double* weights, const double* mode_grads, podecm_rom** out);
+void podecm_rom_destroy(podecm_rom* rom);
+/* Replaces rom_solve (rom.hpp:86-88; rom.cpp:177-200) with
+ * rom_solve_step_adaptive (rom.cpp:152-175) for n_inst instances:
+ *   geom [n_inst][2]; sched [n_inst][K][4] macro F per increment;
+ *   outputs pbar [n_inst][K][4] homogenised stress history,
+ *   iters [n_inst][K] (nullable), resid [n_inst][K] (nullable),
+ *   a_final [n_inst][N] (nullable), status [n_inst] (nullable). */
+int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* rom, int64_t n_inst,
+                           const double* geom, const double* sched, int K,
+                           const podecm_newton* opts, double* pbar, int32_t* iters, double* resid,
+                           double* a_final, int32_t* status);
+
+/* ---- diagnostics ---------------------------------------------------------
+ * FP64 roofline probes (mode 0: DFMA chain, mode 1: mma.sync m8n8k4 f64);
+ * *flops receives the flop count of the launch, time it on `stream`. */
+int podecm_probe_fp64(podecm_ctx* ctx, void* stream, int mode, int iters, double* scratch,
+                      double* flops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PODECM_CUDA_H */

@@ -1,0 +1,153 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+ctypes front end of ``liboracle.so``, the CPU restatement of the reference
+hot path (see oracle.hpp for the citations and the parity-pinning status).
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's cpu_baseline /
+``--impl reference`` legs may import this package; the product never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+LIB = HERE / "liboracle.so"
+_lib = None
+
+P = C.c_void_p
+L = C.c_long
+D = C.c_double
+I = C.c_int
+
+
+def build() -> Path:
+    r = subprocess.run(["make", "-C", str(HERE), "-s"], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"oracle build failed:\n{r.stdout}\n{r.stderr}")
+    return LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIB.exists():
+            build()
+        l = C.CDLL(str(LIB))
+        l.orc_material_batch.restype = L
+        l.orc_material_batch.argtypes = [L, P, I, P, P, P, P, P, P, P, P, D, I]
+        l.orc_rve_create.restype = P
+        l.orc_rve_create.argtypes = [I, D, P, I]
+        l.orc_rve_destroy.argtypes = [P]
+        l.orc_rve_info.argtypes = [P, P]
+        l.orc_rve_export.argtypes = [P] + [P] * 8
+        l.orc_rve_morph.restype = I
+        l.orc_rve_morph.argtypes = [P, D, D, P, P]
+        l.orc_rve_assemble.restype = L
+        l.orc_rve_assemble.argtypes = [P, L, P, P, P, P, P, P, P, P, P, I]
+        l.orc_rom_solve.restype = L
+        l.orc_rom_solve.argtypes = [P, I, I, P, P, P, L, P, P, I, D, D, I, I, P, P, P, P, P, I]
+        l.orc_max_threads.restype = I
+        _lib = l
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _mats(mats):
+    return np.ascontiguousarray([[m.E, m.nu, m.sigma_y0, m.H] for m in mats], dtype=np.float64)
+
+
+def max_threads() -> int:
+    return int(lib().orc_max_threads())
+
+
+def material_batch(F, st, mats, region=None, h_rel=1e-7, tangent=True, nthreads=0):
+    """large_strain_update + large_strain_tangent per point (material.cpp)."""
+    F = np.ascontiguousarray(F, dtype=np.float64)
+    st = np.ascontiguousarray(st, dtype=np.float64)
+    n = F.shape[1]
+    P_ = np.empty((4, n))
+    A = np.empty((16, n)) if tangent else None
+    so = np.empty((6, n))
+    ex = np.empty((4, n))
+    status = np.empty(n, np.int32)
+    m = _mats(mats)
+    reg = None if region is None else np.ascontiguousarray(region, dtype=np.int32)
+    lib().orc_material_batch(n, _p(m), len(mats), _p(reg), _p(F), _p(st), _p(P_), _p(A), _p(so),
+                             _p(status), _p(ex), h_rel, nthreads)
+    return {"P": P_, "A": A, "st": so, "status": status, "dgamma": ex[0], "f_trial": ex[1],
+            "q_trial": ex[2], "mises": ex[3]}
+
+
+class Rve:
+    """Structured Q4 RveProblem restated on the CPU."""
+
+    def __init__(self, n_cells, mats, r0=0.25):
+        m = _mats(mats)
+        self.h = lib().orc_rve_create(n_cells, r0, _p(m), len(mats))
+        info = np.zeros(6, dtype=np.int64)
+        lib().orc_rve_info(self.h, _p(info))
+        self.n_nodes, self.n_elems, self.n_qp, self.n_red, self.nnz, self.anchor = (int(x) for x in info)
+
+    def export(self):
+        t = {"nodes": np.empty((self.n_nodes, 2)), "elems": np.empty((self.n_elems, 4), np.int32),
+             "regions": np.empty(self.n_elems, np.int32), "grad": np.empty((self.n_qp, 4, 2)),
+             "w": np.empty(self.n_qp), "node_dof": np.empty(self.n_nodes, np.int32),
+             "row_ptr": np.empty(self.n_red + 1, np.int32), "col_idx": np.empty(self.nnz, np.int32)}
+        lib().orc_rve_export(self.h, *(_p(t[k]) for k in ("nodes", "elems", "regions", "grad", "w",
+                                                          "node_dof", "row_ptr", "col_idx")))
+        return t
+
+    def morph(self, a, b):
+        fmi = np.empty((4, self.n_qp))
+        det = np.empty(self.n_qp)
+        rc = lib().orc_rve_morph(self.h, a, b, _p(fmi), _p(det))
+        return fmi, det, rc
+
+    def assemble(self, geom, fbar, w_red, st0, tangent=True, states1=True, store_stress=False,
+                 nthreads=0):
+        n = geom.shape[0]
+        geom = np.ascontiguousarray(geom, dtype=np.float64)
+        fbar = np.ascontiguousarray(fbar, dtype=np.float64)
+        w_red = np.ascontiguousarray(w_red, dtype=np.float64)
+        st0 = np.ascontiguousarray(st0, dtype=np.float64)
+        f = np.empty((n, self.n_red))
+        K = np.empty((n, self.nnz)) if tangent else None
+        s1 = np.empty((n, 6, self.n_qp)) if states1 else None
+        pf = np.empty((n, 4, self.n_qp)) if store_stress else None
+        status = np.empty(n, np.int32)
+        lib().orc_rve_assemble(self.h, n, _p(geom), _p(fbar), _p(w_red), _p(st0), _p(s1), _p(f), _p(K),
+                               _p(pf), _p(status), nthreads)
+        return {"f": f, "K": K, "st1": s1, "p_field": pf, "status": status}
+
+    def rom_solve(self, ids, weights, mode_grads, geom, sched, eps_rel=1e-8, eps_abs=1e-12,
+                  max_iter=25, max_bisect=5, nthreads=0):
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        weights = np.ascontiguousarray(weights, dtype=np.float64)
+        mg = np.ascontiguousarray(mode_grads, dtype=np.float64)
+        geom = np.ascontiguousarray(geom, dtype=np.float64)
+        sched = np.ascontiguousarray(sched, dtype=np.float64)
+        Q, N = mg.shape[0], mg.shape[1]
+        n, K = sched.shape[0], sched.shape[1]
+        pbar = np.empty((n, K, 4))
+        iters = np.empty((n, K), np.int32)
+        resid = np.empty((n, K))
+        af = np.empty((n, N))
+        status = np.empty(n, np.int32)
+        lib().orc_rom_solve(self.h, N, Q, _p(ids), _p(weights), _p(mg), n, _p(geom), _p(sched), K,
+                            eps_rel, eps_abs, max_iter, max_bisect, _p(pbar), _p(iters), _p(resid),
+                            _p(af), _p(status), nthreads)
+        return {"pbar": pbar, "iters": iters, "resid": resid, "a_final": af, "status": status}
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().orc_rve_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass

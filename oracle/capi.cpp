@@ -1,0 +1,265 @@
+// ORACLE — TEST INFRASTRUCTURE ONLY (see oracle.hpp).
+// Flat extern "C" surface for the checker (ctypes from tests/ and bench.py's
+// cpu_baseline leg).  Layouts mirror include/podecm_cuda.h so the same host
+// buffers feed both sides.  OpenMP runs over independent units (points,
+// instances); per-unit results do not depend on the thread count.
+#include <omp.h>
+
+#include <cstring>
+#include <memory>
+
+#include "oracle.hpp"
+
+using namespace orc;
+
+namespace {
+
+PlasticityParams param_from(const double* m) {
+  PlasticityParams p;
+  p.E = m[0];
+  p.nu = m[1];
+  p.sigma_y0 = m[2];
+  p.H = m[3];
+  return p;
+}
+
+struct OrcRve {
+  RveProblem prob;
+  double r0 = 0.25;
+  Csr pattern;
+};
+
+void set_threads(int nt) {
+  if (nt > 0) omp_set_num_threads(nt);
+}
+
+}  // namespace
+
+extern "C" {
+
+// SoA over n points: F[4][n] flatten order, st[6][n] = Fp00,Fp10,Fp01,Fp11,
+// Fp_zz,xi; P[4][n]; A[16][n] plane r+4c; extra[4][n] = dgamma, f_trial,
+// q_trial, mises (nullable).  status[i] = 0 ok / 3 SolveError.  Returns the
+// number of failed points.
+long orc_material_batch(long n, const double* mats, int n_mats, const int* region, const double* F,
+                        const double* st_in, double* P, double* A, double* st_out, int* status,
+                        double* extra, double h_rel, int nthreads) {
+  set_threads(nthreads);
+  std::vector<PlasticityParams> pm;
+  for (int k = 0; k < n_mats; ++k) pm.push_back(param_from(mats + 4 * k));
+  long fails = 0;
+#pragma omp parallel for schedule(static) reduction(+ : fails)
+  for (long i = 0; i < n; ++i) {
+    const PlasticityParams& p = pm[region ? region[i] : 0];
+    PlasticState s0;
+    for (int k = 0; k < 4; ++k) s0.Fp.a[k] = st_in[k * n + i];
+    s0.Fp_zz = st_in[4 * n + i];
+    s0.xi = st_in[5 * n + i];
+    Mat2 f;
+    for (int k = 0; k < 4; ++k) f.a[k] = F[k * n + i];
+    try {
+      PlasticState s1;
+      const LargeResult r = large_strain_update(p, s0, f, &s1);
+      if (P)
+        for (int k = 0; k < 4; ++k) P[k * n + i] = r.P.a[k];
+      if (st_out) {
+        for (int k = 0; k < 4; ++k) st_out[k * n + i] = s1.Fp.a[k];
+        st_out[4 * n + i] = s1.Fp_zz;
+        st_out[5 * n + i] = s1.xi;
+      }
+      if (extra) {
+        extra[i] = r.dgamma;
+        extra[n + i] = r.f_trial;
+        extra[2 * n + i] = r.q_trial;
+        extra[3 * n + i] = r.mises;
+      }
+      if (A) {
+        double a[16];
+        large_strain_tangent(p, s0, f, h_rel, a);
+        for (int k = 0; k < 16; ++k) A[k * n + i] = a[k];
+      }
+      if (status) status[i] = 0;
+    } catch (const SolveError&) {
+      if (status) status[i] = 3;
+      ++fails;
+    }
+  }
+  return fails;
+}
+
+void* orc_rve_create(int n_cells, double r0, const double* mats, int n_mats) {
+  auto* h = new OrcRve;
+  h->r0 = r0;
+  h->prob.mesh = structured_q4(n_cells, r0);
+  h->prob.cache = build_quad_cache(h->prob.mesh);
+  h->prob.dofs = periodic_dof_map(h->prob.mesh);
+  for (int k = 0; k < n_mats; ++k) h->prob.materials.push_back(param_from(mats + 4 * k));
+  // CSR pattern: one elastic assembly at the identity (values discarded).
+  RveProblem pat = h->prob;
+  for (auto& m : pat.materials) m.sigma_y0 = 1e300;
+  const int nq = pat.cache.n_qp();
+  Morph id;
+  id.fmu_inv.assign(nq, Mat2::identity());
+  id.det.assign(nq, 1.0);
+  std::vector<PlasticState> s0(nq);
+  std::vector<double> w(pat.dofs.n_red, 0.0), f;
+  assemble(pat, id, s0, nullptr, Mat2::identity(), w, true, f, &h->pattern, nullptr);
+  return h;
+}
+
+void orc_rve_destroy(void* h) { delete static_cast<OrcRve*>(h); }
+
+// out: n_nodes, n_elems, n_qp, n_red, nnz, anchor
+void orc_rve_info(void* hp, long* out) {
+  auto* h = static_cast<OrcRve*>(hp);
+  out[0] = h->prob.mesh.n_nodes;
+  out[1] = h->prob.mesh.n_elems;
+  out[2] = h->prob.cache.n_qp();
+  out[3] = h->prob.dofs.n_red;
+  out[4] = (long)h->pattern.col.size();
+  out[5] = h->prob.dofs.anchor;
+}
+
+void orc_rve_export(void* hp, double* nodes, int* elems, int* regions, double* grad, double* w,
+                    int* node_dof, int* row_ptr, int* col) {
+  auto* h = static_cast<OrcRve*>(hp);
+  const auto& m = h->prob.mesh;
+  if (nodes) std::memcpy(nodes, m.nodes.data(), m.nodes.size() * sizeof(double));
+  if (elems) std::memcpy(elems, m.elems.data(), m.elems.size() * sizeof(int));
+  if (regions) std::memcpy(regions, m.regions.data(), m.regions.size() * sizeof(int));
+  if (grad) std::memcpy(grad, h->prob.cache.grad.data(), h->prob.cache.grad.size() * sizeof(double));
+  if (w) std::memcpy(w, h->prob.cache.w.data(), h->prob.cache.w.size() * sizeof(double));
+  if (node_dof)
+    std::memcpy(node_dof, h->prob.dofs.node_dof.data(), h->prob.dofs.node_dof.size() * sizeof(int));
+  if (row_ptr)
+    std::memcpy(row_ptr, h->pattern.row_ptr.data(), h->pattern.row_ptr.size() * sizeof(int));
+  if (col) std::memcpy(col, h->pattern.col.data(), h->pattern.col.size() * sizeof(int));
+}
+
+// Morph of one instance at every qp: fmu_inv[4][nqp], det[nqp].  Returns 0 or 3.
+int orc_rve_morph(void* hp, double a, double b, double* fmu_inv, double* det_out) {
+  auto* h = static_cast<OrcRve*>(hp);
+  try {
+    const Morph mo = derive(h->prob.mesh, h->prob.cache,
+                            analytic_morph_d(h->prob.mesh, a, b, h->r0));
+    const int nq = h->prob.cache.n_qp();
+    for (int q = 0; q < nq; ++q) {
+      for (int k = 0; k < 4; ++k) fmu_inv[(size_t)k * nq + q] = mo.fmu_inv[q].a[k];
+      det_out[q] = mo.det[q];
+    }
+    return 0;
+  } catch (const SolveError&) {
+    return 3;
+  }
+}
+
+// Batched assemble over n_inst instances (instance-major arrays):
+// geom[2] (a,b), fbar[4], w_red[n_red], st0[6][nqp], st1[6][nqp] (nullable),
+// f[n_red], kvals[nnz] (nullable => no tangent), p_field[4][nqp] (nullable).
+long orc_rve_assemble(void* hp, long n_inst, const double* geom, const double* fbar,
+                      const double* w_red, const double* st0, double* st1, double* f, double* kvals,
+                      double* p_field, int* status, int nthreads) {
+  set_threads(nthreads);
+  auto* h = static_cast<OrcRve*>(hp);
+  const RveProblem& prob = h->prob;
+  const int nq = prob.cache.n_qp(), nr = prob.dofs.n_red;
+  const long nnz = (long)h->pattern.col.size();
+  long fails = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : fails)
+  for (long s = 0; s < n_inst; ++s) {
+    try {
+      const Morph mo = derive(prob.mesh, prob.cache,
+                              analytic_morph_d(prob.mesh, geom[2 * s], geom[2 * s + 1], h->r0));
+      std::vector<PlasticState> s0(nq), s1;
+      const double* sp = st0 + (size_t)s * 6 * nq;
+      for (int q = 0; q < nq; ++q) {
+        for (int k = 0; k < 4; ++k) s0[q].Fp.a[k] = sp[(size_t)k * nq + q];
+        s0[q].Fp_zz = sp[(size_t)4 * nq + q];
+        s0[q].xi = sp[(size_t)5 * nq + q];
+      }
+      Mat2 fb;
+      for (int k = 0; k < 4; ++k) fb.a[k] = fbar[4 * s + k];
+      std::vector<double> w(w_red + (size_t)s * nr, w_red + (size_t)(s + 1) * nr), ff, pf;
+      Csr K;
+      assemble(prob, mo, s0, st1 ? &s1 : nullptr, fb, w, kvals != nullptr, ff, kvals ? &K : nullptr,
+               p_field ? &pf : nullptr);
+      std::memcpy(f + (size_t)s * nr, ff.data(), nr * sizeof(double));
+      if (kvals) {
+        if ((long)K.val.size() != nnz) throw SolveError("pattern mismatch");
+        std::memcpy(kvals + (size_t)s * nnz, K.val.data(), nnz * sizeof(double));
+      }
+      if (p_field)
+        for (int q = 0; q < nq; ++q)
+          for (int k = 0; k < 4; ++k) p_field[(size_t)s * 4 * nq + (size_t)k * nq + q] = pf[4 * (size_t)q + k];
+      if (st1) {
+        double* o = st1 + (size_t)s * 6 * nq;
+        for (int q = 0; q < nq; ++q) {
+          for (int k = 0; k < 4; ++k) o[(size_t)k * nq + q] = s1[q].Fp.a[k];
+          o[(size_t)4 * nq + q] = s1[q].Fp_zz;
+          o[(size_t)5 * nq + q] = s1[q].xi;
+        }
+      }
+      if (status) status[s] = 0;
+    } catch (const SolveError&) {
+      if (status) status[s] = 3;
+      ++fails;
+    }
+  }
+  return fails;
+}
+
+// Batched hyper-reduced solve (rom_solve, rom.cpp:177-200) over instances.
+// ids[Q] ascending, weights[Q], mode_grads[Q][N][4]; geom[n_inst][2];
+// sched[n_inst][K][4] (flatten order); outputs pbar[n_inst][K][4],
+// iters[n_inst][K], resid[n_inst][K], a_final[n_inst][N]; status 0/3.
+long orc_rom_solve(void* hp, int N, int Q, const int* ids, const double* weights,
+                   const double* mode_grads, long n_inst, const double* geom, const double* sched,
+                   int K, double eps_rel, double eps_abs, int max_iter, int max_bisect, double* pbar,
+                   int* iters, double* resid, double* a_final, int* status, int nthreads) {
+  set_threads(nthreads);
+  auto* h = static_cast<OrcRve*>(hp);
+  const RveProblem& prob = h->prob;
+  RomModel model;
+  model.N = N;
+  model.ids.assign(ids, ids + Q);
+  model.weights.assign(weights, weights + Q);
+  model.mode_grads.assign(mode_grads, mode_grads + (size_t)Q * N * 4);
+  NewtonOpts o;
+  o.eps_rel = eps_rel;
+  o.eps_abs = eps_abs;
+  o.max_iter = max_iter;
+  long fails = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : fails)
+  for (long s = 0; s < n_inst; ++s) {
+    try {
+      const Morph mo = derive(prob.mesh, prob.cache,
+                              analytic_morph_d(prob.mesh, geom[2 * s], geom[2 * s + 1], h->r0));
+      std::vector<Mat2> fmi(Q);
+      std::vector<double> dt(Q);
+      for (int p = 0; p < Q; ++p) {  // slice_morph (rom.cpp:111-120)
+        fmi[p] = mo.fmu_inv[ids[p]];
+        dt[p] = mo.det[ids[p]];
+      }
+      std::vector<Mat2> sc(K);
+      for (int k = 0; k < K; ++k)
+        for (int c = 0; c < 4; ++c) sc[k].a[c] = sched[((size_t)s * K + k) * 4 + c];
+      std::vector<double> af;
+      const auto recs = rom_solve(prob, model, fmi, dt, sc, o, max_bisect, &af);
+      for (int k = 0; k < K; ++k) {
+        for (int c = 0; c < 4; ++c) pbar[((size_t)s * K + k) * 4 + c] = recs[k].pbar.a[c];
+        if (iters) iters[(size_t)s * K + k] = recs[k].iters;
+        if (resid) resid[(size_t)s * K + k] = recs[k].residual;
+      }
+      if (a_final) std::memcpy(a_final + (size_t)s * N, af.data(), N * sizeof(double));
+      if (status) status[s] = 0;
+    } catch (const SolveError&) {
+      if (status) status[s] = 3;
+      ++fails;
+    }
+  }
+  return fails;
+}
+
+int orc_max_threads() { return omp_get_max_threads(); }
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+"""ctypes binding of the C-ABI in include/podecm_cuda.h.
+
+The product path has exactly one implementation: the sm_100a kernels in
+``libpodecm_cuda.so``.  There is no CPU fallback — if the library is missing
+or no CUDA device is present, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libpodecm_cuda.so"
+
+_lib = None
+
+P = C.c_void_p
+I64 = C.c_int64
+I32 = C.c_int32
+D = C.c_double
+
+
+class podecm_params(C.Structure):
+    _fields_ = [("E", D), ("nu", D), ("sigma_y0", D), ("H", D)]
+
+
+class podecm_newton(C.Structure):
+    _fields_ = [("eps_rel", D), ("eps_abs", D), ("force_ref", D), ("max_iter", I32),
+                ("max_bisect", I32)]
+
+
+_SIGS = {
+    "podecm_ctx_create": (C.c_int, [C.c_int, C.POINTER(P)]),
+    "podecm_ctx_destroy": (None, [P]),
+    "podecm_last_error": (C.c_char_p, [P]),
+    "podecm_check": (C.c_int, [P, P]),
+    "podecm_launch_count": (I64, [P]),
+    "podecm_material_batch": (C.c_int, [P, P, I64, C.POINTER(podecm_params), C.c_int, P, P, P, P,
+                                        P, P, P, D]),
+    "podecm_rve_create_q4": (C.c_int, [P, C.c_int, D, C.POINTER(podecm_params), C.c_int,
+                                       C.POINTER(P)]),
+    "podecm_rve_destroy": (None, [P]),
+    "podecm_rve_info": (C.c_int, [P, C.POINTER(I64)]),
+    "podecm_rve_export": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P]),
+    "podecm_rve_n_triplets": (I64, [P]),
+    "podecm_rve_morph": (C.c_int, [P, P, P, I64, P, P, P, P]),
+    "podecm_assemble_batch": (C.c_int, [P, P, P, I64, P, P, P, P, P, P, P, P, P, P]),
+    "podecm_rom_create": (C.c_int, [P, P, C.c_int, C.c_int, P, P, P, C.POINTER(P)]),
+    "podecm_rom_destroy": (None, [P]),
+    "podecm_probe_fp64": (C.c_int, [P, P, C.c_int, C.c_int, P, C.POINTER(D)]),
+    "podecm_rom_solve_batch": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton),
+                                         P, P, P, P, P]),
+}
+
+# every symbol include/podecm_cuda.h declares (checked by tests on CPU)
+EXPORTED = tuple(_SIGS)
+
+
+class PodecmError(RuntimeError):
+    pass
+
+
+class ConfigError(PodecmError):
+    """Reference ConfigError (types.hpp:60-63); C-ABI code 2."""
+
+
+class SolveError(PodecmError):
+    """Reference SolveError (types.hpp:65-68); C-ABI code 3."""
+
+
+class CudaError(PodecmError):
+    """C-ABI code 4."""
+
+
+def load(path: Path | str | None = None):
+    """Load the library (without touching the GPU) and bind every signature."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise PodecmError(f"{p} is missing: run `python -m paper_2307_16894_b200._build` "
+                          "(the CUDA path has no CPU fallback)")
+    lib = C.CDLL(str(p))
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def raise_for(rc: int, ctx=None, what: str = "") -> None:
+    if rc == 0:
+        return
+    msg = what
+    if ctx:
+        m = load().podecm_last_error(ctx)
+        msg = f"{what}: {m.decode() if m else ''}"
+    if rc == 2:
+        raise ConfigError(msg)
+    if rc == 3:
+        raise SolveError(msg)
+    if rc == 4:
+        raise CudaError(msg)
+    raise PodecmError(f"{msg} (code {rc})")

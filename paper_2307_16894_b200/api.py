@@ -1,0 +1,285 @@
+"""Host-side mirror of the reference interfaces for the hot path.
+
+Names and argument meaning follow /root/reference/proj/include/podecm:
+``PlasticityParams`` (material.hpp:9-17), ``large_strain_update`` +
+``large_strain_tangent`` (material.hpp:69-75) batched as
+:func:`material_batch`, ``RveProblem``/``assemble`` (microfem.hpp:16-77) as
+:class:`Rve` / :meth:`Rve.assemble`, ``RomModel``/``rom_solve``
+(rom.hpp:15-88) as :class:`Rom` / :meth:`Rom.solve`.  Errors surface as the
+reference's exception kinds (``SolveError``, ``ConfigError``).
+
+Device memory, streams and tensors come from PyTorch (plumbing only); every
+computation runs in the sm_100a kernels of ``libpodecm_cuda.so`` through the
+C-ABI.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import ConfigError, SolveError, podecm_newton, podecm_params
+
+__all__ = ["PlasticityParams", "NewtonOpts", "Context", "material_batch", "Rve", "Rom",
+           "ConfigError", "SolveError", "matrix_params", "inclusion_params"]
+
+
+@dataclass(frozen=True)
+class PlasticityParams:
+    """material.hpp:9-17 (defaults: E=1, nu=0.3, elastic sigma_y0=1e300, H=0)."""
+    E: float = 1.0
+    nu: float = 0.3
+    sigma_y0: float = 1e300
+    H: float = 0.0
+
+    def c(self) -> podecm_params:
+        return podecm_params(self.E, self.nu, self.sigma_y0, self.H)
+
+
+def matrix_params() -> PlasticityParams:
+    """BASELINE config-0 matrix phase: E=1, nu=0.3, sigma_y=0.01, H=0.1."""
+    return PlasticityParams(1.0, 0.3, 0.01, 0.1)
+
+
+def inclusion_params() -> PlasticityParams:
+    """BASELINE config-0 inclusion: E=10, nu=0.3, elastic."""
+    return PlasticityParams(10.0, 0.3, 1e300, 0.0)
+
+
+@dataclass
+class NewtonOpts:
+    """microfem.hpp:45-56 plus the bisection depth of rom.hpp:66-73."""
+    eps_rel: float = 1e-8
+    eps_abs: float = 1e-12
+    max_iter: int = 25
+    force_ref: float = 0.0
+    max_bisect: int = 5
+
+    def c(self) -> podecm_newton:
+        return podecm_newton(self.eps_rel, self.eps_abs, self.force_ref, self.max_iter,
+                             self.max_bisect)
+
+
+def _mats(mats) -> tuple:
+    arr = (podecm_params * len(mats))(*[m.c() for m in mats])
+    return arr, len(mats)
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ConfigError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ConfigError("expected a contiguous tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def _f64(t: torch.Tensor, shape, name: str) -> torch.Tensor:
+    if t.dtype != torch.float64 or tuple(t.shape) != tuple(shape):
+        raise ConfigError(f"{name}: expected float64 {tuple(shape)}, got {t.dtype} {tuple(t.shape)}")
+    return t
+
+
+class Context:
+    """One C-ABI context per device (podecm_ctx)."""
+
+    _default: dict = {}
+
+    def __init__(self, device: int = 0):
+        if not torch.cuda.is_available():
+            raise _lib.CudaError("no CUDA device: the hot path has no CPU fallback")
+        self.lib = _lib.load()
+        self.device = device
+        torch.cuda.set_device(device)
+        h = C.c_void_p()
+        _lib.raise_for(self.lib.podecm_ctx_create(device, C.byref(h)), None, "podecm_ctx_create")
+        self.h = h
+
+    @classmethod
+    def default(cls, device: int = 0) -> "Context":
+        if device not in cls._default:
+            cls._default[device] = Context(device)
+        return cls._default[device]
+
+    def stream(self):
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def check(self) -> None:
+        """Synchronise and raise SolveError if any item failed (podecm_check)."""
+        _lib.raise_for(self.lib.podecm_check(self.h, self.stream()), self.h, "podecm_check")
+
+    def launches(self) -> int:
+        return int(self.lib.podecm_launch_count(self.h))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.podecm_ctx_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def material_batch(F: torch.Tensor, st: torch.Tensor, mats, region: torch.Tensor | None = None,
+                   h_rel: float = 1e-7, tangent: bool = True, state: bool = True,
+                   ctx: Context | None = None, out: dict | None = None):
+    """Batched large_strain_update + large_strain_tangent (material.hpp:69-75).
+
+    F: [4, n] float64 (flatten order), st: [6, n] (Fp00, Fp10, Fp01, Fp11,
+    Fp_zz, xi).  Returns dict P [4, n], A [16, n] (plane r + 4c), st [6, n],
+    status [n] int32.  Raises nothing per point: check ``status`` or call
+    ``ctx.check()`` for the reference's throw-on-first-failure behaviour.
+    """
+    ctx = ctx or Context.default(F.device.index or 0)
+    n = F.shape[1]
+    _f64(F, (4, n), "F")
+    _f64(st, (6, n), "st")
+    o = out or {}
+    P = o.get("P") if o.get("P") is not None else torch.empty((4, n), dtype=torch.float64, device=F.device)
+    A = (o.get("A") if o.get("A") is not None else torch.empty((16, n), dtype=torch.float64, device=F.device)) if tangent else None
+    S = (o.get("st") if o.get("st") is not None else torch.empty((6, n), dtype=torch.float64, device=F.device)) if state else None
+    status = o.get("status") if o.get("status") is not None else torch.empty(n, dtype=torch.int32, device=F.device)
+    arr, nm = _mats(mats)
+    rc = ctx.lib.podecm_material_batch(ctx.h, ctx.stream(), n, arr, nm, _ptr(region), _ptr(F),
+                                       _ptr(st), _ptr(P), _ptr(A), _ptr(S), _ptr(status), h_rel)
+    _lib.raise_for(rc, ctx.h, "podecm_material_batch")
+    return {"P": P, "A": A, "st": S, "status": status}
+
+
+class Rve:
+    """RveProblem (microfem.hpp:16-30) of the structured Q4 unit cell."""
+
+    def __init__(self, n_cells: int, mats, r0: float = 0.25, ctx: Context | None = None):
+        self.ctx = ctx or Context.default()
+        self.lib = self.ctx.lib
+        arr, nm = _mats(mats)
+        h = C.c_void_p()
+        _lib.raise_for(self.lib.podecm_rve_create_q4(self.ctx.h, n_cells, r0, arr, nm, C.byref(h)),
+                       self.ctx.h, "podecm_rve_create_q4")
+        self.h = h
+        self.mats = list(mats)
+        self.n_cells = n_cells
+        self.r0 = r0
+        info = (C.c_int64 * 6)()
+        self.lib.podecm_rve_info(h, info)
+        self.n_nodes, self.n_elems, self.n_qp, self.n_red, self.nnz, self.anchor = (int(x) for x in info)
+        self.n_trip = int(self.lib.podecm_rve_n_triplets(h))
+
+    def export(self) -> dict:
+        import numpy as np
+        t = {
+            "nodes": np.empty((self.n_nodes, 2)), "elems": np.empty((self.n_elems, 4), np.int32),
+            "regions": np.empty(self.n_elems, np.int32), "grad": np.empty((self.n_qp, 4, 2)),
+            "w": np.empty(self.n_qp), "node_dof": np.empty(self.n_nodes, np.int32),
+            "row_ptr": np.empty(self.n_red + 1, np.int32), "col_idx": np.empty(self.nnz, np.int32),
+            "slot_ptr": np.empty(self.nnz + 1, np.int32), "slot_terms": np.empty(self.n_trip, np.int32),
+        }
+        p = lambda a: a.ctypes.data_as(C.c_void_p)
+        self.lib.podecm_rve_export(self.h, *(p(t[k]) for k in ("nodes", "elems", "regions", "grad", "w",
+                                                                "node_dof", "row_ptr", "col_idx",
+                                                                "slot_ptr", "slot_terms")))
+        return t
+
+    def morph(self, geom: torch.Tensor):
+        """Analytic morph at every qp: (fmu_inv [n,4,nqp], det [n,nqp], status)."""
+        n = geom.shape[0]
+        _f64(geom, (n, 2), "geom")
+        fmi = torch.empty((n, 4, self.n_qp), dtype=torch.float64, device=geom.device)
+        det = torch.empty((n, self.n_qp), dtype=torch.float64, device=geom.device)
+        status = torch.empty(n, dtype=torch.int32, device=geom.device)
+        rc = self.lib.podecm_rve_morph(self.ctx.h, self.ctx.stream(), self.h, n, _ptr(geom), _ptr(fmi),
+                                       _ptr(det), _ptr(status))
+        _lib.raise_for(rc, self.ctx.h, "podecm_rve_morph")
+        return fmi, det, status
+
+    def assemble(self, fbar: torch.Tensor, w_red: torch.Tensor, st0: torch.Tensor,
+                 geom: torch.Tensor | None = None, morph: torch.Tensor | None = None,
+                 tangent: bool = True, states1: bool = True, store_stress: bool = False,
+                 out: dict | None = None) -> dict:
+        """Batched assemble (microfem.cpp:56-130): f [n, n_red], K values
+        [n, nnz] (CSR pattern of :meth:`export`), st1 [n, 6, nqp], p_field."""
+        n = fbar.shape[0]
+        dev = fbar.device
+        _f64(fbar, (n, 4), "fbar")
+        _f64(w_red, (n, self.n_red), "w_red")
+        _f64(st0, (n, 6, self.n_qp), "st0")
+        if geom is not None:
+            _f64(geom, (n, 2), "geom")
+        if morph is not None:
+            _f64(morph, (n, 5, self.n_qp), "morph")
+        o = out or {}
+        mk = lambda k, shape: o[k] if o.get(k) is not None else torch.empty(shape, dtype=torch.float64, device=dev)
+        f = mk("f", (n, self.n_red))
+        K = mk("K", (n, self.nnz)) if tangent else None
+        S1 = mk("st1", (n, 6, self.n_qp)) if states1 else None
+        PF = mk("p_field", (n, 4, self.n_qp)) if store_stress else None
+        status = o["status"] if o.get("status") is not None else torch.empty(n, dtype=torch.int32, device=dev)
+        rc = self.lib.podecm_assemble_batch(self.ctx.h, self.ctx.stream(), self.h, n, _ptr(geom),
+                                            _ptr(morph), _ptr(fbar), _ptr(w_red), _ptr(st0), _ptr(S1),
+                                            _ptr(f), _ptr(K), _ptr(PF), _ptr(status))
+        _lib.raise_for(rc, self.ctx.h, "podecm_assemble_batch")
+        return {"f": f, "K": K, "st1": S1, "p_field": PF, "status": status}
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.podecm_rve_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class Rom:
+    """RomModel (rom.hpp:15-30) bound to an Rve: ECM ids, weights, mode_grads."""
+
+    def __init__(self, rve: Rve, ids, weights, mode_grads):
+        import numpy as np
+        self.rve = rve
+        self.ctx = rve.ctx
+        self.lib = rve.lib
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        weights = np.ascontiguousarray(weights, dtype=np.float64)
+        mode_grads = np.ascontiguousarray(mode_grads, dtype=np.float64)
+        self.Q = ids.shape[0]
+        self.N = mode_grads.shape[1]
+        if mode_grads.shape != (self.Q, self.N, 4) or weights.shape != (self.Q,):
+            raise ConfigError("rom: inconsistent ids/weights/mode_grads shapes")
+        p = lambda a: a.ctypes.data_as(C.c_void_p)
+        h = C.c_void_p()
+        _lib.raise_for(self.lib.podecm_rom_create(self.ctx.h, rve.h, self.N, self.Q, p(ids), p(weights),
+                                                  p(mode_grads), C.byref(h)),
+                       self.ctx.h, "podecm_rom_create")
+        self.h = h
+
+    def solve(self, geom: torch.Tensor, sched: torch.Tensor, opts: NewtonOpts | None = None,
+              out: dict | None = None) -> dict:
+        """Batched rom_solve (rom.cpp:177-200): pbar [n, K, 4] history,
+        iters [n, K], resid [n, K], a_final [n, N], status [n]."""
+        opts = opts or NewtonOpts()
+        n, K = sched.shape[0], sched.shape[1]
+        dev = sched.device
+        _f64(geom, (n, 2), "geom")
+        _f64(sched, (n, K, 4), "sched")
+        o = out or {}
+        pbar = o.get("pbar") if o.get("pbar") is not None else torch.empty((n, K, 4), dtype=torch.float64, device=dev)
+        iters = o.get("iters") if o.get("iters") is not None else torch.empty((n, K), dtype=torch.int32, device=dev)
+        resid = o.get("resid") if o.get("resid") is not None else torch.empty((n, K), dtype=torch.float64, device=dev)
+        af = o.get("a_final") if o.get("a_final") is not None else torch.empty((n, self.N), dtype=torch.float64, device=dev)
+        status = o.get("status") if o.get("status") is not None else torch.empty(n, dtype=torch.int32, device=dev)
+        oc = opts.c()
+        rc = self.lib.podecm_rom_solve_batch(self.ctx.h, self.ctx.stream(), self.h, n, _ptr(geom),
+                                             _ptr(sched), K, C.byref(oc), _ptr(pbar), _ptr(iters),
+                                             _ptr(resid), _ptr(af), _ptr(status))
+        _lib.raise_for(rc, self.ctx.h, "podecm_rom_solve_batch")
+        return {"pbar": pbar, "iters": iters, "resid": resid, "a_final": af, "status": status}
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.podecm_rom_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass

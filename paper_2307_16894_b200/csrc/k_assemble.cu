@@ -1,0 +1,344 @@
+// K2 — batched full-order assembly of the Q4 RVE (BASELINE configs 0 and 2).
+//
+// Two kernels per chunk of instances, no atomics, bitwise reproducible:
+//   k_asm_qp     one thread per (instance, quadrature point): analytic morph
+//                (derive), F = Fbar + grad(w) Fmu^-1, the material point
+//                (P, FD tangent, history), then the 64 K-terms
+//                wq * gt_a . A . gt_b and 8 f-terms of that point
+//                (microfem.cpp:76-123) into an element-blocked scratch
+//                [e][term][k] that stays L2-resident for the chunk;
+//   k_asm_gather one thread per (instance, CSR slot or residual row): sums its
+//                terms in the reference's triplet order — exactly the order
+//                Eigen's setFromTriplets collapses duplicates in
+//                (microfem.cpp:125-128) — through the precomputed map.
+// Per chunk the scratch holds 72 doubles per qp; chunk size is chosen so it
+// fits comfortably in the 126 MB L2.
+#include <algorithm>
+
+#include "rve.cuh"
+
+using namespace podecm_dev;
+using namespace podecm_impl;
+
+namespace {
+
+struct AsmArgs {
+  int n_qp, n_red;
+  int64_t nnz;
+  int64_t inst0;  // first instance of the chunk
+  int n_inst;     // instances in this chunk
+  double r0;
+  const double* nodes;
+  const int32_t* elems;
+  const int32_t* regions;
+  const double* grad;
+  const double* w;
+  const int32_t* node_dof;
+  const double* geom;
+  const double* morph;
+  const double* fbar;
+  const double* w_red;
+  const double* st0;
+  double* st1;
+  double* p_field;
+  double* scratch;  // [chunk inst][n_elems][72][4]
+  int32_t* status;
+  unsigned int* fail;
+  bool tangent;
+};
+
+__global__ void __launch_bounds__(128) k_asm_qp(AsmArgs g, MatTable tab) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)g.n_inst * g.n_qp;
+  if (tid >= total) return;
+  const int c = (int)(tid / g.n_qp);
+  const int q = (int)(tid - (int64_t)c * g.n_qp);
+  const int64_t inst = g.inst0 + c;
+  const int e = q >> 2, k = q & 3;
+  const int nq = g.n_qp;
+
+  double gq[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) gq[t] = __ldg(g.grad + (size_t)q * 8 + t);
+  int node[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) node[a] = __ldg(g.elems + 4 * e + a);
+
+  // morph at this qp
+  double fmi[4], det;
+  if (g.morph) {
+    const double* mo = g.morph + (size_t)inst * 5 * nq;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) fmi[t] = __ldg(mo + (size_t)t * nq + q);
+    det = __ldg(mo + (size_t)4 * nq + q);
+  } else {
+    const double ka = __ldg(g.geom + 2 * inst) / g.r0 - 1.0;
+    const double kb = __ldg(g.geom + 2 * inst + 1) / g.r0 - 1.0;
+    double d[4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+      morph_d(__ldg(g.nodes + 2 * node[a]), __ldg(g.nodes + 2 * node[a] + 1), ka, kb, g.r0, d[a][0],
+              d[a][1]);
+    det = derive_qp(d, gq, fmi);
+  }
+  // fluctuation gradient gw(i,j) = sum_a w(2 node_a + i) g(a,j), then F
+  const double* wr = g.w_red + (size_t)inst * g.n_red;
+  double wn[4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int dof = __ldg(g.node_dof + node[a]);
+    wn[a][0] = dof >= 0 ? __ldg(wr + dof) : 0.0;
+    wn[a][1] = dof >= 0 ? __ldg(wr + dof + 1) : 0.0;
+  }
+  double gw[4];
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) s = s + wn[a][i] * gq[2 * a + j];
+      gw[i + 2 * j] = s;
+    }
+  double F[4];
+  const double* fb = g.fbar + 4 * inst;
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      F[i + 2 * j] = __ldg(fb + i + 2 * j) + (gw[i] * fmi[2 * j] + gw[i + 2] * fmi[1 + 2 * j]);
+
+  // material point with frozen history
+  int reg = __ldg(g.regions + e);
+  const MatConst& p = tab.m[reg];
+  const double* s0 = g.st0 + (size_t)inst * 6 * nq;
+  double fp[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) fp[t] = __ldg(s0 + (size_t)t * nq + q);
+  Frozen z;
+  freeze(fp, __ldg(s0 + (size_t)4 * nq + q), __ldg(s0 + (size_t)5 * nq + q), z);
+  double P[4], A[16];
+  FullOut fo;
+  bool ok;
+  if (g.tangent) {
+    ok = point_update(p, z, F, 1e-7, P, A, fo);
+  } else {
+    ok = lsu_eval<true>(p, z, F, P, &fo);
+  }
+  if (!ok) {
+    if (g.status) g.status[inst] = PODECM_ESOLVE;
+    atomicAdd(g.fail, 1u);
+  }
+  if (g.st1) {
+    double* s1 = g.st1 + (size_t)inst * 6 * nq;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) s1[(size_t)t * nq + q] = fo.fp[t];
+    s1[(size_t)4 * nq + q] = fo.fpzz;
+    s1[(size_t)5 * nq + q] = fo.xi;
+  }
+  if (g.p_field) {
+    double* pf = g.p_field + (size_t)inst * 4 * nq;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) pf[(size_t)t * nq + q] = P[t];
+  }
+
+  const double wq = __ldg(g.w + q) * det;
+  double gt[4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) gt[a][j] = gq[2 * a] * fmi[2 * j] + gq[2 * a + 1] * fmi[1 + 2 * j];
+
+  // element-blocked scratch: [c][e][72][4], slot (term, k)
+  double* sc = g.scratch + ((size_t)c * (nq >> 2) + e) * 72 * 4 + k;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      sc[(64 + a * 2 + i) * 4] = wq * (P[i] * gt[a][0] + P[i + 2] * gt[a][1]);
+  if (!g.tangent) return;
+  // A(i,c,j,d) = A[(i+2c) + 4(j+2d)]
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const double v =
+              gt[a][0] * (A[i + 4 * j] * gt[b][0] + A[i + 4 * (j + 2)] * gt[b][1]) +
+              gt[a][1] * (A[(i + 2) + 4 * j] * gt[b][0] + A[(i + 2) + 4 * (j + 2)] * gt[b][1]);
+          sc[((a * 4 + b) * 4 + i * 2 + j) * 4] = wq * v;
+        }
+}
+
+struct GatherArgs {
+  int n_red, n_elems;
+  int64_t nnz;
+  int64_t inst0;
+  int n_inst;
+  const int32_t* slot_gptr;
+  const int32_t* slot_grp;
+  const int32_t* frow_gptr;
+  const int32_t* frow_grp;
+  const double* scratch;
+  double* f;
+  double* kvals;
+};
+
+// One thread per (instance, item): items [0, nnz) are CSR slots (if kvals),
+// items [nnz, nnz + n_red) residual rows.
+__global__ void __launch_bounds__(256) k_asm_gather(GatherArgs g) {
+  const int64_t n_items = (g.kvals ? g.nnz : 0) + g.n_red;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= n_items * g.n_inst) return;
+  const int c = (int)(tid / n_items);
+  const int64_t it = tid - (int64_t)c * n_items;
+  const double* sc = g.scratch + (size_t)c * g.n_elems * 72 * 4;
+  const int64_t inst = g.inst0 + c;
+  if (g.kvals && it < g.nnz) {
+    const int b0 = __ldg(g.slot_gptr + it), b1 = __ldg(g.slot_gptr + it + 1);
+    double s = 0.0;
+    for (int m = b0; m < b1; ++m) {
+      const int grp = __ldg(g.slot_grp + m);  // e*64 + tl
+      const int e = grp >> 6, tl = grp & 63;
+      const double4 t = *reinterpret_cast<const double4*>(sc + ((size_t)e * 72 + tl) * 4);
+      if (m == b0) {
+        s = t.x;  // setFromTriplets: first duplicate is copied, the rest added
+      } else {
+        s = s + t.x;
+      }
+      s = s + t.y;
+      s = s + t.z;
+      s = s + t.w;
+    }
+    g.kvals[(size_t)inst * g.nnz + it] = s;
+  } else {
+    const int64_t row = it - (g.kvals ? g.nnz : 0);
+    const int b0 = __ldg(g.frow_gptr + row), b1 = __ldg(g.frow_gptr + row + 1);
+    double s = 0.0;  // out.f = VecX::Zero(...); f(ra+i) += ...
+    for (int m = b0; m < b1; ++m) {
+      const int grp = __ldg(g.frow_grp + m);  // e*8 + fl
+      const int e = grp >> 3, fl = grp & 7;
+      const double4 t = *reinterpret_cast<const double4*>(sc + ((size_t)e * 72 + 64 + fl) * 4);
+      s = s + t.x;
+      s = s + t.y;
+      s = s + t.z;
+      s = s + t.w;
+    }
+    g.f[(size_t)inst * g.n_red + row] = s;
+  }
+}
+
+__global__ void k_morph(int64_t n_inst, int nq, double r0, const double* nodes, const int32_t* elems,
+                        const double* grad, const double* geom, double* fmu_inv, double* det,
+                        int32_t* status, unsigned int* fail) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= n_inst * nq) return;
+  const int64_t inst = tid / nq;
+  const int q = (int)(tid - inst * nq);
+  const int e = q >> 2;
+  const double ka = geom[2 * inst] / r0 - 1.0, kb = geom[2 * inst + 1] / r0 - 1.0;
+  double d[4][2], gq[8], fmi[4];
+  for (int t = 0; t < 8; ++t) gq[t] = grad[(size_t)q * 8 + t];
+  for (int a = 0; a < 4; ++a) {
+    const int nd = elems[4 * e + a];
+    morph_d(nodes[2 * nd], nodes[2 * nd + 1], ka, kb, r0, d[a][0], d[a][1]);
+  }
+  const double dt = derive_qp(d, gq, fmi);
+  for (int t = 0; t < 4; ++t) fmu_inv[(size_t)inst * 4 * nq + (size_t)t * nq + q] = fmi[t];
+  det[(size_t)inst * nq + q] = dt;
+  if (!(dt > 0.0)) {
+    if (status) status[inst] = PODECM_ESOLVE;
+    atomicAdd(fail, 1u);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int podecm_rve_morph(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst,
+                     const double* geom, double* fmu_inv, double* det, int32_t* status) {
+  if (!ctx || !r || !geom || !fmu_inv || !det) return set_err(ctx, PODECM_ECONFIG, "null argument");
+  if (n_inst <= 0) return PODECM_OK;
+  auto s = static_cast<cudaStream_t>(stream);
+  if (status) PODECM_CUDA_TRY(ctx, cudaMemsetAsync(status, 0, n_inst * sizeof(int32_t), s));
+  const int64_t total = n_inst * r->n_qp;
+  k_morph<<<grid_for(total, 256), 256, 0, s>>>(n_inst, r->n_qp, r->r0, r->d_nodes, r->d_elems,
+                                               r->d_grad, geom, fmu_inv, det, status, ctx->d_fail);
+  PODECM_LAUNCHED(ctx, 1);
+  return PODECM_OK;
+}
+
+int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst,
+                          const double* geom, const double* morph, const double* fbar,
+                          const double* w_red, const double* st0, double* st1, double* f,
+                          double* kvals, double* p_field, int32_t* status) {
+  if (!ctx || !r) return PODECM_ECONFIG;
+  if (n_inst < 0) return set_err(ctx, PODECM_ECONFIG, "negative instance count");
+  if (n_inst == 0) return PODECM_OK;
+  if ((!geom && !morph) || !fbar || !w_red || !st0 || !f)
+    return set_err(ctx, PODECM_ECONFIG, "geom|morph, fbar, w_red, st0 and f are required");
+  auto s = static_cast<cudaStream_t>(stream);
+  const size_t per_inst = (size_t)r->n_elems * 72 * 4 * sizeof(double);
+  // chunk: scratch <= ~48 MB (L2-resident), at least one instance
+  int64_t chunk = std::max<int64_t>(1, (int64_t)(48ull << 20) / (int64_t)per_inst);
+  chunk = std::min<int64_t>(chunk, n_inst);
+  if (r->scratch_inst < chunk) {
+    cudaFree(r->d_scratch);
+    r->d_scratch = nullptr;
+    PODECM_CUDA_TRY(ctx, cudaMalloc(&r->d_scratch, per_inst * chunk));
+    r->scratch_inst = chunk;
+  }
+  if (status) PODECM_CUDA_TRY(ctx, cudaMemsetAsync(status, 0, n_inst * sizeof(int32_t), s));
+  for (int64_t i0 = 0; i0 < n_inst; i0 += chunk) {
+    const int nc = (int)std::min<int64_t>(chunk, n_inst - i0);
+    AsmArgs a;
+    a.n_qp = r->n_qp;
+    a.n_red = r->n_red;
+    a.nnz = r->nnz;
+    a.inst0 = i0;
+    a.n_inst = nc;
+    a.r0 = r->r0;
+    a.nodes = r->d_nodes;
+    a.elems = r->d_elems;
+    a.regions = r->d_regions;
+    a.grad = r->d_grad;
+    a.w = r->d_w;
+    a.node_dof = r->d_node_dof;
+    a.geom = geom;
+    a.morph = morph;
+    a.fbar = fbar;
+    a.w_red = w_red;
+    a.st0 = st0;
+    a.st1 = st1;
+    a.p_field = p_field;
+    a.scratch = r->d_scratch;
+    a.status = status;
+    a.fail = ctx->d_fail;
+    a.tangent = kvals != nullptr;
+    const int64_t nthr = (int64_t)nc * r->n_qp;
+    k_asm_qp<<<grid_for(nthr, 128), 128, 0, s>>>(a, r->mats);
+    GatherArgs gg;
+    gg.n_red = r->n_red;
+    gg.n_elems = r->n_elems;
+    gg.nnz = r->nnz;
+    gg.inst0 = i0;
+    gg.n_inst = nc;
+    gg.slot_gptr = r->d_slot_gptr;
+    gg.slot_grp = r->d_slot_grp;
+    gg.frow_gptr = r->d_frow_gptr;
+    gg.frow_grp = r->d_frow_grp;
+    gg.scratch = r->d_scratch;
+    gg.f = f;
+    gg.kvals = kvals;
+    const int64_t nitems = ((kvals ? r->nnz : 0) + r->n_red) * nc;
+    k_asm_gather<<<grid_for(nitems, 256), 256, 0, s>>>(gg);
+    PODECM_LAUNCHED(ctx, 2);
+  }
+  return PODECM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,323 @@
+// Host-side construction of the RVE tables (C++): structured Q4 mesh,
+// quadrature cache, periodic dof map, CSR pattern and the deterministic
+// gather ("scatter map") that sums every CSR slot in the reference's
+// setFromTriplets order.  Everything here runs once per mesh; the per-
+// instance work is on the device (k_assemble.cu, k_rom.cu).
+//
+// Reference interfaces restated: build_quad_cache (mesh.cpp:412-451),
+// periodic_pairs / periodic_dof_map (mesh.cpp:307-374), the triplet loop of
+// assemble (microfem.cpp:108-122) and Eigen setFromTriplets
+// (microfem.cpp:125-128): duplicates summed in triplet order, pattern rows
+// sorted, structural zeros kept.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+
+#include "rve.cuh"
+
+using namespace podecm_impl;
+
+namespace {
+
+const double kCx[4] = {-1, 1, 1, -1};
+const double kCy[4] = {-1, -1, 1, 1};
+
+// Structured n x n grid; node j*(n+1)+i; CCW corners; region by centroid.
+void build_mesh(podecm_rve& r) {
+  const int n = r.n_cells, np = n + 1;
+  r.n_nodes = np * np;
+  r.n_elems = n * n;
+  r.nodes.resize(2 * (size_t)r.n_nodes);
+  for (int j = 0; j < np; ++j)
+    for (int i = 0; i < np; ++i) {
+      r.nodes[2 * (j * np + i)] = i / (double)n;
+      r.nodes[2 * (j * np + i) + 1] = j / (double)n;
+    }
+  r.elems.resize(4 * (size_t)r.n_elems);
+  r.regions.resize(r.n_elems);
+  for (int cj = 0; cj < n; ++cj)
+    for (int ci = 0; ci < n; ++ci) {
+      const int e = cj * n + ci;
+      const int c[4] = {cj * np + ci, cj * np + ci + 1, (cj + 1) * np + ci + 1, (cj + 1) * np + ci};
+      double cx = 0, cy = 0;
+      for (int a = 0; a < 4; ++a) {
+        r.elems[4 * e + a] = c[a];
+        cx += r.nodes[2 * c[a]];
+        cy += r.nodes[2 * c[a] + 1];
+      }
+      cx = 0.25 * cx - 0.5;
+      cy = 0.25 * cy - 0.5;
+      r.regions[e] = std::sqrt(cx * cx + cy * cy) <= r.r0 ? 1 : 0;
+    }
+}
+
+void build_cache(podecm_rve& r) {
+  const double g = 1.0 / std::sqrt(3.0);
+  const double qx[4] = {-g, g, g, -g}, qy[4] = {-g, -g, g, g};
+  double dn[4][4][2];
+  for (int q = 0; q < 4; ++q)
+    for (int a = 0; a < 4; ++a) {
+      dn[q][a][0] = 0.25 * kCx[a] * (1 + qy[q] * kCy[a]);
+      dn[q][a][1] = 0.25 * kCy[a] * (1 + qx[q] * kCx[a]);
+    }
+  r.n_qp = 4 * r.n_elems;
+  r.grad.resize((size_t)r.n_qp * 8);
+  r.w.resize(r.n_qp);
+  for (int e = 0; e < r.n_elems; ++e) {
+    double X[4][2];
+    for (int a = 0; a < 4; ++a)
+      for (int i = 0; i < 2; ++i) X[a][i] = r.nodes[2 * r.elems[4 * e + a] + i];
+    for (int q = 0; q < 4; ++q) {
+      double J[4];
+      for (int j = 0; j < 2; ++j)
+        for (int i = 0; i < 2; ++i) {
+          const double t0 = X[0][i] * dn[q][0][j], t1 = X[1][i] * dn[q][1][j];
+          const double t2 = X[2][i] * dn[q][2][j], t3 = X[3][i] * dn[q][3][j];
+          J[i + 2 * j] = (t0 + t2) + (t1 + t3);
+        }
+      const double dj = J[0] * J[3] - J[1] * J[2];
+      if (dj <= 0.0) throw std::runtime_error("element has non-positive Jacobian");
+      const double inv = 1.0 / dj;
+      const double Ji[4] = {J[3] * inv, -J[1] * inv, -J[2] * inv, J[0] * inv};
+      const int gq = 4 * e + q;
+      for (int a = 0; a < 4; ++a)
+        for (int j = 0; j < 2; ++j)
+          r.grad[(size_t)gq * 8 + 2 * a + j] = dn[q][a][0] * Ji[0 + 2 * j] + dn[q][a][1] * Ji[1 + 2 * j];
+      r.w[gq] = 1.0 * dj;
+    }
+  }
+}
+
+void build_dofs(podecm_rve& r) {
+  const double tol = 1e-8;
+  auto near = [tol](double a, double b) { return std::abs(a - b) <= tol; };
+  int anchor = -1;
+  std::vector<int> corners, left, right, bottom, top;
+  for (int i = 0; i < r.n_nodes; ++i) {
+    const double x = r.nodes[2 * i], y = r.nodes[2 * i + 1];
+    const bool x0 = near(x, 0), x1 = near(x, 1), y0 = near(y, 0), y1 = near(y, 1);
+    if (x0 && y0) anchor = i;
+    else if ((x1 && y0) || (x0 && y1) || (x1 && y1)) corners.push_back(i);
+    else if (x0) left.push_back(i);
+    else if (x1) right.push_back(i);
+    else if (y0) bottom.push_back(i);
+    else if (y1) top.push_back(i);
+  }
+  if (anchor < 0 || corners.size() != 3) throw std::runtime_error("periodic pairing needs 4 corners");
+  std::map<int, int> slave_of;
+  for (int c : corners) slave_of[c] = anchor;
+  auto pair = [&](std::vector<int>& ma, std::vector<int>& sl, int coord) {
+    auto key = [&](int n) { return r.nodes[2 * n + coord]; };
+    std::sort(ma.begin(), ma.end(), [&](int a, int b) { return key(a) < key(b); });
+    std::sort(sl.begin(), sl.end(), [&](int a, int b) { return key(a) < key(b); });
+    if (ma.size() != sl.size()) throw std::runtime_error("periodic faces differ in node count");
+    for (size_t k = 0; k < ma.size(); ++k) {
+      if (!near(key(ma[k]), key(sl[k]))) throw std::runtime_error("unmatched periodic node");
+      slave_of[sl[k]] = ma[k];
+    }
+  };
+  pair(left, right, 1);
+  pair(bottom, top, 0);
+  r.anchor = anchor;
+  r.node_dof.assign(r.n_nodes, -2);
+  int next = 0;
+  for (int i = 0; i < r.n_nodes; ++i) {
+    if (i == anchor || slave_of.count(i)) continue;
+    r.node_dof[i] = next;
+    next += 2;
+  }
+  r.node_dof[anchor] = -1;
+  for (const auto& kv : slave_of) r.node_dof[kv.first] = r.node_dof[kv.second];
+  r.n_red = next;
+}
+
+// Triplet ids in reference order (q, a, b, i, j) -> CSR slots, then the
+// per-slot term lists.  Term id t = q*64 + tl, tl = (a*4+b)*4 + i*2 + j.
+void build_pattern(podecm_rve& r) {
+  const int nr = r.n_red;
+  std::vector<std::vector<std::pair<int, int>>> rows(nr);  // (col, term) in triplet order
+  std::vector<std::vector<int>> frows(nr);                 // f terms q*8 + a*2 + i
+  for (int q = 0; q < r.n_qp; ++q) {
+    const int e = q >> 2;
+    for (int a = 0; a < 4; ++a) {
+      const int ra = r.node_dof[r.elems[4 * e + a]];
+      if (ra < 0) continue;
+      for (int i = 0; i < 2; ++i) frows[ra + i].push_back(q * 8 + a * 2 + i);
+      for (int b = 0; b < 4; ++b) {
+        const int rb = r.node_dof[r.elems[4 * e + b]];
+        if (rb < 0) continue;
+        for (int i = 0; i < 2; ++i)
+          for (int j = 0; j < 2; ++j) rows[ra + i].push_back({rb + j, q * 64 + (a * 4 + b) * 4 + i * 2 + j});
+      }
+    }
+  }
+  r.row_ptr.assign(nr + 1, 0);
+  r.col_idx.clear();
+  r.slot_ptr.assign(1, 0);
+  r.slot_terms.clear();
+  r.slot_gptr.assign(1, 0);
+  r.slot_grp.clear();
+  for (int row = 0; row < nr; ++row) {
+    auto& v = rows[row];
+    std::stable_sort(v.begin(), v.end(),
+                     [](const std::pair<int, int>& x, const std::pair<int, int>& y) { return x.first < y.first; });
+    size_t k = 0;
+    while (k < v.size()) {
+      const int c = v[k].first;
+      size_t k1 = k;
+      while (k1 < v.size() && v[k1].first == c) ++k1;
+      r.col_idx.push_back(c);
+      // group runs of 4 consecutive qps of one element with the same tl
+      size_t m = k;
+      while (m < k1) {
+        const int t = v[m].second, q = t / 64, tl = t % 64;
+        if ((q & 3) != 0 || m + 4 > k1) throw std::runtime_error("scatter map: ungroupable slot");
+        for (int kk = 1; kk < 4; ++kk)
+          if (v[m + kk].second != (q + kk) * 64 + tl)
+            throw std::runtime_error("scatter map: element aliases itself (mesh too coarse)");
+        r.slot_grp.push_back((q >> 2) * 64 + tl);
+        m += 4;
+      }
+      for (size_t m2 = k; m2 < k1; ++m2) r.slot_terms.push_back(v[m2].second);
+      r.slot_ptr.push_back((int32_t)r.slot_terms.size());
+      r.slot_gptr.push_back((int32_t)r.slot_grp.size());
+      k = k1;
+    }
+    r.row_ptr[row + 1] = (int32_t)r.col_idx.size();
+    std::vector<std::pair<int, int>>().swap(v);
+  }
+  r.nnz = (int64_t)r.col_idx.size();
+  r.n_trip = (int64_t)r.slot_terms.size();
+  r.frow_gptr.assign(1, 0);
+  r.frow_grp.clear();
+  for (int row = 0; row < nr; ++row) {
+    const auto& v = frows[row];
+    size_t m = 0;
+    while (m < v.size()) {
+      const int t = v[m], q = t / 8, fl = t % 8;
+      if ((q & 3) != 0 || m + 4 > v.size()) throw std::runtime_error("residual map: ungroupable row");
+      for (int kk = 1; kk < 4; ++kk)
+        if (v[m + kk] != (q + kk) * 8 + fl) throw std::runtime_error("residual map: aliasing");
+      r.frow_grp.push_back((q >> 2) * 8 + fl);
+      m += 4;
+    }
+    r.frow_gptr.push_back((int32_t)r.frow_grp.size());
+  }
+}
+
+template <class T>
+int upload(podecm_ctx* ctx, T** d, const std::vector<T>& h) {
+  PODECM_CUDA_TRY(ctx, cudaMalloc(d, std::max<size_t>(1, h.size()) * sizeof(T)));
+  if (!h.empty()) PODECM_CUDA_TRY(ctx, cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return PODECM_OK;
+}
+
+void free_rve(podecm_rve* r) {
+  cudaFree(r->d_nodes);
+  cudaFree(r->d_grad);
+  cudaFree(r->d_w);
+  cudaFree(r->d_elems);
+  cudaFree(r->d_regions);
+  cudaFree(r->d_node_dof);
+  cudaFree(r->d_slot_gptr);
+  cudaFree(r->d_slot_grp);
+  cudaFree(r->d_frow_gptr);
+  cudaFree(r->d_frow_grp);
+  cudaFree(r->d_scratch);
+}
+
+}  // namespace
+
+extern "C" {
+
+int podecm_rve_create_q4(podecm_ctx* ctx, int n_cells, double r0, const podecm_params* mats,
+                         int n_mats, podecm_rve** out) {
+  if (!ctx || !out) return PODECM_ECONFIG;
+  *out = nullptr;
+  if (n_cells < 2) return set_err(ctx, PODECM_ECONFIG, "structured Q4 RVE needs n_cells >= 2");
+  if (!(r0 > 0 && r0 < 0.5)) return set_err(ctx, PODECM_ECONFIG, "r0 must lie in (0, 0.5)");
+  if (int rc = check_params(ctx, mats, n_mats)) return rc;
+  auto* r = new podecm_rve;
+  r->ctx = ctx;
+  r->n_cells = n_cells;
+  r->r0 = r0;
+  r->n_mats = n_mats;
+  r->mats = make_table(mats, n_mats);
+  try {
+    build_mesh(*r);
+    build_cache(*r);
+    build_dofs(*r);
+    build_pattern(*r);
+    for (int reg : r->regions)
+      if (reg < 0 || reg >= n_mats) {  // RveProblem::build, microfem.cpp:17-21
+        delete r;
+        return set_err(ctx, PODECM_ECONFIG, "element region " + std::to_string(reg) + " has no material");
+      }
+  } catch (const std::exception& ex) {
+    delete r;
+    return set_err(ctx, PODECM_ESOLVE, ex.what());
+  }
+  int rc = PODECM_OK;
+  if (!rc) rc = upload(ctx, &r->d_nodes, r->nodes);
+  if (!rc) rc = upload(ctx, &r->d_grad, r->grad);
+  if (!rc) rc = upload(ctx, &r->d_w, r->w);
+  if (!rc) rc = upload(ctx, &r->d_elems, r->elems);
+  if (!rc) rc = upload(ctx, &r->d_regions, r->regions);
+  if (!rc) rc = upload(ctx, &r->d_node_dof, r->node_dof);
+  if (!rc) rc = upload(ctx, &r->d_slot_gptr, r->slot_gptr);
+  if (!rc) rc = upload(ctx, &r->d_slot_grp, r->slot_grp);
+  if (!rc) rc = upload(ctx, &r->d_frow_gptr, r->frow_gptr);
+  if (!rc) rc = upload(ctx, &r->d_frow_grp, r->frow_grp);
+  if (rc) {
+    free_rve(r);
+    delete r;
+    return rc;
+  }
+  *out = r;
+  return PODECM_OK;
+}
+
+void podecm_rve_destroy(podecm_rve* r) {
+  if (!r) return;
+  free_rve(r);
+  delete r;
+}
+
+int podecm_rve_info(const podecm_rve* r, int64_t out[6]) {
+  if (!r || !out) return PODECM_ECONFIG;
+  out[0] = r->n_nodes;
+  out[1] = r->n_elems;
+  out[2] = r->n_qp;
+  out[3] = r->n_red;
+  out[4] = r->nnz;
+  out[5] = r->anchor;
+  return PODECM_OK;
+}
+
+int64_t podecm_rve_n_triplets(const podecm_rve* r) { return r ? r->n_trip : 0; }
+
+int podecm_rve_export(const podecm_rve* r, double* nodes, int32_t* elems, int32_t* regions,
+                      double* grad, double* w, int32_t* node_dof, int32_t* row_ptr,
+                      int32_t* col_idx, int32_t* slot_ptr, int32_t* slot_terms) {
+  if (!r) return PODECM_ECONFIG;
+  auto cp = [](auto* dst, const auto& v) {
+    if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+  };
+  cp(nodes, r->nodes);
+  cp(elems, r->elems);
+  cp(regions, r->regions);
+  cp(grad, r->grad);
+  cp(w, r->w);
+  cp(node_dof, r->node_dof);
+  cp(row_ptr, r->row_ptr);
+  cp(col_idx, r->col_idx);
+  cp(slot_ptr, r->slot_ptr);
+  cp(slot_terms, r->slot_terms);
+  return PODECM_OK;
+}
+
+}  // extern "C"

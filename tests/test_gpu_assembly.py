@@ -1,0 +1,137 @@
+"""K2 parity: batched Q4 assembly (configs 0 and 2) vs the CPU oracle.
+
+Bit-exact: mesh tables, quadrature cache, periodic dof map, CSR pattern
+(row_ptr / col_idx) and the morph (no transcendental on that path).
+Tolerances: residual 1e-10 (vector 2-norm relative), K 1e-9
+(||dK||_F / ||K||_F per instance), history 1e-10 per point.
+"""
+import numpy as np
+import pytest
+
+from paper_2307_16894_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _mats():
+    from paper_2307_16894_b200.api import inclusion_params, matrix_params
+    return [matrix_params(), inclusion_params()]
+
+
+@pytest.fixture(scope="module")
+def pair64(orc):
+    from paper_2307_16894_b200 import api
+    return api.Rve(64, _mats()), orc.Rve(64, _mats())
+
+
+@pytest.fixture(scope="module")
+def pair128(orc):
+    from paper_2307_16894_b200 import api
+    return api.Rve(128, _mats()), orc.Rve(128, _mats())
+
+
+def test_tables_bit_exact(pair64):
+    g, o = pair64
+    tg, to = g.export(), o.export()
+    assert (g.n_red, g.nnz) == (8190, 147388)
+    for k in ("nodes", "elems", "regions", "grad", "w", "node_dof", "row_ptr", "col_idx"):
+        assert np.array_equal(tg[k], to[k]), k
+
+
+def test_tables_bit_exact_128(pair128):
+    g, o = pair128
+    assert (g.n_red, g.nnz) == (32766, 589756)
+    tg, to = g.export(), o.export()
+    for k in ("row_ptr", "col_idx", "node_dof", "grad", "w"):
+        assert np.array_equal(tg[k], to[k]), k
+
+
+def test_morph_bit_exact(pair64):
+    import torch
+    g, o = pair64
+    geom = torch.tensor([[0.3, 0.2], [0.15, 0.35]], dtype=torch.float64, device="cuda")
+    fmi, det, st = g.morph(geom)
+    for s, (a, b) in enumerate(((0.3, 0.2), (0.15, 0.35))):
+        ofmi, odet, rc = o.morph(a, b)
+        assert rc == 0 and int(st[s]) == 0
+        assert np.array_equal(fmi[s].cpu().numpy(), ofmi)
+        assert np.array_equal(det[s].cpu().numpy(), odet)
+
+
+def _assemble_both(g, o, n_inst, seed, hm, geom_range=None):
+    import torch
+    tg = g.export()
+    regions_qp = np.repeat(tg["regions"], 4)
+    geom, fbar, w_red, st0 = synth.rve_instances(n_inst, g.n_red, regions_qp, seed, hm,
+                                                 geom_range=geom_range)
+    dev = torch.device("cuda:0")
+    T = lambda a: torch.from_numpy(a).to(dev)
+    rg = g.assemble(T(fbar), T(w_red), T(st0), geom=T(geom), store_stress=True)
+    torch.cuda.synchronize()
+    rg = {k: v.cpu().numpy() for k, v in rg.items() if v is not None}
+    ro = o.assemble(geom, fbar, w_red, st0, store_stress=True)
+    return rg, ro
+
+
+def _check(rg, ro, n_inst):
+    assert np.array_equal(rg["status"], ro["status"])
+    for s in range(n_inst):
+        ef = np.linalg.norm(rg["f"][s] - ro["f"][s]) / np.linalg.norm(ro["f"][s])
+        eK = np.linalg.norm(rg["K"][s] - ro["K"][s]) / np.linalg.norm(ro["K"][s])
+        dP = rg["p_field"][s] - ro["p_field"][s]
+        eP = (np.sqrt((dP ** 2).sum(0)) / np.maximum(np.sqrt((ro["p_field"][s] ** 2).sum(0)), 1e-14)).max()
+        dS = rg["st1"][s] - ro["st1"][s]
+        eS = (np.sqrt((dS ** 2).sum(0)) / np.maximum(np.sqrt((ro["st1"][s] ** 2).sum(0)), 1e-14)).max()
+        print(f"inst {s}: f {ef:.2e} K {eK:.2e} P {eP:.2e} st {eS:.2e} "
+              f"K bitwise {np.mean(rg['K'][s] == ro['K'][s]):.4f}")
+        assert ef <= 1e-10 and eP <= 1e-10 and eS <= 1e-10 and eK <= 1e-9
+
+
+def test_config0_single_rve(pair64):
+    g, o = pair64
+    rg, ro = _assemble_both(g, o, 1, 2026, 0.1)
+    _check(rg, ro, 1)
+
+
+def test_config2_instances(pair128):
+    g, o = pair128
+    rg, ro = _assemble_both(g, o, 3, 2028, 0.2, geom_range=(0.15, 0.35))
+    _check(rg, ro, 3)
+
+
+def test_residual_only_matches_full(pair64):
+    """AssemblyOpts.tangent = false gives the same residual and history."""
+    import torch
+    g, _ = pair64
+    tg = g.export()
+    geom, fbar, w_red, st0 = synth.rve_instances(2, g.n_red, np.repeat(tg["regions"], 4), 5, 0.1)
+    T = lambda a: torch.from_numpy(a).cuda()
+    a = g.assemble(T(fbar), T(w_red), T(st0), geom=T(geom))
+    b = g.assemble(T(fbar), T(w_red), T(st0), geom=T(geom), tangent=False)
+    assert torch.equal(a["f"], b["f"]) and torch.equal(a["st1"], b["st1"])
+
+
+def test_morph_field_input_equals_geom(pair64):
+    """Passing the MorphField (fmu_inv, det) instead of (a, b) is identical."""
+    import torch
+    g, _ = pair64
+    tg = g.export()
+    geom, fbar, w_red, st0 = synth.rve_instances(2, g.n_red, np.repeat(tg["regions"], 4), 6, 0.1,
+                                                 geom_range=(0.15, 0.35))
+    T = lambda a: torch.from_numpy(a).cuda()
+    fmi, det, _ = g.morph(T(geom))
+    morph = torch.cat([fmi, det[:, None, :]], 1).contiguous()
+    a = g.assemble(T(fbar), T(w_red), T(st0), geom=T(geom))
+    b = g.assemble(T(fbar), T(w_red), T(st0), morph=morph)
+    assert torch.equal(a["f"], b["f"]) and torch.equal(a["K"], b["K"])
+
+
+def test_deterministic(pair64):
+    import torch
+    g, _ = pair64
+    tg = g.export()
+    geom, fbar, w_red, st0 = synth.rve_instances(1, g.n_red, np.repeat(tg["regions"], 4), 9, 0.1)
+    T = lambda a: torch.from_numpy(a).cuda()
+    a = g.assemble(T(fbar), T(w_red), T(st0), geom=T(geom))
+    b = g.assemble(T(fbar), T(w_red), T(st0), geom=T(geom))
+    assert torch.equal(a["K"], b["K"]) and torch.equal(a["f"], b["f"])
