@@ -47,7 +47,7 @@ struct AsmArgs {
   bool tangent;
 };
 
-__global__ void __launch_bounds__(128) k_asm_qp(AsmArgs g, MatTable tab) {
+__global__ void __launch_bounds__(128, 5) k_asm_qp(AsmArgs g, MatTable tab) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)g.n_inst * g.n_qp;
   if (tid >= total) return;
@@ -117,18 +117,9 @@ __global__ void __launch_bounds__(128) k_asm_qp(AsmArgs g, MatTable tab) {
   for (int t = 0; t < 4; ++t) fp[t] = __ldg(s0 + (size_t)t * nq + q);
   Frozen z;
   freeze(fp, __ldg(s0 + (size_t)4 * nq + q), __ldg(s0 + (size_t)5 * nq + q), z);
-  double P[4], A[16];
+  double P[4];
   FullOut fo;
-  bool ok;
-  if (g.tangent) {
-    ok = point_update(p, z, F, 1e-7, P, A, fo);
-  } else {
-    ok = lsu_eval<true>(p, z, F, P, &fo);
-  }
-  if (!ok) {
-    if (g.status) g.status[inst] = PODECM_ESOLVE;
-    atomicAdd(g.fail, 1u);
-  }
+  bool ok = lsu_eval<true>(p, z, F, P, &fo);
   if (g.st1) {
     double* s1 = g.st1 + (size_t)inst * 6 * nq;
 #pragma unroll
@@ -149,28 +140,44 @@ __global__ void __launch_bounds__(128) k_asm_qp(AsmArgs g, MatTable tab) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) gt[a][j] = gq[2 * a] * fmi[2 * j] + gq[2 * a + 1] * fmi[1 + 2 * j];
 
-  // element-blocked scratch: [c][e][72][4], slot (term, k)
+  // element-blocked scratch: [c][e][72][4], entry (term, k)
   double* sc = g.scratch + ((size_t)c * (nq >> 2) + e) * 72 * 4 + k;
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int i = 0; i < 2; ++i)
       sc[(64 + a * 2 + i) * 4] = wq * (P[i] * gt[a][0] + P[i + 2] * gt[a][1]);
-  if (!g.tangent) return;
-  // A(i,c,j,d) = A[(i+2c) + 4(j+2d)]
+  if (ok && g.tangent) {
+    // A(i,c,j,d) = A[(i+2c) + 4(j+2d)]: column e = j + 2d.  Columns arrive in
+    // the order 0, 2, 1, 3, so after the second column of each j the 32 terms
+    // K(a i, b j) += wq * sum_cd gt_ac A(i,c,j,d) gt_bd are emitted
+    // (microfem.cpp:113-117 order).
+    double cd[2][4];
+    auto sink = [&](int ecol, const double col[4]) {
+      const int d = ecol >> 1, j = ecol & 1;
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+      for (int r = 0; r < 4; ++r) {
+        cd[0][r] = d == 0 ? col[r] : cd[0][r];
+        cd[1][r] = d == 1 ? col[r] : cd[1][r];
+      }
+      if (d == 0) return;
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+        for (int b = 0; b < 4; ++b)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const double v =
-              gt[a][0] * (A[i + 4 * j] * gt[b][0] + A[i + 4 * (j + 2)] * gt[b][1]) +
-              gt[a][1] * (A[(i + 2) + 4 * j] * gt[b][0] + A[(i + 2) + 4 * (j + 2)] * gt[b][1]);
-          sc[((a * 4 + b) * 4 + i * 2 + j) * 4] = wq * v;
-        }
+          for (int i = 0; i < 2; ++i) {
+            const double v = gt[a][0] * (cd[0][i] * gt[b][0] + cd[1][i] * gt[b][1]) +
+                             gt[a][1] * (cd[0][i + 2] * gt[b][0] + cd[1][i + 2] * gt[b][1]);
+            sc[((a * 4 + b) * 4 + i * 2 + j) * 4] = wq * v;
+          }
+    };
+    ok = fd_tangent<false>(p, z, F, 1e-7, sink);
+  }
+  if (!ok) {
+    if (g.status) g.status[inst] = PODECM_ESOLVE;
+    atomicAdd(g.fail, 1u);
+  }
 }
 
 struct GatherArgs {

@@ -8,6 +8,7 @@
 // point against 288 B of HBM traffic); see DESIGN.md §K1.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -17,7 +18,8 @@ using namespace podecm_impl;
 
 namespace {
 
-__global__ void __launch_bounds__(128) k_material_batch(
+template <bool PAIR, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_material_batch(
     int64_t n, MatTable tab, int n_mats, const int32_t* __restrict__ region,
     const double* __restrict__ F, const double* __restrict__ st, double* __restrict__ P,
     double* __restrict__ A, double* __restrict__ st_out, int32_t* __restrict__ status,
@@ -34,24 +36,44 @@ __global__ void __launch_bounds__(128) k_material_batch(
     for (int k = 0; k < 4; ++k) fp[k] = __ldg(st + k * n + i);
     Frozen z;
     freeze(fp, __ldg(st + 4 * n + i), __ldg(st + 5 * n + i), z);
-    double pv[4], av[16];
+    double pv[4];
     FullOut fo;
-    const bool ok = point_update(p, z, f, h_rel, pv, av, fo);
+    bool ok = lsu_eval<true>(p, z, f, pv, &fo);
 #pragma unroll
     for (int k = 0; k < 4; ++k) __stcs(P + k * n + i, pv[k]);
-    if (A) {
-#pragma unroll
-      for (int k = 0; k < 16; ++k) __stcs(A + k * n + i, av[k]);
-    }
     if (st_out) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) __stcs(st_out + k * n + i, fo.fp[k]);
       __stcs(st_out + 4 * n + i, fo.fpzz);
       __stcs(st_out + 5 * n + i, fo.xi);
     }
+    if (ok && A) {
+      // columns go straight to their planes: A[(r + 4e) * n + i]
+      auto sink = [&](int e, const double col[4]) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) __stcs(A + (int64_t)(r + 4 * e) * n + i, col[r]);
+      };
+      ok = fd_tangent<PAIR>(p, z, f, h_rel, sink);
+    }
     if (status) status[i] = ok ? 0 : PODECM_ESOLVE;
     if (!ok) atomicAdd(fail, 1u);
   }
+}
+
+// Variant table (FD pairing x register budget); the default was chosen by
+// measurement on B200, PODECM_K1_VARIANT overrides it.
+using KFn = void (*)(int64_t, MatTable, int, const int32_t*, const double*, const double*, double*,
+                     double*, double*, int32_t*, unsigned int*, double);
+const KFn kVariants[] = {k_material_batch<true, 3>, k_material_batch<true, 4>,
+                         k_material_batch<false, 4>, k_material_batch<false, 5>};
+
+int k1_variant() {
+  static int v = [] {
+    const char* e = getenv("PODECM_K1_VARIANT");
+    int x = e ? atoi(e) : 3;
+    return (x >= 0 && x < 4) ? x : 3;
+  }();
+  return v;
 }
 
 }  // namespace
@@ -115,7 +137,7 @@ int podecm_material_batch(podecm_ctx* ctx, void* stream, int64_t n, const podecm
   const int block = 128;
   const int64_t blocks = (n + block - 1) / block;
   const int grid = (int)(blocks < (int64_t)ctx->n_sm * 64 ? blocks : (int64_t)ctx->n_sm * 64);
-  k_material_batch<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
+  kVariants[k1_variant()]<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
       n, tab, n_mats, region, F, st_in, P, A, st_out, status, ctx->d_fail, h_rel);
   PODECM_LAUNCHED(ctx, 1);
   return PODECM_OK;
