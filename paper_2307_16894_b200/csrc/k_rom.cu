@@ -1,30 +1,761 @@
-// K3 — batched hyper-reduced online stage (BASELINE config 3).  [in progress]
+// K3 — batched ECM hyper-reduced online stage (BASELINE config 3).
+//
+// Replaces rom_solve + rom_solve_step_adaptive + rom_solve_step +
+// rom_assemble (/root/reference/proj/src/rom.cpp:34-200) for a batch of
+// independent RVE instances sharing one RomModel.  Every instance runs its
+// own Newton / bisection state machine; one "global iteration" is one
+// reduced assembly for every still-active instance:
+//
+//   k_rom_point     (instance, ECM point): F = Fbar + R(Fmu^-1)^T (G_p^T a),
+//                   material point (P, FD tangent, trial history), then the
+//                   mapped per-point operators
+//                     At_p = c_p R_p A_p R_p^T   (4x4),  Pt_p = c_p R_p P_p
+//                   with c_p = w_p det Fmu_p and R_p = right_mult_op(Fmu^-1)
+//                   (rom.cpp:16-26);
+//   k_rom_contract  K = sum_p G_p At_p G_p^T and f = sum_p G_p Pt_p as one
+//                   FP64 tensor-core GEMM per instance, K_ext = Gm^T Y with
+//                   Gm the (4Q x N) stack of the shared mode gradients and
+//                   Y = blockdiag(At) Gm | Pt (f rides in the padding column
+//                   N of the N+1 -> 8-aligned tile width); mma.sync m8n8k4
+//                   f64 (DMMA — tcgen05 has no f64 kind on sm_100a);
+//   k_rom_newton    one warp per instance: ||f||, the reference's convergence
+//                   test (tolerance frozen at iteration 0), dense LU with
+//                   partial pivoting (Eigen PartialPivLU semantics) and the
+//                   update, or the adaptive bisection / commit logic.
+//
+// Summation order of the contractions differs from Eigen's; the stated
+// tolerance for the homogenised stress history is 1e-8 (BASELINE north star).
+#include <algorithm>
+#include <cstring>
+#include <type_traits>
+#include <vector>
+
 #include "rve.cuh"
 
+using namespace podecm_dev;
 using namespace podecm_impl;
+
+namespace {
+
+constexpr int kMaxStack = 8;    // max_bisect + 1 frames (max_bisect <= 7)
+constexpr int kPC = 8;          // points per contraction chunk (32 k-rows)
+constexpr int kIPC = 2;         // instances per contraction CTA
+constexpr int kPtsTile = 32;    // material kernel: points per CTA
+constexpr int kInstTile = 8;    // material kernel: instances per CTA
+
+struct RomCtl {
+  double tol, resid;
+  double fstack[kMaxStack][8];  // (F_prev[4], F_target[4]) per pending task
+  int dstack[kMaxStack];        // remaining bisection depth per task
+  int sp, it, k, iters_acc, cur, active, status, asm_fail;
+};
+
+}  // namespace
 
 struct podecm_rom {
   podecm_rve* rve = nullptr;
-  int N = 0, Q = 0;
+  podecm_ctx* ctx = nullptr;
+  int N = 0, Q = 0, Qpad = 0, NT = 0, NP = 0;
+  int32_t* d_ids = nullptr;
+  int32_t* d_reg = nullptr;  // material index per ECM point
+  double* d_w = nullptr;
+  double* d_G = nullptr;   // Gm padded [Qpad*4][NP] row-major: rows (p, r), cols i
+  double* d_Gt = nullptr;  // [N][4][Qpad]: G_p[i][r], p fastest (material kernel)
+  int64_t cap = 0;
+  double *d_morph = nullptr, *d_S = nullptr, *d_At = nullptr, *d_P = nullptr, *d_K = nullptr,
+         *d_f = nullptr, *d_a = nullptr, *d_a0 = nullptr;
+  RomCtl* d_ctl = nullptr;
+  int* d_nactive = nullptr;
+  int* h_nactive = nullptr;
 };
+
+namespace {
+
+void free_work(podecm_rom* r) {
+  cudaFree(r->d_morph);
+  cudaFree(r->d_S);
+  cudaFree(r->d_At);
+  cudaFree(r->d_P);
+  cudaFree(r->d_K);
+  cudaFree(r->d_f);
+  cudaFree(r->d_a);
+  cudaFree(r->d_a0);
+  cudaFree(r->d_ctl);
+  r->d_morph = r->d_S = r->d_At = r->d_P = r->d_K = r->d_f = r->d_a = r->d_a0 = nullptr;
+  r->d_ctl = nullptr;
+  r->cap = 0;
+}
+
+// ---- init: morph slice at the ECM points, virgin history, control blocks
+__global__ void k_rom_init_points(int64_t n, int Q, int nq, double r0, const int32_t* ids,
+                                  const double* nodes, const int32_t* elems, const double* grad,
+                                  const double* geom, double* morph, double* S, int64_t cap,
+                                  RomCtl* ctl) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= n * Q) return;
+  const int64_t s = tid / Q;
+  const int p = (int)(tid - s * Q);
+  const int qp = ids[p], e = qp >> 2;
+  const double ka = geom[2 * s] / r0 - 1.0, kb = geom[2 * s + 1] / r0 - 1.0;
+  double d[4][2], gq[8], fmi[4];
+  for (int t = 0; t < 8; ++t) gq[t] = grad[(size_t)qp * 8 + t];
+  for (int a = 0; a < 4; ++a) {
+    const int nd = elems[4 * e + a];
+    morph_d(nodes[2 * nd], nodes[2 * nd + 1], ka, kb, r0, d[a][0], d[a][1]);
+  }
+  const double dt = derive_qp(d, gq, fmi);
+  double* mo = morph + (size_t)s * 5 * Q;
+  for (int t = 0; t < 4; ++t) mo[(size_t)t * Q + p] = fmi[t];
+  mo[(size_t)4 * Q + p] = dt;
+  if (!(dt > 0.0)) {  // morph folds the mesh: SolveError (morph.cpp:116-119)
+    ctl[s].status = PODECM_ESOLVE;
+    ctl[s].active = 0;
+  }
+  double* st = S + (size_t)s * 6 * Q;  // buffer 0 = committed virgin history
+  const double v[6] = {1.0, 0.0, 0.0, 1.0, 1.0, 0.0};
+  for (int t = 0; t < 6; ++t) st[(size_t)t * Q + p] = v[t];
+  (void)cap;
+  (void)nq;
+}
+
+__global__ void k_rom_init_inst(int64_t n, int N, int max_bisect, const double* sched, int K,
+                                double* a, double* a0, RomCtl* ctl, int32_t* status) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  RomCtl c;
+  memset(&c, 0, sizeof(c));
+  c.active = 1;
+  c.sp = 1;
+  c.dstack[0] = max_bisect;
+  const double I[4] = {1.0, 0.0, 0.0, 1.0};
+  for (int t = 0; t < 4; ++t) {
+    c.fstack[0][t] = I[t];
+    c.fstack[0][4 + t] = sched[((size_t)s * K + 0) * 4 + t];
+  }
+  ctl[s] = c;
+  for (int i = 0; i < N; ++i) a[(size_t)s * N + i] = a0[(size_t)s * N + i] = 0.0;
+  if (status) status[s] = 0;
+}
+
+// status of morph failures written by k_rom_init_points lands after init_inst
+__global__ void k_rom_fix_status(int64_t n, RomCtl* ctl, int32_t* status, unsigned int* fail) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  if (ctl[s].status) {
+    ctl[s].active = 0;
+    if (status) status[s] = PODECM_ESOLVE;
+    atomicAdd(fail, 1u);
+  }
+}
+
+// ---- material at the ECM points -----------------------------------------
+struct PointArgs {
+  int64_t n;
+  int N, Q, Qpad;
+  int64_t cap;
+  const double* Gt;
+  const double* a;
+  const double* morph;
+  const double* w;
+  const int32_t* reg;
+  double* S;   // [2][cap][6][Q]
+  double* At;  // [n][Qpad][20]
+  double* P;   // [n][Q][4]
+  RomCtl* ctl;
+};
+
+__global__ void __launch_bounds__(256, 2) k_rom_point(PointArgs g, MatTable tab) {
+  extern __shared__ double sm[];
+  double* sG = sm;                            // [N][4][32]
+  double* sa = sm + (size_t)g.N * 4 * kPtsTile;  // [8][N]
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int p0 = blockIdx.x * kPtsTile;
+  const int64_t s0 = (int64_t)blockIdx.y * kInstTile;
+  for (int t = threadIdx.x; t < g.N * 4 * kPtsTile; t += blockDim.x) {
+    const int ir = t / kPtsTile, pl = t - ir * kPtsTile;
+    sG[t] = (p0 + pl < g.Qpad) ? g.Gt[(size_t)ir * g.Qpad + p0 + pl] : 0.0;
+  }
+  for (int t = threadIdx.x; t < kInstTile * g.N; t += blockDim.x) {
+    const int si = t / g.N, i = t - si * g.N;
+    sa[t] = (s0 + si < g.n) ? g.a[(size_t)(s0 + si) * g.N + i] : 0.0;
+  }
+  __syncthreads();
+  const int64_t s = s0 + ty;
+  const int p = p0 + tx;
+  if (s >= g.n || p >= g.Q) return;
+  RomCtl* c = g.ctl + s;
+  if (!c->active) return;
+  // u = G_p^T a ; F = Fbar + R(fmi)^T u  (mapped^T a, rom.cpp:48-50)
+  double u[4] = {0.0, 0.0, 0.0, 0.0};
+  const double* ai = sa + ty * g.N;
+  for (int i = 0; i < g.N; ++i) {
+    const double av = ai[i];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) u[r] = fma(sG[(i * 4 + r) * kPtsTile + tx], av, u[r]);
+  }
+  const double* mo = g.morph + (size_t)s * 5 * g.Q;
+  double m[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) m[t] = mo[(size_t)t * g.Q + p];
+  const double det = mo[(size_t)4 * g.Q + p];
+  const int top = c->sp - 1;
+  double F[4];
+#pragma unroll
+  for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+    for (int l = 0; l < 2; ++l)
+      F[ii + 2 * l] = c->fstack[top][4 + ii + 2 * l] + (u[ii] * m[2 * l] + u[ii + 2] * m[1 + 2 * l]);
+
+  const MatConst& pm = tab.m[g.reg[p]];
+  const int cur = c->cur;
+  const double* s0p = g.S + ((size_t)cur * g.cap + s) * 6 * g.Q;
+  double* s1p = g.S + ((size_t)(cur ^ 1) * g.cap + s) * 6 * g.Q;
+  double fp[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) fp[t] = s0p[(size_t)t * g.Q + p];
+  Frozen z;
+  freeze(fp, s0p[(size_t)4 * g.Q + p], s0p[(size_t)5 * g.Q + p], z);
+  double P[4];
+  FullOut fo;
+  bool ok = lsu_eval<true>(pm, z, F, P, &fo);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) s1p[(size_t)t * g.Q + p] = fo.fp[t];
+  s1p[(size_t)4 * g.Q + p] = fo.fpzz;
+  s1p[(size_t)5 * g.Q + p] = fo.xi;
+  double* Pp = g.P + ((size_t)s * g.Q + p) * 4;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) Pp[t] = P[t];
+  const double cw = g.w[p] * det;  // rom.cpp:56
+  double* at = g.At + ((size_t)s * g.Qpad + p) * 20;
+  // Pt = c R P : (R P)[i + 2j] = sum_l m(j,l) P[i + 2l]
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int i = r & 1, j = r >> 1;
+    at[16 + r] = cw * (m[j] * P[i] + m[j + 2] * P[i + 2]);
+  }
+  if (ok) {
+    TangentRegs A;
+    ok = fd_tangent<false>(pm, z, F, 1e-7, A);
+    // At = c R A R^T: At[r][s] = sum_{l,l'} m(r>>1,l) A[(r&1)+2l][(s&1)+2l'] m(s>>1,l')
+#pragma unroll
+    for (int sc = 0; sc < 4; ++sc)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int ir = r & 1, jr = r >> 1, is = sc & 1, js = sc >> 1;
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < 2; ++l)
+#pragma unroll
+          for (int l2 = 0; l2 < 2; ++l2)
+            acc = fma(m[jr + 2 * l] * A.A[(ir + 2 * l) + 4 * (is + 2 * l2)], m[js + 2 * l2], acc);
+        at[r + 4 * sc] = cw * acc;
+      }
+  }
+  if (!ok) c->asm_fail = 1;  // SolveError inside rom_assemble -> attempt fails
+}
+
+// ---- K and f: DMMA contraction ---------------------------------------------
+struct ContractArgs {
+  int64_t n;
+  int N, Q, Qpad, NT, NP;
+  const double* G;   // [Qpad*4][NP]
+  const double* At;  // [n][Qpad][20]
+  double* K;         // [n][N][N]
+  double* f;         // [n][N]
+  const RomCtl* ctl;
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int NT>
+__global__ void __launch_bounds__(32 * NT * kIPC) k_rom_contract(ContractArgs g) {
+  constexpr int NP = NT * 8;
+  constexpr int KR = kPC * 4;  // k-rows per chunk
+  __shared__ double sGm[KR][NP];
+  __shared__ double sY[kIPC][KR][NP];
+  __shared__ double sAt[kIPC][kPC][20];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int si = warp / NT, trow = warp - si * NT;
+  const int64_t sbase = (int64_t)blockIdx.x * kIPC;
+  bool any = false;
+  for (int q = 0; q < kIPC; ++q)
+    if (sbase + q < g.n && g.ctl[sbase + q].active) any = true;
+  if (!any) return;
+  const int gid = lane >> 2, tig = lane & 3;
+  double acc[NT][2];
+#pragma unroll
+  for (int ct = 0; ct < NT; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
+  const int nthr = blockDim.x;
+  for (int p0 = 0; p0 < g.Qpad; p0 += kPC) {
+    // stage the shared Gm rows and the instances' per-point operators
+    const double* gsrc = g.G + (size_t)p0 * 4 * NP;
+    for (int t = threadIdx.x; t < KR * NP; t += nthr) (&sGm[0][0])[t] = gsrc[t];
+    for (int t = threadIdx.x; t < kIPC * kPC * 20; t += nthr) {
+      const int q = t / (kPC * 20), rem = t - q * kPC * 20;
+      const int64_t s = sbase + q;
+      (&sAt[0][0][0])[t] = (s < g.n) ? g.At[((size_t)s * g.Qpad + p0) * 20 + rem] : 0.0;
+    }
+    __syncthreads();
+    // Y[(p,r)][j] = sum_t At_p[r][t] Gm[(p,t)][j] (j < N); Y[.][N] = Pt; else 0
+    for (int t = threadIdx.x; t < kIPC * KR * NP; t += nthr) {
+      const int q = t / (KR * NP), rem = t - q * KR * NP;
+      const int row = rem / NP, j = rem - row * NP;
+      const int pl = row >> 2, r = row & 3;
+      const double* at = sAt[q][pl];
+      double y;
+      if (j < g.N) {
+        y = at[r] * sGm[pl * 4][j];
+        y = fma(at[r + 4], sGm[pl * 4 + 1][j], y);
+        y = fma(at[r + 8], sGm[pl * 4 + 2][j], y);
+        y = fma(at[r + 12], sGm[pl * 4 + 3][j], y);
+      } else {
+        y = (j == g.N) ? at[16 + r] : 0.0;
+      }
+      sY[q][row][j] = y;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < KR / 4; ++ks) {
+      const double afr = sGm[ks * 4 + tig][trow * 8 + gid];  // (Gm^T)[i][k]
+#pragma unroll
+      for (int ct = 0; ct < NT; ++ct) dmma(acc[ct][0], acc[ct][1], afr, sY[si][ks * 4 + tig][ct * 8 + gid]);
+    }
+    __syncthreads();
+  }
+  const int64_t s = sbase + si;
+  if (s >= g.n || !g.ctl[s].active) return;
+  const int i = trow * 8 + gid;
+  if (i >= g.N) return;
+#pragma unroll
+  for (int ct = 0; ct < NT; ++ct)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = ct * 8 + 2 * tig + h;
+      if (j < g.N)
+        g.K[((size_t)s * g.N + i) * g.N + j] = acc[ct][h];
+      else if (j == g.N)
+        g.f[(size_t)s * g.N + i] = acc[ct][h];
+    }
+}
+
+// ---- Newton / bisection state machine + LU --------------------------------
+struct NewtonArgs {
+  int64_t n;
+  int N, Q, K, max_iter, max_bisect;
+  double eps_rel, eps_abs, force_ref;
+  const double* Kg;
+  const double* f;
+  const double* P;
+  const double* morph;
+  const double* w;
+  const double* sched;
+  double* a;
+  double* a0;
+  RomCtl* ctl;
+  double* pbar;
+  int32_t* iters;
+  double* resid;
+  double* a_final;
+  int32_t* status;
+  int* nactive;
+  unsigned int* fail;
+};
+
+constexpr int kNW = 4;  // warps (instances) per Newton CTA
+
+__global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
+  extern __shared__ double smn[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int N = g.N, LD = N + 1;
+  double* Ks = smn + (size_t)warp * (N * LD + 2 * N);  // column-major, ld = N+1
+  double* rhs = Ks + N * LD;
+  int* piv = reinterpret_cast<int*>(rhs + N);
+  const int64_t s = (int64_t)blockIdx.x * kNW + warp;
+  if (s >= g.n) return;
+  RomCtl* c = g.ctl + s;
+  if (!c->active) return;
+  // residual norm
+  double ss = 0.0;
+  for (int i = lane; i < N; i += 32) {
+    const double v = g.f[(size_t)s * N + i];
+    ss = fma(v, v, ss);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const double r = sqrt(ss);
+  bool fail = c->asm_fail != 0;
+  bool conv = false;
+  int it = c->it;
+  if (!fail) {
+    if (it == 0) c->tol = fmax(g.eps_rel * fmax(r, g.force_ref), g.eps_abs);
+    if (r <= c->tol) {
+      conv = true;
+    } else if (it == g.max_iter) {
+      fail = true;
+    }
+  }
+  __syncwarp();
+  if (!fail && !conv) {
+    // K da = -f  (dense LU, partial pivoting: first row of max |a_ik|)
+    for (int t = lane; t < N * N; t += 32) {
+      const int i = t / N, j = t - i * N;  // K row-major [i][j]
+      Ks[j * LD + i] = g.Kg[(size_t)s * N * N + t];
+    }
+    for (int i = lane; i < N; i += 32) rhs[i] = -g.f[(size_t)s * N + i];
+    __syncwarp();
+    for (int k = 0; k < N; ++k) {
+      double best = -1.0;
+      int bi = N;
+      for (int i = k + lane; i < N; i += 32) {
+        const double v = fabs(Ks[k * LD + i]);
+        if (v > best) {
+          best = v;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (lane == 0) piv[k] = bi;
+      if (bi != k) {
+        for (int j = lane; j < N; j += 32) {
+          const double t0 = Ks[j * LD + k];
+          Ks[j * LD + k] = Ks[j * LD + bi];
+          Ks[j * LD + bi] = t0;
+        }
+      }
+      __syncwarp();
+      const double d = Ks[k * LD + k];
+      if (best != 0.0)
+        for (int i = k + 1 + lane; i < N; i += 32) Ks[k * LD + i] /= d;
+      __syncwarp();
+      for (int i = k + 1 + lane; i < N; i += 32) {
+        const double l = Ks[k * LD + i];
+        for (int j = k + 1; j < N; ++j) Ks[j * LD + i] -= l * Ks[j * LD + k];
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      for (int k = 0; k < N; ++k) {
+        const int pk = piv[k];
+        const double t0 = rhs[k];
+        rhs[k] = rhs[pk];
+        rhs[pk] = t0;
+      }
+      for (int k = 0; k < N; ++k)
+        for (int i = k + 1; i < N; ++i) rhs[i] -= Ks[k * LD + i] * rhs[k];
+      for (int k = N - 1; k >= 0; --k) {
+        rhs[k] /= Ks[k * LD + k];
+        for (int i = 0; i < k; ++i) rhs[i] -= Ks[k * LD + i] * rhs[k];
+      }
+    }
+    __syncwarp();
+    for (int i = lane; i < N; i += 32) g.a[(size_t)s * N + i] += rhs[i];
+    if (lane == 0) c->it = it + 1;
+  }
+  if (conv) {
+    // rom_effective_stress at the converged state (rom.cpp:68-76)
+    const bool last_sub = c->sp == 1;
+    if (last_sub && lane < 4) {
+      double pb = 0.0;
+      const double* mo = g.morph + (size_t)s * 5 * g.Q;
+      for (int p = 0; p < g.Q; ++p) pb += (g.w[p] * mo[(size_t)4 * g.Q + p]) * g.P[((size_t)s * g.Q + p) * 4 + lane];
+      g.pbar[((size_t)s * g.K + c->k) * 4 + lane] = pb / 1.0;
+    }
+    for (int i = lane; i < N; i += 32) g.a0[(size_t)s * N + i] = g.a[(size_t)s * N + i];
+    __syncwarp();
+    if (lane == 0) {
+      c->iters_acc += it;
+      c->cur ^= 1;  // commit the trial history
+      c->sp -= 1;
+      c->it = 0;
+      if (c->sp == 0) {
+        if (g.iters) g.iters[(size_t)s * g.K + c->k] = c->iters_acc;
+        if (g.resid) g.resid[(size_t)s * g.K + c->k] = r;
+        c->iters_acc = 0;
+        c->k += 1;
+        if (c->k == g.K) {
+          c->active = 0;
+        } else {
+          for (int t = 0; t < 4; ++t) {
+            c->fstack[0][t] = g.sched[((size_t)s * g.K + c->k - 1) * 4 + t];
+            c->fstack[0][4 + t] = g.sched[((size_t)s * g.K + c->k) * 4 + t];
+          }
+          c->dstack[0] = g.max_bisect;
+          c->sp = 1;
+        }
+      }
+    }
+    __syncwarp();
+    if (!c->active && g.a_final)
+      for (int i = lane; i < N; i += 32) g.a_final[(size_t)s * N + i] = g.a[(size_t)s * N + i];
+  }
+  if (fail) {
+    for (int i = lane; i < N; i += 32) g.a[(size_t)s * N + i] = g.a0[(size_t)s * N + i];
+    __syncwarp();
+    if (lane == 0) {
+      c->asm_fail = 0;
+      c->it = 0;
+      const int top = c->sp - 1;
+      if (c->dstack[top] <= 0 || c->sp + 1 > kMaxStack) {
+        c->active = 0;  // rom.cpp:159: rethrow -> SolveError for this instance
+        c->status = PODECM_ESOLVE;
+        if (g.status) g.status[s] = PODECM_ESOLVE;
+        atomicAdd(g.fail, 1u);
+      } else {
+        double fp[4], ft[4], mid[4];
+        for (int t = 0; t < 4; ++t) {
+          fp[t] = c->fstack[top][t];
+          ft[t] = c->fstack[top][4 + t];
+          mid[t] = 0.5 * (fp[t] + ft[t]);
+        }
+        const int d = c->dstack[top] - 1;
+        for (int t = 0; t < 4; ++t) {  // second half below, first half on top
+          c->fstack[top][t] = mid[t];
+          c->fstack[top][4 + t] = ft[t];
+          c->fstack[top + 1][t] = fp[t];
+          c->fstack[top + 1][4 + t] = mid[t];
+        }
+        c->dstack[top] = d;
+        c->dstack[top + 1] = d;
+        c->sp += 1;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0 && c->active) atomicAdd(g.nactive, 1);
+}
+
+template <class T>
+int dalloc(podecm_ctx* ctx, T** p, size_t count) {
+  PODECM_CUDA_TRY(ctx, cudaMalloc(p, std::max<size_t>(1, count) * sizeof(T)));
+  return PODECM_OK;
+}
+
+int ensure_cap(podecm_rom* r, int64_t n) {
+  if (r->cap >= n) return PODECM_OK;
+  free_work(r);
+  podecm_ctx* ctx = r->ctx;
+  const size_t Q = r->Q, N = r->N;
+  int rc = PODECM_OK;
+  if (!rc) rc = dalloc(ctx, &r->d_morph, (size_t)n * 5 * Q);
+  if (!rc) rc = dalloc(ctx, &r->d_S, (size_t)2 * n * 6 * Q);
+  if (!rc) rc = dalloc(ctx, &r->d_At, (size_t)n * r->Qpad * 20);
+  if (!rc) rc = dalloc(ctx, &r->d_P, (size_t)n * Q * 4);
+  if (!rc) rc = dalloc(ctx, &r->d_K, (size_t)n * N * N);
+  if (!rc) rc = dalloc(ctx, &r->d_f, (size_t)n * N);
+  if (!rc) rc = dalloc(ctx, &r->d_a, (size_t)n * N);
+  if (!rc) rc = dalloc(ctx, &r->d_a0, (size_t)n * N);
+  if (!rc) rc = dalloc(ctx, &r->d_ctl, (size_t)n);
+  if (rc) {
+    free_work(r);
+    return rc;
+  }
+  // padding rows of At (p >= Q) stay zero forever
+  PODECM_CUDA_TRY(ctx, cudaMemset(r->d_At, 0, (size_t)n * r->Qpad * 20 * sizeof(double)));
+  r->cap = n;
+  return PODECM_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
 int podecm_rom_create(podecm_ctx* ctx, podecm_rve* rve, int N, int Q, const int32_t* ids,
                       const double* weights, const double* mode_grads, podecm_rom** out) {
-  (void)rve; (void)N; (void)Q; (void)ids; (void)weights; (void)mode_grads; (void)out;
-  return set_err(ctx, PODECM_ECONFIG, "podecm_rom_create: not built yet");
+  if (!ctx || !rve || !out) return PODECM_ECONFIG;
+  *out = nullptr;
+  if (N < 1 || N > 55) return set_err(ctx, PODECM_ECONFIG, "rom: need 1 <= N <= 55 modes");
+  if (Q < 1) return set_err(ctx, PODECM_ECONFIG, "rom: empty cubature rule");
+  if (!ids || !weights || !mode_grads) return set_err(ctx, PODECM_ECONFIG, "rom: null model arrays");
+  for (int p = 0; p < Q; ++p) {
+    if (ids[p] < 0 || ids[p] >= rve->n_qp)
+      return set_err(ctx, PODECM_ECONFIG, "rom: ECM id out of range");
+    if (p > 0 && ids[p] <= ids[p - 1])
+      return set_err(ctx, PODECM_ECONFIG, "rom: ECM ids must be strictly ascending");
+  }
+  auto* r = new podecm_rom;
+  r->rve = rve;
+  r->ctx = ctx;
+  r->N = N;
+  r->Q = Q;
+  r->Qpad = (Q + kPC - 1) / kPC * kPC;
+  r->NT = (N + 1 + 7) / 8;  // + 1: f rides in column N
+  r->NP = r->NT * 8;
+  std::vector<double> G((size_t)r->Qpad * 4 * r->NP, 0.0), Gt((size_t)N * 4 * r->Qpad, 0.0);
+  std::vector<int32_t> reg(Q);
+  for (int p = 0; p < Q; ++p) {
+    reg[p] = rve->regions[ids[p] >> 2];
+    for (int i = 0; i < N; ++i)
+      for (int c = 0; c < 4; ++c) {
+        const double v = mode_grads[((size_t)p * N + i) * 4 + c];
+        G[((size_t)p * 4 + c) * r->NP + i] = v;
+        Gt[((size_t)i * 4 + c) * r->Qpad + p] = v;
+      }
+  }
+  std::vector<int32_t> hid(ids, ids + Q);
+  std::vector<double> hw(weights, weights + Q);
+  int rc = PODECM_OK;
+  auto up = [&](auto** d, const auto& h) {
+    if (rc) return;
+    using T = std::remove_reference_t<decltype(h[0])>;
+    if (cudaMalloc(d, h.size() * sizeof(T)) != cudaSuccess ||
+        cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess)
+      rc = set_err(ctx, PODECM_ECUDA, "rom: device upload failed");
+  };
+  up(&r->d_ids, hid);
+  up(&r->d_reg, reg);
+  up(&r->d_w, hw);
+  up(&r->d_G, G);
+  up(&r->d_Gt, Gt);
+  if (!rc && cudaMalloc(&r->d_nactive, sizeof(int)) != cudaSuccess) rc = PODECM_ECUDA;
+  if (!rc && cudaMallocHost(&r->h_nactive, sizeof(int)) != cudaSuccess) rc = PODECM_ECUDA;
+  if (rc) {
+    podecm_rom_destroy(r);
+    return rc;
+  }
+  *out = r;
+  return PODECM_OK;
 }
 
-void podecm_rom_destroy(podecm_rom* rom) { delete rom; }
+void podecm_rom_destroy(podecm_rom* r) {
+  if (!r) return;
+  free_work(r);
+  cudaFree(r->d_ids);
+  cudaFree(r->d_reg);
+  cudaFree(r->d_w);
+  cudaFree(r->d_G);
+  cudaFree(r->d_Gt);
+  cudaFree(r->d_nactive);
+  if (r->h_nactive) cudaFreeHost(r->h_nactive);
+  delete r;
+}
 
-int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* rom, int64_t n_inst,
+int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
                            const double* geom, const double* sched, int K,
                            const podecm_newton* opts, double* pbar, int32_t* iters, double* resid,
                            double* a_final, int32_t* status) {
-  (void)stream; (void)rom; (void)n_inst; (void)geom; (void)sched; (void)K; (void)opts;
-  (void)pbar; (void)iters; (void)resid; (void)a_final; (void)status;
-  return set_err(ctx, PODECM_ECONFIG, "podecm_rom_solve_batch: not built yet");
+  if (!ctx || !r || !opts) return PODECM_ECONFIG;
+  if (n_inst < 0 || K < 0) return set_err(ctx, PODECM_ECONFIG, "negative batch or schedule size");
+  if (n_inst == 0 || K == 0) return PODECM_OK;
+  if (!geom || !sched || !pbar) return set_err(ctx, PODECM_ECONFIG, "geom, sched, pbar required");
+  if (opts->max_bisect < 0 || opts->max_bisect + 1 > kMaxStack)
+    return set_err(ctx, PODECM_ECONFIG, "max_bisect must lie in [0, 7]");
+  if (opts->max_iter < 0) return set_err(ctx, PODECM_ECONFIG, "max_iter must be >= 0");
+  if (r->NT > 7) return set_err(ctx, PODECM_ECONFIG, "rom: N > 55 exceeds the contraction tile");
+  if (int rc = ensure_cap(r, n_inst)) return rc;
+  auto s = static_cast<cudaStream_t>(stream);
+  podecm_rve* rv = r->rve;
+  const int Q = r->Q, N = r->N;
+  k_rom_init_inst<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, N, opts->max_bisect, sched, K,
+                                                        r->d_a, r->d_a0, r->d_ctl, status);
+  k_rom_init_points<<<grid_for(n_inst * Q, 128), 128, 0, s>>>(
+      n_inst, Q, rv->n_qp, rv->r0, r->d_ids, rv->d_nodes, rv->d_elems, rv->d_grad, geom,
+      r->d_morph, r->d_S, r->cap, r->d_ctl);
+  k_rom_fix_status<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, r->d_ctl, status, ctx->d_fail);
+  PODECM_LAUNCHED(ctx, 3);
+
+  PointArgs pa;
+  pa.n = n_inst;
+  pa.N = N;
+  pa.Q = Q;
+  pa.Qpad = r->Qpad;
+  pa.cap = r->cap;
+  pa.Gt = r->d_Gt;
+  pa.a = r->d_a;
+  pa.morph = r->d_morph;
+  pa.w = r->d_w;
+  pa.reg = r->d_reg;
+  pa.S = r->d_S;
+  pa.At = r->d_At;
+  pa.P = r->d_P;
+  pa.ctl = r->d_ctl;
+  const size_t smem_pt = ((size_t)N * 4 * kPtsTile + (size_t)kInstTile * N) * sizeof(double);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_rom_point, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_rom_newton, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_set = true;
+  }
+  const dim3 gpt((Q + kPtsTile - 1) / kPtsTile, (unsigned)((n_inst + kInstTile - 1) / kInstTile));
+
+  ContractArgs ca;
+  ca.n = n_inst;
+  ca.N = N;
+  ca.Q = Q;
+  ca.Qpad = r->Qpad;
+  ca.NT = r->NT;
+  ca.NP = r->NP;
+  ca.G = r->d_G;
+  ca.At = r->d_At;
+  ca.K = r->d_K;
+  ca.f = r->d_f;
+  ca.ctl = r->d_ctl;
+  const int gct = (int)((n_inst + kIPC - 1) / kIPC);
+
+  NewtonArgs na;
+  na.n = n_inst;
+  na.N = N;
+  na.Q = Q;
+  na.K = K;
+  na.max_iter = opts->max_iter;
+  na.max_bisect = opts->max_bisect;
+  na.eps_rel = opts->eps_rel;
+  na.eps_abs = opts->eps_abs;
+  na.force_ref = opts->force_ref;
+  na.Kg = r->d_K;
+  na.f = r->d_f;
+  na.P = r->d_P;
+  na.morph = r->d_morph;
+  na.w = r->d_w;
+  na.sched = sched;
+  na.a = r->d_a;
+  na.a0 = r->d_a0;
+  na.ctl = r->d_ctl;
+  na.pbar = pbar;
+  na.iters = iters;
+  na.resid = resid;
+  na.a_final = a_final;
+  na.status = status;
+  na.nactive = r->d_nactive;
+  na.fail = ctx->d_fail;
+  const size_t smem_nt = (size_t)kNW * ((size_t)N * (N + 1) + 2 * N) * sizeof(double);
+  const int gnt = (int)((n_inst + kNW - 1) / kNW);
+
+  const int64_t max_global = (int64_t)K * (opts->max_iter + 1) * (2ll << opts->max_bisect) + 8;
+  for (int64_t it = 0; it < max_global; ++it) {
+    k_rom_point<<<gpt, 256, smem_pt, s>>>(pa, rv->mats);
+    switch (r->NT) {
+      case 1: k_rom_contract<1><<<gct, 32 * 1 * kIPC, 0, s>>>(ca); break;
+      case 2: k_rom_contract<2><<<gct, 32 * 2 * kIPC, 0, s>>>(ca); break;
+      case 3: k_rom_contract<3><<<gct, 32 * 3 * kIPC, 0, s>>>(ca); break;
+      case 4: k_rom_contract<4><<<gct, 32 * 4 * kIPC, 0, s>>>(ca); break;
+      case 5: k_rom_contract<5><<<gct, 32 * 5 * kIPC, 0, s>>>(ca); break;
+      case 6: k_rom_contract<6><<<gct, 32 * 6 * kIPC, 0, s>>>(ca); break;
+      default: k_rom_contract<7><<<gct, 32 * 7 * kIPC, 0, s>>>(ca); break;
+    }
+    PODECM_CUDA_TRY(ctx, cudaMemsetAsync(r->d_nactive, 0, sizeof(int), s));
+    k_rom_newton<<<gnt, 32 * kNW, smem_nt, s>>>(na);
+    PODECM_LAUNCHED(ctx, 3);
+    if ((it & 3) == 3) {
+      PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(r->h_nactive, r->d_nactive, sizeof(int),
+                                           cudaMemcpyDeviceToHost, s));
+      PODECM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+      if (*r->h_nactive == 0) break;
+    }
+  }
+  // failed instances -> context flag (podecm_check reports SolveError)
+  return PODECM_OK;
 }
 
 }  // extern "C"

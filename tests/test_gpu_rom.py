@@ -1,0 +1,81 @@
+"""K3 parity: batched hyper-reduced online stage (config 3) vs the CPU oracle
+(rom.cpp:16-200 restated).  Homogenised stress histories within 1e-8
+relative per increment; Newton iteration counts per increment equal; the
+bisection state machine is exercised by forcing failures (tight max_iter).
+"""
+import numpy as np
+import pytest
+
+from paper_2307_16894_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _mats():
+    from paper_2307_16894_b200.api import inclusion_params, matrix_params
+    return [matrix_params(), inclusion_params()]
+
+
+@pytest.fixture(scope="module")
+def setup(orc):
+    from paper_2307_16894_b200 import api
+    g = api.Rve(128, _mats())
+    o = orc.Rve(128, _mats())
+    model = synth.rom_model(g.export(), g.n_red, N=50, Q=400, seed=2029)
+    rom = api.Rom(g, model["ids"], model["weights"], model["mode_grads"])
+    return g, o, model, rom
+
+
+def _solve(setup, n, K, seed, hm, opts_kw):
+    import torch
+    from paper_2307_16894_b200 import api
+    g, o, model, rom = setup
+    geom, sched = synth.rom_instances(n, K, seed, hm)
+    T = lambda a: torch.from_numpy(a).cuda()
+    opts = api.NewtonOpts(**opts_kw)
+    rg = rom.solve(T(geom), T(sched), opts)
+    torch.cuda.synchronize()
+    rg = {k: v.cpu().numpy() for k, v in rg.items()}
+    ro = o.rom_solve(model["ids"], model["weights"], model["mode_grads"], geom, sched,
+                     eps_rel=opts.eps_rel, eps_abs=opts.eps_abs, max_iter=opts.max_iter,
+                     max_bisect=opts.max_bisect)
+    return rg, ro
+
+
+def _check(rg, ro, tol=1e-8, iters_exact=True):
+    assert np.array_equal(rg["status"], ro["status"]), (rg["status"], ro["status"])
+    ok = ro["status"] == 0
+    d = np.linalg.norm(rg["pbar"][ok] - ro["pbar"][ok], axis=-1)
+    nrm = np.maximum(np.linalg.norm(ro["pbar"][ok], axis=-1), 1e-14)
+    rel = d / nrm
+    mism = int((rg["iters"][ok] != ro["iters"][ok]).sum())
+    print(f"pbar max rel {rel.max():.3e}; iteration-count mismatches {mism}/{rg['iters'][ok].size}; "
+          f"mean iters/increment {ro['iters'][ok].mean():.2f}")
+    assert rel.max() <= tol
+    if iters_exact:
+        assert mism == 0
+
+
+def test_config3_instances(setup):
+    rg, ro = _solve(setup, 6, 20, 2030, 0.2, dict(eps_rel=1e-10, eps_abs=1e-12, max_iter=25))
+    assert np.all(ro["status"] == 0)
+    _check(rg, ro)
+
+
+def test_bisection_path(setup):
+    """One big increment with max_iter = 3 forces failed attempts -> recursive
+    bisection (rom.cpp:152-175) to depths 1-3; histories and the summed
+    iteration counts must match."""
+    rg, ro = _solve(setup, 6, 1, 77, 0.2, dict(eps_rel=1e-10, eps_abs=1e-12, max_iter=3,
+                                               max_bisect=5))
+    assert ro["iters"].max() > 3  # bisection happened
+    _check(rg, ro)
+
+
+def test_bisection_exhausted_is_solveerror(setup):
+    """max_iter = 0 with max_bisect = 1 cannot converge: every instance fails
+    with SolveError like the reference's rethrow."""
+    rg, ro = _solve(setup, 3, 2, 5, 0.2, dict(eps_rel=1e-10, eps_abs=1e-12, max_iter=0,
+                                              max_bisect=1))
+    assert np.all(ro["status"] == 3)
+    assert np.array_equal(rg["status"], ro["status"])
