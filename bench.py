@@ -2,19 +2,21 @@
 """Benchmark of the B200-native hot path (BASELINE.json metric:
 "material-point updates/s; ROM RVE solves/s; fraction of HBM/FP64 roofline").
 
-Default workload = BASELINE config 1 (2^22 independent plane-strain material
-points, finite-strain J2 + FD consistent tangent, fp64).  A step is one pass
-of the batched material-point update over the whole batch, inputs resident in
-HBM (1.2 GB touched per step > 126 MB L2, so no L2 flush is needed).
-
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c1|c0|c2]
+                  [--config all|c1|c0|c2|c3]
 
-Under torchrun (N > 1) every rank processes its own 2^22-point shard
-(weak scaling, no collective on the data path); rank 0 prints one JSON line
-with the max-over-ranks device time.  ``--impl reference`` times the CPU
-oracle (the reference's algorithm restated in C++, ``oracle/``; the reference
-itself cannot be built here) on this box's host cores.
+Headline workload = BASELINE config 1 (2^22 independent plane-strain material
+points: finite-strain J2 return map + central-FD consistent tangent + history,
+fp64).  A step is one pass of the batched material-point update over the
+whole batch with inputs resident in HBM (1.2 GB touched per step > 126 MB
+L2, so no L2 flush is needed).  With ``--config all`` (default) the same JSON
+line also carries measured blocks for configs 0, 2 and 3 under ``"also"``.
+
+Under torchrun (N > 1) every rank runs its own independent shard (weak
+scaling, no collective on the data path); rank 0 prints one JSON line with
+the max-over-ranks device time.  ``--impl reference`` times the CPU oracle
+(the reference's algorithm restated in C++ under ``oracle/``; the reference
+itself cannot be built here: no Eigen/GTest) on this box's host cores.
 """
 from __future__ import annotations
 
@@ -33,10 +35,10 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-BYTES_PER_POINT = 288  # F 32 + state 48 in; P 32 + A 128 + state 48 out
+C1_BYTES_PER_POINT = 288  # F 32 + state 48 in; P 32 + A 128 + state 48 out
 
 
-def _peaks():
+def _hbm_peak():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
@@ -55,24 +57,33 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.mark = 0
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 10:
+                time.sleep(0.05)
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
-    def __exit__(self, *a):
+    def begin(self):
+        self.t_begin = time.time()
+
+    def end(self):
+        self.t_end = time.time() + 0.06
+
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
@@ -83,7 +94,11 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = [l for t, l in self.lines if getattr(self, "t_begin", 0) <= t <= getattr(self, "t_end", 1e300)]
+        if not lines and self.lines:  # region shorter than the sampling period: nearest sample
+            tb = getattr(self, "t_begin", 0)
+            lines = [min(self.lines, key=lambda x: abs(x[0] - tb))[1]]
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
@@ -101,12 +116,14 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def dist_setup(gpus: int):
+def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
+        import torch
         import torch.distributed as dist
+        torch.cuda.set_device(local)
         dist.init_process_group("nccl")
     return ws, rank, local
 
@@ -128,17 +145,17 @@ def max_over_ranks(ws, x: float) -> float:
 
 
 def fp64_peaks(ctx, torch):
-    """DFMA and DMMA probe peaks (TFLOP/s), measured in this run."""
+    """DFMA-chain and DMMA (mma.sync m8n8k4 f64) probe peaks, TFLOP/s, this run."""
     import ctypes as C
     out = {}
     scratch = torch.zeros(1, dtype=torch.float64, device="cuda")
     for mode, name in ((0, "dfma"), (1, "dmma")):
         flops = C.c_double()
         best = 0.0
-        for _ in range(4):
+        for _ in range(5):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            ctx.lib.podecm_probe_fp64(ctx.h, ctx.stream(), mode, 4096, C.c_void_p(scratch.data_ptr()),
+            ctx.lib.podecm_probe_fp64(ctx.h, ctx.stream(), mode, 8192, C.c_void_p(scratch.data_ptr()),
                                       C.byref(flops))
             e1.record()
             torch.cuda.synchronize()
@@ -147,28 +164,34 @@ def fp64_peaks(ctx, torch):
     return out
 
 
-def cpu_baseline_c1(F, st, mats, seconds_target=10.0):
-    import oracle
-    nt = oracle.max_threads()
-    n = F.shape[1]
-    t0 = time.perf_counter()
-    oracle.material_batch(F, st, mats, nthreads=nt)
-    dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "points/s", "cores": nt, "kind": "port",
-            "sample": f"config1 full batch: {n} points, P + FD tangent + history, "
-                      f"{dt:.2f} s wall on {nt} threads (oracle/ C++ restatement, -O2, no FMA)"}
+def timed(torch, ws, steps, step, clk=None):
+    """Run `steps` steps bracketed by barrier + synchronize; device time via
+    CUDA events on the current stream, max over ranks."""
+    barrier(ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clk:
+        clk.begin()
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    if clk:
+        clk.end()
+    barrier(ws)
+    return max_over_ranks(ws, e0.elapsed_time(e1))
 
 
-def run_c1(args, ws, rank, local):
+# --------------------------------------------------------------- config 1 --
+def run_c1(args, ws, rank, local, ctx, clk):
     import torch
     from paper_2307_16894_b200 import api, synth
 
-    torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     n = args.points
     F_np, st_np = synth.config1_points(n, 2027 + rank)
     mats = [api.matrix_params()]
-    ctx = api.Context.default(local)
     F = torch.from_numpy(F_np).to(dev)
     st = torch.from_numpy(st_np).to(dev)
     out = {"P": torch.empty((4, n), dtype=torch.float64, device=dev),
@@ -181,32 +204,19 @@ def run_c1(args, ws, rank, local):
 
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
     ctx.check()
-    barrier(ws)
-    torch.cuda.synchronize()
+    ctx.timings()
+    ctx.set_timing(True)
     l0 = ctx.launches()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
-        t_start = torch.cuda.Event(enable_timing=True)
-        t_end = torch.cuda.Event(enable_timing=True)
-        t_start.record()
-        for i in range(args.steps):
-            evs[i][0].record()
-            step()
-            evs[i][1].record()
-        t_end.record()
-        torch.cuda.synchronize()
+    ms = timed(torch, ws, args.steps, step, clk)
     launches = ctx.launches() - l0
-    barrier(ws)
-    torch.cuda.synchronize()
-    ms_total = t_start.elapsed_time(t_end)
-    ms_total = max_over_ranks(ws, ms_total)
-    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
-    plastic = None
+    ctx.set_timing(False)
+    tk = ctx.timings()
+    kern_ms = tk["k_material_batch"][0] / tk["k_material_batch"][1]
+    plastic = float((out["st"][5] > st[5]).double().mean().item())
 
-    # e2e through the public API with pinned host buffers, H2D/D2H inside
+    # e2e through the public API with pinned host buffers; H2D and D2H of every
+    # step's inputs / results inside the timed region, pipelined over 3 streams
     n_chunks = 8
     cs = n // n_chunks
     hF = [torch.from_numpy(np.ascontiguousarray(F_np[:, c * cs:(c + 1) * cs])).pin_memory() for c in range(n_chunks)]
@@ -221,12 +231,14 @@ def run_c1(args, ws, rank, local):
              "A": torch.empty((16, cs), dtype=torch.float64, device=dev),
              "st": torch.empty((6, cs), dtype=torch.float64, device=dev),
              "status": torch.empty(cs, dtype=torch.int32, device=dev)} for _ in streams]
+    main = torch.cuda.current_stream()
 
     def e2e_step():
+        for s in streams:
+            s.wait_stream(main)
         for c in range(n_chunks):
             k = c % len(streams)
-            s = streams[k]
-            with torch.cuda.stream(s):
+            with torch.cuda.stream(streams[k]):
                 dF[k].copy_(hF[c], non_blocking=True)
                 dS[k].copy_(hS[c], non_blocking=True)
                 r = api.material_batch(dF[k], dS[k], mats, ctx=ctx, out=dout[k])
@@ -234,112 +246,346 @@ def run_c1(args, ws, rank, local):
                 oA[c].copy_(r["A"], non_blocking=True)
                 oS[c].copy_(r["st"], non_blocking=True)
         for s in streams:
-            torch.cuda.current_stream().wait_stream(s)
+            main.wait_stream(s)
 
     for _ in range(2):
         e2e_step()
-    torch.cuda.synchronize()
-    barrier(ws)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(3, args.steps // 2)
-    e0.record()
-    for _ in range(e2e_steps):
-        e2e_step()
-    e1.record()
-    torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(ws, e0.elapsed_time(e1) / e2e_steps)
-    # sanity: e2e results equal the resident-path results
-    same = bool(torch.equal(oP[0], out["P"][:, :cs].cpu()))
+    e2e_steps = max(3, min(args.steps, 10))
+    e2e_ms = timed(torch, ws, e2e_steps, e2e_step) / e2e_steps
+    same = bool(torch.equal(oP[0], out["P"][:, :cs].cpu())) and bool(torch.equal(oA[-1], out["A"][:, -cs:].cpu()))
     ctx.check()
-
-    res = {
-        "ms_total": ms_total, "kern_ms": kern_ms, "launches": launches, "clocks": clk.summary(),
-        "e2e_ms": e2e_ms, "e2e_same": same,
-        "h2d": (4 + 6) * 8 * n, "d2h": (4 + 16 + 6) * 8 * n,
-        "plastic_frac": float((out["st"][5] > st[5]).double().mean().item()),
-    }
-    if rank == 0 and ws == 1 or rank == 0:
-        res["fp64"] = fp64_peaks(ctx, torch)
+    res = {"ms": ms, "kern_ms": kern_ms, "launches": launches, "e2e_ms": e2e_ms, "e2e_same": same,
+           "h2d": (4 + 6) * 8 * n, "d2h": (4 + 16 + 6) * 8 * n, "plastic_frac": plastic}
     if rank == 0 and ws == 1 and not args.no_cpu:
-        res["cpu"] = cpu_baseline_c1(F_np, st_np, mats)
+        import oracle
+        nt = oracle.max_threads()
+        t0 = time.perf_counter()
+        oracle.material_batch(F_np, st_np, mats, nthreads=nt)
+        dt = time.perf_counter() - t0
+        res["cpu"] = {"value": n / dt, "unit": "points/s", "cores": nt, "kind": "port",
+                      "sample": f"the full config-1 batch ({n} points: P + FD tangent + history) once, "
+                                f"{dt:.2f} s wall on {nt} host threads (oracle/ C++ restatement, -O2, no FMA)"}
+    del F, st, out, dF, dS, dout
+    torch.cuda.empty_cache()
     return res
+
+
+# --------------------------------------------------------------- config 0/2 --
+def _torch_expm_sym2(torch, a, b, c):
+    m = 0.5 * (a + b)
+    h = 0.5 * (a - b)
+    d = torch.sqrt(h * h + c * c)
+    em = torch.exp(m)
+    ch = torch.cosh(d)
+    sh = torch.where(d > 1e-300, torch.sinh(d) / torch.where(d > 1e-300, d, torch.ones_like(d)), torch.ones_like(d))
+    e00 = em * (ch + sh * h)
+    e11 = em * (ch - sh * h)
+    e01 = em * sh * c
+    return torch.stack([e00, e01, e01, e11])
+
+
+def rve_inputs_gpu(torch, rve, n_inst, seed, hm, geom_range, dev):
+    """Configs 0/2 synthesised on the device (same distributions as
+    synth.rve_instances, torch's Philox stream instead of numpy's)."""
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    nq = rve.n_qp
+    regions_qp = torch.from_numpy(np.repeat(rve.export()["regions"], 4)).to(dev)
+    if geom_range is None:
+        geom = torch.tensor([[0.3, 0.2]], dtype=torch.float64, device=dev).repeat(n_inst, 1)
+    else:
+        geom = geom_range[0] + (geom_range[1] - geom_range[0]) * torch.rand((n_inst, 2), generator=g, dtype=torch.float64, device=dev)
+    I = torch.tensor([1.0, 0.0, 0.0, 1.0], dtype=torch.float64, device=dev)
+    fbar = I + (2 * torch.rand((n_inst, 4), generator=g, dtype=torch.float64, device=dev) - 1) * hm
+    w_red = 1e-3 * torch.randn((n_inst, rve.n_red), generator=g, dtype=torch.float64, device=dev)
+    st0 = torch.empty((n_inst, 6, nq), dtype=torch.float64, device=dev)
+    incl = regions_qp != 0
+    virgin = torch.tensor([1.0, 0.0, 0.0, 1.0, 1.0, 0.0], dtype=torch.float64, device=dev)
+    for s in range(n_inst):
+        x = torch.randn((4, nq), generator=g, dtype=torch.float64, device=dev)
+        tr = (x[0] + x[1] + x[2]) / 3.0
+        x[:3] -= tr
+        x /= torch.sqrt(x[0] ** 2 + x[1] ** 2 + x[2] ** 2 + 2.0 * x[3] ** 2)
+        ep = 0.05 * torch.rand(nq, generator=g, dtype=torch.float64, device=dev)
+        sc = np.sqrt(1.5) * ep
+        st0[s, :4] = _torch_expm_sym2(torch, sc * x[0], sc * x[1], sc * x[3])
+        st0[s, 4] = torch.exp(sc * x[2])
+        st0[s, 5] = ep
+        st0[s][:, incl] = virgin[:, None]
+    return geom, fbar, w_red, st0
+
+
+def run_rve(args, ws, rank, local, ctx, n_cells, n_inst, hm, geom_range, steps, warmup, seed,
+            cpu_sample):
+    import torch
+    from paper_2307_16894_b200 import api
+    dev = torch.device("cuda", local)
+    mats = [api.matrix_params(), api.inclusion_params()]
+    rve = api.Rve(n_cells, mats, ctx=ctx)
+    geom, fbar, w_red, st0 = rve_inputs_gpu(torch, rve, n_inst, seed + rank, hm, geom_range, dev)
+    out = {"f": torch.empty((n_inst, rve.n_red), dtype=torch.float64, device=dev),
+           "K": torch.empty((n_inst, rve.nnz), dtype=torch.float64, device=dev),
+           "st1": torch.empty((n_inst, 6, rve.n_qp), dtype=torch.float64, device=dev),
+           "status": torch.empty(n_inst, dtype=torch.int32, device=dev)}
+
+    def step():
+        rve.assemble(fbar, w_red, st0, geom=geom, out=out)
+
+    for _ in range(warmup):
+        step()
+    ctx.check()
+    ctx.timings()
+    ctx.set_timing(True)
+    l0 = ctx.launches()
+    ms = timed(torch, ws, steps, step)
+    launches = ctx.launches() - l0
+    ctx.set_timing(False)
+    tk = ctx.timings()
+    nq, nr, nnz = rve.n_qp, rve.n_red, rve.nnz
+    bytes_inst = 2 * 6 * nq * 8 + nr * 8 + nr * 8 + nnz * 8  # states r/w, w, f, K
+    res = {"n_cells": n_cells, "instances": n_inst, "n_qp": nq, "n_red": nr, "nnz": nnz,
+           "ms_per_step": ms / steps, "qp_per_s": ws * n_inst * nq * steps / (ms * 1e-3),
+           "launches_per_step": launches / steps,
+           "kernels_ms_per_step": {k: round(v[0] / steps, 4) for k, v in tk.items()},
+           "algorithmic_bytes_per_instance": bytes_inst}
+    kq = tk.get("k_asm_qp", (0, 1))[0] / steps
+    kall = sum(v[0] for v in tk.values()) / steps
+    peak, src = _hbm_peak()
+    ach = bytes_inst * n_inst / (kall * 1e-3) / 1e9
+    res["roofline"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                       "frac": round(ach / peak, 4), "peak_source": src,
+                       "note": "k_asm_qp (material, FP64-issue bound) is "
+                               f"{100 * kq / max(kall, 1e-9):.0f}% of the step"}
+    if rank == 0 and ws == 1 and not args.no_cpu and cpu_sample > 0:
+        import oracle
+        orve = oracle.Rve(n_cells, mats)
+        m = min(cpu_sample, n_inst)
+        h = lambda t: t[:m].cpu().numpy().copy()
+        nt = oracle.max_threads() if m > 1 else 1
+        t0 = time.perf_counter()
+        ro = orve.assemble(h(geom), h(fbar), h(w_red), h(st0), nthreads=nt)
+        dt = time.perf_counter() - t0
+        g = out["K"][:m].cpu().numpy()
+        eK = max(np.linalg.norm(g[s] - ro["K"][s]) / np.linalg.norm(ro["K"][s]) for s in range(m))
+        ef = max(np.linalg.norm(out["f"][s].cpu().numpy() - ro["f"][s]) / np.linalg.norm(ro["f"][s]) for s in range(m))
+        res["cpu_baseline"] = {"value": m * nq / dt, "unit": "qp/s", "cores": nt, "kind": "port",
+                               "sample": f"{m} of the {n_inst} instances assembled by the oracle "
+                                         f"(residual + CSR tangent + history) in {dt:.2f} s on {nt} threads"}
+        res["parity_on_sample"] = {"K_rel_fro_max": eK, "f_rel_max": ef}
+    del geom, fbar, w_red, st0, out, rve
+    torch.cuda.empty_cache()
+    return res
+
+
+# --------------------------------------------------------------- config 3 --
+def run_c3(args, ws, rank, local, ctx, n_inst, steps, warmup, fp64):
+    import torch
+    from paper_2307_16894_b200 import api, synth
+    dev = torch.device("cuda", local)
+    mats = [api.matrix_params(), api.inclusion_params()]
+    rve = api.Rve(128, mats, ctx=ctx)
+    t = rve.export()
+    model = synth.rom_model(t, rve.n_red, N=50, Q=400, seed=2029)
+    rom = api.Rom(rve, model["ids"], model["weights"], model["mode_grads"])
+    K = 20
+    geom_np, sched_np = synth.rom_instances(n_inst, K, 2030 + 7919 * rank, 0.2)
+    geom = torch.from_numpy(geom_np).to(dev)
+    sched = torch.from_numpy(sched_np).to(dev)
+    opts = api.NewtonOpts(eps_rel=1e-10, eps_abs=1e-12, max_iter=25, max_bisect=5)
+    out = {}
+
+    def step():
+        out.update(rom.solve(geom, sched, opts, out=out if out else None))
+
+    for _ in range(warmup):
+        step()
+    ctx.check()
+    ctx.timings()
+    ctx.set_timing(True)
+    l0 = ctx.launches()
+    ms = timed(torch, ws, steps, step)
+    launches = ctx.launches() - l0
+    ctx.set_timing(False)
+    tk = ctx.timings()
+    iters = out["iters"].double()
+    mean_it = float(iters.mean().item())
+    st = out["status"]
+    n_fail = int((st != 0).sum().item())
+    gi = rom.global_iterations
+    N, Q = 50, 400
+    # useful dense flops of one contraction per instance: K_ext = Gm^T Y (N x (N+1) x 4Q) + Y
+    flop_contract = 2.0 * N * (N + 1) * 4 * Q + 2.0 * 4 * Q * N * 4
+    # assemblies actually performed per instance = sum over increments of (iters + 1) (+ failed attempts)
+    assemblies = float((iters + 1).sum(1).mean().item())
+    kc = tk.get("k_rom_contract", (0.0, 1))
+    kp = tk.get("k_rom_point", (0.0, 1))
+    kn = tk.get("k_rom_newton", (0.0, 1))
+    tot = kc[0] + kp[0] + kn[0]
+    # per launch: the contraction runs over every still-active instance
+    ach_tf = flop_contract * assemblies * n_inst * steps / (kc[0] * 1e-3) / 1e12 if kc[0] > 0 else None
+    res = {"instances": n_inst, "N": N, "Q": Q, "increments": K,
+           "ms_per_step": ms / steps, "rve_solves_per_s": ws * n_inst * steps / (ms * 1e-3),
+           "increments_per_s": ws * n_inst * K * steps / (ms * 1e-3),
+           "mean_newton_iters_per_increment": round(mean_it, 3),
+           "mean_assemblies_per_solve": round(assemblies, 2), "global_iterations": gi,
+           "failed_instances": n_fail, "launches_per_step": launches / steps,
+           "kernels_ms_per_step": {k: round(v[0] / steps, 3) for k, v in tk.items()},
+           "roofline": {"bound": "fp64-tensor (DMMA)", "kernel": "k_rom_contract",
+                        "achieved": round(ach_tf, 2) if ach_tf else None,
+                        "peak": fp64.get("dmma") if fp64 else None, "unit": "TFLOP/s",
+                        "frac": round(ach_tf / fp64["dmma"], 4) if (ach_tf and fp64) else None,
+                        "peak_source": "DMMA probe measured in this run (mma.sync m8n8k4 f64)",
+                        "share_of_step": {"contract": round(kc[0] / tot, 3), "material": round(kp[0] / tot, 3),
+                                          "newton_lu": round(kn[0] / tot, 3)} if tot > 0 else None}}
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        import oracle
+        orve = oracle.Rve(128, mats)
+        nt = oracle.max_threads()
+        m = min(max(nt, 16), n_inst)
+        t0 = time.perf_counter()
+        ro = orve.rom_solve(model["ids"], model["weights"], model["mode_grads"], geom_np[:m], sched_np[:m],
+                            eps_rel=1e-10, eps_abs=1e-12, max_iter=25, max_bisect=5, nthreads=nt)
+        dt = time.perf_counter() - t0
+        pg = out["pbar"][:m].cpu().numpy()
+        rel = np.linalg.norm(pg - ro["pbar"], axis=-1) / np.maximum(np.linalg.norm(ro["pbar"], axis=-1), 1e-14)
+        res["cpu_baseline"] = {"value": m / dt, "unit": "RVE solves/s", "cores": nt, "kind": "port",
+                               "sample": f"first {m} of the {n_inst} instances (20-increment rom_solve each) "
+                                         f"in {dt:.2f} s on {nt} threads"}
+        res["parity_on_sample"] = {"pbar_rel_max": float(rel.max()),
+                                   "iteration_count_mismatches": int((out["iters"][:m].cpu().numpy() != ro["iters"]).sum())}
+    del rom, rve
+    torch.cuda.empty_cache()
+    return res
+
+
+# --------------------------------------------------------------------------
+def reference_arm(args, ws, rank, base):
+    """--impl reference: the reference's CPU algorithm (oracle/ restatement)
+    on all host threads, same metric/config; each step a bounded sample."""
+    if rank != 0:
+        return
+    import oracle
+    from paper_2307_16894_b200 import api, synth
+    nt = oracle.max_threads()
+    F_np, st_np = synth.config1_points(args.points, 2027)
+    mats = [api.matrix_params()]
+    for _ in range(args.warmup):
+        oracle.material_batch(F_np[:, :4096], st_np[:, :4096], mats, nthreads=nt)
+    sample = min(args.points, 1 << 20)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.material_batch(F_np[:, :sample], st_np[:, :sample], mats, nthreads=nt)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = sample / dt
+    line = dict(base, impl="reference", value=v, ms_per_step=dt * 1e3 * args.points / sample,
+                config={"workload": base["config"]["workload"], "points": args.points,
+                        "sample_points_per_step": sample},
+                cpu_baseline={"value": v, "unit": "points/s", "cores": nt, "kind": "port",
+                              "sample": f"{sample} of the {args.points} config-1 points per step on "
+                                        f"{nt} host threads (oracle/ C++ restatement of material.cpp)"},
+                e2e={"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+    print(json.dumps(line))
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c1", choices=["c1"])
+    ap.add_argument("--config", default="all", choices=["all", "c1", "c0", "c2", "c3"])
     ap.add_argument("--points", type=int, default=1 << 22)
+    ap.add_argument("--c2-inst", type=int, default=1024)
+    ap.add_argument("--c3-inst", type=int, default=65536)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "ours":
+        args.warmup = max(args.warmup, 3)
 
-    ws, rank, local = dist_setup(args.gpus)
+    ws, rank, local = dist_setup()
     workload = (f"config1: {args.points} independent plane-strain material points per GPU "
                 "(finite-strain J2 + central-FD consistent tangent + history), matrix material "
                 "E=1 nu=0.3 sigma_y=0.01 H=0.1")
     base = {"metric": "material-point updates/s", "unit": "points/s", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config 1 distribution)"}
-
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded; BASELINE config distributions, see paper_2307_16894_b200/synth.py)",
+            "config": {"workload": workload}}
     if args.impl == "reference":
-        if rank != 0:
-            return
-        import oracle
-        from paper_2307_16894_b200 import api, synth
-        F_np, st_np = synth.config1_points(args.points, 2027)
-        mats = [api.matrix_params()]
-        nt = oracle.max_threads()
-        for _ in range(args.warmup):
-            oracle.material_batch(F_np[:, :4096], st_np[:, :4096], mats, nthreads=nt)
-        sample = min(args.points, 1 << 20)
-        t0 = time.perf_counter()
-        for k in range(args.steps):
-            oracle.material_batch(F_np[:, :sample], st_np[:, :sample], mats, nthreads=nt)
-        dt = (time.perf_counter() - t0) / args.steps
-        v = sample / dt
-        line = dict(base, impl="reference", value=v, ms_per_step=dt * 1e3 * args.points / sample,
-                    config={"workload": workload, "points": args.points,
-                            "sample_points_per_step": sample},
-                    cpu_baseline={"value": v, "unit": "points/s", "cores": nt, "kind": "port",
-                                  "sample": f"{sample} of the {args.points} config-1 points per step "
-                                            f"on {nt} host threads (oracle/ C++ restatement)"},
-                    e2e={"value": v, "unit": "points/s", "h2d_bytes_per_step": 0,
-                         "d2h_bytes_per_step": 0})
-        print(json.dumps(line))
+        reference_arm(args, ws, rank, base)
         return
 
-    r = run_c1(args, ws, rank, local)
+    import torch
+    from paper_2307_16894_b200 import api
+    torch.cuda.set_device(local)
+    ctx = api.Context.default(local)
+    clk = ClockSampler(local).start() if rank == 0 else None
+    fp64 = fp64_peaks(ctx, torch)
+    line = dict(base)
+    also = {}
+    try:
+        if args.config in ("all", "c1"):
+            r = run_c1(args, ws, rank, local, ctx, clk)
+            n = args.points
+            peak, src = _hbm_peak()
+            ach = C1_BYTES_PER_POINT * n / (r["kern_ms"] * 1e-3) / 1e9
+            line.update({
+                "value": ws * n * args.steps / (r["ms"] * 1e-3),
+                "ms_per_step": r["ms"] / args.steps,
+                "config": {"workload": workload, "points_per_gpu": n,
+                           "parallelism": f"{ws} independent shard(s), no collective",
+                           "l2": "1.2 GB touched per step > 126 MB L2 (no flush needed)",
+                           "plastic_fraction": round(r["plastic_frac"], 4)},
+                "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                             "frac": round(ach / peak, 4), "traffic": None, "peak_source": src,
+                             "kernel": "k_material_batch", "algorithmic_bytes_per_point": C1_BYTES_PER_POINT,
+                             "kernel_ms": round(r["kern_ms"], 4),
+                             "note": "FP64-issue bound (9 evaluations/point); see fp64 block"},
+                "fp64": {"probe_peak_tflops": fp64},
+                "e2e": {"value": ws * n / (r["e2e_ms"] * 1e-3), "unit": "points/s",
+                        "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
+                        "matches_resident_path": r["e2e_same"],
+                        "how": "public API (api.material_batch) on pinned host buffers, 8 chunks x 3 streams"},
+                "gpu_launches": r["launches"],
+            })
+            if "cpu" in r:
+                line["cpu_baseline"] = r["cpu"]
+        if args.config in ("all", "c0"):
+            also["c0"] = run_rve(args, ws, rank, local, ctx, 64, 1, 0.1, None,
+                                 steps=200 if args.config == "all" else args.steps,
+                                 warmup=args.warmup, seed=2026, cpu_sample=1)
+        if args.config in ("all", "c2"):
+            also["c2"] = run_rve(args, ws, rank, local, ctx, 128, args.c2_inst, 0.2, (0.15, 0.35),
+                                 steps=5 if args.config == "all" else args.steps,
+                                 warmup=args.warmup, seed=2028, cpu_sample=8)
+        if args.config in ("all", "c3"):
+            also["c3"] = run_c3(args, ws, rank, local, ctx, args.c3_inst,
+                                steps=2 if args.config == "all" else args.steps,
+                                warmup=1 if args.config == "all" else args.warmup, fp64=fp64)
+    finally:
+        if clk:
+            clk.stop()
     if rank != 0:
         return
-    n = args.points
-    value = ws * n * args.steps / (r["ms_total"] * 1e-3)
-    peak, peak_src = _peaks()
-    achieved = BYTES_PER_POINT * n / (r["kern_ms"] * 1e-3) / 1e9
-    line = dict(base)
-    line.update({
-        "value": value,
-        "ms_per_step": r["ms_total"] / args.steps,
-        "config": {"workload": workload, "points_per_gpu": n, "parallelism": f"replicas x{ws} (independent shards)",
-                   "l2": "inputs+outputs 1.2 GB per step > 126 MB L2 (no flush needed)",
-                   "plastic_fraction": round(r["plastic_frac"], 4)},
-        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
-                     "peak_source": peak_src, "kernel": "k_material_batch",
-                     "algorithmic_bytes_per_point": BYTES_PER_POINT,
-                     "note": "FP64-issue bound, see fp64"},
-        "fp64": {"probe_peak_tflops": r.get("fp64")},
-        "e2e": {"value": ws * n / (r["e2e_ms"] * 1e-3), "unit": "points/s",
-                "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
-                "matches_resident_path": r["e2e_same"]},
-        "gpu_launches": r["launches"],
-        "clocks": r["clocks"],
-    })
-    if "cpu" in r:
-        line["cpu_baseline"] = r["cpu"]
+    if clk:
+        line["clocks"] = clk.summary()
+    if args.config != "c1" and args.config != "all":
+        key = args.config
+        blk = also[key]
+        if key == "c3":
+            line.update({"metric": "ROM RVE solves/s", "unit": "RVE solves/s",
+                         "value": blk["rve_solves_per_s"], "ms_per_step": blk["ms_per_step"],
+                         "roofline": blk["roofline"]})
+        else:
+            line.update({"metric": "quadrature-point updates/s (full-order assembly)", "unit": "qp/s",
+                         "value": blk["qp_per_s"], "ms_per_step": blk["ms_per_step"],
+                         "roofline": blk["roofline"]})
+        line["config"] = {"workload": key, **{k: v for k, v in blk.items() if k in ("instances", "n_cells", "N", "Q")}}
+        if "cpu_baseline" in blk:
+            line["cpu_baseline"] = blk["cpu_baseline"]
+        line["gpu_launches"] = int(blk["launches_per_step"] * args.steps)
+    if also:
+        line["also"] = also
     print(json.dumps(line))
 
 

@@ -66,6 +66,13 @@ const char* podecm_last_error(const podecm_ctx* ctx);
 int podecm_check(podecm_ctx* ctx, void* stream);
 /* Number of kernels this context has launched (for bench accounting). */
 int64_t podecm_launch_count(const podecm_ctx* ctx);
+/* Optional per-kernel CUDA-event timing of every launch on its own stream
+ * (bench roofline accounting).  podecm_get_timings synchronises the device
+ * and returns, per kernel name ('\n'-separated in `names`), the summed ms
+ * and launch count since the previous call; returns the number of names. */
+void podecm_set_timing(podecm_ctx* ctx, int on);
+int podecm_get_timings(podecm_ctx* ctx, char* names, int names_len, double* ms, int64_t* counts,
+                       int max_items);
 
 /* ---- (i) material point -------------------------------------------------
  * Replaces large_strain_update + large_strain_tangent per point
@@ -130,6 +137,8 @@ int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* rve, int64_
 int podecm_rom_create(podecm_ctx* ctx, podecm_rve* rve, int N, int Q, const int32_t* ids,
                       const double* weights, const double* mode_grads, podecm_rom** out);
 void podecm_rom_destroy(podecm_rom* rom);
+/* Batch-wide reduced assemblies ("global iterations") of the last solve. */
+int64_t podecm_rom_global_iterations(const podecm_rom* rom);
 /* Replaces rom_solve (rom.hpp:86-88; rom.cpp:177-200) with
  * rom_solve_step_adaptive (rom.cpp:152-175) for n_inst instances:
  *   geom [n_inst][2]; sched [n_inst][K][4] macro F per increment;

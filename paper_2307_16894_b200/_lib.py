@@ -35,6 +35,8 @@ _SIGS = {
     "podecm_last_error": (C.c_char_p, [P]),
     "podecm_check": (C.c_int, [P, P]),
     "podecm_launch_count": (I64, [P]),
+    "podecm_set_timing": (None, [P, C.c_int]),
+    "podecm_get_timings": (C.c_int, [P, C.c_char_p, C.c_int, P, P, C.c_int]),
     "podecm_material_batch": (C.c_int, [P, P, I64, C.POINTER(podecm_params), C.c_int, P, P, P, P,
                                         P, P, P, D]),
     "podecm_rve_create_q4": (C.c_int, [P, C.c_int, D, C.POINTER(podecm_params), C.c_int,
@@ -47,6 +49,7 @@ _SIGS = {
     "podecm_assemble_batch": (C.c_int, [P, P, P, I64, P, P, P, P, P, P, P, P, P, P]),
     "podecm_rom_create": (C.c_int, [P, P, C.c_int, C.c_int, P, P, P, C.POINTER(P)]),
     "podecm_rom_destroy": (None, [P]),
+    "podecm_rom_global_iterations": (I64, [P]),
     "podecm_probe_fp64": (C.c_int, [P, P, C.c_int, C.c_int, P, C.POINTER(D)]),
     "podecm_rom_solve_batch": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton),
                                          P, P, P, P, P]),

@@ -114,6 +114,19 @@ class Context:
     def launches(self) -> int:
         return int(self.lib.podecm_launch_count(self.h))
 
+    def set_timing(self, on: bool) -> None:
+        """Per-kernel CUDA-event timing inside the library (bench only)."""
+        self.lib.podecm_set_timing(self.h, 1 if on else 0)
+
+    def timings(self) -> dict:
+        """{kernel name: (total ms, launches)} since the previous call."""
+        buf = C.create_string_buffer(4096)
+        ms = (C.c_double * 64)()
+        cnt = (C.c_int64 * 64)()
+        n = self.lib.podecm_get_timings(self.h, buf, 4096, ms, cnt, 64)
+        names = buf.value.decode().split("\n")[:n]
+        return {nm: (ms[k], int(cnt[k])) for k, nm in enumerate(names)}
+
     def __del__(self):
         try:
             if getattr(self, "h", None):
@@ -274,6 +287,7 @@ class Rom:
                                              _ptr(sched), K, C.byref(oc), _ptr(pbar), _ptr(iters),
                                              _ptr(resid), _ptr(af), _ptr(status))
         _lib.raise_for(rc, self.ctx.h, "podecm_rom_solve_batch")
+        self.global_iterations = int(self.lib.podecm_rom_global_iterations(self.h))
         return {"pbar": pbar, "iters": iters, "resid": resid, "a_final": af, "status": status}
 
     def __del__(self):

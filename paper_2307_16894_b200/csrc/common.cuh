@@ -18,6 +18,14 @@ struct podecm_ctx {
   std::string last_error;
   unsigned int* d_fail = nullptr;  // device-side SolveError counter
   std::atomic<int64_t> launches{0};
+  // optional per-kernel event timing (podecm_set_timing)
+  bool timing = false;
+  struct Rec {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
 };
 
 namespace podecm_impl {
@@ -79,5 +87,38 @@ inline MatTable make_table(const podecm_params* mats, int n_mats) {
 }
 
 inline int grid_for(int64_t n, int block) { return (int)((n + block - 1) / block); }
+
+inline cudaEvent_t pool_event(podecm_ctx* ctx) {
+  if (!ctx->pool.empty()) {
+    cudaEvent_t e = ctx->pool.back();
+    ctx->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// RAII bracket that records start/stop events around one launch on `s`
+// when the context's timing mode is on.
+struct KTimer {
+  podecm_ctx* ctx;
+  cudaStream_t s;
+  const char* name;
+  cudaEvent_t a = nullptr;
+  KTimer(podecm_ctx* c, cudaStream_t st, const char* n) : ctx(c), s(st), name(n) {
+    if (ctx->timing) {
+      a = pool_event(ctx);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~KTimer() {
+    if (a) {
+      cudaEvent_t b = pool_event(ctx);
+      cudaEventRecord(b, s);
+      ctx->recs.push_back({name, a, b});
+    }
+  }
+};
 
 }  // namespace podecm_impl

@@ -327,7 +327,10 @@ int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t 
     a.fail = ctx->d_fail;
     a.tangent = kvals != nullptr;
     const int64_t nthr = (int64_t)nc * r->n_qp;
-    k_asm_qp<<<grid_for(nthr, 128), 128, 0, s>>>(a, r->mats);
+    {
+      KTimer kt(ctx, s, "k_asm_qp");
+      k_asm_qp<<<grid_for(nthr, 128), 128, 0, s>>>(a, r->mats);
+    }
     GatherArgs gg;
     gg.n_red = r->n_red;
     gg.n_elems = r->n_elems;
@@ -342,7 +345,10 @@ int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t 
     gg.f = f;
     gg.kvals = kvals;
     const int64_t nitems = ((kvals ? r->nnz : 0) + r->n_red) * nc;
-    k_asm_gather<<<grid_for(nitems, 256), 256, 0, s>>>(gg);
+    {
+      KTimer kt(ctx, s, "k_asm_gather");
+      k_asm_gather<<<grid_for(nitems, 256), 256, 0, s>>>(gg);
+    }
     PODECM_LAUNCHED(ctx, 2);
   }
   return PODECM_OK;

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 
 #include "common.cuh"
@@ -109,6 +110,50 @@ const char* podecm_last_error(const podecm_ctx* ctx) {
 
 int64_t podecm_launch_count(const podecm_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
 
+void podecm_set_timing(podecm_ctx* ctx, int on) {
+  if (ctx) ctx->timing = on != 0;
+}
+
+// Synchronises the device, then returns the per-kernel-name totals (ms) and
+// launch counts recorded since the last call; names are '\n'-separated.
+int podecm_get_timings(podecm_ctx* ctx, char* names, int names_len, double* ms, int64_t* counts,
+                       int max_items) {
+  if (!ctx) return -1;
+  cudaDeviceSynchronize();
+  std::vector<std::string> nm;
+  std::vector<double> tot;
+  std::vector<int64_t> cnt;
+  for (auto& r : ctx->recs) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    size_t k = 0;
+    while (k < nm.size() && nm[k] != r.name) ++k;
+    if (k == nm.size()) {
+      nm.push_back(r.name);
+      tot.push_back(0.0);
+      cnt.push_back(0);
+    }
+    tot[k] += t;
+    cnt[k] += 1;
+    ctx->pool.push_back(r.a);
+    ctx->pool.push_back(r.b);
+  }
+  ctx->recs.clear();
+  std::string joined;
+  const int n = (int)std::min<size_t>(nm.size(), (size_t)max_items);
+  for (int k = 0; k < n; ++k) {
+    joined += nm[k];
+    joined += '\n';
+    if (ms) ms[k] = tot[k];
+    if (counts) counts[k] = cnt[k];
+  }
+  if (names && names_len > 0) {
+    std::strncpy(names, joined.c_str(), names_len - 1);
+    names[names_len - 1] = 0;
+  }
+  return n;
+}
+
 int podecm_check(podecm_ctx* ctx, void* stream) {
   if (!ctx) return PODECM_ECONFIG;
   unsigned int h = 0;
@@ -137,6 +182,7 @@ int podecm_material_batch(podecm_ctx* ctx, void* stream, int64_t n, const podecm
   const int block = 128;
   const int64_t blocks = (n + block - 1) / block;
   const int grid = (int)(blocks < (int64_t)ctx->n_sm * 64 ? blocks : (int64_t)ctx->n_sm * 64);
+  KTimer kt(ctx, static_cast<cudaStream_t>(stream), "k_material_batch");
   kVariants[k1_variant()]<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
       n, tab, n_mats, region, F, st_in, P, A, st_out, status, ctx->d_fail, h_rel);
   PODECM_LAUNCHED(ctx, 1);

@@ -67,6 +67,7 @@ struct podecm_rom {
   RomCtl* d_ctl = nullptr;
   int* d_nactive = nullptr;
   int* h_nactive = nullptr;
+  int64_t last_global_iters = 0;
 };
 
 namespace {
@@ -628,6 +629,8 @@ int podecm_rom_create(podecm_ctx* ctx, podecm_rve* rve, int N, int Q, const int3
   return PODECM_OK;
 }
 
+int64_t podecm_rom_global_iterations(const podecm_rom* r) { return r ? r->last_global_iters : 0; }
+
 void podecm_rom_destroy(podecm_rom* r) {
   if (!r) return;
   free_work(r);
@@ -734,25 +737,38 @@ int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t
 
   const int64_t max_global = (int64_t)K * (opts->max_iter + 1) * (2ll << opts->max_bisect) + 8;
   for (int64_t it = 0; it < max_global; ++it) {
-    k_rom_point<<<gpt, 256, smem_pt, s>>>(pa, rv->mats);
-    switch (r->NT) {
-      case 1: k_rom_contract<1><<<gct, 32 * 1 * kIPC, 0, s>>>(ca); break;
-      case 2: k_rom_contract<2><<<gct, 32 * 2 * kIPC, 0, s>>>(ca); break;
-      case 3: k_rom_contract<3><<<gct, 32 * 3 * kIPC, 0, s>>>(ca); break;
-      case 4: k_rom_contract<4><<<gct, 32 * 4 * kIPC, 0, s>>>(ca); break;
-      case 5: k_rom_contract<5><<<gct, 32 * 5 * kIPC, 0, s>>>(ca); break;
-      case 6: k_rom_contract<6><<<gct, 32 * 6 * kIPC, 0, s>>>(ca); break;
-      default: k_rom_contract<7><<<gct, 32 * 7 * kIPC, 0, s>>>(ca); break;
+    {
+      KTimer kt(ctx, s, "k_rom_point");
+      k_rom_point<<<gpt, 256, smem_pt, s>>>(pa, rv->mats);
+    }
+    {
+      KTimer kt(ctx, s, "k_rom_contract");
+      switch (r->NT) {
+        case 1: k_rom_contract<1><<<gct, 32 * 1 * kIPC, 0, s>>>(ca); break;
+        case 2: k_rom_contract<2><<<gct, 32 * 2 * kIPC, 0, s>>>(ca); break;
+        case 3: k_rom_contract<3><<<gct, 32 * 3 * kIPC, 0, s>>>(ca); break;
+        case 4: k_rom_contract<4><<<gct, 32 * 4 * kIPC, 0, s>>>(ca); break;
+        case 5: k_rom_contract<5><<<gct, 32 * 5 * kIPC, 0, s>>>(ca); break;
+        case 6: k_rom_contract<6><<<gct, 32 * 6 * kIPC, 0, s>>>(ca); break;
+        default: k_rom_contract<7><<<gct, 32 * 7 * kIPC, 0, s>>>(ca); break;
+      }
     }
     PODECM_CUDA_TRY(ctx, cudaMemsetAsync(r->d_nactive, 0, sizeof(int), s));
-    k_rom_newton<<<gnt, 32 * kNW, smem_nt, s>>>(na);
+    {
+      KTimer kt(ctx, s, "k_rom_newton");
+      k_rom_newton<<<gnt, 32 * kNW, smem_nt, s>>>(na);
+    }
     PODECM_LAUNCHED(ctx, 3);
     if ((it & 3) == 3) {
       PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(r->h_nactive, r->d_nactive, sizeof(int),
                                            cudaMemcpyDeviceToHost, s));
       PODECM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-      if (*r->h_nactive == 0) break;
+      if (*r->h_nactive == 0) {
+        r->last_global_iters = it + 1;
+        break;
+      }
     }
+    r->last_global_iters = it + 1;
   }
   // failed instances -> context flag (podecm_check reports SolveError)
   return PODECM_OK;
