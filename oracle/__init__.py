@@ -63,7 +63,13 @@ def _mats(mats):
 
 
 def max_threads() -> int:
-    return int(lib().orc_max_threads())
+    """Host threads available to this process (not OpenMP's current setting,
+    which a previous nthreads=1 call may have lowered)."""
+    import os
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
 def material_batch(F, st, mats, region=None, h_rel=1e-7, tangent=True, nthreads=0):

@@ -29,9 +29,7 @@ struct OrcRve {
   Csr pattern;
 };
 
-void set_threads(int nt) {
-  if (nt > 0) omp_set_num_threads(nt);
-}
+void set_threads(int nt) { omp_set_num_threads(nt > 0 ? nt : omp_get_num_procs()); }
 
 }  // namespace
 
