@@ -150,6 +150,49 @@ int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* rom, int64
                            const podecm_newton* opts, double* pbar, int32_t* iters, double* resid,
                            double* a_final, int32_t* status);
 
+/* ---- (iv) offline POD / ECM (BASELINE config 4) -------------------------
+ * Replaces pod_impl / pod_diag (podkit.cpp:43-72, 117-127):
+ * C = S^T diag(g) S (n_snap x n_snap, symmetric) for the column-major
+ * snapshot matrix S (n_dof x n_snap); gram_diag nullable = identity. */
+int podecm_pod_gram(podecm_ctx* ctx, void* stream, const double* S, int64_t n_dof, int n_snap,
+                    const double* gram_diag, double* C);
+/* Eigen-decomposition of C (overwritten), keep lambda > tol_rel^2 lambda_0,
+ * lambda > 0, at most max_modes; modes (column-major n_dof x kept) =
+ * S v_i / sqrt(lambda_i) followed by one MGS pass in the diag(g) metric
+ * (mgs_pass, podkit.cpp:75-86); evals (device, n_snap) descending;
+ * *n_kept on the host.  Synchronises the stream. */
+int podecm_pod_modes(podecm_ctx* ctx, void* stream, const double* S, int64_t n_dof, int n_snap,
+                     double* C, const double* gram_diag, int max_modes, double tol_rel,
+                     double* modes, double* evals, int* n_kept);
+
+/* EcmOpts (ecm.hpp:28-32) plus stop_at_count: configs 3/4 stop at
+ * max_points selected points instead of throwing (documented deviation). */
+typedef struct podecm_ecm_opts {
+  double eps;
+  int32_t volume_row;
+  int32_t max_points;
+  int32_t stop_at_count;
+} podecm_ecm_opts;
+/* Mode gradients at every quadrature point, H [n_qp][N][4] flatten order
+ * (build_rom's per-point formula, rom.cpp:91-104), from full nodal modes
+ * (column-major 2 n_nodes x N). */
+int podecm_ecm_mode_grads(podecm_ctx* ctx, void* stream, podecm_rve* rve, const double* modes,
+                          int N, double* H);
+/* Weighted stress snapshots W [L][n_qp][4] (weighted_stress_field,
+ * ecm.cpp:10-18) of L full nodal displacement snapshots U (column-major
+ * 2 n_nodes x L): stress-only update from a virgin history at F = I + grad u
+ * on the parent (identity-morph) cell. */
+int podecm_ecm_stress_snapshots(podecm_ctx* ctx, void* stream, podecm_rve* rve, const double* U,
+                                int64_t L, double* W, int32_t* status);
+/* Greedy ECM (ecm_integrand + ecm_select, ecm.cpp:20-48, 132-204) on the
+ * factored integrand J[(i L + s), q] = H_q[i] . W_s(q) (+ volume row).
+ * ids / weights (host, capacity max_points or n_qp) ascending; *n_sel,
+ * *resid_rel, *iterations on the host.  Returns 3 on budget exhaustion
+ * (without stop_at_count) or stall, like the reference. */
+int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const double* H, int N,
+                      const double* W, int64_t L, const podecm_ecm_opts* opts, int32_t* ids,
+                      double* weights, int* n_sel, double* resid_rel, int* iterations);
+
 /* ---- diagnostics ---------------------------------------------------------
  * FP64 roofline probes (mode 0: DFMA chain, mode 1: mma.sync m8n8k4 f64);
  * *flops receives the flop count of the launch, time it on `stream`. */

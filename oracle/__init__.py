@@ -49,6 +49,8 @@ def lib():
         l.orc_rve_assemble.argtypes = [P, L, P, P, P, P, P, P, P, P, P, I]
         l.orc_rom_solve.restype = L
         l.orc_rom_solve.argtypes = [P, I, I, P, P, P, L, P, P, I, D, D, I, I, P, P, P, P, P, I]
+        l.orc_stress_snapshots.restype = L
+        l.orc_stress_snapshots.argtypes = [P, P, L, P, I]
         l.orc_max_threads.restype = I
         _lib = l
     return _lib
@@ -130,6 +132,14 @@ class Rve:
         lib().orc_rve_assemble(self.h, n, _p(geom), _p(fbar), _p(w_red), _p(st0), _p(s1), _p(f), _p(K),
                                _p(pf), _p(status), nthreads)
         return {"f": f, "K": K, "st1": s1, "p_field": pf, "status": status}
+
+    def stress_snapshots(self, U, nthreads=0):
+        """Weighted stress snapshots W [L][n_qp][4] of nodal fields U (2n x L)."""
+        U = np.asfortranarray(U, dtype=np.float64)
+        L = U.shape[1]
+        W = np.empty((L, self.n_qp, 4))
+        fails = lib().orc_stress_snapshots(self.h, U.ctypes.data_as(C.c_void_p), L, _p(W), nthreads)
+        return W, int(fails)
 
     def rom_solve(self, ids, weights, mode_grads, geom, sched, eps_rel=1e-8, eps_abs=1e-12,
                   max_iter=25, max_bisect=5, nthreads=0):

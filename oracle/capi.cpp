@@ -258,6 +258,44 @@ long orc_rom_solve(void* hp, int N, int Q, const int* ids, const double* weights
   return fails;
 }
 
+// Weighted stress snapshots for ECM (ecm.cpp:10-18 on the parent cell):
+// W[s][q][c] = flatten(P Fmu^-T det) with P from large_strain_update at
+// F = I + grad u_s (assemble's F with Fbar = I, identity morph) from a virgin
+// history.  U: column-major 2 n_nodes x L.  Returns the number of failures.
+long orc_stress_snapshots(void* hp, const double* U, long L, double* W, int nthreads) {
+  set_threads(nthreads);
+  auto* h = static_cast<OrcRve*>(hp);
+  const RveProblem& prob = h->prob;
+  const int nq = prob.cache.n_qp();
+  const long ndof = 2L * prob.mesh.n_nodes;
+  long fails = 0;
+#pragma omp parallel for schedule(static) reduction(+ : fails)
+  for (long t = 0; t < L * nq; ++t) {
+    const long s = t / nq;
+    const int q = (int)(t - s * nq);
+    const int e = prob.cache.elem_of[q];
+    const double* g = &prob.cache.grad[(size_t)q * 8];
+    Mat2 gw;
+    for (int a = 0; a < 4; ++a) {
+      const int node = prob.mesh.elems[4 * e + a];
+      for (int i = 0; i < 2; ++i)
+        for (int j = 0; j < 2; ++j) gw(i, j) += U[s * ndof + 2 * node + i] * g[2 * a + j];
+    }
+    const Mat2 I = Mat2::identity();
+    const Mat2 gf = mul(gw, I);
+    Mat2 F;
+    for (int k = 0; k < 4; ++k) F.a[k] = I.a[k] + gf.a[k];
+    try {
+      const LargeResult r = large_strain_update(prob.material_at(q), PlasticState{}, F, nullptr);
+      Mat2 wq = mul(r.P, transpose(I));
+      for (int k = 0; k < 4; ++k) W[(s * nq + q) * 4 + k] = wq.a[k] * 1.0;
+    } catch (const SolveError&) {
+      ++fails;
+    }
+  }
+  return fails;
+}
+
 int orc_max_threads() { return omp_get_max_threads(); }
 
 }  // extern "C"

@@ -24,6 +24,10 @@ class podecm_params(C.Structure):
     _fields_ = [("E", D), ("nu", D), ("sigma_y0", D), ("H", D)]
 
 
+class podecm_ecm_opts(C.Structure):
+    _fields_ = [("eps", D), ("volume_row", I32), ("max_points", I32), ("stop_at_count", I32)]
+
+
 class podecm_newton(C.Structure):
     _fields_ = [("eps_rel", D), ("eps_abs", D), ("force_ref", D), ("max_iter", I32),
                 ("max_bisect", I32)]
@@ -50,6 +54,12 @@ _SIGS = {
     "podecm_rom_create": (C.c_int, [P, P, C.c_int, C.c_int, P, P, P, C.POINTER(P)]),
     "podecm_rom_destroy": (None, [P]),
     "podecm_rom_global_iterations": (I64, [P]),
+    "podecm_pod_gram": (C.c_int, [P, P, P, I64, C.c_int, P, P]),
+    "podecm_pod_modes": (C.c_int, [P, P, P, I64, C.c_int, P, P, C.c_int, D, P, P, C.POINTER(C.c_int)]),
+    "podecm_ecm_mode_grads": (C.c_int, [P, P, P, P, C.c_int, P]),
+    "podecm_ecm_stress_snapshots": (C.c_int, [P, P, P, P, I64, P, P]),
+    "podecm_ecm_select": (C.c_int, [P, P, P, P, C.c_int, P, I64, C.POINTER(podecm_ecm_opts), P, P,
+                                    C.POINTER(C.c_int), C.POINTER(D), C.POINTER(C.c_int)]),
     "podecm_probe_fp64": (C.c_int, [P, P, C.c_int, C.c_int, P, C.POINTER(D)]),
     "podecm_rom_solve_batch": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton),
                                          P, P, P, P, P]),

@@ -20,9 +20,10 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import ConfigError, SolveError, podecm_newton, podecm_params
+from ._lib import ConfigError, SolveError, podecm_ecm_opts, podecm_newton, podecm_params
 
 __all__ = ["PlasticityParams", "NewtonOpts", "Context", "material_batch", "Rve", "Rom",
+           "pod", "EcmOpts", "ecm_mode_grads", "ecm_stress_snapshots", "ecm_select",
            "ConfigError", "SolveError", "matrix_params", "inclusion_params"]
 
 
@@ -297,3 +298,74 @@ class Rom:
                 self.h = None
         except Exception:
             pass
+
+
+# ---------------------------------------------------------------- POD / ECM --
+def pod(S_cm: torch.Tensor, max_modes: int, tol_rel: float = 1e-10, gram_diag=None,
+        ctx: Context | None = None):
+    """pod_diag (podkit.cpp:117-127) of a column-major snapshot matrix given as
+    its transpose ``S_cm`` [n_snap, n_dof] (row s = snapshot s, contiguous).
+    Returns (modes^T [kept, n_dof], eigenvalues [n_snap] descending)."""
+    ctx = ctx or Context.default(S_cm.device.index or 0)
+    n_snap, n_dof = S_cm.shape
+    C_ = torch.empty((n_snap, n_snap), dtype=torch.float64, device=S_cm.device)
+    rc = ctx.lib.podecm_pod_gram(ctx.h, ctx.stream(), _ptr(S_cm), n_dof, n_snap, _ptr(gram_diag), _ptr(C_))
+    _lib.raise_for(rc, ctx.h, "podecm_pod_gram")
+    modes = torch.empty((max_modes, n_dof), dtype=torch.float64, device=S_cm.device)
+    ev = torch.empty(n_snap, dtype=torch.float64, device=S_cm.device)
+    kept = C.c_int()
+    rc = ctx.lib.podecm_pod_modes(ctx.h, ctx.stream(), _ptr(S_cm), n_dof, n_snap, _ptr(C_),
+                                  _ptr(gram_diag), max_modes, tol_rel, _ptr(modes), _ptr(ev), C.byref(kept))
+    _lib.raise_for(rc, ctx.h, "podecm_pod_modes")
+    return modes[: kept.value], ev
+
+
+@dataclass
+class EcmOpts:
+    """EcmOpts (ecm.hpp:28-32) + stop_at_count (configs 3/4 stop at a count)."""
+    eps: float = 0.01
+    volume_row: bool = True
+    max_points: int = 0
+    stop_at_count: bool = False
+
+    def c(self) -> podecm_ecm_opts:
+        return podecm_ecm_opts(self.eps, int(self.volume_row), self.max_points, int(self.stop_at_count))
+
+
+def ecm_mode_grads(rve: Rve, modes_t: torch.Tensor) -> torch.Tensor:
+    """H [n_qp, N, 4] from nodal modes given as modes^T [N, 2 n_nodes]."""
+    N = modes_t.shape[0]
+    H = torch.empty((rve.n_qp, N, 4), dtype=torch.float64, device=modes_t.device)
+    rc = rve.lib.podecm_ecm_mode_grads(rve.ctx.h, rve.ctx.stream(), rve.h, _ptr(modes_t), N, _ptr(H))
+    _lib.raise_for(rc, rve.ctx.h, "podecm_ecm_mode_grads")
+    return H
+
+
+def ecm_stress_snapshots(rve: Rve, U_t: torch.Tensor):
+    """W [L, n_qp, 4] of snapshots U^T [L, 2 n_nodes]; returns (W, status)."""
+    L = U_t.shape[0]
+    W = torch.empty((L, rve.n_qp, 4), dtype=torch.float64, device=U_t.device)
+    st = torch.zeros(1, dtype=torch.int32, device=U_t.device)
+    rc = rve.lib.podecm_ecm_stress_snapshots(rve.ctx.h, rve.ctx.stream(), rve.h, _ptr(U_t), L, _ptr(W), _ptr(st))
+    _lib.raise_for(rc, rve.ctx.h, "podecm_ecm_stress_snapshots")
+    return W, st
+
+
+def ecm_select(rve: Rve, H: torch.Tensor, W: torch.Tensor, opts: EcmOpts):
+    """ecm_select (ecm.cpp:132-204) on the factored integrand.  Returns
+    (ids ascending, weights, residual_rel, iterations)."""
+    import numpy as np
+    nq, N = H.shape[0], H.shape[1]
+    L = W.shape[0]
+    cap = opts.max_points if opts.max_points > 0 else nq
+    ids = np.empty(cap, np.int32)
+    w = np.empty(cap)
+    n = C.c_int()
+    rr = C.c_double()
+    it = C.c_int()
+    oc = opts.c()
+    rc = rve.lib.podecm_ecm_select(rve.ctx.h, rve.ctx.stream(), rve.h, _ptr(H), N, _ptr(W), L, C.byref(oc),
+                                   ids.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p),
+                                   C.byref(n), C.byref(rr), C.byref(it))
+    _lib.raise_for(rc, rve.ctx.h, "podecm_ecm_select")
+    return ids[: n.value].copy(), w[: n.value].copy(), rr.value, it.value

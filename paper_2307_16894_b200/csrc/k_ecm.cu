@@ -1,0 +1,633 @@
+// K4b — Empirical Cubature Method greedy selection (BASELINE config 4).
+//
+// Replaces weighted_stress_field / ecm_integrand / ecm_select /
+// restore_feasible (/root/reference/proj/src/ecm.cpp:10-204) without ever
+// materialising the integrand J ((N L + 1) x n_qp, 105 GB at config 4): J is
+// kept factored as J[(i,s), q] = sum_c H[q][i][c] W[s][q][c] (mode gradient
+// x weighted stress snapshot) plus the all-ones volume row.
+//
+//   k_ecm_mode_grads   H[q][i][c] (build_rom's formula at every qp)
+//   k_ecm_stress       W[s][q][c]: stress-only material update of snapshot s
+//                      (virgin history, identity morph => W = P)
+//   k_ecm_colnorm      ||J_q||^2 = sum_cd (H_q^T H_q)_cd (W_q^T W_q)_cd + 1
+//   k_ecm_score        corr = J^T r as one DMMA GEMM T = R W (R = r reshaped
+//                      N x L) fused with the H contraction, the score
+//                      corr/||J_q|| and a per-CTA argmax (strict '>', first
+//                      index wins, positive scores only: ecm.cpp:164-173)
+//   refit              least squares on the selected columns by an
+//                      incrementally updated QR (classical Gram-Schmidt with
+//                      re-orthogonalisation); the Lawson-Hanson feasibility
+//                      steps of restore_feasible (ecm.cpp:56-90) run on the
+//                      host over k <= max_points weights; a drop rebuilds the
+//                      QR of the kept set.
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <vector>
+
+#include "rve.cuh"
+#include "dmma_gemm.cuh"
+
+using namespace podecm_dev;
+using namespace podecm_impl;
+
+namespace {
+
+__global__ void k_ecm_mode_grads(int nq, int N, int64_t ndof, const int32_t* elems,
+                                 const double* grad, const double* modes, double* H) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nq * N) return;
+  const int q = (int)(t / N), i = (int)(t - (int64_t)q * N);
+  const int e = q >> 2;
+  double h[4] = {0.0, 0.0, 0.0, 0.0};  // h(0,0), h(1,0), h(0,1), h(1,1)
+  for (int a = 0; a < 4; ++a) {
+    const int node = elems[4 * e + a];
+    const double ux = modes[(int64_t)i * ndof + 2 * node], uy = modes[(int64_t)i * ndof + 2 * node + 1];
+    const double g0 = grad[(size_t)q * 8 + 2 * a], g1 = grad[(size_t)q * 8 + 2 * a + 1];
+    h[0] = h[0] + ux * g0;  // h.row(0) += u_x g.row(a)  (rom.cpp:96-100)
+    h[2] = h[2] + ux * g1;
+    h[1] = h[1] + uy * g0;
+    h[3] = h[3] + uy * g1;
+  }
+  for (int c = 0; c < 4; ++c) H[((int64_t)q * N + i) * 4 + c] = h[c];
+}
+
+__global__ void __launch_bounds__(128, 5) k_ecm_stress(int64_t L, int nq, int64_t ndof,
+                                                        const int32_t* elems, const int32_t* regions,
+                                                        const double* grad, const double* U,
+                                                        MatTable tab, double* W, int32_t* status,
+                                                        unsigned int* fail) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= L * nq) return;
+  const int64_t s = t / nq;
+  const int q = (int)(t - s * nq);
+  const int e = q >> 2;
+  double gw[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int a = 0; a < 4; ++a) {
+    const int node = elems[4 * e + a];
+    const double ux = U[s * ndof + 2 * node], uy = U[s * ndof + 2 * node + 1];
+    const double g0 = grad[(size_t)q * 8 + 2 * a], g1 = grad[(size_t)q * 8 + 2 * a + 1];
+    gw[0] = gw[0] + ux * g0;
+    gw[2] = gw[2] + ux * g1;
+    gw[1] = gw[1] + uy * g0;
+    gw[3] = gw[3] + uy * g1;
+  }
+  // F = I + gw * I (identity morph, microfem.cpp:87)
+  double F[4];
+  F[0] = 1.0 + (gw[0] * 1.0 + gw[2] * 0.0);
+  F[1] = 0.0 + (gw[1] * 1.0 + gw[3] * 0.0);
+  F[2] = 0.0 + (gw[0] * 0.0 + gw[2] * 1.0);
+  F[3] = 1.0 + (gw[1] * 0.0 + gw[3] * 1.0);
+  const double fp[4] = {1.0, 0.0, 0.0, 1.0};
+  Frozen z;
+  freeze(fp, 1.0, 0.0, z);
+  double P[4];
+  const bool ok = lsu_eval<false>(tab.m[regions[e]], z, F, P, nullptr);
+  // W = P Fmu^-T det = P for the identity morph (ecm.cpp:10-18)
+  double* w = W + (s * nq + q) * 4;
+  for (int c = 0; c < 4; ++c) w[c] = P[c];
+  if (!ok) {
+    if (status) status[0] = PODECM_ESOLVE;
+    atomicAdd(fail, 1u);
+  }
+}
+
+// sum_{i,s} J[(i,s),q]^2 + vol via the 4x4 Gram factorisation
+__global__ void k_ecm_colnorm(int64_t L, int nq, int N, const double* H, const double* W, int vol,
+                              double* cn) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  double ww[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t s = 0; s < L; ++s) {
+    const double4 v = *reinterpret_cast<const double4*>(W + (s * nq + q) * 4);
+    const double a[4] = {v.x, v.y, v.z, v.w};
+    int k = 0;
+    for (int c = 0; c < 4; ++c)
+      for (int d = c; d < 4; ++d, ++k) ww[k] = fma(a[c], a[d], ww[k]);
+  }
+  double hh[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (int i = 0; i < N; ++i) {
+    const double* h = H + ((int64_t)q * N + i) * 4;
+    int k = 0;
+    for (int c = 0; c < 4; ++c)
+      for (int d = c; d < 4; ++d, ++k) hh[k] = fma(h[c], h[d], hh[k]);
+  }
+  double ssum = 0.0;
+  int k = 0;
+  for (int c = 0; c < 4; ++c)
+    for (int d = c; d < 4; ++d, ++k) ssum += (c == d ? 1.0 : 2.0) * hh[k] * ww[k];
+  cn[q] = sqrt(fmax(ssum, 0.0) + (vol ? 1.0 : 0.0));
+}
+
+// corr_q = sum_{i,s,c} r[i L + s] H[q][i][c] W[s][q][c] + r_vol, score, CTA argmax.
+// CTA: 16 qps (64 columns of T), 7 warps x 8 rows (N <= 56), K-loop over s.
+constexpr int kSQ = 16, kSC = 64, kSK = 16, kSLD = kSK + 4;
+
+__global__ void __launch_bounds__(224) k_ecm_score(int64_t L, int nq, int N, const double* r,
+                                                   double r_vol, const double* H, const double* W,
+                                                   const double* cn, const uint8_t* unavailable,
+                                                   double* cta_best, int* cta_idx) {
+  __shared__ double sR[2][56][kSLD];
+  __shared__ double sW[2][kSC][kSLD];
+  __shared__ double red[7][kSQ];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int q0 = blockIdx.x * kSQ;
+  double acc[8][2];
+#pragma unroll
+  for (int ct = 0; ct < 8; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
+  auto load = [&](int buf, int64_t s0) {
+    for (int t = tid; t < 56 * kSK; t += blockDim.x) {
+      const int i = t / kSK, k = t % kSK;
+      const int64_t s = s0 + k;
+      sR[buf][i][k] = (i < N && s < L) ? r[(int64_t)i * L + s] : 0.0;
+    }
+    for (int t = tid; t < kSK * kSC; t += blockDim.x) {
+      const int k = t / kSC, col = t % kSC;
+      const int64_t s = s0 + k;
+      const int q = q0 + col / 4;
+      sW[buf][col][k] = (s < L && q < nq) ? W[(s * nq + q0) * 4 + col] : 0.0;
+    }
+  };
+  const int64_t nk = (L + kSK - 1) / kSK;
+  load(0, 0);
+  __syncthreads();
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    const int buf = (int)(kt & 1);
+    if (kt + 1 < nk) load(buf ^ 1, (kt + 1) * kSK);
+#pragma unroll
+    for (int kk = 0; kk < kSK / 4; ++kk) {
+      const double af = sR[buf][warp * 8 + gid][kk * 4 + tig];
+#pragma unroll
+      for (int ct = 0; ct < 8; ++ct) dmma884(acc[ct][0], acc[ct][1], af, sW[buf][ct * 8 + gid][kk * 4 + tig]);
+    }
+    __syncthreads();
+  }
+  // epilogue: thread holds T[i][col], i = 8 warp + gid, col = 8 ct + 2 tig + h
+  const int i = warp * 8 + gid;
+  double part[8];
+#pragma unroll
+  for (int ct = 0; ct < 8; ++ct) {
+    const int ql = 2 * ct + (tig >> 1);
+    const int q = q0 + ql;
+    double v = 0.0;
+    if (i < N && q < nq) {
+      const double* h = H + ((int64_t)q * N + i) * 4;
+      const int c0 = 2 * (tig & 1);
+      v = h[c0] * acc[ct][0] + h[c0 + 1] * acc[ct][1];
+    }
+    // reduce over gid (rows) and tig&1 (c pairs): lanes sharing tig>>1
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    part[ct] = v;
+  }
+  if (gid == 0 && (tig & 1) == 0)
+#pragma unroll
+    for (int ct = 0; ct < 8; ++ct) red[warp][2 * ct + (tig >> 1)] = part[ct];
+  __syncthreads();
+  if (tid < kSQ) {
+    const int q = q0 + tid;
+    double best = 0.0;
+    int bi = -1;
+    if (q < nq && !unavailable[q] && cn[q] != 0.0) {
+      double corr = 0.0;
+      for (int w = 0; w < 7; ++w) corr += red[w][tid];
+      corr += r_vol;
+      const double sc = corr / cn[q];
+      if (sc > 0.0) {
+        best = sc;
+        bi = q;
+      }
+    }
+    // CTA argmax: larger score wins, ties -> smaller index
+    for (int o = 8; o > 0; o >>= 1) {
+      const double ob = __shfl_down_sync(0x0000ffffu, best, o, 16);
+      const int oi = __shfl_down_sync(0x0000ffffu, bi, o, 16);
+      if (oi >= 0 && (bi < 0 || ob > best || (ob == best && oi < bi))) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (tid == 0) {
+      cta_best[blockIdx.x] = best;
+      cta_idx[blockIdx.x] = bi;
+    }
+  }
+}
+
+__global__ void k_ecm_argmax(int n, const double* best, const int* idx, double* out_b, int* out_i) {
+  __shared__ double sb[1024];
+  __shared__ int si[1024];
+  double b = 0.0;
+  int i = -1;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const int oi = idx[k];
+    const double ob = best[k];
+    if (oi >= 0 && (i < 0 || ob > b || (ob == b && oi < i))) {
+      b = ob;
+      i = oi;
+    }
+  }
+  sb[threadIdx.x] = b;
+  si[threadIdx.x] = i;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double ob = sb[threadIdx.x + o];
+      const int oi = si[threadIdx.x + o];
+      if (oi >= 0 && (si[threadIdx.x] < 0 || ob > sb[threadIdx.x] || (ob == sb[threadIdx.x] && oi < si[threadIdx.x]))) {
+        sb[threadIdx.x] = ob;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *out_b = sb[0];
+    *out_i = si[0];
+  }
+}
+
+// column q of J: m = N L (+1) entries
+__global__ void k_ecm_column(int64_t L, int nq, int N, int q, const double* H, const double* W, int vol,
+                             double* col) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t m = (int64_t)N * L;
+  if (t < m) {
+    const int i = (int)(t / L);
+    const int64_t s = t - (int64_t)i * L;
+    const double* h = H + ((int64_t)q * N + i) * 4;
+    const double* w = W + (s * nq + q) * 4;
+    col[t] = h[0] * w[0] + h[1] * w[1] + h[2] * w[2] + h[3] * w[3];
+  } else if (vol && t == m) {
+    col[t] = 1.0;
+  }
+}
+
+// out[j] = sum_r A[j*m + r] * v[r] for j < k (one CTA per j, fixed-tree sum)
+__global__ void __launch_bounds__(256) k_dots(int64_t m, int k, const double* A, const double* v, double* out) {
+  __shared__ double red[256];
+  const int j = blockIdx.x;
+  if (j >= k) return;
+  double p = 0.0;
+  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) p = fma(A[(int64_t)j * m + r], v[r], p);
+  red[threadIdx.x] = p;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[j] = red[0];
+}
+
+// v -= sum_j A[:,j] h[j]  (j < k)
+__global__ void k_axpy_cols(int64_t m, int k, const double* A, const double* h, double* v) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  double s = v[r];
+  for (int j = 0; j < k; ++j) s = fma(-A[(int64_t)j * m + r], h[j], s);
+  v[r] = s;
+}
+
+// out = b - sum_j A[:,j] x[j]; also per-CTA sum of squares and max |.|
+__global__ void __launch_bounds__(256) k_resid(int64_t m, int k, const double* A, const double* x,
+                                               const double* b, double* out, double* part_ss,
+                                               double* part_max) {
+  __shared__ double s1[256], s2[256];
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double v = 0.0;
+  if (r < m) {
+    v = b[r];
+    for (int j = 0; j < k; ++j) v = v - x[j] * A[(int64_t)j * m + r];
+    out[r] = v;
+  }
+  s1[threadIdx.x] = v * v;
+  s2[threadIdx.x] = fabs(v);
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      s1[threadIdx.x] += s1[threadIdx.x + o];
+      s2[threadIdx.x] = fmax(s2[threadIdx.x], s2[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part_ss[blockIdx.x] = s1[0];
+    part_max[blockIdx.x] = s2[0];
+  }
+}
+
+__global__ void k_scale(int64_t m, double* v, double inv_div, double div) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < m) v[r] = v[r] / div;
+  (void)inv_div;
+}
+
+struct Ecm {
+  podecm_ctx* ctx;
+  cudaStream_t s;
+  int64_t m;
+  int kmax;
+  double *Jsel, *Q, *tmp, *h;
+  std::vector<double> R;    // host upper-triangular, column-major kmax x kmax
+  std::vector<double> qtb;  // Q^T rhs
+  const double* rhs;
+  int k = 0;
+
+  double dot_host(const double* a, const double* b) {  // a . b  (device vectors)
+    k_dots<<<1, 256, 0, s>>>(m, 1, a, b, h);
+    double out;
+    cudaMemcpyAsync(&out, h, sizeof(double), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    return out;
+  }
+
+  // append column Jsel[:, k] to the QR (CGS2)
+  void append() {
+    double* v = tmp;
+    cudaMemcpyAsync(v, Jsel + (int64_t)k * m, sizeof(double) * m, cudaMemcpyDeviceToDevice, s);
+    std::vector<double> hh(k + 1, 0.0);
+    for (int pass = 0; pass < 2 && k > 0; ++pass) {
+      k_dots<<<k, 256, 0, s>>>(m, k, Q, v, h);
+      std::vector<double> hp(k);
+      cudaMemcpyAsync(hp.data(), h, sizeof(double) * k, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      k_axpy_cols<<<grid_for(m, 256), 256, 0, s>>>(m, k, Q, h, v);
+      for (int j = 0; j < k; ++j) hh[j] += hp[j];
+    }
+    const double nrm = sqrt(dot_host(v, v));
+    hh[k] = nrm;
+    k_scale<<<grid_for(m, 256), 256, 0, s>>>(m, v, 0.0, nrm);
+    cudaMemcpyAsync(Q + (int64_t)k * m, v, sizeof(double) * m, cudaMemcpyDeviceToDevice, s);
+    for (int j = 0; j <= k; ++j) R[(size_t)k * kmax + j] = hh[j];
+    qtb[k] = dot_host(Q + (int64_t)k * m, rhs);
+    ctx->launches += 6;
+    ++k;
+  }
+
+  std::vector<double> solve() const {  // R z = Q^T b
+    std::vector<double> z(k);
+    for (int i = k - 1; i >= 0; --i) {
+      double s0 = qtb[i];
+      for (int j = i + 1; j < k; ++j) s0 -= R[(size_t)j * kmax + i] * z[j];
+      z[i] = s0 / R[(size_t)i * kmax + i];
+    }
+    return z;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int podecm_ecm_mode_grads(podecm_ctx* ctx, void* stream, podecm_rve* rve, const double* modes,
+                          int N, double* H) {
+  if (!ctx || !rve || !modes || !H || N <= 0) return PODECM_ECONFIG;
+  auto s = static_cast<cudaStream_t>(stream);
+  const int64_t n = (int64_t)rve->n_qp * N;
+  k_ecm_mode_grads<<<grid_for(n, 256), 256, 0, s>>>(rve->n_qp, N, 2 * (int64_t)rve->n_nodes,
+                                                    rve->d_elems, rve->d_grad, modes, H);
+  PODECM_LAUNCHED(ctx, 1);
+  return PODECM_OK;
+}
+
+int podecm_ecm_stress_snapshots(podecm_ctx* ctx, void* stream, podecm_rve* rve, const double* U,
+                                int64_t L, double* W, int32_t* status) {
+  if (!ctx || !rve || !U || !W || L <= 0) return PODECM_ECONFIG;
+  auto s = static_cast<cudaStream_t>(stream);
+  if (status) PODECM_CUDA_TRY(ctx, cudaMemsetAsync(status, 0, sizeof(int32_t), s));
+  const int64_t n = L * rve->n_qp;
+  {
+    KTimer kt(ctx, s, "k_ecm_stress");
+    k_ecm_stress<<<grid_for(n, 128), 128, 0, s>>>(L, rve->n_qp, 2 * (int64_t)rve->n_nodes,
+                                                  rve->d_elems, rve->d_regions, rve->d_grad, U,
+                                                  rve->mats, W, status, ctx->d_fail);
+  }
+  PODECM_LAUNCHED(ctx, 1);
+  return PODECM_OK;
+}
+
+int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const double* H, int N,
+                      const double* W, int64_t L, const podecm_ecm_opts* opts, int32_t* ids,
+                      double* weights, int* n_sel, double* resid_rel, int* iterations) {
+  if (!ctx || !rve || !H || !W || !opts || !ids || !weights || !n_sel) return PODECM_ECONFIG;
+  if (N < 1 || N > 56) return set_err(ctx, PODECM_ECONFIG, "ecm: need 1 <= N <= 56 displacement modes");
+  auto s = static_cast<cudaStream_t>(stream);
+  const int nq = rve->n_qp;
+  const int vol = opts->volume_row ? 1 : 0;
+  const int64_t m = (int64_t)N * L + vol;
+  const int cap = opts->max_points > 0 ? std::min(opts->max_points, nq) : nq;
+  int rc = PODECM_OK;
+  auto fail = [&](int code, const char* msg) { return set_err(ctx, code, msg); };
+
+  double *Hw = nullptr, *rhs = nullptr, *r = nullptr, *cn = nullptr, *cta_b = nullptr, *best_b = nullptr;
+  double *Jsel = nullptr, *Q = nullptr, *tmp = nullptr, *hbuf = nullptr, *xdev = nullptr, *pss = nullptr, *pmx = nullptr;
+  int *cta_i = nullptr, *best_i = nullptr;
+  uint8_t* unav = nullptr;
+  const int n_cta = (nq + kSQ - 1) / kSQ;
+  const int n_rb = grid_for(m, 256);
+  auto alloc = [&](auto** p, size_t n) {
+    if (!rc && cudaMalloc(p, std::max<size_t>(n, 1) * sizeof(**p)) != cudaSuccess)
+      rc = fail(PODECM_ECUDA, "ecm: device allocation failed");
+  };
+  alloc(&Hw, (size_t)N * 4 * nq);
+  alloc(&rhs, m);
+  alloc(&r, m);
+  alloc(&cn, nq);
+  alloc(&cta_b, n_cta);
+  alloc(&cta_i, n_cta);
+  alloc(&best_b, 1);
+  alloc(&best_i, 1);
+  alloc(&Jsel, (size_t)m * cap);
+  alloc(&Q, (size_t)m * cap);
+  alloc(&tmp, m);
+  alloc(&hbuf, std::max(cap, 1));
+  alloc(&xdev, std::max(cap, 1));
+  alloc(&pss, n_rb);
+  alloc(&pmx, n_rb);
+  alloc(&unav, nq);
+  std::vector<int> selected;
+  std::vector<double> x;
+  double rhs_norm = 0.0, rnorm = 0.0;
+  int iters = 0;
+  if (!rc) {
+    cudaMemsetAsync(unav, 0, nq, s);
+    // rhs = J w: Hw[i][(q,c)] = w_q H[q][i][c]; rhs[(i,s)] = sum_k Hw[i][k] W[s][k]
+    std::vector<double> hH((size_t)nq * N * 4), hHw((size_t)N * 4 * nq);
+    cudaMemcpyAsync(hH.data(), H, sizeof(double) * hH.size(), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    for (int q = 0; q < nq; ++q)
+      for (int i = 0; i < N; ++i)
+        for (int c = 0; c < 4; ++c)
+          hHw[(size_t)i * 4 * nq + (size_t)q * 4 + c] = rve->w[q] * hH[((size_t)q * N + i) * 4 + c];
+    cudaMemcpyAsync(Hw, hHw.data(), sizeof(double) * hHw.size(), cudaMemcpyHostToDevice, s);
+    GemmArgs a{};
+    a.M = N;
+    a.N = L;
+    a.K = 4 * (int64_t)nq;
+    a.A = Hw;
+    a.a_rs = 4 * (int64_t)nq;
+    a.a_cs = 1;
+    a.B = W;
+    a.b_rs = 1;
+    a.b_cs = 4 * (int64_t)nq;
+    a.C = rhs;
+    a.c_rs = L;  // rhs[i * L + s]
+    a.c_cs = 1;
+    dim3 grid((unsigned)((a.N + kGBN - 1) / kGBN), (unsigned)((a.M + kGBM - 1) / kGBM));
+    k_gemm_dmma<<<grid, 128, 0, s>>>(a);
+    if (vol) {
+      double wsum = 0.0;
+      for (int q = 0; q < nq; ++q) wsum += rve->w[q];
+      cudaMemcpyAsync(rhs + m - 1, &wsum, sizeof(double), cudaMemcpyHostToDevice, s);
+    }
+    k_ecm_colnorm<<<grid_for(nq, 128), 128, 0, s>>>(L, nq, N, H, W, vol, cn);
+    cudaMemcpyAsync(r, rhs, sizeof(double) * m, cudaMemcpyDeviceToDevice, s);
+    ctx->launches += 2;
+    std::vector<double> hr(m);
+    cudaMemcpyAsync(hr.data(), rhs, sizeof(double) * m, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double ss = 0.0;
+    for (double v : hr) ss += v * v;
+    rhs_norm = std::sqrt(ss);
+    rnorm = rhs_norm;
+  }
+  const double row_tol = opts->eps * rhs_norm / std::sqrt((double)m);
+  double rmax = rhs_norm;  // max |r| of the initial residual computed below
+  if (!rc) {
+    std::vector<double> hr(m);
+    cudaMemcpyAsync(hr.data(), r, sizeof(double) * m, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    rmax = 0.0;
+    for (double v : hr) rmax = std::max(rmax, std::fabs(v));
+  }
+  Ecm qr{ctx, s, m, cap, Jsel, Q, tmp, hbuf, std::vector<double>((size_t)cap * cap, 0.0),
+         std::vector<double>(cap, 0.0), rhs, 0};
+  auto converged = [&]() {
+    if (rhs_norm == 0.0) return true;
+    return rnorm <= opts->eps * rhs_norm && rmax <= row_tol;
+  };
+  bool stopped_at_count = false;
+  while (!rc && !converged()) {
+    if ((int)selected.size() >= cap) {
+      if (opts->stop_at_count) {
+        stopped_at_count = true;
+        break;
+      }
+      rc = fail(PODECM_ESOLVE, "cubature did not reach the requested accuracy within the point budget");
+      break;
+    }
+    // corr = J^T r ; argmax of corr / ||J_q|| over available columns
+    double r_vol = 0.0;
+    if (vol) cudaMemcpyAsync(&r_vol, r + m - 1, sizeof(double), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    {
+      KTimer kt(ctx, s, "k_ecm_score");
+      k_ecm_score<<<n_cta, 224, 0, s>>>(L, nq, N, r, r_vol, H, W, cn, unav, cta_b, cta_i);
+    }
+    k_ecm_argmax<<<1, 1024, 0, s>>>(n_cta, cta_b, cta_i, best_b, best_i);
+    ctx->launches += 2;
+    int best = -1;
+    cudaMemcpyAsync(&best, best_i, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    if (best < 0) {
+      rc = fail(PODECM_ESOLVE, "cubature stalled: no remaining point improves the residual");
+      break;
+    }
+    selected.push_back(best);
+    const uint8_t one = 1;
+    cudaMemcpyAsync(unav + best, &one, 1, cudaMemcpyHostToDevice, s);
+    x.push_back(0.0);
+    // materialise the new column and extend the QR
+    k_ecm_column<<<grid_for(m, 256), 256, 0, s>>>(L, nq, N, best, H, W, vol, Jsel + (int64_t)qr.k * m);
+    ctx->launches += 1;
+    qr.append();
+    // restore_feasible (ecm.cpp:56-90)
+    while (!selected.empty()) {
+      std::vector<double> z = qr.solve();
+      double zmin = 1e300;
+      for (double v : z) zmin = std::min(zmin, v);
+      if (zmin > 0.0) {
+        x = z;
+        break;
+      }
+      double alpha = 1.0;
+      for (size_t k = 0; k < z.size(); ++k)
+        if (z[k] <= 0.0) alpha = std::min(alpha, x[k] / (x[k] - z[k]));
+      double xmax = 0.0;
+      for (size_t k = 0; k < x.size(); ++k) {
+        x[k] += alpha * (z[k] - x[k]);
+        xmax = std::max(xmax, std::fabs(x[k]));
+      }
+      const double zero_tol = 1e-12 * std::max(xmax, 1e-30);
+      std::vector<int> keep_ids;
+      std::vector<double> keep_x;
+      std::vector<int> keep_pos;
+      for (size_t k = 0; k < x.size(); ++k)
+        if (x[k] > zero_tol) {
+          keep_ids.push_back(selected[k]);
+          keep_x.push_back(x[k]);
+          keep_pos.push_back((int)k);
+        }
+      // compact Jsel columns and rebuild the QR of the kept set
+      for (size_t k = 0; k < keep_pos.size(); ++k)
+        if (keep_pos[k] != (int)k)
+          cudaMemcpyAsync(Jsel + (int64_t)k * m, Jsel + (int64_t)keep_pos[k] * m, sizeof(double) * m,
+                          cudaMemcpyDeviceToDevice, s);
+      selected = keep_ids;
+      x = keep_x;
+      qr.k = 0;
+      std::fill(qr.R.begin(), qr.R.end(), 0.0);
+      for (size_t k = 0; k < selected.size(); ++k) qr.append();
+    }
+    ++iters;
+    // resid = rhs - J_sel x
+    cudaMemcpyAsync(xdev, x.data(), sizeof(double) * x.size(), cudaMemcpyHostToDevice, s);
+    k_resid<<<n_rb, 256, 0, s>>>(m, (int)x.size(), Jsel, xdev, rhs, r, pss, pmx);
+    ctx->launches += 1;
+    std::vector<double> hs(n_rb), hm(n_rb);
+    cudaMemcpyAsync(hs.data(), pss, sizeof(double) * n_rb, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(hm.data(), pmx, sizeof(double) * n_rb, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    double ss = 0.0;
+    rmax = 0.0;
+    for (int b = 0; b < n_rb; ++b) {
+      ss += hs[b];
+      rmax = std::max(rmax, hm[b]);
+    }
+    rnorm = std::sqrt(ss);
+  }
+  (void)stopped_at_count;
+  if (!rc) {
+    std::vector<int> order(selected.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](int p, int q) { return selected[p] < selected[q]; });
+    for (size_t k = 0; k < order.size(); ++k) {
+      ids[k] = selected[order[k]];
+      weights[k] = x[order[k]];
+    }
+    *n_sel = (int)selected.size();
+    if (resid_rel) *resid_rel = rhs_norm == 0.0 ? 0.0 : rnorm / rhs_norm;
+    if (iterations) *iterations = iters;
+  }
+  cudaFree(Hw);
+  cudaFree(rhs);
+  cudaFree(r);
+  cudaFree(cn);
+  cudaFree(cta_b);
+  cudaFree(cta_i);
+  cudaFree(best_b);
+  cudaFree(best_i);
+  cudaFree(Jsel);
+  cudaFree(Q);
+  cudaFree(tmp);
+  cudaFree(hbuf);
+  cudaFree(xdev);
+  cudaFree(pss);
+  cudaFree(pmx);
+  cudaFree(unav);
+  return rc;
+}
+
+}  // extern "C"

@@ -144,3 +144,51 @@ def rom_instances(n_inst: int, K: int = 20, seed: int = 2030, hm: float = 0.2):
     k = (np.arange(1, K + 1) / K)[None, :, None]
     sched = IDENT[None, None, :] + k * H[:, None, :]
     return np.ascontiguousarray(geom), np.ascontiguousarray(sched)
+
+
+def c4_snapshots(tables: dict, L: int = 4000, n_terms: int = 20, kmax: int = 8, seed: int = 2030,
+                 target_rms: float = 0.05, xp=np, device=None):
+    """Config 4 snapshots: L periodic displacement fields at the mesh nodes,
+    u_comp(X) = sum_m A_m cos(2 pi k_m . X + phi_m) per component, integer
+    wave vectors with 1 <= |k|_inf <= kmax, A ~ N(0, 1/|k|_2^2).  The literal
+    amplitudes give RMS |grad u| = 2 pi sqrt(n_terms) (~28 for 20 terms,
+    SURVEY §8d), so one global scale pins RMS |grad u| = target_rms.  The
+    anchor node's value is subtracted (fluctuation convention: anchor dof
+    pinned, mesh.cpp:370).  Returns U column-major [2 n_nodes, L] (numpy or,
+    with xp=torch, a device tensor of shape [L, 2 n_nodes] whose transpose is
+    the column-major matrix)."""
+    rng = np.random.default_rng(seed)
+    X = tables["nodes"]
+    n_nodes = X.shape[0]
+    anchor = int(np.nonzero((np.abs(X[:, 0]) < 1e-12) & (np.abs(X[:, 1]) < 1e-12))[0][0])
+    k = rng.integers(-kmax, kmax + 1, size=(L, 2, n_terms, 2))
+    zero = (k[..., 0] == 0) & (k[..., 1] == 0)
+    while zero.any():
+        k[zero] = rng.integers(-kmax, kmax + 1, size=(int(zero.sum()), 2))
+        zero = (k[..., 0] == 0) & (k[..., 1] == 0)
+    kn = np.sqrt((k.astype(np.float64) ** 2).sum(-1))
+    amp = rng.standard_normal((L, 2, n_terms)) / kn
+    phi = rng.uniform(0.0, 2 * np.pi, (L, 2, n_terms))
+    scale = target_rms / (2 * np.pi * np.sqrt(n_terms))
+    if xp is np:
+        U = np.zeros((L, n_nodes, 2))
+        for m in range(n_terms):
+            arg = 2 * np.pi * (k[:, :, m, 0, None] * X[None, None, :, 0] +
+                               k[:, :, m, 1, None] * X[None, None, :, 1]) + phi[:, :, m, None]
+            U += np.transpose(amp[:, :, m, None] * np.cos(arg), (0, 2, 1))
+        U -= U[:, anchor:anchor + 1, :]
+        U *= scale
+        return np.asfortranarray(U.reshape(L, 2 * n_nodes).T)
+    torch = xp
+    Xt = torch.from_numpy(X).to(device)
+    kt = torch.from_numpy(k.astype(np.float64)).to(device)
+    at = torch.from_numpy(amp).to(device)
+    pt = torch.from_numpy(phi).to(device)
+    U = torch.zeros((L, n_nodes, 2), dtype=torch.float64, device=device)
+    for m in range(n_terms):
+        arg = 2 * np.pi * (kt[:, :, m, 0, None] * Xt[None, None, :, 0] +
+                           kt[:, :, m, 1, None] * Xt[None, None, :, 1]) + pt[:, :, m, None]
+        U += (at[:, :, m, None] * torch.cos(arg)).permute(0, 2, 1)
+    U -= U[:, anchor:anchor + 1, :].clone()
+    U *= scale
+    return U.reshape(L, 2 * n_nodes).contiguous()
