@@ -79,3 +79,28 @@ def test_bisection_exhausted_is_solveerror(setup):
                                               max_bisect=1))
     assert np.all(ro["status"] == 3)
     assert np.array_equal(rg["status"], ro["status"])
+
+
+def test_exact_limit_gpu_equals_full_order(orc):
+    """test_rom.cpp:44-125 on the GPU: full periodic basis (N = n_red = 30)
+    and full quadrature on a 4x4 cell => the batched ROM reproduces the
+    full-order response (oracle FE Newton) to 1e-8."""
+    import torch
+    from paper_2307_16894_b200 import api
+    from tests.test_oracle_rve import exact_limit_model, fe_newton_pbar
+    o = orc.Rve(4, _mats())
+    t = o.export()
+    ids, wts, mg = exact_limit_model(o, t)
+    g = api.Rve(4, _mats())
+    rom = api.Rom(g, ids, wts, mg)
+    geom = (0.3, 0.2)
+    H = np.array([0.06, 0.02, -0.03, -0.04])
+    sched = np.array([[1, 0, 0, 1] + (k / 6) * H for k in range(1, 7)])
+    fe = fe_newton_pbar(o, t, geom, sched)
+    r = rom.solve(torch.tensor([geom], dtype=torch.float64).cuda(),
+                  torch.from_numpy(sched[None].copy()).cuda(), api.NewtonOpts(eps_rel=1e-10))
+    torch.cuda.synchronize()
+    assert int(r["status"][0]) == 0
+    err = np.abs(r["pbar"][0].cpu().numpy() - fe).max() / np.abs(fe).max()
+    print(f"exact limit: GPU ROM vs FE max rel {err:.2e}")
+    assert err <= 1e-8
