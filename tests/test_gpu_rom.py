@@ -87,7 +87,7 @@ def test_exact_limit_gpu_equals_full_order(orc):
     full-order response (oracle FE Newton) to 1e-8."""
     import torch
     from paper_2307_16894_b200 import api
-    from tests.test_oracle_rve import exact_limit_model, fe_newton_pbar
+    from oracle.fe import exact_limit_model, fe_newton_pbar
     o = orc.Rve(4, _mats())
     t = o.export()
     ids, wts, mg = exact_limit_model(o, t)
