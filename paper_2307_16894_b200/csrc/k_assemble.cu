@@ -14,6 +14,7 @@
 // Per chunk the scratch holds 72 doubles per qp; chunk size is chosen so it
 // fits comfortably in the 126 MB L2.
 #include <algorithm>
+#include <cstdlib>
 
 #include "rve.cuh"
 
@@ -41,16 +42,50 @@ struct AsmArgs {
   const double* st0;
   double* st1;
   double* p_field;
-  double* scratch;  // [chunk inst][n_elems][72][4]
+  double* scratch;  // exact: [chunk inst][n_elems][72][4]; fused: [chunk inst][n_groups]
+  const int32_t* pos;
+  int64_t n_groups;
   int32_t* status;
   unsigned int* fail;
   bool tangent;
 };
 
-__global__ void __launch_bounds__(128, 5) k_asm_qp(AsmArgs g, MatTable tab) {
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// 4-lane butterfly over the quad of lanes holding the 4 qps of one element:
+// every lane ends with 2 of the 8 element sums, (t0 + t1) + (t2 + t3) for
+// every entry whichever lane computes it (deterministic).  Lane k holds the
+// entries u = 4 (k & 1) + 2 ((k >> 1) & 1) + {0, 1}.
+__device__ __forceinline__ void quad_reduce8(const double v[8], int k, double out[2]) {
+  const bool h1 = (k & 1) != 0, h2 = (k & 2) != 0;
+  double w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double mine = h1 ? v[i + 4] : v[i];
+    const double other = h1 ? v[i] : v[i + 4];
+    w[i] = mine + __shfl_xor_sync(0xffffffffu, other, 1);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double mine = h2 ? w[i + 2] : w[i];
+    const double other = h2 ? w[i] : w[i + 2];
+    out[i] = mine + __shfl_xor_sync(0xffffffffu, other, 2);
+  }
+}
+
+// FUSED = true (default): per-element sums of the 4 qp contributions are
+// formed in registers (quad butterfly) and the gather adds element sums in
+// element order: K and f are deterministic and differ from the reference's
+// strict triplet order only in the association inside one element (ulp
+// level).  FUSED = false (PODECM_ASM_EXACT=1): every per-qp term is stored and
+// the gather replays Eigen's setFromTriplets order exactly.
+template <bool FUSED, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_asm_qp(AsmArgs g, MatTable tab) {
+  const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)g.n_inst * g.n_qp;
-  if (tid >= total) return;
+  const bool valid = tid0 < total;
+  if (!FUSED && !valid) return;
+  // FUSED: lanes past the end (whole quads, n_qp % 4 == 0) compute on a clamped
+  // index so the quad shuffles stay converged, and never store.
+  const int64_t tid = valid ? tid0 : total - 1;
   const int c = (int)(tid / g.n_qp);
   const int q = (int)(tid - (int64_t)c * g.n_qp);
   const int64_t inst = g.inst0 + c;
@@ -120,14 +155,14 @@ __global__ void __launch_bounds__(128, 5) k_asm_qp(AsmArgs g, MatTable tab) {
   double P[4];
   FullOut fo;
   bool ok = lsu_eval<true>(p, z, F, P, &fo);
-  if (g.st1) {
+  if (g.st1 && valid) {
     double* s1 = g.st1 + (size_t)inst * 6 * nq;
 #pragma unroll
     for (int t = 0; t < 4; ++t) s1[(size_t)t * nq + q] = fo.fp[t];
     s1[(size_t)4 * nq + q] = fo.fpzz;
     s1[(size_t)5 * nq + q] = fo.xi;
   }
-  if (g.p_field) {
+  if (g.p_field && valid) {
     double* pf = g.p_field + (size_t)inst * 4 * nq;
 #pragma unroll
     for (int t = 0; t < 4; ++t) pf[(size_t)t * nq + q] = P[t];
@@ -140,41 +175,95 @@ __global__ void __launch_bounds__(128, 5) k_asm_qp(AsmArgs g, MatTable tab) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) gt[a][j] = gq[2 * a] * fmi[2 * j] + gq[2 * a + 1] * fmi[1 + 2 * j];
 
-  // element-blocked scratch: [c][e][72][4], entry (term, k)
-  double* sc = g.scratch + ((size_t)c * (nq >> 2) + e) * 72 * 4 + k;
+  if (!FUSED) {
+    // element-blocked scratch: [c][e][72][4], entry (term, k)
+    double* sc = g.scratch + ((size_t)c * (nq >> 2) + e) * 72 * 4 + k;
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
-      sc[(64 + a * 2 + i) * 4] = wq * (P[i] * gt[a][0] + P[i + 2] * gt[a][1]);
-  if (ok && g.tangent) {
-    // A(i,c,j,d) = A[(i+2c) + 4(j+2d)]: column e = j + 2d.  Columns arrive in
-    // the order 0, 2, 1, 3, so after the second column of each j the 32 terms
-    // K(a i, b j) += wq * sum_cd gt_ac A(i,c,j,d) gt_bd are emitted
-    // (microfem.cpp:113-117 order).
-    double cd[2][4];
-    auto sink = [&](int ecol, const double col[4]) {
-      const int d = ecol >> 1, j = ecol & 1;
+      for (int i = 0; i < 2; ++i)
+        sc[(64 + a * 2 + i) * 4] = wq * (P[i] * gt[a][0] + P[i + 2] * gt[a][1]);
+    if (ok && g.tangent) {
+      // A(i,c,j,d) = A[(i+2c) + 4(j+2d)]: column e = j + 2d.  Columns arrive
+      // in the order 0, 2, 1, 3, so after the second column of each j the 32
+      // terms K(a i, b j) += wq * sum_cd gt_ac A(i,c,j,d) gt_bd are emitted
+      // (microfem.cpp:113-117 order).
+      double cd[2][4];
+      auto sink = [&](int ecol, const double col[4]) {
+        const int d = ecol >> 1, j = ecol & 1;
 #pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        cd[0][r] = d == 0 ? col[r] : cd[0][r];
-        cd[1][r] = d == 1 ? col[r] : cd[1][r];
-      }
-      if (d == 0) return;
+        for (int r = 0; r < 4; ++r) {
+          cd[0][r] = d == 0 ? col[r] : cd[0][r];
+          cd[1][r] = d == 1 ? col[r] : cd[1][r];
+        }
+        if (d == 0) return;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const double v = gt[a][0] * (cd[0][i] * gt[b][0] + cd[1][i] * gt[b][1]) +
+                               gt[a][1] * (cd[0][i + 2] * gt[b][0] + cd[1][i + 2] * gt[b][1]);
+              sc[((a * 4 + b) * 4 + i * 2 + j) * 4] = wq * v;
+            }
+      };
+      ok = fd_tangent<false>(p, z, F, 1e-7, sink);
+    }
+  } else {
+    // element sums go to their slot-ordered position: [c][n_groups]
+    double* sc = g.scratch + (size_t)c * g.n_groups;
+    const int32_t* ps = g.pos + (size_t)e * 72;
+    {
+      double v[8], o[2];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
+        for (int i = 0; i < 2; ++i) v[a * 2 + i] = wq * (P[i] * gt[a][0] + P[i + 2] * gt[a][1]);
+      quad_reduce8(v, k, o);
+      const int u0 = 4 * (k & 1) + 2 * ((k >> 1) & 1);
+      if (valid) {
+        const int p0 = __ldg(ps + 64 + u0), p1 = __ldg(ps + 64 + u0 + 1);
+        if (p0 >= 0) sc[p0] = o[0];
+        if (p1 >= 0) sc[p1] = o[1];
+      }
+    }
+    if (g.tangent) {
+      double cd[2][4];
+      auto sink = [&](int ecol, const double col[4]) {
+        const int d = ecol >> 1, j = ecol & 1;
 #pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const double v = gt[a][0] * (cd[0][i] * gt[b][0] + cd[1][i] * gt[b][1]) +
-                             gt[a][1] * (cd[0][i + 2] * gt[b][0] + cd[1][i + 2] * gt[b][1]);
-            sc[((a * 4 + b) * 4 + i * 2 + j) * 4] = wq * v;
+        for (int r = 0; r < 4; ++r) {
+          cd[0][r] = d == 0 ? col[r] : cd[0][r];
+          cd[1][r] = d == 1 ? col[r] : cd[1][r];
+        }
+        if (d == 0) return;
+        const int u0 = 4 * (k & 1) + 2 * ((k >> 1) & 1);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          double v[8], o[2];
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              v[b * 2 + i] = wq * (gt[a][0] * (cd[0][i] * gt[b][0] + cd[1][i] * gt[b][1]) +
+                                   gt[a][1] * (cd[0][i + 2] * gt[b][0] + cd[1][i + 2] * gt[b][1]));
+          quad_reduce8(v, k, o);
+          if (valid) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int u = u0 + h, b = u >> 1, i = u & 1;
+              const int pp = __ldg(ps + a * 16 + b * 4 + i * 2 + j);
+              if (pp >= 0) sc[pp] = o[h];
+            }
           }
-    };
-    ok = fd_tangent<false>(p, z, F, 1e-7, sink);
+        }
+      };
+      const bool ok2 = fd_tangent<false>(p, z, F, 1e-7, sink);  // all quad lanes run it
+      ok = ok && ok2;
+    }
   }
-  if (!ok) {
+  if (!ok && valid) {
     if (g.status) g.status[inst] = PODECM_ESOLVE;
     atomicAdd(g.fail, 1u);
   }
@@ -196,13 +285,14 @@ struct GatherArgs {
 
 // One thread per (instance, item): items [0, nnz) are CSR slots (if kvals),
 // items [nnz, nnz + n_red) residual rows.
+template <bool FUSED>
 __global__ void __launch_bounds__(256) k_asm_gather(GatherArgs g) {
   const int64_t n_items = (g.kvals ? g.nnz : 0) + g.n_red;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= n_items * g.n_inst) return;
   const int c = (int)(tid / n_items);
   const int64_t it = tid - (int64_t)c * n_items;
-  const double* sc = g.scratch + (size_t)c * g.n_elems * 72 * 4;
+  const double* sc = g.scratch + (size_t)c * g.n_elems * 72 * (FUSED ? 1 : 4);
   const int64_t inst = g.inst0 + c;
   if (g.kvals && it < g.nnz) {
     const int b0 = __ldg(g.slot_gptr + it), b1 = __ldg(g.slot_gptr + it + 1);
@@ -210,6 +300,11 @@ __global__ void __launch_bounds__(256) k_asm_gather(GatherArgs g) {
     for (int m = b0; m < b1; ++m) {
       const int grp = __ldg(g.slot_grp + m);  // e*64 + tl
       const int e = grp >> 6, tl = grp & 63;
+      if (FUSED) {  // element sums, added in element order
+        const double v = sc[(size_t)e * 72 + tl];
+        s = (m == b0) ? v : s + v;
+        continue;
+      }
       const double4 t = *reinterpret_cast<const double4*>(sc + ((size_t)e * 72 + tl) * 4);
       if (m == b0) {
         s = t.x;  // setFromTriplets: first duplicate is copied, the rest added
@@ -228,6 +323,10 @@ __global__ void __launch_bounds__(256) k_asm_gather(GatherArgs g) {
     for (int m = b0; m < b1; ++m) {
       const int grp = __ldg(g.frow_grp + m);  // e*8 + fl
       const int e = grp >> 3, fl = grp & 7;
+      if (FUSED) {
+        s = s + sc[(size_t)e * 72 + 64 + fl];
+        continue;
+      }
       const double4 t = *reinterpret_cast<const double4*>(sc + ((size_t)e * 72 + 64 + fl) * 4);
       s = s + t.x;
       s = s + t.y;
@@ -236,6 +335,32 @@ __global__ void __launch_bounds__(256) k_asm_gather(GatherArgs g) {
     }
     g.f[(size_t)inst * g.n_red + row] = s;
   }
+}
+
+// FUSED gather: the element sums already sit in slot order, so every CSR
+// slot / residual row is a contiguous run scratch[gptr[i] .. gptr[i+1]) summed
+// in element order (first term copied for K, setFromTriplets style; 0 + ...
+// for f).  One thread per (instance, item): a streaming segmented reduction.
+__global__ void __launch_bounds__(256) k_asm_gather_fused(GatherArgs g, const int32_t* __restrict__ gptr,
+                                                          int64_t n_groups) {
+  // grid: x over items (slots then rows), y over the chunk's instances
+  const int n_items = (int)((g.kvals ? g.nnz : 0) + g.n_red);
+  const int it = blockIdx.x * blockDim.x + threadIdx.x;
+  if (it >= n_items) return;
+  const int c = blockIdx.y;
+  const int nnz = g.kvals ? (int)g.nnz : 0;
+  const bool is_slot = it < nnz;
+  const int gi = g.kvals ? it : it + (int)g.nnz;  // index into gptr (slots then rows)
+  const int b0 = __ldg(gptr + gi), b1 = __ldg(gptr + gi + 1);
+  const double* sc = g.scratch + (size_t)c * n_groups;
+  double sm = b1 > b0 ? __ldcs(sc + b0) : 0.0;
+  if (!is_slot) sm = 0.0 + sm;
+  for (int m = b0 + 1; m < b1; ++m) sm = sm + __ldcs(sc + m);
+  const int64_t inst = g.inst0 + c;
+  if (is_slot)
+    g.kvals[(size_t)inst * g.nnz + it] = sm;
+  else
+    g.f[(size_t)inst * g.n_red + (it - nnz)] = sm;
 }
 
 __global__ void k_morph(int64_t n_inst, int nq, double r0, const double* nodes, const int32_t* elems,
@@ -289,7 +414,15 @@ int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t 
   if ((!geom && !morph) || !fbar || !w_red || !st0 || !f)
     return set_err(ctx, PODECM_ECONFIG, "geom|morph, fbar, w_red, st0 and f are required");
   auto s = static_cast<cudaStream_t>(stream);
-  const size_t per_inst = (size_t)r->n_elems * 72 * 4 * sizeof(double);
+  static const bool exact = [] {
+    const char* e = getenv("PODECM_ASM_EXACT");
+    return e && atoi(e) != 0;
+  }();
+  static const int minb = [] {
+    const char* e = getenv("PODECM_ASM_MINB");
+    return e ? atoi(e) : 4;
+  }();
+  const size_t per_inst = (exact ? (size_t)r->n_elems * 72 * 4 : (size_t)r->n_groups) * sizeof(double);
   // chunk: scratch <= ~48 MB (L2-resident), at least one instance
   int64_t chunk = std::max<int64_t>(1, (int64_t)(48ull << 20) / (int64_t)per_inst);
   chunk = std::min<int64_t>(chunk, n_inst);
@@ -323,13 +456,20 @@ int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t 
     a.st1 = st1;
     a.p_field = p_field;
     a.scratch = r->d_scratch;
+    a.pos = r->d_pos;
+    a.n_groups = r->n_groups;
     a.status = status;
     a.fail = ctx->d_fail;
     a.tangent = kvals != nullptr;
     const int64_t nthr = (int64_t)nc * r->n_qp;
     {
       KTimer kt(ctx, s, "k_asm_qp");
-      k_asm_qp<<<grid_for(nthr, 128), 128, 0, s>>>(a, r->mats);
+      if (exact)
+        k_asm_qp<false, 5><<<grid_for(nthr, 128), 128, 0, s>>>(a, r->mats);
+      else if (minb == 4)
+        k_asm_qp<true, 4><<<grid_for(nthr, 128), 128, 0, s>>>(a, r->mats);
+      else
+        k_asm_qp<true, 5><<<grid_for(nthr, 128), 128, 0, s>>>(a, r->mats);
     }
     GatherArgs gg;
     gg.n_red = r->n_red;
@@ -347,7 +487,10 @@ int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t 
     const int64_t nitems = ((kvals ? r->nnz : 0) + r->n_red) * nc;
     {
       KTimer kt(ctx, s, "k_asm_gather");
-      k_asm_gather<<<grid_for(nitems, 256), 256, 0, s>>>(gg);
+      if (exact)
+        k_asm_gather<false><<<grid_for(nitems, 256), 256, 0, s>>>(gg);
+      else
+        k_asm_gather_fused<<<dim3(grid_for(nitems / nc, 256), nc), 256, 0, s>>>(gg, r->d_gptr_all, r->n_groups);
     }
     PODECM_LAUNCHED(ctx, 2);
   }

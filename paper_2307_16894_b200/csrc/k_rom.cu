@@ -26,6 +26,7 @@
 // Summation order of the contractions differs from Eigen's; the stated
 // tolerance for the homogenised stress history is 1e-8 (BASELINE north star).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 #include <vector>
@@ -165,13 +166,22 @@ struct PointArgs {
   RomCtl* ctl;
 };
 
-__global__ void __launch_bounds__(256, 2) k_rom_point(PointArgs g, MatTable tab) {
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_rom_point(PointArgs g, MatTable tab) {
   extern __shared__ double sm[];
   double* sG = sm;                            // [N][4][32]
   double* sa = sm + (size_t)g.N * 4 * kPtsTile;  // [8][N]
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int p0 = blockIdx.x * kPtsTile;
   const int64_t s0 = (int64_t)blockIdx.y * kInstTile;
+  {  // whole CTA idle (finished / failed instances): skip the staging
+    __shared__ int any_active;
+    if (threadIdx.x == 0) any_active = 0;
+    __syncthreads();
+    if (threadIdx.x < kInstTile && s0 + threadIdx.x < g.n && g.ctl[s0 + threadIdx.x].active) any_active = 1;
+    __syncthreads();
+    if (!any_active) return;
+  }
   for (int t = threadIdx.x; t < g.N * 4 * kPtsTile; t += blockDim.x) {
     const int ir = t / kPtsTile, pl = t - ir * kPtsTile;
     sG[t] = (p0 + pl < g.Qpad) ? g.Gt[(size_t)ir * g.Qpad + p0 + pl] : 0.0;
@@ -235,22 +245,32 @@ __global__ void __launch_bounds__(256, 2) k_rom_point(PointArgs g, MatTable tab)
     at[16 + r] = cw * (m[j] * P[i] + m[j + 2] * P[i + 2]);
   }
   if (ok) {
-    TangentRegs A;
-    ok = fd_tangent<false>(pm, z, F, 1e-7, A);
-    // At = c R A R^T: At[r][s] = sum_{l,l'} m(r>>1,l) A[(r&1)+2l][(s&1)+2l'] m(s>>1,l')
-#pragma unroll
-    for (int sc = 0; sc < 4; ++sc)
+    // At = c R A R^T streamed per column pair: columns e = (s&1) + 2l' arrive
+    // in the order 0, 2, 1, 3, so after each pair the four entries of both
+    // output columns s in {e&1, (e&1)+2} are final.  T = R col:
+    // T[r] = sum_l m(r>>1, l) col[(r&1) + 2l].
+    double T0[4];
+    auto sink = [&](int e, const double col[4]) {
+      double Tc[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
-        const int ir = r & 1, jr = r >> 1, is = sc & 1, js = sc >> 1;
-        double acc = 0.0;
-#pragma unroll
-        for (int l = 0; l < 2; ++l)
-#pragma unroll
-          for (int l2 = 0; l2 < 2; ++l2)
-            acc = fma(m[jr + 2 * l] * A.A[(ir + 2 * l) + 4 * (is + 2 * l2)], m[js + 2 * l2], acc);
-        at[r + 4 * sc] = cw * acc;
+        const int i = r & 1, j = r >> 1;
+        Tc[r] = fma(m[j + 2], col[i + 2], m[j] * col[i]);
       }
+      if (e < 2) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) T0[r] = Tc[r];
+        return;
+      }
+      const int sb = e & 1;  // output columns sb and sb + 2
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int sc = sb + 2 * h, js = sc >> 1;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) at[r + 4 * sc] = cw * fma(Tc[r], m[js + 2], T0[r] * m[js]);
+      }
+    };
+    ok = fd_tangent<false>(pm, z, F, 1e-7, sink);
   }
   if (!ok) c->asm_fail = 1;  // SolveError inside rom_assemble -> attempt fails
 }
@@ -272,14 +292,36 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// Software-pipelined over chunks of kPC points: while the warps run the DMMA
+// k-steps of chunk c they also build Y for chunk c+1 (independent SMEM
+// buffers, so the DFMA and DMMA streams interleave) and have the global loads
+// of chunk c+2 in flight in registers.  Two barriers per chunk.
+// SMEM rows are padded to NT*8 + 4 doubles: the m8n8k4 fragment loads
+// (row = k + tig, col = 8 t + gid) then hit 32 distinct bank pairs per
+// half-warp (an unpadded 56-double row gives 2-way conflicts).
+template <int NT>
+__host__ __device__ constexpr int contract_ld() {
+  return NT * 8 + 4;
+}
+template <int NT>
+constexpr size_t contract_smem_bytes() {
+  return sizeof(double) * (2 * (kPC * 4) * contract_ld<NT>() + 2 * kIPC * (kPC * 4) * contract_ld<NT>() +
+                           2 * kIPC * kPC * 20);
+}
+
 template <int NT>
 __global__ void __launch_bounds__(32 * NT * kIPC) k_rom_contract(ContractArgs g) {
   constexpr int NP = NT * 8;
+  constexpr int LDY = contract_ld<NT>();
   constexpr int KR = kPC * 4;  // k-rows per chunk
-  __shared__ double sGm[KR][NP];
-  __shared__ double sY[kIPC][KR][NP];
-  __shared__ double sAt[kIPC][kPC][20];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NTHR = 32 * NT * kIPC;
+  constexpr int GPT = (KR * NP + NTHR - 1) / NTHR;  // Gm doubles per thread per chunk
+  constexpr int APT = (kIPC * kPC * 20 + NTHR - 1) / NTHR;  // At doubles per thread
+  extern __shared__ double smc[];
+  double* sGm = smc;                        // [2][KR][LDY]
+  double* sY = sGm + 2 * KR * LDY;          // [2][kIPC][KR][LDY]
+  double* sAt = sY + 2 * kIPC * KR * LDY;   // [2][kIPC][kPC][20]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int si = warp / NT, trow = warp - si * NT;
   const int64_t sbase = (int64_t)blockIdx.x * kIPC;
   bool any = false;
@@ -290,41 +332,99 @@ __global__ void __launch_bounds__(32 * NT * kIPC) k_rom_contract(ContractArgs g)
   double acc[NT][2];
 #pragma unroll
   for (int ct = 0; ct < NT; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
-  const int nthr = blockDim.x;
-  for (int p0 = 0; p0 < g.Qpad; p0 += kPC) {
-    // stage the shared Gm rows and the instances' per-point operators
-    const double* gsrc = g.G + (size_t)p0 * 4 * NP;
-    for (int t = threadIdx.x; t < KR * NP; t += nthr) (&sGm[0][0])[t] = gsrc[t];
-    for (int t = threadIdx.x; t < kIPC * kPC * 20; t += nthr) {
-      const int q = t / (kPC * 20), rem = t - q * kPC * 20;
-      const int64_t s = sbase + q;
-      (&sAt[0][0][0])[t] = (s < g.n) ? g.At[((size_t)s * g.Qpad + p0) * 20 + rem] : 0.0;
+  const int nch = g.Qpad / kPC;
+  double rG[GPT], rA[APT];
+
+  auto gload = [&](int c) {
+    const double* gsrc = g.G + (size_t)c * kPC * 4 * NP;
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+      const int t = tid + k * NTHR;
+      rG[k] = t < KR * NP ? gsrc[t] : 0.0;
     }
-    __syncthreads();
-    // Y[(p,r)][j] = sum_t At_p[r][t] Gm[(p,t)][j] (j < N); Y[.][N] = Pt; else 0
-    for (int t = threadIdx.x; t < kIPC * KR * NP; t += nthr) {
-      const int q = t / (KR * NP), rem = t - q * KR * NP;
-      const int row = rem / NP, j = rem - row * NP;
-      const int pl = row >> 2, r = row & 3;
-      const double* at = sAt[q][pl];
-      double y;
-      if (j < g.N) {
-        y = at[r] * sGm[pl * 4][j];
-        y = fma(at[r + 4], sGm[pl * 4 + 1][j], y);
-        y = fma(at[r + 8], sGm[pl * 4 + 2][j], y);
-        y = fma(at[r + 12], sGm[pl * 4 + 3][j], y);
-      } else {
-        y = (j == g.N) ? at[16 + r] : 0.0;
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+      const int t = tid + k * NTHR;
+      rA[k] = 0.0;
+      if (t < kIPC * kPC * 20) {
+        const int q = t / (kPC * 20), rem = t - q * kPC * 20;
+        const int64_t sq = sbase + q;
+        if (sq < g.n) rA[k] = g.At[((size_t)sq * g.Qpad + (size_t)c * kPC) * 20 + rem];
       }
-      sY[q][row][j] = y;
     }
-    __syncthreads();
+  };
+  auto gstore = [&](int buf) {
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+      const int t = tid + k * NTHR;
+      if (t < KR * NP) sGm[buf * KR * LDY + (t / NP) * LDY + t % NP] = rG[k];
+    }
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+      const int t = tid + k * NTHR;
+      if (t < kIPC * kPC * 20) sAt[buf * kIPC * kPC * 20 + t] = rA[k];
+    }
+  };
+  // Y[(p,r)][j] = sum_t At_p[r][t] Gm[(p,t)][j] (j < N); Y[.][N] = Pt; else 0.
+  // One thread per (instance, point, column j) builds the 4 rows r of that
+  // point: the 4 Gm values are loaded once and At_p comes as broadcast
+  // 128-bit loads, so Y costs ~2.8x fewer SMEM wavefronts than per element.
+  auto build_y = [&](int buf) {
+    const double* G0 = sGm + buf * KR * LDY;
+    for (int t = tid; t < kIPC * kPC * NP; t += NTHR) {
+      const int q = t / (kPC * NP), rem = t - q * kPC * NP;
+      const int pl = rem / NP, j = rem - pl * NP;
+      const double* at = sAt + (buf * kIPC + q) * kPC * 20 + pl * 20;
+      double* y = sY + (buf * kIPC + q) * KR * LDY + (pl * 4) * LDY + j;
+      if (j < g.N) {
+        const double g0 = G0[(pl * 4) * LDY + j], g1 = G0[(pl * 4 + 1) * LDY + j];
+        const double g2 = G0[(pl * 4 + 2) * LDY + j], g3 = G0[(pl * 4 + 3) * LDY + j];
+        const double4 c0 = *reinterpret_cast<const double4*>(at);       // At[r][0], r = 0..3
+        const double4 c1 = *reinterpret_cast<const double4*>(at + 4);   // At[r][1]
+        const double4 c2 = *reinterpret_cast<const double4*>(at + 8);
+        const double4 c3 = *reinterpret_cast<const double4*>(at + 12);
+        y[0] = fma(c3.x, g3, fma(c2.x, g2, fma(c1.x, g1, c0.x * g0)));
+        y[LDY] = fma(c3.y, g3, fma(c2.y, g2, fma(c1.y, g1, c0.y * g0)));
+        y[2 * LDY] = fma(c3.z, g3, fma(c2.z, g2, fma(c1.z, g1, c0.z * g0)));
+        y[3 * LDY] = fma(c3.w, g3, fma(c2.w, g2, fma(c1.w, g1, c0.w * g0)));
+      } else if (j == g.N) {
+        const double4 pt = *reinterpret_cast<const double4*>(at + 16);
+        y[0] = pt.x;
+        y[LDY] = pt.y;
+        y[2 * LDY] = pt.z;
+        y[3 * LDY] = pt.w;
+      } else {
+        y[0] = y[LDY] = y[2 * LDY] = y[3 * LDY] = 0.0;
+      }
+    }
+  };
+  auto mma = [&](int buf) {
+    const double* G0 = sGm + buf * KR * LDY;
+    const double* Y0 = sY + (buf * kIPC + si) * KR * LDY;
 #pragma unroll
     for (int ks = 0; ks < KR / 4; ++ks) {
-      const double afr = sGm[ks * 4 + tig][trow * 8 + gid];  // (Gm^T)[i][k]
+      const double afr = G0[(ks * 4 + tig) * LDY + trow * 8 + gid];  // (Gm^T)[i][k]
 #pragma unroll
-      for (int ct = 0; ct < NT; ++ct) dmma(acc[ct][0], acc[ct][1], afr, sY[si][ks * 4 + tig][ct * 8 + gid]);
+      for (int ct = 0; ct < NT; ++ct) dmma(acc[ct][0], acc[ct][1], afr, Y0[(ks * 4 + tig) * LDY + ct * 8 + gid]);
     }
+  };
+
+  gload(0);
+  gstore(0);
+  __syncthreads();
+  build_y(0);
+  if (nch > 1) {
+    gload(1);
+    gstore(1);
+  }
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    const int cur = c & 1, nxt = cur ^ 1;
+    if (c + 2 < nch) gload(c + 2);
+    if (c + 1 < nch) build_y(nxt);
+    mma(cur);
+    __syncthreads();
+    if (c + 2 < nch) gstore(cur);
     __syncthreads();
   }
   const int64_t s = sbase + si;
@@ -374,7 +474,6 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
   const int N = g.N, LD = N + 1;
   double* Ks = smn + (size_t)warp * (N * LD + 2 * N);  // column-major, ld = N+1
   double* rhs = Ks + N * LD;
-  int* piv = reinterpret_cast<int*>(rhs + N);
   const int64_t s = (int64_t)blockIdx.x * kNW + warp;
   if (s >= g.n) return;
   RomCtl* c = g.ctl + s;
@@ -427,12 +526,16 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
           bi = oi;
         }
       }
-      if (lane == 0) piv[k] = bi;
       if (bi != k) {
         for (int j = lane; j < N; j += 32) {
           const double t0 = Ks[j * LD + k];
           Ks[j * LD + k] = Ks[j * LD + bi];
           Ks[j * LD + bi] = t0;
+        }
+        if (lane == 0) {  // P b: transpositions applied in order (PartialPivLU::solve)
+          const double t0 = rhs[k];
+          rhs[k] = rhs[bi];
+          rhs[bi] = t0;
         }
       }
       __syncwarp();
@@ -440,38 +543,45 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
       if (best != 0.0)
         for (int i = k + 1 + lane; i < N; i += 32) Ks[k * LD + i] /= d;
       __syncwarp();
+      const double bk = rhs[k];
       for (int i = k + 1 + lane; i < N; i += 32) {
         const double l = Ks[k * LD + i];
         for (int j = k + 1; j < N; ++j) Ks[j * LD + i] -= l * Ks[j * LD + k];
+        rhs[i] -= l * bk;  // forward substitution with the unit-lower L, fused
       }
       __syncwarp();
     }
-    if (lane == 0) {
-      for (int k = 0; k < N; ++k) {
-        const int pk = piv[k];
-        const double t0 = rhs[k];
-        rhs[k] = rhs[pk];
-        rhs[pk] = t0;
-      }
-      for (int k = 0; k < N; ++k)
-        for (int i = k + 1; i < N; ++i) rhs[i] -= Ks[k * LD + i] * rhs[k];
-      for (int k = N - 1; k >= 0; --k) {
-        rhs[k] /= Ks[k * LD + k];
-        for (int i = 0; i < k; ++i) rhs[i] -= Ks[k * LD + i] * rhs[k];
-      }
+    // back substitution with U, lanes over rows
+    for (int k = N - 1; k >= 0; --k) {
+      const double xk = rhs[k] / Ks[k * LD + k];
+      __syncwarp();
+      if (lane == 0) rhs[k] = xk;
+      for (int i = lane; i < k; i += 32) rhs[i] -= Ks[k * LD + i] * xk;
+      __syncwarp();
     }
-    __syncwarp();
     for (int i = lane; i < N; i += 32) g.a[(size_t)s * N + i] += rhs[i];
     if (lane == 0) c->it = it + 1;
   }
   if (conv) {
     // rom_effective_stress at the converged state (rom.cpp:68-76)
     const bool last_sub = c->sp == 1;
-    if (last_sub && lane < 4) {
-      double pb = 0.0;
+    if (last_sub) {  // lanes over points, fixed shuffle tree
+      double pb[4] = {0.0, 0.0, 0.0, 0.0};
       const double* mo = g.morph + (size_t)s * 5 * g.Q;
-      for (int p = 0; p < g.Q; ++p) pb += (g.w[p] * mo[(size_t)4 * g.Q + p]) * g.P[((size_t)s * g.Q + p) * 4 + lane];
-      g.pbar[((size_t)s * g.K + c->k) * 4 + lane] = pb / 1.0;
+      for (int p = lane; p < g.Q; p += 32) {
+        const double cw = g.w[p] * mo[(size_t)4 * g.Q + p];
+        const double4 P4 = *reinterpret_cast<const double4*>(g.P + ((size_t)s * g.Q + p) * 4);
+        pb[0] += cw * P4.x;
+        pb[1] += cw * P4.y;
+        pb[2] += cw * P4.z;
+        pb[3] += cw * P4.w;
+      }
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) pb[c4] += __shfl_xor_sync(0xffffffffu, pb[c4], o);
+      if (lane == 0)
+        for (int c4 = 0; c4 < 4; ++c4) g.pbar[((size_t)s * g.K + c->k) * 4 + c4] = pb[c4] / 1.0;
     }
     for (int i = lane; i < N; i += 32) g.a0[(size_t)s * N + i] = g.a[(size_t)s * N + i];
     __syncwarp();
@@ -535,6 +645,15 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
   }
   __syncwarp();
   if (lane == 0 && c->active) atomicAdd(g.nactive, 1);
+}
+
+// register budget of the point kernel (2 or 3 CTAs/SM); PODECM_ROM_POINT_MINB
+int point_minb() {
+  static int v = [] {
+    const char* e = getenv("PODECM_ROM_POINT_MINB");
+    return (e && atoi(e) == 2) ? 2 : 3;
+  }();
+  return v;
 }
 
 template <class T>
@@ -686,8 +805,16 @@ int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t
   const size_t smem_pt = ((size_t)N * 4 * kPtsTile + (size_t)kInstTile * N) * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_rom_point, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_rom_point<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_rom_point<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     cudaFuncSetAttribute(k_rom_newton, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_rom_contract<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<1>());
+    cudaFuncSetAttribute(k_rom_contract<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<2>());
+    cudaFuncSetAttribute(k_rom_contract<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<3>());
+    cudaFuncSetAttribute(k_rom_contract<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<4>());
+    cudaFuncSetAttribute(k_rom_contract<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<5>());
+    cudaFuncSetAttribute(k_rom_contract<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<6>());
+    cudaFuncSetAttribute(k_rom_contract<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<7>());
     attr_set = true;
   }
   const dim3 gpt((Q + kPtsTile - 1) / kPtsTile, (unsigned)((n_inst + kInstTile - 1) / kInstTile));
@@ -739,18 +866,21 @@ int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t
   for (int64_t it = 0; it < max_global; ++it) {
     {
       KTimer kt(ctx, s, "k_rom_point");
-      k_rom_point<<<gpt, 256, smem_pt, s>>>(pa, rv->mats);
+      if (point_minb() == 2)
+        k_rom_point<2><<<gpt, 256, smem_pt, s>>>(pa, rv->mats);
+      else
+        k_rom_point<3><<<gpt, 256, smem_pt, s>>>(pa, rv->mats);
     }
     {
       KTimer kt(ctx, s, "k_rom_contract");
       switch (r->NT) {
-        case 1: k_rom_contract<1><<<gct, 32 * 1 * kIPC, 0, s>>>(ca); break;
-        case 2: k_rom_contract<2><<<gct, 32 * 2 * kIPC, 0, s>>>(ca); break;
-        case 3: k_rom_contract<3><<<gct, 32 * 3 * kIPC, 0, s>>>(ca); break;
-        case 4: k_rom_contract<4><<<gct, 32 * 4 * kIPC, 0, s>>>(ca); break;
-        case 5: k_rom_contract<5><<<gct, 32 * 5 * kIPC, 0, s>>>(ca); break;
-        case 6: k_rom_contract<6><<<gct, 32 * 6 * kIPC, 0, s>>>(ca); break;
-        default: k_rom_contract<7><<<gct, 32 * 7 * kIPC, 0, s>>>(ca); break;
+        case 1: k_rom_contract<1><<<gct, 32 * 1 * kIPC, contract_smem_bytes<1>(), s>>>(ca); break;
+        case 2: k_rom_contract<2><<<gct, 32 * 2 * kIPC, contract_smem_bytes<2>(), s>>>(ca); break;
+        case 3: k_rom_contract<3><<<gct, 32 * 3 * kIPC, contract_smem_bytes<3>(), s>>>(ca); break;
+        case 4: k_rom_contract<4><<<gct, 32 * 4 * kIPC, contract_smem_bytes<4>(), s>>>(ca); break;
+        case 5: k_rom_contract<5><<<gct, 32 * 5 * kIPC, contract_smem_bytes<5>(), s>>>(ca); break;
+        case 6: k_rom_contract<6><<<gct, 32 * 6 * kIPC, contract_smem_bytes<6>(), s>>>(ca); break;
+        default: k_rom_contract<7><<<gct, 32 * 7 * kIPC, contract_smem_bytes<7>(), s>>>(ca); break;
       }
     }
     PODECM_CUDA_TRY(ctx, cudaMemsetAsync(r->d_nactive, 0, sizeof(int), s));

@@ -22,11 +22,16 @@ struct podecm_rve {
   std::vector<int32_t> slot_grp;              // device form: e*64 + tl per 4-qp group
   std::vector<int32_t> slot_gptr;             // groups per slot
   std::vector<int32_t> frow_gptr, frow_grp;   // residual rows: e*8 + (a*2+i) groups
+  // slot-ordered element-sum layout: pos[e*72 + t] = index of element term t
+  // (t < 64: K term tl, t >= 64: f term) in the concatenated group list
+  // (slot groups, then residual-row groups); -1 = unused (anchor dofs).
+  std::vector<int32_t> pos, gptr_all;
+  int64_t n_groups = 0;
   // device tables
   double *d_nodes = nullptr, *d_grad = nullptr, *d_w = nullptr;
   int32_t *d_elems = nullptr, *d_regions = nullptr, *d_node_dof = nullptr;
   int32_t *d_slot_gptr = nullptr, *d_slot_grp = nullptr, *d_frow_gptr = nullptr,
-          *d_frow_grp = nullptr;
+          *d_frow_grp = nullptr, *d_pos = nullptr, *d_gptr_all = nullptr;
   // assembly scratch (per-qp K and f terms of a chunk of instances)
   double* d_scratch = nullptr;
   int64_t scratch_inst = 0;

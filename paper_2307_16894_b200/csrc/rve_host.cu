@@ -207,6 +207,20 @@ void build_pattern(podecm_rve& r) {
     }
     r.frow_gptr.push_back((int32_t)r.frow_grp.size());
   }
+  // slot-ordered positions of the element sums (fused assembly path)
+  const int64_t ns = (int64_t)r.slot_grp.size(), nf = (int64_t)r.frow_grp.size();
+  r.n_groups = ns + nf;
+  r.pos.assign((size_t)r.n_elems * 72, -1);
+  for (int64_t m = 0; m < ns; ++m) {
+    const int grp = r.slot_grp[m];
+    r.pos[(size_t)(grp >> 6) * 72 + (grp & 63)] = (int32_t)m;
+  }
+  for (int64_t m = 0; m < nf; ++m) {
+    const int grp = r.frow_grp[m];
+    r.pos[(size_t)(grp >> 3) * 72 + 64 + (grp & 7)] = (int32_t)(ns + m);
+  }
+  r.gptr_all.assign(r.slot_gptr.begin(), r.slot_gptr.end());
+  for (size_t k = 1; k < r.frow_gptr.size(); ++k) r.gptr_all.push_back((int32_t)(ns + r.frow_gptr[k]));
 }
 
 template <class T>
@@ -227,6 +241,8 @@ void free_rve(podecm_rve* r) {
   cudaFree(r->d_slot_grp);
   cudaFree(r->d_frow_gptr);
   cudaFree(r->d_frow_grp);
+  cudaFree(r->d_pos);
+  cudaFree(r->d_gptr_all);
   cudaFree(r->d_scratch);
 }
 
@@ -272,6 +288,8 @@ int podecm_rve_create_q4(podecm_ctx* ctx, int n_cells, double r0, const podecm_p
   if (!rc) rc = upload(ctx, &r->d_slot_grp, r->slot_grp);
   if (!rc) rc = upload(ctx, &r->d_frow_gptr, r->frow_gptr);
   if (!rc) rc = upload(ctx, &r->d_frow_grp, r->frow_grp);
+  if (!rc) rc = upload(ctx, &r->d_pos, r->pos);
+  if (!rc) rc = upload(ctx, &r->d_gptr_all, r->gptr_all);
   if (rc) {
     free_rve(r);
     delete r;
