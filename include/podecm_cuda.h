@@ -198,6 +198,11 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
  * *flops receives the flop count of the launch, time it on `stream`. */
 int podecm_probe_fp64(podecm_ctx* ctx, void* stream, int mode, int iters, double* scratch,
                       double* flops);
+/* Elementwise device arithmetic used by the material kernels (tests only):
+ * which 0: a/b, 1: reciprocal-based division, 2: correctly rounded 1/b,
+ * 3: 1.0/b, 4: exp(a), 5: log(a). */
+int podecm_probe_math(podecm_ctx* ctx, void* stream, int which, int64_t n, const double* a,
+                      const double* b, double* out);
 
 #ifdef __cplusplus
 }

@@ -61,6 +61,7 @@ _SIGS = {
     "podecm_ecm_select": (C.c_int, [P, P, P, P, C.c_int, P, I64, C.POINTER(podecm_ecm_opts), P, P,
                                     C.POINTER(C.c_int), C.POINTER(D), C.POINTER(C.c_int)]),
     "podecm_probe_fp64": (C.c_int, [P, P, C.c_int, C.c_int, P, C.POINTER(D)]),
+    "podecm_probe_math": (C.c_int, [P, P, C.c_int, I64, P, P, P]),
     "podecm_rom_solve_batch": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton),
                                          P, P, P, P, P]),
 }

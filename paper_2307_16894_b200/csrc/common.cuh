@@ -63,7 +63,7 @@ inline podecm_dev::MatConst make_const(const podecm_params& p) {
   c.three_mu_H = 3 * c.mu + p.H;
   c.yield0 = p.sigma_y0 + p.H * 0.0;  // SmallState{}.xi == 0 (material.cpp:137)
   c.H = p.H;
-  c.pad = 0;
+  c.rcp_3muH = 1.0 / c.three_mu_H;
   return c;
 }
 
