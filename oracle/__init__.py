@@ -14,8 +14,9 @@ from pathlib import Path
 import numpy as np
 
 HERE = Path(__file__).resolve().parent
-LIB = HERE / "liboracle.so"
-_lib = None
+LIB = HERE / "liboracle.so"          # faithful: glibc exp/log, like the reference
+LIB_PDM = HERE / "liboracle_pdm.so"  # same algorithm with the device's portable exp/log
+_libs = {}
 
 P = C.c_void_p
 L = C.c_long
@@ -30,12 +31,12 @@ def build() -> Path:
     return LIB
 
 
-def lib():
-    global _lib
-    if _lib is None:
-        if not LIB.exists():
+def lib(libm: str = "glibc"):
+    if libm not in _libs:
+        path = LIB if libm == "glibc" else LIB_PDM
+        if not path.exists():
             build()
-        l = C.CDLL(str(LIB))
+        l = C.CDLL(str(path))
         l.orc_material_batch.restype = L
         l.orc_material_batch.argtypes = [L, P, I, P, P, P, P, P, P, P, P, D, I]
         l.orc_rve_create.restype = P
@@ -52,8 +53,18 @@ def lib():
         l.orc_stress_snapshots.restype = L
         l.orc_stress_snapshots.argtypes = [P, P, L, P, I]
         l.orc_max_threads.restype = I
-        _lib = l
-    return _lib
+        l.orc_libm.argtypes = [I, L, P, P]
+        _libs[libm] = l
+    return _libs[libm]
+
+
+def libm(which: str, x):
+    """Host exp/log: 'exp'/'log' (glibc) or 'pdm_exp'/'pdm_log' (portable)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.empty_like(x)
+    code = {"exp": 0, "log": 1, "pdm_exp": 2, "pdm_log": 3}[which]
+    lib().orc_libm(code, x.size, _p(x), _p(out))
+    return out
 
 
 def _p(a):
@@ -74,8 +85,9 @@ def max_threads() -> int:
         return os.cpu_count() or 1
 
 
-def material_batch(F, st, mats, region=None, h_rel=1e-7, tangent=True, nthreads=0):
-    """large_strain_update + large_strain_tangent per point (material.cpp)."""
+def material_batch(F, st, mats, region=None, h_rel=1e-7, tangent=True, nthreads=0, libm="glibc"):
+    """large_strain_update + large_strain_tangent per point (material.cpp).
+    libm="pdm" uses the device's portable exp/log (algorithm-only check)."""
     F = np.ascontiguousarray(F, dtype=np.float64)
     st = np.ascontiguousarray(st, dtype=np.float64)
     n = F.shape[1]
@@ -86,8 +98,8 @@ def material_batch(F, st, mats, region=None, h_rel=1e-7, tangent=True, nthreads=
     status = np.empty(n, np.int32)
     m = _mats(mats)
     reg = None if region is None else np.ascontiguousarray(region, dtype=np.int32)
-    lib().orc_material_batch(n, _p(m), len(mats), _p(reg), _p(F), _p(st), _p(P_), _p(A), _p(so),
-                             _p(status), _p(ex), h_rel, nthreads)
+    lib(libm).orc_material_batch(n, _p(m), len(mats), _p(reg), _p(F), _p(st), _p(P_), _p(A), _p(so),
+                                 _p(status), _p(ex), h_rel, nthreads)
     return {"P": P_, "A": A, "st": so, "status": status, "dgamma": ex[0], "f_trial": ex[1],
             "q_trial": ex[2], "mises": ex[3]}
 

@@ -9,6 +9,7 @@
 #include <memory>
 
 #include "oracle.hpp"
+#include "../paper_2307_16894_b200/csrc/pdmath.h"
 
 using namespace orc;
 
@@ -294,6 +295,19 @@ long orc_stress_snapshots(void* hp, const double* U, long L, double* W, int nthr
     }
   }
   return fails;
+}
+
+// libm probes: 0 glibc exp, 1 glibc log, 2 pdm exp, 3 pdm log (host build of
+// the device's portable functions).
+void orc_libm(int which, long n, const double* x, double* out) {
+  for (long i = 0; i < n; ++i) {
+    switch (which) {
+      case 0: out[i] = std::exp(x[i]); break;
+      case 1: out[i] = std::log(x[i]); break;
+      case 2: out[i] = pdm::exp(x[i]); break;
+      default: out[i] = pdm::log(x[i]); break;
+    }
+  }
 }
 
 int orc_max_threads() { return omp_get_max_threads(); }

@@ -4,6 +4,19 @@
 
 #include <algorithm>
 
+// The reference calls glibc's std::log / std::exp.  Built with -DORC_PDMATH
+// (liboracle_pdm.so) the oracle uses the device's portable exp/log instead:
+// that variant isolates the libm from the algorithm (GPU == oracle bit for
+// bit), while the default build is the faithful glibc restatement.
+#ifdef ORC_PDMATH
+#include "../paper_2307_16894_b200/csrc/pdmath.h"
+#define ORC_LOG pdm::log
+#define ORC_EXP pdm::exp
+#else
+#define ORC_LOG std::log
+#define ORC_EXP std::exp
+#endif
+
 namespace orc {
 
 namespace {
@@ -90,8 +103,7 @@ LargeResult large_strain_update(const PlasticityParams& p, const PlasticState& s
     throw SolveError("plasticity update hit a non-positive elastic stretch (det F = " +
                      std::to_string(det(F)) + ")");
 
-  const double eps_tr[4] = {0.5 * std::log(eg.l1), 0.5 * std::log(eg.l2), 0.5 * std::log(czz),
-                            0.0};
+  const double eps_tr[4] = {0.5 * ORC_LOG(eg.l1), 0.5 * ORC_LOG(eg.l2), 0.5 * ORC_LOG(czz), 0.0};
   // Quirk replicated: the inner return map always starts
   // from a virgin SmallState, so xi never hardens the yield stress.
   const double zero4[4] = {0, 0, 0, 0};
@@ -107,15 +119,15 @@ LargeResult large_strain_update(const PlasticityParams& p, const PlasticState& s
     }
 
   PlasticState next = s0;
-  const double e0 = std::exp(ep[0]), e1 = std::exp(ep[1]);
+  const double e0 = ORC_EXP(ep[0]), e1 = ORC_EXP(ep[1]);
   Mat2 m;
   for (int k = 0; k < 4; ++k) m.a[k] = e0 * vv1.a[k] + e1 * vv2.a[k];
   next.Fp = mul(m, s0.Fp);
-  next.Fp_zz = std::exp(ep[2]) * s0.Fp_zz;
+  next.Fp_zz = ORC_EXP(ep[2]) * s0.Fp_zz;
   next.xi = s0.xi + sr.dgamma;
 
-  const double l1n = std::exp(2.0 * (eps_tr[0] - ep[0]));
-  const double l2n = std::exp(2.0 * (eps_tr[1] - ep[1]));
+  const double l1n = ORC_EXP(2.0 * (eps_tr[0] - ep[0]));
+  const double l2n = ORC_EXP(2.0 * (eps_tr[1] - ep[1]));
   const double a1 = sr.sigma[0] / l1n, a2 = sr.sigma[1] / l2n;
   Mat2 s_hat;
   for (int k = 0; k < 4; ++k) s_hat.a[k] = a1 * vv1.a[k] + a2 * vv2.a[k];
