@@ -64,7 +64,7 @@ struct podecm_rom {
   double* d_Gt = nullptr;  // [N][4][Qpad]: G_p[i][r], p fastest (material kernel)
   int64_t cap = 0;
   double *d_morph = nullptr, *d_S = nullptr, *d_At = nullptr, *d_P = nullptr, *d_K = nullptr,
-         *d_f = nullptr, *d_a = nullptr, *d_a0 = nullptr;
+         *d_f = nullptr, *d_a = nullptr, *d_a0 = nullptr, *d_Fb = nullptr;
   RomCtl* d_ctl = nullptr;
   int* d_nactive = nullptr;
   int* h_nactive = nullptr;
@@ -82,8 +82,9 @@ void free_work(podecm_rom* r) {
   cudaFree(r->d_f);
   cudaFree(r->d_a);
   cudaFree(r->d_a0);
+  cudaFree(r->d_Fb);
   cudaFree(r->d_ctl);
-  r->d_morph = r->d_S = r->d_At = r->d_P = r->d_K = r->d_f = r->d_a = r->d_a0 = nullptr;
+  r->d_morph = r->d_S = r->d_At = r->d_P = r->d_K = r->d_f = r->d_a = r->d_a0 = r->d_Fb = nullptr;
   r->d_ctl = nullptr;
   r->cap = 0;
 }
@@ -163,22 +164,26 @@ struct PointArgs {
   double* S;   // [2][cap][6][Q]
   double* At;  // [n][Qpad][20]
   double* P;   // [n][Q][4]
+  double* Fb;  // [n][4][Q]
   RomCtl* ctl;
 };
 
-template <int MINB>
-__global__ void __launch_bounds__(256, MINB) k_rom_point(PointArgs g, MatTable tab) {
+// F at every ECM point: F = Fbar + R(Fmu^-1)^T (G_p^T a) (rom.cpp:48-50).  CTA =
+// 32 points x 8 instances sharing one SMEM tile of the mode gradients.
+constexpr int kFInst = 32;  // k_rom_F: instances per CTA (4 per thread)
+
+__global__ void __launch_bounds__(256) k_rom_F(PointArgs g) {
   extern __shared__ double sm[];
-  double* sG = sm;                            // [N][4][32]
-  double* sa = sm + (size_t)g.N * 4 * kPtsTile;  // [8][N]
+  double* sG = sm;                               // [N][4][32]
+  double* sa = sm + (size_t)g.N * 4 * kPtsTile;  // [kFInst][N]
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int p0 = blockIdx.x * kPtsTile;
-  const int64_t s0 = (int64_t)blockIdx.y * kInstTile;
+  const int64_t s0 = (int64_t)blockIdx.y * kFInst;
   {  // whole CTA idle (finished / failed instances): skip the staging
     __shared__ int any_active;
     if (threadIdx.x == 0) any_active = 0;
     __syncthreads();
-    if (threadIdx.x < kInstTile && s0 + threadIdx.x < g.n && g.ctl[s0 + threadIdx.x].active) any_active = 1;
+    if (threadIdx.x < kFInst && s0 + threadIdx.x < g.n && g.ctl[s0 + threadIdx.x].active) any_active = 1;
     __syncthreads();
     if (!any_active) return;
   }
@@ -186,37 +191,70 @@ __global__ void __launch_bounds__(256, MINB) k_rom_point(PointArgs g, MatTable t
     const int ir = t / kPtsTile, pl = t - ir * kPtsTile;
     sG[t] = (p0 + pl < g.Qpad) ? g.Gt[(size_t)ir * g.Qpad + p0 + pl] : 0.0;
   }
-  for (int t = threadIdx.x; t < kInstTile * g.N; t += blockDim.x) {
+  for (int t = threadIdx.x; t < kFInst * g.N; t += blockDim.x) {
     const int si = t / g.N, i = t - si * g.N;
     sa[t] = (s0 + si < g.n) ? g.a[(size_t)(s0 + si) * g.N + i] : 0.0;
   }
   __syncthreads();
-  const int64_t s = s0 + ty;
   const int p = p0 + tx;
-  if (s >= g.n || p >= g.Q) return;
+  if (p >= g.Q) return;
+  // u = G_p^T a for 4 instances per thread: each G value from SMEM feeds 4 FMAs
+  double u[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) u[q][r] = 0.0;
+  for (int i = 0; i < g.N; ++i) {
+    double gv[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) gv[r] = sG[(i * 4 + r) * kPtsTile + tx];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double av = sa[(ty + 8 * q) * g.N + i];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) u[q][r] = fma(gv[r], av, u[q][r]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t s = s0 + ty + 8 * q;
+    if (s >= g.n) break;
+    const RomCtl* c = g.ctl + s;
+    if (!c->active) continue;
+    // F = Fbar + R(fmi)^T u  (mapped^T a, rom.cpp:48-50)
+    const double* mo = g.morph + (size_t)s * 5 * g.Q;
+    double m[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) m[t] = mo[(size_t)t * g.Q + p];
+    const int top = c->sp - 1;
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+      for (int l = 0; l < 2; ++l)
+        g.Fb[((size_t)s * 4 + ii + 2 * l) * g.Q + p] =
+            c->fstack[top][4 + ii + 2 * l] + (u[q][ii] * m[2 * l] + u[q][ii + 2] * m[1 + 2 * l]);
+  }
+}
+
+// Material at every ECM point (one thread per point, C1-style register
+// budget): P, FD tangent, trial history, then the mapped operators
+// At = c R A R^T and Pt = c R P.
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable tab) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= g.n * g.Q) return;
+  const int64_t s = tid / g.Q;
+  const int p = tid - (int)s * g.Q;
   RomCtl* c = g.ctl + s;
   if (!c->active) return;
-  // u = G_p^T a ; F = Fbar + R(fmi)^T u  (mapped^T a, rom.cpp:48-50)
-  double u[4] = {0.0, 0.0, 0.0, 0.0};
-  const double* ai = sa + ty * g.N;
-  for (int i = 0; i < g.N; ++i) {
-    const double av = ai[i];
-#pragma unroll
-    for (int r = 0; r < 4; ++r) u[r] = fma(sG[(i * 4 + r) * kPtsTile + tx], av, u[r]);
-  }
   const double* mo = g.morph + (size_t)s * 5 * g.Q;
-  double m[4];
+  double m[4], F[4];
 #pragma unroll
-  for (int t = 0; t < 4; ++t) m[t] = mo[(size_t)t * g.Q + p];
+  for (int t = 0; t < 4; ++t) {
+    m[t] = mo[(size_t)t * g.Q + p];
+    F[t] = g.Fb[((size_t)s * 4 + t) * g.Q + p];
+  }
   const double det = mo[(size_t)4 * g.Q + p];
-  const int top = c->sp - 1;
-  double F[4];
-#pragma unroll
-  for (int ii = 0; ii < 2; ++ii)
-#pragma unroll
-    for (int l = 0; l < 2; ++l)
-      F[ii + 2 * l] = c->fstack[top][4 + ii + 2 * l] + (u[ii] * m[2 * l] + u[ii + 2] * m[1 + 2 * l]);
-
   const MatConst& pm = tab.m[g.reg[p]];
   const int cur = c->cur;
   const double* s0p = g.S + ((size_t)cur * g.cap + s) * 6 * g.Q;
@@ -540,23 +578,38 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
       }
       __syncwarp();
       const double d = Ks[k * LD + k];
-      if (best != 0.0)
-        for (int i = k + 1 + lane; i < N; i += 32) Ks[k * LD + i] /= d;
+      if (best != 0.0) {
+        const double rd = __drcp_rn(d);  // correctly rounded: div_rcp == '/'
+        for (int i = k + 1 + lane; i < N; i += 32) Ks[k * LD + i] = div_rcp(Ks[k * LD + i], d, rd);
+      }
       __syncwarp();
       const double bk = rhs[k];
       for (int i = k + 1 + lane; i < N; i += 32) {
         const double l = Ks[k * LD + i];
-        for (int j = k + 1; j < N; ++j) Ks[j * LD + i] -= l * Ks[j * LD + k];
-        rhs[i] -= l * bk;  // forward substitution with the unit-lower L, fused
+        // rank-1 update of the trailing block, 4 independent columns in flight
+        int j = k + 1;
+        for (; j + 3 < N; j += 4) {
+          const double u0 = Ks[j * LD + k], u1 = Ks[(j + 1) * LD + k];
+          const double u2 = Ks[(j + 2) * LD + k], u3 = Ks[(j + 3) * LD + k];
+          const double a0 = Ks[j * LD + i], a1 = Ks[(j + 1) * LD + i];
+          const double a2 = Ks[(j + 2) * LD + i], a3 = Ks[(j + 3) * LD + i];
+          Ks[j * LD + i] = fma(-l, u0, a0);
+          Ks[(j + 1) * LD + i] = fma(-l, u1, a1);
+          Ks[(j + 2) * LD + i] = fma(-l, u2, a2);
+          Ks[(j + 3) * LD + i] = fma(-l, u3, a3);
+        }
+        for (; j < N; ++j) Ks[j * LD + i] = fma(-l, Ks[j * LD + k], Ks[j * LD + i]);
+        rhs[i] = fma(-l, bk, rhs[i]);  // forward substitution with the unit-lower L, fused
       }
       __syncwarp();
     }
     // back substitution with U, lanes over rows
     for (int k = N - 1; k >= 0; --k) {
-      const double xk = rhs[k] / Ks[k * LD + k];
+      const double ukk = Ks[k * LD + k];
+      const double xk = div_rcp(rhs[k], ukk, __drcp_rn(ukk));
       __syncwarp();
       if (lane == 0) rhs[k] = xk;
-      for (int i = lane; i < k; i += 32) rhs[i] -= Ks[k * LD + i] * xk;
+      for (int i = lane; i < k; i += 32) rhs[i] = fma(-Ks[k * LD + i], xk, rhs[i]);
       __syncwarp();
     }
     for (int i = lane; i < N; i += 32) g.a[(size_t)s * N + i] += rhs[i];
@@ -651,7 +704,7 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
 int point_minb() {
   static int v = [] {
     const char* e = getenv("PODECM_ROM_POINT_MINB");
-    return (e && atoi(e) == 2) ? 2 : 3;
+    return (e && atoi(e) == 4) ? 4 : 5;
   }();
   return v;
 }
@@ -676,6 +729,7 @@ int ensure_cap(podecm_rom* r, int64_t n) {
   if (!rc) rc = dalloc(ctx, &r->d_f, (size_t)n * N);
   if (!rc) rc = dalloc(ctx, &r->d_a, (size_t)n * N);
   if (!rc) rc = dalloc(ctx, &r->d_a0, (size_t)n * N);
+  if (!rc) rc = dalloc(ctx, &r->d_Fb, (size_t)n * 4 * Q);
   if (!rc) rc = dalloc(ctx, &r->d_ctl, (size_t)n);
   if (rc) {
     free_work(r);
@@ -801,12 +855,12 @@ int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t
   pa.S = r->d_S;
   pa.At = r->d_At;
   pa.P = r->d_P;
+  pa.Fb = r->d_Fb;
   pa.ctl = r->d_ctl;
-  const size_t smem_pt = ((size_t)N * 4 * kPtsTile + (size_t)kInstTile * N) * sizeof(double);
+  const size_t smem_pt = ((size_t)N * 4 * kPtsTile + (size_t)kFInst * N) * sizeof(double);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_rom_point<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    cudaFuncSetAttribute(k_rom_point<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_rom_F, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     cudaFuncSetAttribute(k_rom_newton, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_rom_contract<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<1>());
     cudaFuncSetAttribute(k_rom_contract<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<2>());
@@ -817,7 +871,7 @@ int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t
     cudaFuncSetAttribute(k_rom_contract<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<7>());
     attr_set = true;
   }
-  const dim3 gpt((Q + kPtsTile - 1) / kPtsTile, (unsigned)((n_inst + kInstTile - 1) / kInstTile));
+  const dim3 gpt((Q + kPtsTile - 1) / kPtsTile, (unsigned)((n_inst + kFInst - 1) / kFInst));
 
   ContractArgs ca;
   ca.n = n_inst;
@@ -865,11 +919,16 @@ int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t
   const int64_t max_global = (int64_t)K * (opts->max_iter + 1) * (2ll << opts->max_bisect) + 8;
   for (int64_t it = 0; it < max_global; ++it) {
     {
+      KTimer kt(ctx, s, "k_rom_F");
+      k_rom_F<<<gpt, 256, smem_pt, s>>>(pa);
+    }
+    {
       KTimer kt(ctx, s, "k_rom_point");
-      if (point_minb() == 2)
-        k_rom_point<2><<<gpt, 256, smem_pt, s>>>(pa, rv->mats);
+      const int gp = grid_for(n_inst * Q, 128);
+      if (point_minb() == 4)
+        k_rom_point<4><<<gp, 128, 0, s>>>(pa, rv->mats);
       else
-        k_rom_point<3><<<gpt, 256, smem_pt, s>>>(pa, rv->mats);
+        k_rom_point<5><<<gp, 128, 0, s>>>(pa, rv->mats);
     }
     {
       KTimer kt(ctx, s, "k_rom_contract");
@@ -888,7 +947,7 @@ int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t
       KTimer kt(ctx, s, "k_rom_newton");
       k_rom_newton<<<gnt, 32 * kNW, smem_nt, s>>>(na);
     }
-    PODECM_LAUNCHED(ctx, 3);
+    PODECM_LAUNCHED(ctx, 4);
     if ((it & 3) == 3) {
       PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(r->h_nactive, r->d_nactive, sizeof(int),
                                            cudaMemcpyDeviceToHost, s));
