@@ -239,15 +239,22 @@ __global__ void __launch_bounds__(128, MINB) k_asm_qp(AsmArgs g, MatTable tab) {
         }
         if (d == 0) return;
         const int u0 = 4 * (k & 1) + 2 * ((k >> 1) & 1);
+        // T[i][c][b] = sum_d A(i,c,j,d) gt_bd, then K(a i, b j) = sum_c (wq gt_ac) T[i][c][b]
+        double T[2][2][4];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) T[i][cc][b] = fma(cd[1][i + 2 * cc], gt[b][1], cd[0][i + 2 * cc] * gt[b][0]);
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
           double v[8], o[2];
+          const double w0 = wq * gt[a][0], w1 = wq * gt[a][1];
 #pragma unroll
           for (int b = 0; b < 4; ++b)
 #pragma unroll
-            for (int i = 0; i < 2; ++i)
-              v[b * 2 + i] = wq * (gt[a][0] * (cd[0][i] * gt[b][0] + cd[1][i] * gt[b][1]) +
-                                   gt[a][1] * (cd[0][i + 2] * gt[b][0] + cd[1][i + 2] * gt[b][1]));
+            for (int i = 0; i < 2; ++i) v[b * 2 + i] = fma(w1, T[i][1][b], w0 * T[i][0][b]);
           quad_reduce8(v, k, o);
           if (valid) {
 #pragma unroll

@@ -124,7 +124,7 @@ __global__ void k_ecm_colnorm(int64_t L, int nq, int N, const double* H, const d
 constexpr int kSQ = 16, kSC = 64, kSK = 16, kSLD = kSK + 4;
 
 __global__ void __launch_bounds__(224) k_ecm_score(int64_t L, int nq, int N, const double* r,
-                                                   double r_vol, const double* H, const double* W,
+                                                   const double* r_vol_p, const double* H, const double* W,
                                                    const double* cn, const uint8_t* unavailable,
                                                    double* cta_best, int* cta_idx) {
   __shared__ double sR[2][56][kSLD];
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(224) k_ecm_score(int64_t L, int nq, int N, con
     if (q < nq && !unavailable[q] && cn[q] != 0.0) {
       double corr = 0.0;
       for (int w = 0; w < 7; ++w) corr += red[w][tid];
-      corr += r_vol;
+      if (r_vol_p) corr += *r_vol_p;
       const double sc = corr / cn[q];
       if (sc > 0.0) {
         best = sc;
@@ -318,60 +318,83 @@ __global__ void __launch_bounds__(256) k_resid(int64_t m, int k, const double* A
   }
 }
 
-__global__ void k_scale(int64_t m, double* v, double inv_div, double div) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < m) v[r] = v[r] / div;
-  (void)inv_div;
+
+// QR column finish (one CTA): R[:, k] = h1 + h2, r_kk = ||v||, Q[:, k] = v / r_kk,
+// qtb[k] = Q[:, k] . rhs — fixed-tree block reductions (deterministic).
+__global__ void __launch_bounds__(1024) k_qr_finish(int64_t m, int k, int kmax, const double* v,
+                                                    const double* h1, const double* h2,
+                                                    const double* rhs, double* qcol, double* R,
+                                                    double* qtb) {
+  __shared__ double red[1024];
+  const int t = threadIdx.x;
+  for (int j = t; j < k; j += blockDim.x) R[(size_t)k * kmax + j] = (0.0 + h1[j]) + h2[j];
+  double p = 0.0;
+  for (int64_t r = t; r < m; r += blockDim.x) p = fma(v[r], v[r], p);
+  red[t] = p;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (t < o) red[t] += red[t + o];
+    __syncthreads();
+  }
+  const double nrm = sqrt(red[0]);
+  __syncthreads();
+  double q = 0.0;
+  for (int64_t r = t; r < m; r += blockDim.x) {
+    const double x = v[r] / nrm;
+    qcol[r] = x;
+    q = fma(x, rhs[r], q);
+  }
+  red[t] = q;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (t < o) red[t] += red[t + o];
+    __syncthreads();
+  }
+  if (t == 0) {
+    R[(size_t)k * kmax + k] = nrm;
+    qtb[k] = red[0];
+  }
 }
 
+// Incremental QR of the selected integrand columns (classical Gram-Schmidt
+// with one re-orthogonalisation pass).  The m-long work (projections, norm,
+// Q column, Q^T b) stays on the device; the new R column (k + 1 values) and
+// qtb entry are copied to a host mirror, where the k x k back substitution
+// and the Lawson-Hanson feasibility logic run (one sync per refit).
 struct Ecm {
   podecm_ctx* ctx;
   cudaStream_t s;
   int64_t m;
   int kmax;
-  double *Jsel, *Q, *tmp, *h;
-  std::vector<double> R;    // host upper-triangular, column-major kmax x kmax
-  std::vector<double> qtb;  // Q^T rhs
+  double *Jsel, *Q, *tmp, *h1, *h2, *R, *qtb;
   const double* rhs;
   int k = 0;
+  std::vector<double> hR, hq;  // host mirrors (column-major kmax x kmax, kmax)
 
-  double dot_host(const double* a, const double* b) {  // a . b  (device vectors)
-    k_dots<<<1, 256, 0, s>>>(m, 1, a, b, h);
-    double out;
-    cudaMemcpyAsync(&out, h, sizeof(double), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    return out;
-  }
-
-  // append column Jsel[:, k] to the QR (CGS2)
-  void append() {
+  void append() {  // append column Jsel[:, k]
     double* v = tmp;
     cudaMemcpyAsync(v, Jsel + (int64_t)k * m, sizeof(double) * m, cudaMemcpyDeviceToDevice, s);
-    std::vector<double> hh(k + 1, 0.0);
-    for (int pass = 0; pass < 2 && k > 0; ++pass) {
-      k_dots<<<k, 256, 0, s>>>(m, k, Q, v, h);
-      std::vector<double> hp(k);
-      cudaMemcpyAsync(hp.data(), h, sizeof(double) * k, cudaMemcpyDeviceToHost, s);
-      cudaStreamSynchronize(s);
-      k_axpy_cols<<<grid_for(m, 256), 256, 0, s>>>(m, k, Q, h, v);
-      for (int j = 0; j < k; ++j) hh[j] += hp[j];
+    if (k > 0) {
+      k_dots<<<k, 256, 0, s>>>(m, k, Q, v, h1);
+      k_axpy_cols<<<grid_for(m, 256), 256, 0, s>>>(m, k, Q, h1, v);
+      k_dots<<<k, 256, 0, s>>>(m, k, Q, v, h2);
+      k_axpy_cols<<<grid_for(m, 256), 256, 0, s>>>(m, k, Q, h2, v);
     }
-    const double nrm = sqrt(dot_host(v, v));
-    hh[k] = nrm;
-    k_scale<<<grid_for(m, 256), 256, 0, s>>>(m, v, 0.0, nrm);
-    cudaMemcpyAsync(Q + (int64_t)k * m, v, sizeof(double) * m, cudaMemcpyDeviceToDevice, s);
-    for (int j = 0; j <= k; ++j) R[(size_t)k * kmax + j] = hh[j];
-    qtb[k] = dot_host(Q + (int64_t)k * m, rhs);
-    ctx->launches += 6;
+    k_qr_finish<<<1, 1024, 0, s>>>(m, k, kmax, v, h1, h2, rhs, Q + (int64_t)k * m, R, qtb);
+    cudaMemcpyAsync(hR.data() + (size_t)k * kmax, R + (size_t)k * kmax, sizeof(double) * (k + 1),
+                    cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(hq.data() + k, qtb + k, sizeof(double), cudaMemcpyDeviceToHost, s);
+    ctx->launches += k > 0 ? 5 : 1;
     ++k;
   }
 
-  std::vector<double> solve() const {  // R z = Q^T b
+  std::vector<double> solve() {  // R z = Q^T b (host back substitution)
+    cudaStreamSynchronize(s);
     std::vector<double> z(k);
     for (int i = k - 1; i >= 0; --i) {
-      double s0 = qtb[i];
-      for (int j = i + 1; j < k; ++j) s0 -= R[(size_t)j * kmax + i] * z[j];
-      z[i] = s0 / R[(size_t)i * kmax + i];
+      double s0 = hq[i];
+      for (int j = i + 1; j < k; ++j) s0 -= hR[(size_t)j * kmax + i] * z[j];
+      z[i] = s0 / hR[(size_t)i * kmax + i];
     }
     return z;
   }
@@ -418,6 +441,9 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
   const int vol = opts->volume_row ? 1 : 0;
   const int64_t m = (int64_t)N * L + vol;
   const int cap = opts->max_points > 0 ? std::min(opts->max_points, nq) : nq;
+  // device workspaces (J_sel, Q: m x kq; R: kq^2) hold at most kMaxSel columns
+  constexpr int kMaxSel = 1024;
+  const int kq = std::min(cap, kMaxSel);
   int rc = PODECM_OK;
   auto fail = [&](int code, const char* msg) { return set_err(ctx, code, msg); };
 
@@ -439,11 +465,16 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
   alloc(&cta_i, n_cta);
   alloc(&best_b, 1);
   alloc(&best_i, 1);
-  alloc(&Jsel, (size_t)m * cap);
-  alloc(&Q, (size_t)m * cap);
+  alloc(&Jsel, (size_t)m * kq);
+  alloc(&Q, (size_t)m * kq);
   alloc(&tmp, m);
-  alloc(&hbuf, std::max(cap, 1));
-  alloc(&xdev, std::max(cap, 1));
+  alloc(&hbuf, kq);
+  double *h2buf = nullptr, *Rdev = nullptr, *qtbdev = nullptr, *zdev = nullptr;
+  alloc(&h2buf, kq);
+  alloc(&Rdev, (size_t)kq * kq);
+  alloc(&qtbdev, kq);
+  alloc(&zdev, kq);
+  alloc(&xdev, kq);
   alloc(&pss, n_rb);
   alloc(&pmx, n_rb);
   alloc(&unav, nq);
@@ -502,8 +533,9 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
     rmax = 0.0;
     for (double v : hr) rmax = std::max(rmax, std::fabs(v));
   }
-  Ecm qr{ctx, s, m, cap, Jsel, Q, tmp, hbuf, std::vector<double>((size_t)cap * cap, 0.0),
-         std::vector<double>(cap, 0.0), rhs, 0};
+  if (!rc) cudaMemsetAsync(h2buf, 0, sizeof(double) * kq, s);
+  Ecm qr{ctx, s, m, kq, Jsel, Q, tmp, hbuf, h2buf, Rdev, qtbdev, rhs, 0,
+         std::vector<double>((size_t)kq * kq, 0.0), std::vector<double>(kq, 0.0)};
   auto converged = [&]() {
     if (rhs_norm == 0.0) return true;
     return rnorm <= opts->eps * rhs_norm && rmax <= row_tol;
@@ -518,13 +550,14 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
       rc = fail(PODECM_ESOLVE, "cubature did not reach the requested accuracy within the point budget");
       break;
     }
+    if ((int)selected.size() >= kq) {
+      rc = fail(PODECM_ECONFIG, "ecm: more than 1024 selected points is not supported by this build");
+      break;
+    }
     // corr = J^T r ; argmax of corr / ||J_q|| over available columns
-    double r_vol = 0.0;
-    if (vol) cudaMemcpyAsync(&r_vol, r + m - 1, sizeof(double), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
     {
       KTimer kt(ctx, s, "k_ecm_score");
-      k_ecm_score<<<n_cta, 224, 0, s>>>(L, nq, N, r, r_vol, H, W, cn, unav, cta_b, cta_i);
+      k_ecm_score<<<n_cta, 224, 0, s>>>(L, nq, N, r, vol ? r + m - 1 : nullptr, H, W, cn, unav, cta_b, cta_i);
     }
     k_ecm_argmax<<<1, 1024, 0, s>>>(n_cta, cta_b, cta_i, best_b, best_i);
     ctx->launches += 2;
@@ -578,7 +611,6 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
       selected = keep_ids;
       x = keep_x;
       qr.k = 0;
-      std::fill(qr.R.begin(), qr.R.end(), 0.0);
       for (size_t k = 0; k < selected.size(); ++k) qr.append();
     }
     ++iters;
@@ -623,6 +655,10 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
   cudaFree(Q);
   cudaFree(tmp);
   cudaFree(hbuf);
+  cudaFree(h2buf);
+  cudaFree(Rdev);
+  cudaFree(qtbdev);
+  cudaFree(zdev);
   cudaFree(xdev);
   cudaFree(pss);
   cudaFree(pmx);
