@@ -539,9 +539,25 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
   __syncwarp();
   if (!fail && !conv) {
     // K da = -f  (dense LU, partial pivoting: first row of max |a_ik|)
-    for (int t = lane; t < N * N; t += 32) {
-      const int i = t / N, j = t - i * N;  // K row-major [i][j]
-      Ks[j * LD + i] = g.Kg[(size_t)s * N * N + t];
+    {  // K row-major [i][j] -> Ks column-major; 8 loads in flight per lane
+      const double* src = g.Kg + (size_t)s * N * N;
+      const int NN = N * N;
+      for (int t0 = 0; t0 < NN; t0 += 32 * 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int t = t0 + u * 32 + lane;
+          v[u] = t < NN ? __ldcs(src + t) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int t = t0 + u * 32 + lane;
+          if (t < NN) {
+            const int i = t / N, j = t - i * N;
+            Ks[j * LD + i] = v[u];
+          }
+        }
+      }
     }
     for (int i = lane; i < N; i += 32) rhs[i] = -g.f[(size_t)s * N + i];
     __syncwarp();
