@@ -437,6 +437,24 @@ def run_c3(args, ws, rank, local, ctx, n_inst, steps, warmup, fp64):
                         "peak_source": "DMMA probe measured in this run (mma.sync m8n8k4 f64)",
                         "share_of_step": {"contract": round(kc[0] / tot, 3), "material": round(kp[0] / tot, 3),
                                           "newton_lu": round(kn[0] / tot, 3)} if tot > 0 else None}}
+    # §8(f) row 1: rom_effective_stiffness for every instance at its final
+    # (Fbar_K, a_final) from a virgin history (one reduced assembly + LU with
+    # 4 right-hand sides per instance), outside the headline step.
+    st0 = torch.zeros((n_inst, 6, 400), dtype=torch.float64, device=dev)
+    st0[:, 0] = st0[:, 3] = st0[:, 4] = 1.0
+    fb = sched[:, -1].contiguous()
+    af = out["a_final"]
+    rom.effective_stiffness(geom, st0, fb, af)
+    ctx.check()
+    ctx.timings()
+    ctx.set_timing(True)
+    ms_ab = timed(torch, ws, 3, lambda: rom.effective_stiffness(geom, st0, fb, af))
+    ctx.set_timing(False)
+    tka = ctx.timings()
+    res["effective_stiffness"] = {"instances": n_inst, "ms": round(ms_ab / 3, 3),
+                                  "instances_per_s": ws * n_inst * 3 / (ms_ab * 1e-3),
+                                  "kernels_ms": {k: round(v[0] / 3, 3) for k, v in tka.items()}}
+    del st0
     if rank == 0 and ws == 1 and not args.no_cpu:
         import oracle
         orve = oracle.Rve(128, mats)

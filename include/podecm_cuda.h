@@ -149,6 +149,31 @@ int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* rom, int64
                            const double* geom, const double* sched, int K,
                            const podecm_newton* opts, double* pbar, int32_t* iters, double* resid,
                            double* a_final, int32_t* status);
+/* podecm_rom_solve_batch plus run_online's effective-stiffness request
+ * (pipeline.cpp:456-483): abar [n_inst][16] (nullable) =
+ * rom_effective_stiffness at the last macro gradient sched[K-1], the final
+ * reduced coordinates and the history committed at the start of the last
+ * increment.  Tensor4 storage: abar[s][r + 4c], r = i + 2j, c = k + 2l. */
+int podecm_rom_solve_batch_ex(podecm_ctx* ctx, void* stream, podecm_rom* rom, int64_t n_inst,
+                              const double* geom, const double* sched, int K,
+                              const podecm_newton* opts, double* pbar, int32_t* iters,
+                              double* resid, double* a_final, int32_t* status, double* abar);
+/* Replaces rom_effective_stiffness (rom.hpp:92-95; rom.cpp:202-241) for
+ * n_inst instances: geom [n_inst][2]; st0 [n_inst][6][Q] history at the
+ * ECM points (planes Fp00, Fp10, Fp01, Fp11, Fp_zz, xi); fbar [n_inst][4];
+ * a [n_inst][N] -> abar [n_inst][16] (layout as above), status (nullable). */
+int podecm_rom_effective_stiffness_batch(podecm_ctx* ctx, void* stream, podecm_rom* rom,
+                                         int64_t n_inst, const double* geom, const double* st0,
+                                         const double* fbar, const double* a, double* abar,
+                                         int32_t* status);
+/* Replaces rom_sensitivity (rom.hpp:100-104; rom.cpp:243-263) on the
+ * analytic geometry (a, b): central differences of the final homogenised
+ * stress with step h * max(1, |param|); 4 n_inst reduced solves in one batch.
+ * grad [n_inst][2][4] (d pbar / d a, d pbar / d b), status (nullable). */
+int podecm_rom_sensitivity_batch(podecm_ctx* ctx, void* stream, podecm_rom* rom, int64_t n_inst,
+                                 const double* geom, const double* sched, int K,
+                                 const podecm_newton* opts, double h, double* grad,
+                                 int32_t* status);
 
 /* ---- (iv) offline POD / ECM (BASELINE config 4) -------------------------
  * Replaces pod_impl / pod_diag (podkit.cpp:43-72, 117-127):

@@ -49,7 +49,9 @@ def lib(libm: str = "glibc"):
         l.orc_rve_assemble.restype = L
         l.orc_rve_assemble.argtypes = [P, L, P, P, P, P, P, P, P, P, P, I]
         l.orc_rom_solve.restype = L
-        l.orc_rom_solve.argtypes = [P, I, I, P, P, P, L, P, P, I, D, D, I, I, P, P, P, P, P, I]
+        l.orc_rom_solve.argtypes = [P, I, I, P, P, P, L, P, P, I, D, D, I, I, P, P, P, P, P, P, I]
+        l.orc_rom_effective_stiffness.restype = L
+        l.orc_rom_effective_stiffness.argtypes = [P, I, I, P, P, P, L, P, P, P, P, P, P, I]
         l.orc_stress_snapshots.restype = L
         l.orc_stress_snapshots.argtypes = [P, P, L, P, I]
         l.orc_max_threads.restype = I
@@ -154,7 +156,7 @@ class Rve:
         return W, int(fails)
 
     def rom_solve(self, ids, weights, mode_grads, geom, sched, eps_rel=1e-8, eps_abs=1e-12,
-                  max_iter=25, max_bisect=5, nthreads=0):
+                  max_iter=25, max_bisect=5, nthreads=0, abar=False):
         ids = np.ascontiguousarray(ids, dtype=np.int32)
         weights = np.ascontiguousarray(weights, dtype=np.float64)
         mg = np.ascontiguousarray(mode_grads, dtype=np.float64)
@@ -167,10 +169,49 @@ class Rve:
         resid = np.empty((n, K))
         af = np.empty((n, N))
         status = np.empty(n, np.int32)
+        ab = np.zeros((n, 16)) if abar else None
         lib().orc_rom_solve(self.h, N, Q, _p(ids), _p(weights), _p(mg), n, _p(geom), _p(sched), K,
                             eps_rel, eps_abs, max_iter, max_bisect, _p(pbar), _p(iters), _p(resid),
-                            _p(af), _p(status), nthreads)
-        return {"pbar": pbar, "iters": iters, "resid": resid, "a_final": af, "status": status}
+                            _p(af), _p(status), _p(ab) if abar else None, nthreads)
+        out = {"pbar": pbar, "iters": iters, "resid": resid, "a_final": af, "status": status}
+        if abar:
+            out["abar"] = ab
+        return out
+
+    def rom_effective_stiffness(self, ids, weights, mode_grads, geom, st0, fbar, a, nthreads=0):
+        """rom_effective_stiffness (rom.cpp:202-241): abar [n, 16] (Tensor4
+        storage r + 4c), status [n]."""
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        weights = np.ascontiguousarray(weights, dtype=np.float64)
+        mg = np.ascontiguousarray(mode_grads, dtype=np.float64)
+        geom, st0, fbar, a = (np.ascontiguousarray(x, dtype=np.float64) for x in (geom, st0, fbar, a))
+        Q, N = mg.shape[0], mg.shape[1]
+        n = geom.shape[0]
+        abar = np.zeros((n, 16))
+        status = np.empty(n, np.int32)
+        lib().orc_rom_effective_stiffness(self.h, N, Q, _p(ids), _p(weights), _p(mg), n, _p(geom), _p(st0),
+                                          _p(fbar), _p(a), _p(abar), _p(status), nthreads)
+        return abar, status
+
+    def rom_sensitivity(self, ids, weights, mode_grads, geom, sched, h, **kw):
+        """rom_sensitivity (rom.cpp:243-263) on the analytic geometry (a, b):
+        central differences of the final pbar, step h * max(1, |param|).
+        Returns grad [n, 2, 4] and status [n]."""
+        geom = np.ascontiguousarray(geom, dtype=np.float64)
+        sched = np.ascontiguousarray(sched, dtype=np.float64)
+        n = geom.shape[0]
+        grad = np.empty((n, 2, 4))
+        status = np.zeros(n, np.int32)
+        for k in range(2):
+            step = h * np.maximum(1.0, np.abs(geom[:, k]))
+            lo, hi = geom.copy(), geom.copy()
+            lo[:, k] -= step
+            hi[:, k] += step
+            rl = self.rom_solve(ids, weights, mode_grads, lo, sched, **kw)
+            rh = self.rom_solve(ids, weights, mode_grads, hi, sched, **kw)
+            grad[:, k, :] = (rh["pbar"][:, -1, :] - rl["pbar"][:, -1, :]) / (2.0 * step)[:, None]
+            status |= rl["status"] | rh["status"]
+        return grad, np.where(status != 0, 3, 0).astype(np.int32)
 
     def __del__(self):
         try:

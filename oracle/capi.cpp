@@ -210,11 +210,14 @@ long orc_rve_assemble(void* hp, long n_inst, const double* geom, const double* f
 // Batched hyper-reduced solve (rom_solve, rom.cpp:177-200) over instances.
 // ids[Q] ascending, weights[Q], mode_grads[Q][N][4]; geom[n_inst][2];
 // sched[n_inst][K][4] (flatten order); outputs pbar[n_inst][K][4],
-// iters[n_inst][K], resid[n_inst][K], a_final[n_inst][N]; status 0/3.
+// iters[n_inst][K], resid[n_inst][K], a_final[n_inst][N]; status 0/3;
+// abar[n_inst][16] (nullable): rom_effective_stiffness at the last increment
+// the way run_online requests it (pipeline.cpp:456-483).
 long orc_rom_solve(void* hp, int N, int Q, const int* ids, const double* weights,
                    const double* mode_grads, long n_inst, const double* geom, const double* sched,
                    int K, double eps_rel, double eps_abs, int max_iter, int max_bisect, double* pbar,
-                   int* iters, double* resid, double* a_final, int* status, int nthreads) {
+                   int* iters, double* resid, double* a_final, int* status, double* abar,
+                   int nthreads) {
   set_threads(nthreads);
   auto* h = static_cast<OrcRve*>(hp);
   const RveProblem& prob = h->prob;
@@ -243,13 +246,60 @@ long orc_rom_solve(void* hp, int N, int Q, const int* ids, const double* weights
       for (int k = 0; k < K; ++k)
         for (int c = 0; c < 4; ++c) sc[k].a[c] = sched[((size_t)s * K + k) * 4 + c];
       std::vector<double> af;
-      const auto recs = rom_solve(prob, model, fmi, dt, sc, o, max_bisect, &af);
+      std::vector<PlasticState> prev;
+      const auto recs = rom_solve(prob, model, fmi, dt, sc, o, max_bisect, &af, &prev);
+      if (abar && K > 0) rom_effective_stiffness(prob, model, fmi, dt, prev, sc[K - 1], af, abar + (size_t)s * 16);
       for (int k = 0; k < K; ++k) {
         for (int c = 0; c < 4; ++c) pbar[((size_t)s * K + k) * 4 + c] = recs[k].pbar.a[c];
         if (iters) iters[(size_t)s * K + k] = recs[k].iters;
         if (resid) resid[(size_t)s * K + k] = recs[k].residual;
       }
       if (a_final) std::memcpy(a_final + (size_t)s * N, af.data(), N * sizeof(double));
+      if (status) status[s] = 0;
+    } catch (const SolveError&) {
+      if (status) status[s] = 3;
+      ++fails;
+    }
+  }
+  return fails;
+}
+
+// rom_effective_stiffness (rom.cpp:202-241) per instance: geom[n][2],
+// st0[n][6][Q] planes (Fp00, Fp10, Fp01, Fp11, Fp_zz, xi), fbar[n][4],
+// a[n][N] -> abar[n][16]; status 0/3.
+long orc_rom_effective_stiffness(void* hp, int N, int Q, const int* ids, const double* weights,
+                                 const double* mode_grads, long n_inst, const double* geom,
+                                 const double* st0, const double* fbar, const double* a,
+                                 double* abar, int* status, int nthreads) {
+  set_threads(nthreads);
+  auto* h = static_cast<OrcRve*>(hp);
+  const RveProblem& prob = h->prob;
+  RomModel model;
+  model.N = N;
+  model.ids.assign(ids, ids + Q);
+  model.weights.assign(weights, weights + Q);
+  model.mode_grads.assign(mode_grads, mode_grads + (size_t)Q * N * 4);
+  long fails = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : fails)
+  for (long s = 0; s < n_inst; ++s) {
+    try {
+      const Morph mo = derive(prob.mesh, prob.cache,
+                              analytic_morph_d(prob.mesh, geom[2 * s], geom[2 * s + 1], h->r0));
+      std::vector<Mat2> fmi(Q);
+      std::vector<double> dt(Q);
+      std::vector<PlasticState> s0(Q);
+      const double* st = st0 + (size_t)s * 6 * Q;
+      for (int p = 0; p < Q; ++p) {
+        fmi[p] = mo.fmu_inv[ids[p]];
+        dt[p] = mo.det[ids[p]];
+        for (int c = 0; c < 4; ++c) s0[p].Fp.a[c] = st[(size_t)c * Q + p];
+        s0[p].Fp_zz = st[(size_t)4 * Q + p];
+        s0[p].xi = st[(size_t)5 * Q + p];
+      }
+      Mat2 fb;
+      for (int c = 0; c < 4; ++c) fb.a[c] = fbar[(size_t)s * 4 + c];
+      std::vector<double> av(a + (size_t)s * N, a + (size_t)(s + 1) * N);
+      rom_effective_stiffness(prob, model, fmi, dt, s0, fb, av, abar + (size_t)s * 16);
       if (status) status[s] = 0;
     } catch (const SolveError&) {
       if (status) status[s] = 3;

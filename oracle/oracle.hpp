@@ -193,6 +193,12 @@ std::vector<RomStepRecord> rom_solve(const RveProblem& prob, const RomModel& mod
                                      const std::vector<Mat2>& fmu_inv,
                                      const std::vector<double>& det,
                                      const std::vector<Mat2>& schedule, const NewtonOpts& opts,
-                                     int max_bisect, std::vector<double>* a_final);
+                                     int max_bisect, std::vector<double>* a_final,
+                                     std::vector<PlasticState>* prev_states = nullptr);
+// rom.cpp:202-241; out[r + 4c] (Tensor4 storage).  Throws SolveError.
+void rom_effective_stiffness(const RveProblem& prob, const RomModel& model,
+                             const std::vector<Mat2>& fmi, const std::vector<double>& det,
+                             const std::vector<PlasticState>& s0, const Mat2& fbar,
+                             const std::vector<double>& a, double out[16]);
 
 }  // namespace orc

@@ -1,8 +1,8 @@
 // ORACLE — TEST INFRASTRUCTURE ONLY (see oracle.hpp).
-// Restates /root/reference/proj/src/rom.cpp:16-200: right_mult_op,
+// Restates /root/reference/proj/src/rom.cpp:16-241: right_mult_op,
 // rom_assemble, rom_effective_stress, rom_solve_step (Newton with a dense
-// partial-pivot LU, Eigen::PartialPivLU semantics), the adaptive bisection
-// and rom_solve.
+// partial-pivot LU, Eigen::PartialPivLU semantics), the adaptive bisection,
+// rom_solve and rom_effective_stiffness.
 #include "oracle.hpp"
 
 #include <algorithm>
@@ -179,17 +179,20 @@ StepOut rom_step_adaptive(const RveProblem& prob, const RomModel& model,
 
 }  // namespace
 
-// rom.cpp:177-200
+// rom.cpp:177-200.  prev_states (nullable): the history committed at the
+// start of the last increment (run_online's prev_states, pipeline.cpp:456-468).
 std::vector<RomStepRecord> rom_solve(const RveProblem& prob, const RomModel& model,
                                      const std::vector<Mat2>& fmu_inv,
                                      const std::vector<double>& det,
                                      const std::vector<Mat2>& schedule, const NewtonOpts& opts,
-                                     int max_bisect, std::vector<double>* a_final) {
+                                     int max_bisect, std::vector<double>* a_final,
+                                     std::vector<PlasticState>* prev_states) {
   std::vector<PlasticState> states(model.ids.size());
   std::vector<double> a(model.N, 0.0);
   Mat2 fprev = Mat2::identity();
   std::vector<RomStepRecord> recs;
   for (const Mat2& fbar : schedule) {
+    if (prev_states) *prev_states = states;
     StepOut st = rom_step_adaptive(prob, model, fmu_inv, det, states, fprev, fbar, a, opts, max_bisect);
     fprev = fbar;
     states = st.states;
@@ -202,6 +205,69 @@ std::vector<RomStepRecord> rom_solve(const RveProblem& prob, const RomModel& mod
   }
   if (a_final) *a_final = a;
   return recs;
+}
+
+// rom.cpp:202-241: one reduced assembly at (states0, fbar, a) with the
+// tangent, one PartialPivLU of K and, per unit macro perturbation e_kl, the
+// condensed column  Abar(:, kl) = sum_p c A_p (e_kl + mapped_p^T q),
+// q = K^-1 rhs,  rhs = -sum_p c mapped_p (A_p e_kl).  out[r + 4c] (Tensor4
+// storage, r = i + 2j, c = k + 2l).
+void rom_effective_stiffness(const RveProblem& prob, const RomModel& model,
+                             const std::vector<Mat2>& fmi, const std::vector<double>& det,
+                             const std::vector<PlasticState>& s0, const Mat2& fbar,
+                             const std::vector<double>& a, double out[16]) {
+  const int n = model.N, np = (int)model.ids.size();
+  std::vector<PlasticState> s1(s0.size());
+  const RomAsm as = rom_assemble(prob, model, fmi, det, s0, s1, fbar, a);
+  // a_field: the tangent at every point (rom_assemble's a_field, rom.cpp:58-61)
+  std::vector<double> af((size_t)np * 16), mapped((size_t)np * n * 4);
+  for (int p = 0; p < np; ++p) {
+    const double* mg = &model.mode_grads[(size_t)p * n * 4];
+    const Mat2& m = fmi[p];
+    double* mp = &mapped[(size_t)p * n * 4];
+    for (int i = 0; i < n; ++i)
+      for (int ii = 0; ii < 2; ++ii)
+        for (int l = 0; l < 2; ++l)
+          mp[(size_t)i * 4 + ii + 2 * l] = mg[(size_t)i * 4 + ii] * m(0, l) + mg[(size_t)i * 4 + ii + 2] * m(1, l);
+    double fl[4] = {0, 0, 0, 0};
+    for (int c = 0; c < 4; ++c)
+      for (int i = 0; i < n; ++i) fl[c] += mp[(size_t)i * 4 + c] * a[i];
+    Mat2 F;
+    for (int c = 0; c < 4; ++c) F.a[c] = fbar.a[c] + fl[c];
+    large_strain_tangent(prob.material_at(model.ids[p]), s0[p], F, 1e-7, &af[(size_t)p * 16]);
+  }
+  for (int kl = 0; kl < 4; ++kl) {  // kl = k + 2l, k outer / l inner order is immaterial
+    std::vector<double> rhs(n, 0.0);
+    for (int p = 0; p < np; ++p) {
+      const double c = model.weights[p] * det[p];
+      const double* A = &af[(size_t)p * 16];
+      const double* mp = &mapped[(size_t)p * n * 4];
+      for (int i = 0; i < n; ++i) {
+        double acc = 0;
+        for (int r = 0; r < 4; ++r) acc += mp[(size_t)i * 4 + r] * A[r + 4 * kl];
+        rhs[i] -= c * acc;
+      }
+    }
+    const std::vector<double> q = lu_solve(as.k, n, rhs);
+    double col[4] = {0, 0, 0, 0};
+    for (int p = 0; p < np; ++p) {
+      const double c = model.weights[p] * det[p];
+      const double* A = &af[(size_t)p * 16];
+      const double* mp = &mapped[(size_t)p * n * 4];
+      double df[4];
+      for (int t = 0; t < 4; ++t) {
+        double acc = 0;
+        for (int i = 0; i < n; ++i) acc += mp[(size_t)i * 4 + t] * q[i];
+        df[t] = (t == kl ? 1.0 : 0.0) + acc;
+      }
+      for (int r = 0; r < 4; ++r) {
+        double acc = 0;
+        for (int t = 0; t < 4; ++t) acc += A[r + 4 * t] * df[t];
+        col[r] += c * acc;
+      }
+    }
+    for (int r = 0; r < 4; ++r) out[r + 4 * kl] = col[r] / prob.cell_volume;
+  }
 }
 
 }  // namespace orc

@@ -64,6 +64,11 @@ _SIGS = {
     "podecm_probe_math": (C.c_int, [P, P, C.c_int, I64, P, P, P]),
     "podecm_rom_solve_batch": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton),
                                          P, P, P, P, P]),
+    "podecm_rom_solve_batch_ex": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton),
+                                            P, P, P, P, P, P]),
+    "podecm_rom_effective_stiffness_batch": (C.c_int, [P, P, P, I64, P, P, P, P, P, P]),
+    "podecm_rom_sensitivity_batch": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton),
+                                               D, P, P]),
 }
 
 # every symbol include/podecm_cuda.h declares (checked by tests on CPU)

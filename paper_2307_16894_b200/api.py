@@ -269,9 +269,11 @@ class Rom:
         self.h = h
 
     def solve(self, geom: torch.Tensor, sched: torch.Tensor, opts: NewtonOpts | None = None,
-              out: dict | None = None) -> dict:
+              out: dict | None = None, abar: bool = False) -> dict:
         """Batched rom_solve (rom.cpp:177-200): pbar [n, K, 4] history,
-        iters [n, K], resid [n, K], a_final [n, N], status [n]."""
+        iters [n, K], resid [n, K], a_final [n, N], status [n].  abar=True adds
+        run_online's effective stiffness at the last increment
+        (pipeline.cpp:456-483): abar [n, 16], Tensor4 storage r + 4c."""
         opts = opts or NewtonOpts()
         n, K = sched.shape[0], sched.shape[1]
         dev = sched.device
@@ -283,13 +285,52 @@ class Rom:
         resid = o.get("resid") if o.get("resid") is not None else torch.empty((n, K), dtype=torch.float64, device=dev)
         af = o.get("a_final") if o.get("a_final") is not None else torch.empty((n, self.N), dtype=torch.float64, device=dev)
         status = o.get("status") if o.get("status") is not None else torch.empty(n, dtype=torch.int32, device=dev)
+        ab = torch.zeros((n, 16), dtype=torch.float64, device=dev) if abar else None
         oc = opts.c()
-        rc = self.lib.podecm_rom_solve_batch(self.ctx.h, self.ctx.stream(), self.h, n, _ptr(geom),
-                                             _ptr(sched), K, C.byref(oc), _ptr(pbar), _ptr(iters),
-                                             _ptr(resid), _ptr(af), _ptr(status))
+        rc = self.lib.podecm_rom_solve_batch_ex(self.ctx.h, self.ctx.stream(), self.h, n, _ptr(geom),
+                                                _ptr(sched), K, C.byref(oc), _ptr(pbar), _ptr(iters),
+                                                _ptr(resid), _ptr(af), _ptr(status), _ptr(ab))
         _lib.raise_for(rc, self.ctx.h, "podecm_rom_solve_batch")
         self.global_iterations = int(self.lib.podecm_rom_global_iterations(self.h))
-        return {"pbar": pbar, "iters": iters, "resid": resid, "a_final": af, "status": status}
+        r = {"pbar": pbar, "iters": iters, "resid": resid, "a_final": af, "status": status}
+        if abar:
+            r["abar"] = ab
+        return r
+
+    def effective_stiffness(self, geom: torch.Tensor, st0: torch.Tensor, fbar: torch.Tensor,
+                            a: torch.Tensor) -> dict:
+        """Batched rom_effective_stiffness (rom.cpp:202-241): history st0
+        [n, 6, Q] at the ECM points, fbar [n, 4], reduced coordinates a [n, N]
+        -> abar [n, 16] (Tensor4 storage r + 4c), status [n]."""
+        n = geom.shape[0]
+        _f64(geom, (n, 2), "geom")
+        _f64(st0, (n, 6, self.Q), "st0")
+        _f64(fbar, (n, 4), "fbar")
+        _f64(a, (n, self.N), "a")
+        abar = torch.zeros((n, 16), dtype=torch.float64, device=geom.device)
+        status = torch.empty(n, dtype=torch.int32, device=geom.device)
+        rc = self.lib.podecm_rom_effective_stiffness_batch(self.ctx.h, self.ctx.stream(), self.h, n, _ptr(geom),
+                                                           _ptr(st0), _ptr(fbar), _ptr(a), _ptr(abar),
+                                                           _ptr(status))
+        _lib.raise_for(rc, self.ctx.h, "podecm_rom_effective_stiffness_batch")
+        return {"abar": abar, "status": status}
+
+    def sensitivity(self, geom: torch.Tensor, sched: torch.Tensor, opts: NewtonOpts | None = None,
+                    h: float = 1e-4) -> dict:
+        """Batched rom_sensitivity (rom.cpp:243-263) over the analytic
+        geometry (a, b): grad [n, 2, 4] = d pbar_final / d (a, b), status [n]."""
+        opts = opts or NewtonOpts()
+        n, K = sched.shape[0], sched.shape[1]
+        _f64(geom, (n, 2), "geom")
+        _f64(sched, (n, K, 4), "sched")
+        grad = torch.zeros((n, 2, 4), dtype=torch.float64, device=geom.device)
+        status = torch.empty(n, dtype=torch.int32, device=geom.device)
+        oc = opts.c()
+        rc = self.lib.podecm_rom_sensitivity_batch(self.ctx.h, self.ctx.stream(), self.h, n, _ptr(geom),
+                                                   _ptr(sched), K, C.byref(oc), float(h), _ptr(grad),
+                                                   _ptr(status))
+        _lib.raise_for(rc, self.ctx.h, "podecm_rom_sensitivity_batch")
+        return {"grad": grad, "status": status}
 
     def __del__(self):
         try:

@@ -66,6 +66,9 @@ struct podecm_rom {
   double *d_morph = nullptr, *d_S = nullptr, *d_At = nullptr, *d_P = nullptr, *d_K = nullptr,
          *d_f = nullptr, *d_a = nullptr, *d_a0 = nullptr, *d_Fb = nullptr;
   RomCtl* d_ctl = nullptr;
+  double* d_CA = nullptr;     // effective stiffness: c_p A_p [cap][Q][16] (lazy)
+  double* d_Sprev = nullptr;  // effective stiffness: history at the start of the last increment
+  int64_t abar_cap = 0;
   int* d_nactive = nullptr;
   int* h_nactive = nullptr;
   int64_t last_global_iters = 0;
@@ -84,6 +87,10 @@ void free_work(podecm_rom* r) {
   cudaFree(r->d_a0);
   cudaFree(r->d_Fb);
   cudaFree(r->d_ctl);
+  cudaFree(r->d_CA);
+  cudaFree(r->d_Sprev);
+  r->d_CA = r->d_Sprev = nullptr;
+  r->abar_cap = 0;
   r->d_morph = r->d_S = r->d_At = r->d_P = r->d_K = r->d_f = r->d_a = r->d_a0 = r->d_Fb = nullptr;
   r->d_ctl = nullptr;
   r->cap = 0;
@@ -93,7 +100,7 @@ void free_work(podecm_rom* r) {
 __global__ void k_rom_init_points(int64_t n, int Q, int nq, double r0, const int32_t* ids,
                                   const double* nodes, const int32_t* elems, const double* grad,
                                   const double* geom, double* morph, double* S, int64_t cap,
-                                  RomCtl* ctl) {
+                                  RomCtl* ctl, double* Sprev) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= n * Q) return;
   const int64_t s = tid / Q;
@@ -117,6 +124,8 @@ __global__ void k_rom_init_points(int64_t n, int Q, int nq, double r0, const int
   double* st = S + (size_t)s * 6 * Q;  // buffer 0 = committed virgin history
   const double v[6] = {1.0, 0.0, 0.0, 1.0, 1.0, 0.0};
   for (int t = 0; t < 6; ++t) st[(size_t)t * Q + p] = v[t];
+  if (Sprev)
+    for (int t = 0; t < 6; ++t) Sprev[((size_t)s * 6 + t) * Q + p] = v[t];
   (void)cap;
   (void)nq;
 }
@@ -166,6 +175,8 @@ struct PointArgs {
   double* P;   // [n][Q][4]
   double* Fb;  // [n][4][Q]
   RomCtl* ctl;
+  const double* S0;  // effective-stiffness stage: frozen history [n][6][Q]
+  double* CA;        // effective-stiffness stage: c_p A_p [n][Q][16]
 };
 
 // F at every ECM point: F = Fbar + R(Fmu^-1)^T (G_p^T a) (rom.cpp:48-50).  CTA =
@@ -238,8 +249,9 @@ __global__ void __launch_bounds__(256) k_rom_F(PointArgs g) {
 
 // Material at every ECM point (one thread per point, C1-style register
 // budget): P, FD tangent, trial history, then the mapped operators
-// At = c R A R^T and Pt = c R P.
-template <int MINB>
+// At = c R A R^T and Pt = c R P.  ABAR (rom_effective_stiffness,
+// rom.cpp:206-207): history from g.S0, no trial history, and c A kept too.
+template <int MINB, bool ABAR = false>
 __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable tab) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= g.n * g.Q) return;
@@ -257,7 +269,7 @@ __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable t
   const double det = mo[(size_t)4 * g.Q + p];
   const MatConst& pm = tab.m[g.reg[p]];
   const int cur = c->cur;
-  const double* s0p = g.S + ((size_t)cur * g.cap + s) * 6 * g.Q;
+  const double* s0p = ABAR ? g.S0 + (size_t)s * 6 * g.Q : g.S + ((size_t)cur * g.cap + s) * 6 * g.Q;
   double* s1p = g.S + ((size_t)(cur ^ 1) * g.cap + s) * 6 * g.Q;
   double fp[4];
 #pragma unroll
@@ -267,10 +279,12 @@ __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable t
   double P[4];
   FullOut fo;
   bool ok = lsu_eval<true>(pm, z, F, P, &fo);
+  if (!ABAR) {
 #pragma unroll
-  for (int t = 0; t < 4; ++t) s1p[(size_t)t * g.Q + p] = fo.fp[t];
-  s1p[(size_t)4 * g.Q + p] = fo.fpzz;
-  s1p[(size_t)5 * g.Q + p] = fo.xi;
+    for (int t = 0; t < 4; ++t) s1p[(size_t)t * g.Q + p] = fo.fp[t];
+    s1p[(size_t)4 * g.Q + p] = fo.fpzz;
+    s1p[(size_t)5 * g.Q + p] = fo.xi;
+  }
   double* Pp = g.P + ((size_t)s * g.Q + p) * 4;
 #pragma unroll
   for (int t = 0; t < 4; ++t) Pp[t] = P[t];
@@ -289,6 +303,11 @@ __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable t
     // T[r] = sum_l m(r>>1, l) col[(r&1) + 2l].
     double T0[4];
     auto sink = [&](int e, const double col[4]) {
+      if (ABAR) {
+        double* ca = g.CA + ((size_t)s * g.Q + p) * 16 + 4 * e;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) ca[r] = cw * col[r];
+      }
       double Tc[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
@@ -502,9 +521,103 @@ struct NewtonArgs {
   int32_t* status;
   int* nactive;
   unsigned int* fail;
+  const double* S;  // [2][cap][6][Q]
+  int64_t cap;
+  double* Sprev;  // nullable: committed history at the start of increment K-1
 };
 
 constexpr int kNW = 4;  // warps (instances) per Newton CTA
+
+// Dense LU with partial pivoting (Eigen PartialPivLU semantics: pivot = first
+// row of max |a_ik|, rows swapped whole, unit-lower L) of the column-major
+// Ks (ld LD) in SMEM by one warp, solving NR right-hand sides rhs[c*N + i] in
+// place: the forward substitution is fused into the elimination and the
+// transpositions are applied to the RHS in order (PartialPivLU::solve).
+template <int NR>
+__device__ __forceinline__ void warp_lu_solve(double* Ks, int LD, int N, double* rhs, int lane) {
+  for (int k = 0; k < N; ++k) {
+    double best = -1.0;
+    int bi = N;
+    for (int i = k + lane; i < N; i += 32) {
+      const double v = fabs(Ks[k * LD + i]);
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (bi != k) {
+      for (int j = lane; j < N; j += 32) {
+        const double t0 = Ks[j * LD + k];
+        Ks[j * LD + k] = Ks[j * LD + bi];
+        Ks[j * LD + bi] = t0;
+      }
+      if (lane < NR) {
+        const double t0 = rhs[lane * N + k];
+        rhs[lane * N + k] = rhs[lane * N + bi];
+        rhs[lane * N + bi] = t0;
+      }
+    }
+    __syncwarp();
+    const double d = Ks[k * LD + k];
+    if (best != 0.0) {
+      const double rd = __drcp_rn(d);  // correctly rounded: div_rcp == '/'
+      for (int i = k + 1 + lane; i < N; i += 32) Ks[k * LD + i] = div_rcp(Ks[k * LD + i], d, rd);
+    }
+    __syncwarp();
+    double bk[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) bk[c] = rhs[c * N + k];
+    for (int i = k + 1 + lane; i < N; i += 32) {
+      const double l = Ks[k * LD + i];
+      // rank-1 update of the trailing block, 4 independent columns in flight
+      int j = k + 1;
+      for (; j + 3 < N; j += 4) {
+        const double u0 = Ks[j * LD + k], u1 = Ks[(j + 1) * LD + k];
+        const double u2 = Ks[(j + 2) * LD + k], u3 = Ks[(j + 3) * LD + k];
+        const double a0 = Ks[j * LD + i], a1 = Ks[(j + 1) * LD + i];
+        const double a2 = Ks[(j + 2) * LD + i], a3 = Ks[(j + 3) * LD + i];
+        Ks[j * LD + i] = fma(-l, u0, a0);
+        Ks[(j + 1) * LD + i] = fma(-l, u1, a1);
+        Ks[(j + 2) * LD + i] = fma(-l, u2, a2);
+        Ks[(j + 3) * LD + i] = fma(-l, u3, a3);
+      }
+      for (; j < N; ++j) Ks[j * LD + i] = fma(-l, Ks[j * LD + k], Ks[j * LD + i]);
+#pragma unroll
+      for (int c = 0; c < NR; ++c) rhs[c * N + i] = fma(-l, bk[c], rhs[c * N + i]);
+    }
+    __syncwarp();
+  }
+  // back substitution with U, lanes over rows
+  for (int k = N - 1; k >= 0; --k) {
+    const double ukk = Ks[k * LD + k];
+    const double ru = __drcp_rn(ukk);
+    double xk[NR];
+#pragma unroll
+    for (int c = 0; c < NR; ++c) xk[c] = div_rcp(rhs[c * N + k], ukk, ru);
+    __syncwarp();
+    if (lane < NR) {
+      double v = xk[0];
+#pragma unroll
+      for (int c = 1; c < NR; ++c) v = (c == lane) ? xk[c] : v;
+      rhs[lane * N + k] = v;
+    }
+    for (int i = lane; i < k; i += 32) {
+      const double u = Ks[k * LD + i];
+#pragma unroll
+      for (int c = 0; c < NR; ++c) rhs[c * N + i] = fma(-u, xk[c], rhs[c * N + i]);
+    }
+    __syncwarp();
+  }
+}
 
 __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
   extern __shared__ double smn[];
@@ -561,73 +674,7 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
     }
     for (int i = lane; i < N; i += 32) rhs[i] = -g.f[(size_t)s * N + i];
     __syncwarp();
-    for (int k = 0; k < N; ++k) {
-      double best = -1.0;
-      int bi = N;
-      for (int i = k + lane; i < N; i += 32) {
-        const double v = fabs(Ks[k * LD + i]);
-        if (v > best) {
-          best = v;
-          bi = i;
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) {
-          best = ob;
-          bi = oi;
-        }
-      }
-      if (bi != k) {
-        for (int j = lane; j < N; j += 32) {
-          const double t0 = Ks[j * LD + k];
-          Ks[j * LD + k] = Ks[j * LD + bi];
-          Ks[j * LD + bi] = t0;
-        }
-        if (lane == 0) {  // P b: transpositions applied in order (PartialPivLU::solve)
-          const double t0 = rhs[k];
-          rhs[k] = rhs[bi];
-          rhs[bi] = t0;
-        }
-      }
-      __syncwarp();
-      const double d = Ks[k * LD + k];
-      if (best != 0.0) {
-        const double rd = __drcp_rn(d);  // correctly rounded: div_rcp == '/'
-        for (int i = k + 1 + lane; i < N; i += 32) Ks[k * LD + i] = div_rcp(Ks[k * LD + i], d, rd);
-      }
-      __syncwarp();
-      const double bk = rhs[k];
-      for (int i = k + 1 + lane; i < N; i += 32) {
-        const double l = Ks[k * LD + i];
-        // rank-1 update of the trailing block, 4 independent columns in flight
-        int j = k + 1;
-        for (; j + 3 < N; j += 4) {
-          const double u0 = Ks[j * LD + k], u1 = Ks[(j + 1) * LD + k];
-          const double u2 = Ks[(j + 2) * LD + k], u3 = Ks[(j + 3) * LD + k];
-          const double a0 = Ks[j * LD + i], a1 = Ks[(j + 1) * LD + i];
-          const double a2 = Ks[(j + 2) * LD + i], a3 = Ks[(j + 3) * LD + i];
-          Ks[j * LD + i] = fma(-l, u0, a0);
-          Ks[(j + 1) * LD + i] = fma(-l, u1, a1);
-          Ks[(j + 2) * LD + i] = fma(-l, u2, a2);
-          Ks[(j + 3) * LD + i] = fma(-l, u3, a3);
-        }
-        for (; j < N; ++j) Ks[j * LD + i] = fma(-l, Ks[j * LD + k], Ks[j * LD + i]);
-        rhs[i] = fma(-l, bk, rhs[i]);  // forward substitution with the unit-lower L, fused
-      }
-      __syncwarp();
-    }
-    // back substitution with U, lanes over rows
-    for (int k = N - 1; k >= 0; --k) {
-      const double ukk = Ks[k * LD + k];
-      const double xk = div_rcp(rhs[k], ukk, __drcp_rn(ukk));
-      __syncwarp();
-      if (lane == 0) rhs[k] = xk;
-      for (int i = lane; i < k; i += 32) rhs[i] = fma(-Ks[k * LD + i], xk, rhs[i]);
-      __syncwarp();
-    }
+    warp_lu_solve<1>(Ks, LD, N, rhs, lane);
     for (int i = lane; i < N; i += 32) g.a[(size_t)s * N + i] += rhs[i];
     if (lane == 0) c->it = it + 1;
   }
@@ -654,6 +701,7 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
     }
     for (int i = lane; i < N; i += 32) g.a0[(size_t)s * N + i] = g.a[(size_t)s * N + i];
     __syncwarp();
+    int adv = 0;  // entered the last increment: keep its start history (run_online prev_states)
     if (lane == 0) {
       c->iters_acc += it;
       c->cur ^= 1;  // commit the trial history
@@ -673,10 +721,17 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
           }
           c->dstack[0] = g.max_bisect;
           c->sp = 1;
+          adv = c->k == g.K - 1;
         }
       }
     }
     __syncwarp();
+    adv = __shfl_sync(0xffffffffu, adv, 0);
+    if (adv && g.Sprev) {
+      const double* src = g.S + ((size_t)c->cur * g.cap + s) * 6 * g.Q;
+      double* dst = g.Sprev + (size_t)s * 6 * g.Q;
+      for (int t = lane; t < 6 * g.Q; t += 32) dst[t] = src[t];
+    }
     if (!c->active && g.a_final)
       for (int i = lane; i < N; i += 32) g.a_final[(size_t)s * N + i] = g.a[(size_t)s * N + i];
   }
@@ -714,6 +769,197 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
   }
   __syncwarp();
   if (lane == 0 && c->active) atomicAdd(g.nactive, 1);
+}
+
+
+// ---- effective stiffness (rom_effective_stiffness, rom.cpp:202-241) -------
+// Per instance: K (k_rom_contract at the frozen history), then for the four
+// unit macro perturbations e_kl
+//   rhs_kl = -sum_p c_p B_p A_p e_kl,      q_kl = K^-1 rhs_kl   (one LU, 4 RHS)
+//   Abar(:, kl) = sum_p c_p A_p (e_kl + B_p^T q_kl)
+// with B_p = G_p R(Fmu_p^-1) (rom.cpp:218-219, 227-228).
+struct AbarArgs {
+  int64_t n;
+  int N, Q, Qpad, NP;
+  const double* G;      // [Qpad*4][NP]
+  const double* Gt;     // [N][4][Qpad]
+  const double* CA;     // [n][Q][16]
+  const double* Kg;     // [n][N][N]
+  const double* morph;  // [n][5][Q]
+  RomCtl* ctl;
+  double* abar;  // [n][16] column-major Tensor4::m
+  int32_t* status;
+  unsigned int* fail;
+};
+
+__global__ void __launch_bounds__(32 * kNW) k_rom_abar(AbarArgs g) {
+  extern __shared__ double sma[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int N = g.N, LD = N + 1, Q = g.Q;
+  double* Ks = sma + (size_t)warp * (N * LD + 4 * N + 32 * 17);
+  double* rhs = Ks + N * LD;  // [4][N]
+  double* sX = rhs + 4 * N;   // [32][17]: X_p = R_p (c_p A_p), one point per lane
+  const int64_t s = (int64_t)blockIdx.x * kNW + warp;
+  if (s >= g.n) return;
+  RomCtl* c = g.ctl + s;
+  if (!c->active) return;
+  if (c->asm_fail) {  // rom_assemble threw (material SolveError)
+    if (lane == 0) {
+      c->active = 0;
+      c->status = PODECM_ESOLVE;
+      if (g.status) g.status[s] = PODECM_ESOLVE;
+      atomicAdd(g.fail, 1u);
+    }
+    return;
+  }
+  {
+    const double* src = g.Kg + (size_t)s * N * N;
+    for (int t = lane; t < N * N; t += 32) {
+      const int i = t / N, j = t - i * N;
+      Ks[j * LD + i] = src[t];
+    }
+  }
+  const double* mo = g.morph + (size_t)s * 5 * Q;
+  const double* CA = g.CA + (size_t)s * Q * 16;
+  // rhs[c][i] = -sum_p sum_r G_p[i][r] X_p[r][c]; lanes over modes i
+  double acc[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) acc[h][cc] = 0.0;
+  for (int p0 = 0; p0 < Q; p0 += 32) {
+    const int p = p0 + lane;
+    if (p < Q) {
+      double m[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) m[t] = mo[(size_t)t * Q + p];
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {  // (R v)[i + 2j] = m(j,0) v[i] + m(j,1) v[i+2]
+          const int i = r & 1, j = r >> 1;
+          sX[lane * 17 + r + 4 * cc] =
+              fma(m[j + 2], CA[(size_t)p * 16 + 4 * cc + i + 2], m[j] * CA[(size_t)p * 16 + 4 * cc + i]);
+        }
+    }
+    __syncwarp();
+    const int np = min(32, Q - p0);
+    for (int pl = 0; pl < np; ++pl)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const double* gr = g.G + ((size_t)(p0 + pl) * 4 + r) * g.NP;
+        const double g0 = lane < N ? gr[lane] : 0.0, g1 = lane + 32 < N ? gr[lane + 32] : 0.0;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const double x = sX[pl * 17 + r + 4 * cc];
+          acc[0][cc] = fma(g0, x, acc[0][cc]);
+          acc[1][cc] = fma(g1, x, acc[1][cc]);
+        }
+      }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int cc = 0; cc < 4; ++cc) {
+    if (lane < N) rhs[cc * N + lane] = -acc[0][cc];
+    if (lane + 32 < N) rhs[cc * N + lane + 32] = -acc[1][cc];
+  }
+  __syncwarp();
+  warp_lu_solve<4>(Ks, LD, N, rhs, lane);
+  // Abar(:, cc) = sum_p CA_p (e_cc + R_p^T (G_p^T q_cc)); lanes over points
+  double ab[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) ab[t] = 0.0;
+  for (int p = lane; p < Q; p += 32) {
+    double m[4], ca[16];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) m[t] = mo[(size_t)t * Q + p];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) ca[t] = CA[(size_t)p * 16 + t];
+    double u[4][4];
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) u[cc][r] = 0.0;
+    for (int i = 0; i < N; ++i) {
+      double gv[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) gv[r] = g.Gt[((size_t)i * 4 + r) * g.Qpad + p];
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const double q = rhs[cc * N + i];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) u[cc][r] = fma(gv[r], q, u[cc][r]);
+      }
+    }
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      double df[4];  // e_cc + R^T u: (R^T u)[i + 2l] = m(0,l) u[i] + m(1,l) u[i+2]
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int i = t & 1, l = t >> 1;
+        df[t] = fma(m[1 + 2 * l], u[cc][i + 2], m[2 * l] * u[cc][i]) + (t == cc ? 1.0 : 0.0);
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) ab[r + 4 * cc] = fma(ca[r + 4 * t], df[t], ab[r + 4 * cc]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 16; ++t)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ab[t] += __shfl_xor_sync(0xffffffffu, ab[t], o);
+  if (lane < 16) {
+    double v = ab[0];
+#pragma unroll
+    for (int t = 1; t < 16; ++t) v = (t == lane) ? ab[t] : v;
+    g.abar[(size_t)s * 16 + lane] = v / 1.0;  // cell_volume (microfem.hpp:22)
+  }
+}
+
+// Effective-stiffness stage set-up: instance s is evaluated at fbar =
+// fb[s * fb_stride .. + 4] unless it already failed.
+__global__ void k_rom_abar_prep(int64_t n, const double* fb, int64_t fb_stride, RomCtl* ctl,
+                                const int32_t* status) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  RomCtl* c = ctl + s;
+  const bool ok = c->status == 0 && (!status || status[s] == 0);
+  c->active = ok ? 1 : 0;
+  c->asm_fail = 0;
+  c->sp = 1;
+  for (int t = 0; t < 4; ++t) c->fstack[0][4 + t] = fb[(size_t)s * fb_stride + t];
+}
+
+// rom_sensitivity (rom.cpp:243-263) on the analytic (a, b) geometry: the
+// batch of 4 n solves is ordered (s, k, lo/hi).
+__global__ void k_rom_sens_prep(int64_t n, double h, const double* geom, const double* sched, int K,
+                                double* geom4, double* sched4) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 4 * n) return;
+  const int64_t s = t >> 2;
+  const int k = (int)((t >> 1) & 1), hi = (int)(t & 1);
+  double gm[2] = {geom[2 * s], geom[2 * s + 1]};
+  const double step = h * fmax(1.0, fabs(gm[k]));
+  gm[k] = hi ? gm[k] + step : gm[k] - step;
+  geom4[2 * t] = gm[0];
+  geom4[2 * t + 1] = gm[1];
+  for (int u = 0; u < 4 * K; ++u) sched4[(size_t)t * 4 * K + u] = sched[(size_t)s * 4 * K + u];
+}
+
+__global__ void k_rom_sens_combine(int64_t n, double h, const double* geom, const double* pbar4, int K,
+                                   const int32_t* status4, double* grad, int32_t* status) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  bool ok = true;
+  for (int k = 0; k < 2; ++k) {
+    const double step = h * fmax(1.0, fabs(geom[2 * s + k]));
+    const int64_t lo = 4 * s + 2 * k, hi = lo + 1;
+    ok = ok && status4[lo] == 0 && status4[hi] == 0;
+    for (int c4 = 0; c4 < 4; ++c4)
+      grad[(s * 2 + k) * 4 + c4] = (pbar4[(hi * K + K - 1) * 4 + c4] - pbar4[(lo * K + K - 1) * 4 + c4]) / (2.0 * step);
+  }
+  if (status) status[s] = ok ? 0 : PODECM_ESOLVE;
 }
 
 // register budget of the point kernel (2 or 3 CTAs/SM); PODECM_ROM_POINT_MINB
@@ -757,7 +1003,240 @@ int ensure_cap(podecm_rom* r, int64_t n) {
   return PODECM_OK;
 }
 
+
+int ensure_abar(podecm_rom* r, int64_t n, bool sprev) {
+  if (r->abar_cap >= n && (!sprev || r->d_Sprev)) return PODECM_OK;
+  cudaFree(r->d_CA);
+  cudaFree(r->d_Sprev);
+  r->d_CA = r->d_Sprev = nullptr;
+  r->abar_cap = 0;
+  int rc = dalloc(r->ctx, &r->d_CA, (size_t)n * r->Q * 16);
+  if (!rc && sprev) rc = dalloc(r->ctx, &r->d_Sprev, (size_t)n * 6 * r->Q);
+  if (!rc) r->abar_cap = n;
+  return rc;
+}
+
+void set_attrs() {
+  static bool attr_set = false;
+  if (attr_set) return;
+  cudaFuncSetAttribute(k_rom_F, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(k_rom_newton, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_rom_abar, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_rom_contract<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<1>());
+  cudaFuncSetAttribute(k_rom_contract<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<2>());
+  cudaFuncSetAttribute(k_rom_contract<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<3>());
+  cudaFuncSetAttribute(k_rom_contract<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<4>());
+  cudaFuncSetAttribute(k_rom_contract<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<5>());
+  cudaFuncSetAttribute(k_rom_contract<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<6>());
+  cudaFuncSetAttribute(k_rom_contract<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<7>());
+  attr_set = true;
+}
+
+PointArgs point_args(podecm_rom* r, int64_t n) {
+  PointArgs pa;
+  pa.n = n;
+  pa.N = r->N;
+  pa.Q = r->Q;
+  pa.Qpad = r->Qpad;
+  pa.cap = r->cap;
+  pa.Gt = r->d_Gt;
+  pa.a = r->d_a;
+  pa.morph = r->d_morph;
+  pa.w = r->d_w;
+  pa.reg = r->d_reg;
+  pa.S = r->d_S;
+  pa.At = r->d_At;
+  pa.P = r->d_P;
+  pa.Fb = r->d_Fb;
+  pa.ctl = r->d_ctl;
+  pa.S0 = nullptr;
+  pa.CA = nullptr;
+  return pa;
+}
+
+ContractArgs contract_args(podecm_rom* r, int64_t n) {
+  ContractArgs ca;
+  ca.n = n;
+  ca.N = r->N;
+  ca.Q = r->Q;
+  ca.Qpad = r->Qpad;
+  ca.NT = r->NT;
+  ca.NP = r->NP;
+  ca.G = r->d_G;
+  ca.At = r->d_At;
+  ca.K = r->d_K;
+  ca.f = r->d_f;
+  ca.ctl = r->d_ctl;
+  return ca;
+}
+
+void launch_F(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, const PointArgs& pa) {
+  KTimer kt(ctx, s, "k_rom_F");
+  const dim3 gpt((r->Q + kPtsTile - 1) / kPtsTile, (unsigned)((pa.n + kFInst - 1) / kFInst));
+  const size_t smem_pt = ((size_t)r->N * 4 * kPtsTile + (size_t)kFInst * r->N) * sizeof(double);
+  k_rom_F<<<gpt, 256, smem_pt, s>>>(pa);
+}
+
+void launch_contract(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, const ContractArgs& ca) {
+  KTimer kt(ctx, s, "k_rom_contract");
+  const int gct = (int)((ca.n + kIPC - 1) / kIPC);
+  switch (r->NT) {
+    case 1: k_rom_contract<1><<<gct, 32 * 1 * kIPC, contract_smem_bytes<1>(), s>>>(ca); break;
+    case 2: k_rom_contract<2><<<gct, 32 * 2 * kIPC, contract_smem_bytes<2>(), s>>>(ca); break;
+    case 3: k_rom_contract<3><<<gct, 32 * 3 * kIPC, contract_smem_bytes<3>(), s>>>(ca); break;
+    case 4: k_rom_contract<4><<<gct, 32 * 4 * kIPC, contract_smem_bytes<4>(), s>>>(ca); break;
+    case 5: k_rom_contract<5><<<gct, 32 * 5 * kIPC, contract_smem_bytes<5>(), s>>>(ca); break;
+    case 6: k_rom_contract<6><<<gct, 32 * 6 * kIPC, contract_smem_bytes<6>(), s>>>(ca); break;
+    default: k_rom_contract<7><<<gct, 32 * 7 * kIPC, contract_smem_bytes<7>(), s>>>(ca); break;
+  }
+}
+
+// Effective-stiffness stage over n instances whose morph slice (d_morph),
+// reduced coordinates (d_a) and control blocks are staged: history S0
+// [n][6][Q], macro gradient fb[s * fb_stride ..].  Five launches.
+int abar_stage(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, int64_t n, const double* S0,
+               const double* fb, int64_t fb_stride, double* abar, int32_t* status) {
+  k_rom_abar_prep<<<grid_for(n, 128), 128, 0, s>>>(n, fb, fb_stride, r->d_ctl, status);
+  PointArgs pa = point_args(r, n);
+  pa.S0 = S0;
+  pa.CA = r->d_CA;
+  launch_F(ctx, s, r, pa);
+  {
+    KTimer kt(ctx, s, "k_rom_point_abar");
+    const int gp = grid_for(n * r->Q, 128);
+    if (point_minb() == 4)
+      k_rom_point<4, true><<<gp, 128, 0, s>>>(pa, r->rve->mats);
+    else
+      k_rom_point<5, true><<<gp, 128, 0, s>>>(pa, r->rve->mats);
+  }
+  launch_contract(ctx, s, r, contract_args(r, n));
+  AbarArgs aa;
+  aa.n = n;
+  aa.N = r->N;
+  aa.Q = r->Q;
+  aa.Qpad = r->Qpad;
+  aa.NP = r->NP;
+  aa.G = r->d_G;
+  aa.Gt = r->d_Gt;
+  aa.CA = r->d_CA;
+  aa.Kg = r->d_K;
+  aa.morph = r->d_morph;
+  aa.ctl = r->d_ctl;
+  aa.abar = abar;
+  aa.status = status;
+  aa.fail = ctx->d_fail;
+  {
+    KTimer kt(ctx, s, "k_rom_abar");
+    const size_t smem = (size_t)kNW * ((size_t)r->N * (r->N + 1) + 4 * r->N + 32 * 17) * sizeof(double);
+    k_rom_abar<<<(int)((n + kNW - 1) / kNW), 32 * kNW, smem, s>>>(aa);
+  }
+  PODECM_LAUNCHED(ctx, 5);
+  return PODECM_OK;
+}
+
+int check_solve_args(podecm_ctx* ctx, podecm_rom* r, int64_t n_inst, int K, const podecm_newton* opts) {
+  if (n_inst < 0 || K < 0) return set_err(ctx, PODECM_ECONFIG, "negative batch or schedule size");
+  if (opts->max_bisect < 0 || opts->max_bisect + 1 > kMaxStack)
+    return set_err(ctx, PODECM_ECONFIG, "max_bisect must lie in [0, 7]");
+  if (opts->max_iter < 0) return set_err(ctx, PODECM_ECONFIG, "max_iter must be >= 0");
+  if (r->NT > 7) return set_err(ctx, PODECM_ECONFIG, "rom: N > 55 exceeds the contraction tile");
+  return PODECM_OK;
+}
+
+int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst, const double* geom,
+                   const double* sched, int K, const podecm_newton* opts, double* pbar, int32_t* iters,
+                   double* resid, double* a_final, int32_t* status, double* abar) {
+  if (int rc = check_solve_args(ctx, r, n_inst, K, opts)) return rc;
+  if (n_inst == 0 || K == 0) return PODECM_OK;
+  if (!geom || !sched || !pbar) return set_err(ctx, PODECM_ECONFIG, "geom, sched, pbar required");
+  if (int rc = ensure_cap(r, n_inst)) return rc;
+  if (abar)
+    if (int rc = ensure_abar(r, n_inst, true)) return rc;
+  auto s = static_cast<cudaStream_t>(stream);
+  podecm_rve* rv = r->rve;
+  const int Q = r->Q, N = r->N;
+  set_attrs();
+  k_rom_init_inst<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, N, opts->max_bisect, sched, K,
+                                                        r->d_a, r->d_a0, r->d_ctl, status);
+  k_rom_init_points<<<grid_for(n_inst * Q, 128), 128, 0, s>>>(
+      n_inst, Q, rv->n_qp, rv->r0, r->d_ids, rv->d_nodes, rv->d_elems, rv->d_grad, geom,
+      r->d_morph, r->d_S, r->cap, r->d_ctl, abar ? r->d_Sprev : nullptr);
+  k_rom_fix_status<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, r->d_ctl, status, ctx->d_fail);
+  PODECM_LAUNCHED(ctx, 3);
+
+  const PointArgs pa = point_args(r, n_inst);
+  const ContractArgs ca = contract_args(r, n_inst);
+
+  NewtonArgs na;
+  na.n = n_inst;
+  na.N = N;
+  na.Q = Q;
+  na.K = K;
+  na.max_iter = opts->max_iter;
+  na.max_bisect = opts->max_bisect;
+  na.eps_rel = opts->eps_rel;
+  na.eps_abs = opts->eps_abs;
+  na.force_ref = opts->force_ref;
+  na.Kg = r->d_K;
+  na.f = r->d_f;
+  na.P = r->d_P;
+  na.morph = r->d_morph;
+  na.w = r->d_w;
+  na.sched = sched;
+  na.a = r->d_a;
+  na.a0 = r->d_a0;
+  na.ctl = r->d_ctl;
+  na.pbar = pbar;
+  na.iters = iters;
+  na.resid = resid;
+  na.a_final = a_final;
+  na.status = status;
+  na.nactive = r->d_nactive;
+  na.fail = ctx->d_fail;
+  na.S = r->d_S;
+  na.cap = r->cap;
+  na.Sprev = abar ? r->d_Sprev : nullptr;
+  const size_t smem_nt = (size_t)kNW * ((size_t)N * (N + 1) + 2 * N) * sizeof(double);
+  const int gnt = (int)((n_inst + kNW - 1) / kNW);
+
+  const int64_t max_global = (int64_t)K * (opts->max_iter + 1) * (2ll << opts->max_bisect) + 8;
+  for (int64_t it = 0; it < max_global; ++it) {
+    launch_F(ctx, s, r, pa);
+    {
+      KTimer kt(ctx, s, "k_rom_point");
+      const int gp = grid_for(n_inst * Q, 128);
+      if (point_minb() == 4)
+        k_rom_point<4><<<gp, 128, 0, s>>>(pa, rv->mats);
+      else
+        k_rom_point<5><<<gp, 128, 0, s>>>(pa, rv->mats);
+    }
+    launch_contract(ctx, s, r, ca);
+    PODECM_CUDA_TRY(ctx, cudaMemsetAsync(r->d_nactive, 0, sizeof(int), s));
+    {
+      KTimer kt(ctx, s, "k_rom_newton");
+      k_rom_newton<<<gnt, 32 * kNW, smem_nt, s>>>(na);
+    }
+    PODECM_LAUNCHED(ctx, 4);
+    if ((it & 3) == 3) {
+      PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(r->h_nactive, r->d_nactive, sizeof(int),
+                                           cudaMemcpyDeviceToHost, s));
+      PODECM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+      if (*r->h_nactive == 0) {
+        r->last_global_iters = it + 1;
+        break;
+      }
+    }
+    r->last_global_iters = it + 1;
+  }
+  // failed instances -> context flag (podecm_check reports SolveError)
+  if (abar)  // run_online's effective_stiffness request (pipeline.cpp:481-483)
+    return abar_stage(ctx, s, r, n_inst, r->d_Sprev, sched + (size_t)(K - 1) * 4, (int64_t)K * 4, abar,
+                      status);
+  return PODECM_OK;
+}
+
 }  // namespace
+
 
 extern "C" {
 
@@ -838,145 +1317,77 @@ int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t
                            const podecm_newton* opts, double* pbar, int32_t* iters, double* resid,
                            double* a_final, int32_t* status) {
   if (!ctx || !r || !opts) return PODECM_ECONFIG;
-  if (n_inst < 0 || K < 0) return set_err(ctx, PODECM_ECONFIG, "negative batch or schedule size");
-  if (n_inst == 0 || K == 0) return PODECM_OK;
-  if (!geom || !sched || !pbar) return set_err(ctx, PODECM_ECONFIG, "geom, sched, pbar required");
-  if (opts->max_bisect < 0 || opts->max_bisect + 1 > kMaxStack)
-    return set_err(ctx, PODECM_ECONFIG, "max_bisect must lie in [0, 7]");
-  if (opts->max_iter < 0) return set_err(ctx, PODECM_ECONFIG, "max_iter must be >= 0");
+  return rom_solve_impl(ctx, stream, r, n_inst, geom, sched, K, opts, pbar, iters, resid, a_final, status,
+                        nullptr);
+}
+
+int podecm_rom_solve_batch_ex(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
+                              const double* geom, const double* sched, int K,
+                              const podecm_newton* opts, double* pbar, int32_t* iters,
+                              double* resid, double* a_final, int32_t* status, double* abar) {
+  if (!ctx || !r || !opts) return PODECM_ECONFIG;
+  return rom_solve_impl(ctx, stream, r, n_inst, geom, sched, K, opts, pbar, iters, resid, a_final, status,
+                        abar);
+}
+
+int podecm_rom_effective_stiffness_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
+                                         const double* geom, const double* st0, const double* fbar,
+                                         const double* a, double* abar, int32_t* status) {
+  if (!ctx || !r) return PODECM_ECONFIG;
+  if (n_inst < 0) return set_err(ctx, PODECM_ECONFIG, "negative batch size");
+  if (n_inst == 0) return PODECM_OK;
+  if (!geom || !st0 || !fbar || !a || !abar)
+    return set_err(ctx, PODECM_ECONFIG, "geom, st0, fbar, a, abar required");
   if (r->NT > 7) return set_err(ctx, PODECM_ECONFIG, "rom: N > 55 exceeds the contraction tile");
   if (int rc = ensure_cap(r, n_inst)) return rc;
+  if (int rc = ensure_abar(r, n_inst, false)) return rc;
   auto s = static_cast<cudaStream_t>(stream);
   podecm_rve* rv = r->rve;
-  const int Q = r->Q, N = r->N;
-  k_rom_init_inst<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, N, opts->max_bisect, sched, K,
-                                                        r->d_a, r->d_a0, r->d_ctl, status);
-  k_rom_init_points<<<grid_for(n_inst * Q, 128), 128, 0, s>>>(
-      n_inst, Q, rv->n_qp, rv->r0, r->d_ids, rv->d_nodes, rv->d_elems, rv->d_grad, geom,
-      r->d_morph, r->d_S, r->cap, r->d_ctl);
+  set_attrs();
+  k_rom_init_inst<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, r->N, 0, fbar, 1, r->d_a, r->d_a0,
+                                                        r->d_ctl, status);
+  k_rom_init_points<<<grid_for(n_inst * r->Q, 128), 128, 0, s>>>(
+      n_inst, r->Q, rv->n_qp, rv->r0, r->d_ids, rv->d_nodes, rv->d_elems, rv->d_grad, geom,
+      r->d_morph, r->d_S, r->cap, r->d_ctl, nullptr);
   k_rom_fix_status<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, r->d_ctl, status, ctx->d_fail);
   PODECM_LAUNCHED(ctx, 3);
+  PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(r->d_a, a, (size_t)n_inst * r->N * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, s));
+  return abar_stage(ctx, s, r, n_inst, st0, fbar, 4, abar, status);
+}
 
-  PointArgs pa;
-  pa.n = n_inst;
-  pa.N = N;
-  pa.Q = Q;
-  pa.Qpad = r->Qpad;
-  pa.cap = r->cap;
-  pa.Gt = r->d_Gt;
-  pa.a = r->d_a;
-  pa.morph = r->d_morph;
-  pa.w = r->d_w;
-  pa.reg = r->d_reg;
-  pa.S = r->d_S;
-  pa.At = r->d_At;
-  pa.P = r->d_P;
-  pa.Fb = r->d_Fb;
-  pa.ctl = r->d_ctl;
-  const size_t smem_pt = ((size_t)N * 4 * kPtsTile + (size_t)kFInst * N) * sizeof(double);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_rom_F, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-    cudaFuncSetAttribute(k_rom_newton, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_rom_contract<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<1>());
-    cudaFuncSetAttribute(k_rom_contract<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<2>());
-    cudaFuncSetAttribute(k_rom_contract<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<3>());
-    cudaFuncSetAttribute(k_rom_contract<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<4>());
-    cudaFuncSetAttribute(k_rom_contract<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<5>());
-    cudaFuncSetAttribute(k_rom_contract<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<6>());
-    cudaFuncSetAttribute(k_rom_contract<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<7>());
-    attr_set = true;
+int podecm_rom_sensitivity_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
+                                 const double* geom, const double* sched, int K,
+                                 const podecm_newton* opts, double h, double* grad, int32_t* status) {
+  if (!ctx || !r || !opts) return PODECM_ECONFIG;
+  if (int rc = check_solve_args(ctx, r, n_inst, K, opts)) return rc;
+  if (n_inst == 0) return PODECM_OK;
+  if (K == 0) return set_err(ctx, PODECM_ECONFIG, "rom_sensitivity needs a non-empty schedule");
+  if (!geom || !sched || !grad) return set_err(ctx, PODECM_ECONFIG, "geom, sched, grad required");
+  if (!(h > 0.0)) return set_err(ctx, PODECM_ECONFIG, "rom_sensitivity: h must be > 0");
+  auto s = static_cast<cudaStream_t>(stream);
+  const int64_t n4 = 4 * n_inst;
+  double *geom4 = nullptr, *sched4 = nullptr, *pbar4 = nullptr;
+  int32_t* status4 = nullptr;
+  PODECM_CUDA_TRY(ctx, cudaMallocAsync(&geom4, (size_t)n4 * 2 * sizeof(double), s));
+  PODECM_CUDA_TRY(ctx, cudaMallocAsync(&sched4, (size_t)n4 * K * 4 * sizeof(double), s));
+  PODECM_CUDA_TRY(ctx, cudaMallocAsync(&pbar4, (size_t)n4 * K * 4 * sizeof(double), s));
+  PODECM_CUDA_TRY(ctx, cudaMallocAsync(&status4, (size_t)n4 * sizeof(int32_t), s));
+  k_rom_sens_prep<<<grid_for(n4, 128), 128, 0, s>>>(n_inst, h, geom, sched, K, geom4, sched4);
+  PODECM_LAUNCHED(ctx, 1);
+  int rc = rom_solve_impl(ctx, stream, r, n4, geom4, sched4, K, opts, pbar4, nullptr, nullptr, nullptr,
+                          status4, nullptr);
+  if (!rc) {
+    k_rom_sens_combine<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, h, geom, pbar4, K, status4, grad,
+                                                             status);
+    rc = cudaGetLastError() == cudaSuccess ? PODECM_OK : set_err(ctx, PODECM_ECUDA, "launch");
+    if (!rc) PODECM_LAUNCHED(ctx, 1);
   }
-  const dim3 gpt((Q + kPtsTile - 1) / kPtsTile, (unsigned)((n_inst + kFInst - 1) / kFInst));
-
-  ContractArgs ca;
-  ca.n = n_inst;
-  ca.N = N;
-  ca.Q = Q;
-  ca.Qpad = r->Qpad;
-  ca.NT = r->NT;
-  ca.NP = r->NP;
-  ca.G = r->d_G;
-  ca.At = r->d_At;
-  ca.K = r->d_K;
-  ca.f = r->d_f;
-  ca.ctl = r->d_ctl;
-  const int gct = (int)((n_inst + kIPC - 1) / kIPC);
-
-  NewtonArgs na;
-  na.n = n_inst;
-  na.N = N;
-  na.Q = Q;
-  na.K = K;
-  na.max_iter = opts->max_iter;
-  na.max_bisect = opts->max_bisect;
-  na.eps_rel = opts->eps_rel;
-  na.eps_abs = opts->eps_abs;
-  na.force_ref = opts->force_ref;
-  na.Kg = r->d_K;
-  na.f = r->d_f;
-  na.P = r->d_P;
-  na.morph = r->d_morph;
-  na.w = r->d_w;
-  na.sched = sched;
-  na.a = r->d_a;
-  na.a0 = r->d_a0;
-  na.ctl = r->d_ctl;
-  na.pbar = pbar;
-  na.iters = iters;
-  na.resid = resid;
-  na.a_final = a_final;
-  na.status = status;
-  na.nactive = r->d_nactive;
-  na.fail = ctx->d_fail;
-  const size_t smem_nt = (size_t)kNW * ((size_t)N * (N + 1) + 2 * N) * sizeof(double);
-  const int gnt = (int)((n_inst + kNW - 1) / kNW);
-
-  const int64_t max_global = (int64_t)K * (opts->max_iter + 1) * (2ll << opts->max_bisect) + 8;
-  for (int64_t it = 0; it < max_global; ++it) {
-    {
-      KTimer kt(ctx, s, "k_rom_F");
-      k_rom_F<<<gpt, 256, smem_pt, s>>>(pa);
-    }
-    {
-      KTimer kt(ctx, s, "k_rom_point");
-      const int gp = grid_for(n_inst * Q, 128);
-      if (point_minb() == 4)
-        k_rom_point<4><<<gp, 128, 0, s>>>(pa, rv->mats);
-      else
-        k_rom_point<5><<<gp, 128, 0, s>>>(pa, rv->mats);
-    }
-    {
-      KTimer kt(ctx, s, "k_rom_contract");
-      switch (r->NT) {
-        case 1: k_rom_contract<1><<<gct, 32 * 1 * kIPC, contract_smem_bytes<1>(), s>>>(ca); break;
-        case 2: k_rom_contract<2><<<gct, 32 * 2 * kIPC, contract_smem_bytes<2>(), s>>>(ca); break;
-        case 3: k_rom_contract<3><<<gct, 32 * 3 * kIPC, contract_smem_bytes<3>(), s>>>(ca); break;
-        case 4: k_rom_contract<4><<<gct, 32 * 4 * kIPC, contract_smem_bytes<4>(), s>>>(ca); break;
-        case 5: k_rom_contract<5><<<gct, 32 * 5 * kIPC, contract_smem_bytes<5>(), s>>>(ca); break;
-        case 6: k_rom_contract<6><<<gct, 32 * 6 * kIPC, contract_smem_bytes<6>(), s>>>(ca); break;
-        default: k_rom_contract<7><<<gct, 32 * 7 * kIPC, contract_smem_bytes<7>(), s>>>(ca); break;
-      }
-    }
-    PODECM_CUDA_TRY(ctx, cudaMemsetAsync(r->d_nactive, 0, sizeof(int), s));
-    {
-      KTimer kt(ctx, s, "k_rom_newton");
-      k_rom_newton<<<gnt, 32 * kNW, smem_nt, s>>>(na);
-    }
-    PODECM_LAUNCHED(ctx, 4);
-    if ((it & 3) == 3) {
-      PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(r->h_nactive, r->d_nactive, sizeof(int),
-                                           cudaMemcpyDeviceToHost, s));
-      PODECM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
-      if (*r->h_nactive == 0) {
-        r->last_global_iters = it + 1;
-        break;
-      }
-    }
-    r->last_global_iters = it + 1;
-  }
-  // failed instances -> context flag (podecm_check reports SolveError)
-  return PODECM_OK;
+  cudaFreeAsync(geom4, s);
+  cudaFreeAsync(sched4, s);
+  cudaFreeAsync(pbar4, s);
+  cudaFreeAsync(status4, s);
+  return rc;
 }
 
 }  // extern "C"
