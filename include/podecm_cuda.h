@@ -175,6 +175,27 @@ int podecm_rom_sensitivity_batch(podecm_ctx* ctx, void* stream, podecm_rom* rom,
                                  const podecm_newton* opts, double h, double* grad,
                                  int32_t* status);
 
+/* ---- batched RomMicroEngine (twoscale.hpp:55-80; twoscale.cpp:53-96) ----
+ * n hyper-reduced micro engines (one per macro Gauss point) sharing one
+ * RomModel; each keeps its committed history, reduced coordinates, macro
+ * gradient and force_ref on the device.  geom [n][2] (a, b) of every engine;
+ * stretch_bounds (host, nullable) = [3][2] (lo, hi) of (F00, F11, F01). */
+typedef struct podecm_rom_engines podecm_rom_engines;
+int podecm_rom_engines_create(podecm_ctx* ctx, podecm_rom* rom, int64_t n, const double* geom,
+                              const double* stretch_bounds, podecm_rom_engines** out);
+void podecm_rom_engines_destroy(podecm_rom_engines* eng);
+/* MicroEngine::respond for all engines at once: fbar [n][4] -> pbar [n][4],
+ * abar [n][16] (nullable), Newton iterations [n] (nullable), status [n]
+ * (nullable; 3 = SolveError of that engine's rom_solve_step_adaptive). */
+int podecm_rom_engines_respond(podecm_ctx* ctx, void* stream, podecm_rom_engines* eng,
+                               const double* fbar, const podecm_newton* opts, double* pbar,
+                               double* abar, int32_t* iters, int32_t* status);
+/* MicroEngine::commit for all engines. */
+int podecm_rom_engines_commit(podecm_ctx* ctx, void* stream, podecm_rom_engines* eng);
+/* RomMicroEngine::out_of_range per engine -> counts [n] (device). */
+int podecm_rom_engines_out_of_range(podecm_ctx* ctx, void* stream, const podecm_rom_engines* eng,
+                                    int32_t* counts);
+
 /* ---- (iv) offline POD / ECM (BASELINE config 4) -------------------------
  * Replaces pod_impl / pod_diag (podkit.cpp:43-72, 117-127):
  * C = S^T diag(g) S (n_snap x n_snap, symmetric) for the column-major

@@ -52,6 +52,13 @@ def lib(libm: str = "glibc"):
         l.orc_rom_solve.argtypes = [P, I, I, P, P, P, L, P, P, I, D, D, I, I, P, P, P, P, P, P, I]
         l.orc_rom_effective_stiffness.restype = L
         l.orc_rom_effective_stiffness.argtypes = [P, I, I, P, P, P, L, P, P, P, P, P, P, I]
+        l.orc_rom_engines_create.restype = P
+        l.orc_rom_engines_create.argtypes = [P, I, I, P, P, P, L, P, P, D, D, I, I]
+        l.orc_rom_engines_destroy.argtypes = [P]
+        l.orc_rom_engines_respond.restype = L
+        l.orc_rom_engines_respond.argtypes = [P, P, P, P, P, P, I]
+        l.orc_rom_engines_commit.argtypes = [P]
+        l.orc_rom_engines_out_of_range.argtypes = [P, P]
         l.orc_stress_snapshots.restype = L
         l.orc_stress_snapshots.argtypes = [P, P, L, P, I]
         l.orc_max_threads.restype = I
@@ -109,11 +116,14 @@ def material_batch(F, st, mats, region=None, h_rel=1e-7, tangent=True, nthreads=
 class Rve:
     """Structured Q4 RveProblem restated on the CPU."""
 
-    def __init__(self, n_cells, mats, r0=0.25):
+    def __init__(self, n_cells, mats, r0=0.25, libm="glibc"):
+        """libm="pdm": the device's portable exp/log instead of glibc's
+        (separates the algorithm from the libm floor)."""
         m = _mats(mats)
-        self.h = lib().orc_rve_create(n_cells, r0, _p(m), len(mats))
+        self.L = lib(libm)
+        self.h = self.L.orc_rve_create(n_cells, r0, _p(m), len(mats))
         info = np.zeros(6, dtype=np.int64)
-        lib().orc_rve_info(self.h, _p(info))
+        self.L.orc_rve_info(self.h, _p(info))
         self.n_nodes, self.n_elems, self.n_qp, self.n_red, self.nnz, self.anchor = (int(x) for x in info)
 
     def export(self):
@@ -121,14 +131,14 @@ class Rve:
              "regions": np.empty(self.n_elems, np.int32), "grad": np.empty((self.n_qp, 4, 2)),
              "w": np.empty(self.n_qp), "node_dof": np.empty(self.n_nodes, np.int32),
              "row_ptr": np.empty(self.n_red + 1, np.int32), "col_idx": np.empty(self.nnz, np.int32)}
-        lib().orc_rve_export(self.h, *(_p(t[k]) for k in ("nodes", "elems", "regions", "grad", "w",
+        self.L.orc_rve_export(self.h, *(_p(t[k]) for k in ("nodes", "elems", "regions", "grad", "w",
                                                           "node_dof", "row_ptr", "col_idx")))
         return t
 
     def morph(self, a, b):
         fmi = np.empty((4, self.n_qp))
         det = np.empty(self.n_qp)
-        rc = lib().orc_rve_morph(self.h, a, b, _p(fmi), _p(det))
+        rc = self.L.orc_rve_morph(self.h, a, b, _p(fmi), _p(det))
         return fmi, det, rc
 
     def assemble(self, geom, fbar, w_red, st0, tangent=True, states1=True, store_stress=False,
@@ -143,7 +153,7 @@ class Rve:
         s1 = np.empty((n, 6, self.n_qp)) if states1 else None
         pf = np.empty((n, 4, self.n_qp)) if store_stress else None
         status = np.empty(n, np.int32)
-        lib().orc_rve_assemble(self.h, n, _p(geom), _p(fbar), _p(w_red), _p(st0), _p(s1), _p(f), _p(K),
+        self.L.orc_rve_assemble(self.h, n, _p(geom), _p(fbar), _p(w_red), _p(st0), _p(s1), _p(f), _p(K),
                                _p(pf), _p(status), nthreads)
         return {"f": f, "K": K, "st1": s1, "p_field": pf, "status": status}
 
@@ -152,7 +162,7 @@ class Rve:
         U = np.asfortranarray(U, dtype=np.float64)
         L = U.shape[1]
         W = np.empty((L, self.n_qp, 4))
-        fails = lib().orc_stress_snapshots(self.h, U.ctypes.data_as(C.c_void_p), L, _p(W), nthreads)
+        fails = self.L.orc_stress_snapshots(self.h, U.ctypes.data_as(C.c_void_p), L, _p(W), nthreads)
         return W, int(fails)
 
     def rom_solve(self, ids, weights, mode_grads, geom, sched, eps_rel=1e-8, eps_abs=1e-12,
@@ -170,7 +180,7 @@ class Rve:
         af = np.empty((n, N))
         status = np.empty(n, np.int32)
         ab = np.zeros((n, 16)) if abar else None
-        lib().orc_rom_solve(self.h, N, Q, _p(ids), _p(weights), _p(mg), n, _p(geom), _p(sched), K,
+        self.L.orc_rom_solve(self.h, N, Q, _p(ids), _p(weights), _p(mg), n, _p(geom), _p(sched), K,
                             eps_rel, eps_abs, max_iter, max_bisect, _p(pbar), _p(iters), _p(resid),
                             _p(af), _p(status), _p(ab) if abar else None, nthreads)
         out = {"pbar": pbar, "iters": iters, "resid": resid, "a_final": af, "status": status}
@@ -189,7 +199,7 @@ class Rve:
         n = geom.shape[0]
         abar = np.zeros((n, 16))
         status = np.empty(n, np.int32)
-        lib().orc_rom_effective_stiffness(self.h, N, Q, _p(ids), _p(weights), _p(mg), n, _p(geom), _p(st0),
+        self.L.orc_rom_effective_stiffness(self.h, N, Q, _p(ids), _p(weights), _p(mg), n, _p(geom), _p(st0),
                                           _p(fbar), _p(a), _p(abar), _p(status), nthreads)
         return abar, status
 
@@ -216,7 +226,53 @@ class Rve:
     def __del__(self):
         try:
             if self.h:
-                lib().orc_rve_destroy(self.h)
+                self.L.orc_rve_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class RomEngines:
+    """Batch of RomMicroEngine (twoscale.cpp:53-96) on the oracle: respond /
+    commit / out_of_range, one engine per geometry (a, b)."""
+
+    def __init__(self, rve: "Rve", ids, weights, mode_grads, geom, bounds=None, eps_rel=1e-8,
+                 eps_abs=1e-12, max_iter=25, max_bisect=5):
+        self._keep = [np.ascontiguousarray(ids, dtype=np.int32), np.ascontiguousarray(weights, dtype=np.float64),
+                      np.ascontiguousarray(mode_grads, dtype=np.float64)]
+        ids, weights, mg = self._keep
+        geom = np.ascontiguousarray(geom, dtype=np.float64)
+        self.n = geom.shape[0]
+        self.N = mg.shape[1]
+        b = None if bounds is None else np.ascontiguousarray(bounds, dtype=np.float64).reshape(6)
+        self.rve = rve
+        self.h = self.rve.L.orc_rom_engines_create(rve.h, self.N, ids.shape[0], _p(ids), _p(weights), _p(mg), self.n,
+                                              _p(geom), _p(b), eps_rel, eps_abs, max_iter, max_bisect)
+
+    def respond(self, fbar, abar=False, nthreads=0):
+        fbar = np.ascontiguousarray(fbar, dtype=np.float64)
+        pbar = np.empty((self.n, 4))
+        ab = np.empty((self.n, 16)) if abar else None
+        iters = np.empty(self.n, np.int32)
+        status = np.empty(self.n, np.int32)
+        self.rve.L.orc_rom_engines_respond(self.h, _p(fbar), _p(pbar), _p(ab), _p(iters), _p(status), nthreads)
+        out = {"pbar": pbar, "iters": iters, "status": status}
+        if abar:
+            out["abar"] = ab
+        return out
+
+    def commit(self):
+        self.rve.L.orc_rom_engines_commit(self.h)
+
+    def out_of_range(self):
+        out = np.empty(self.n, np.int32)
+        self.rve.L.orc_rom_engines_out_of_range(self.h, _p(out))
+        return out
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.rve.L.orc_rom_engines_destroy(self.h)
                 self.h = None
         except Exception:
             pass

@@ -30,6 +30,11 @@ struct OrcRve {
   Csr pattern;
 };
 
+struct OrcEngines {
+  RomModel model;
+  std::vector<RomMicroEngine> eng;
+};
+
 void set_threads(int nt) { omp_set_num_threads(nt > 0 ? nt : omp_get_num_procs()); }
 
 }  // namespace
@@ -307,6 +312,77 @@ long orc_rom_effective_stiffness(void* hp, int N, int Q, const int* ids, const d
     }
   }
   return fails;
+}
+
+// Batched RomMicroEngine (twoscale.cpp:53-96): n engines on geometries
+// geom[n][2]; bounds (nullable) [3][2].
+void* orc_rom_engines_create(void* hp, int N, int Q, const int* ids, const double* weights,
+                             const double* mode_grads, long n, const double* geom, const double* bounds,
+                             double eps_rel, double eps_abs, int max_iter, int max_bisect) {
+  auto* h = static_cast<OrcRve*>(hp);
+  auto* e = new OrcEngines;
+  e->model.N = N;
+  e->model.ids.assign(ids, ids + Q);
+  e->model.weights.assign(weights, weights + Q);
+  e->model.mode_grads.assign(mode_grads, mode_grads + (size_t)Q * N * 4);
+  e->eng.resize(n);
+  for (long s = 0; s < n; ++s) {
+    RomMicroEngine& g = e->eng[s];
+    g.prob = &h->prob;
+    g.model = &e->model;
+    const Morph mo = derive(h->prob.mesh, h->prob.cache,
+                            analytic_morph_d(h->prob.mesh, geom[2 * s], geom[2 * s + 1], h->r0));
+    g.fmi.resize(Q);
+    g.det.resize(Q);
+    for (int p = 0; p < Q; ++p) {
+      g.fmi[p] = mo.fmu_inv[ids[p]];
+      g.det[p] = mo.det[ids[p]];
+    }
+    g.opts.eps_rel = eps_rel;
+    g.opts.eps_abs = eps_abs;
+    g.opts.max_iter = max_iter;
+    g.max_bisect = max_bisect;
+    if (bounds) g.bounds.assign(bounds, bounds + 6);
+    g.states.assign(Q, PlasticState());
+    g.a.assign(N, 0.0);
+  }
+  return e;
+}
+
+void orc_rom_engines_destroy(void* eh) { delete static_cast<OrcEngines*>(eh); }
+
+// fbar[n][4] -> pbar[n][4], abar[n][16] (nullable), iters[n], status[n] 0/3
+long orc_rom_engines_respond(void* eh, const double* fbar, double* pbar, double* abar, int* iters,
+                             int* status, int nthreads) {
+  set_threads(nthreads);
+  auto* e = static_cast<OrcEngines*>(eh);
+  const long n = (long)e->eng.size();
+  long fails = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : fails)
+  for (long s = 0; s < n; ++s) {
+    try {
+      Mat2 fb, pb;
+      for (int c = 0; c < 4; ++c) fb.a[c] = fbar[4 * s + c];
+      int it = 0;
+      e->eng[s].respond(fb, &pb, abar ? abar + 16 * s : nullptr, &it);
+      for (int c = 0; c < 4; ++c) pbar[4 * s + c] = pb.a[c];
+      if (iters) iters[s] = it;
+      status[s] = 0;
+    } catch (const SolveError&) {
+      status[s] = 3;
+      ++fails;
+    }
+  }
+  return fails;
+}
+
+void orc_rom_engines_commit(void* eh) {
+  for (auto& g : static_cast<OrcEngines*>(eh)->eng) g.commit();
+}
+
+void orc_rom_engines_out_of_range(void* eh, int* out) {
+  auto* e = static_cast<OrcEngines*>(eh);
+  for (size_t s = 0; s < e->eng.size(); ++s) out[s] = e->eng[s].out_of_range;
 }
 
 // Weighted stress snapshots for ECM (ecm.cpp:10-18 on the parent cell):

@@ -201,4 +201,23 @@ void rom_effective_stiffness(const RveProblem& prob, const RomModel& model,
                              const std::vector<PlasticState>& s0, const Mat2& fbar,
                              const std::vector<double>& a, double out[16]);
 
+// twoscale.hpp:55-80 (RomMicroEngine): per-engine committed history,
+// reduced coordinates, macro gradient and force_ref.
+struct RomMicroEngine {
+  const RveProblem* prob = nullptr;
+  const RomModel* model = nullptr;
+  std::vector<Mat2> fmi;
+  std::vector<double> det;
+  NewtonOpts opts;
+  int max_bisect = 5;
+  std::vector<double> bounds;  // empty or (lo, hi) x 3 for (F00, F11, F01)
+  std::vector<PlasticState> states, states_trial;
+  std::vector<double> a, a_trial;
+  Mat2 fbar_committed = Mat2::identity(), fbar_trial = Mat2::identity();
+  double force_ref = 0.0;
+  int out_of_range = 0;
+  void respond(const Mat2& fbar, Mat2* pbar, double* abar, int* iters);
+  void commit();
+};
+
 }  // namespace orc

@@ -270,4 +270,34 @@ void rom_effective_stiffness(const RveProblem& prob, const RomModel& model,
   }
 }
 
+// twoscale.cpp:53-96
+void RomMicroEngine::respond(const Mat2& fbar, Mat2* pbar, double* abar, int* iters) {
+  if (bounds.size() == 6) {
+    const double comp[3] = {fbar(0, 0), fbar(1, 1), fbar(0, 1)};
+    for (int k = 0; k < 3; ++k)
+      if (comp[k] < bounds[2 * k] || comp[k] > bounds[2 * k + 1]) {
+        ++out_of_range;
+        break;
+      }
+  }
+  NewtonOpts o = opts;
+  o.force_ref = std::max(o.force_ref, force_ref);
+  StepOut step = rom_step_adaptive(*prob, *model, fmi, det, states, fbar_committed, fbar, a, o, max_bisect);
+  force_ref = std::max(force_ref, step.initial_residual);
+  states_trial = std::move(step.states);
+  a_trial = step.a;
+  fbar_trial = fbar;
+  *pbar = step.pbar;
+  if (iters) *iters = step.iters;
+  if (abar) rom_effective_stiffness(*prob, *model, fmi, det, states, fbar, a_trial, abar);
+}
+
+void RomMicroEngine::commit() {
+  if (!states_trial.empty()) {
+    states = states_trial;
+    a = a_trial;
+    fbar_committed = fbar_trial;
+  }
+}
+
 }  // namespace orc

@@ -69,6 +69,11 @@ _SIGS = {
     "podecm_rom_effective_stiffness_batch": (C.c_int, [P, P, P, I64, P, P, P, P, P, P]),
     "podecm_rom_sensitivity_batch": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton),
                                                D, P, P]),
+    "podecm_rom_engines_create": (C.c_int, [P, P, I64, P, P, C.POINTER(P)]),
+    "podecm_rom_engines_destroy": (None, [P]),
+    "podecm_rom_engines_respond": (C.c_int, [P, P, P, P, C.POINTER(podecm_newton), P, P, P, P]),
+    "podecm_rom_engines_commit": (C.c_int, [P, P, P]),
+    "podecm_rom_engines_out_of_range": (C.c_int, [P, P, P, P]),
 }
 
 # every symbol include/podecm_cuda.h declares (checked by tests on CPU)

@@ -410,3 +410,64 @@ def ecm_select(rve: Rve, H: torch.Tensor, W: torch.Tensor, opts: EcmOpts):
                                    C.byref(n), C.byref(rr), C.byref(it))
     _lib.raise_for(rc, rve.ctx.h, "podecm_ecm_select")
     return ids[: n.value].copy(), w[: n.value].copy(), rr.value, it.value
+
+
+class RomEngines:
+    """n RomMicroEngine instances (twoscale.hpp:55-80) on the device, one per
+    macro Gauss point: respond() evaluates all of them for a batch of trial
+    macro gradients from their committed histories, commit() accepts the
+    trials.  geom [n, 2] (a, b); stretch_bounds [(lo, hi)] * 3 for
+    (F00, F11, F01) or None."""
+
+    def __init__(self, rom: Rom, geom: torch.Tensor, stretch_bounds=None):
+        import numpy as np
+        self.rom = rom
+        self.ctx = rom.ctx
+        self.lib = rom.lib
+        self.n = geom.shape[0]
+        _f64(geom, (self.n, 2), "geom")
+        b = None
+        if stretch_bounds is not None:
+            b = np.ascontiguousarray(stretch_bounds, dtype=np.float64).reshape(6)
+        h = C.c_void_p()
+        rc = self.lib.podecm_rom_engines_create(self.ctx.h, rom.h, self.n, _ptr(geom),
+                                                None if b is None else b.ctypes.data_as(C.c_void_p), C.byref(h))
+        _lib.raise_for(rc, self.ctx.h, "podecm_rom_engines_create")
+        self.h = h
+
+    def respond(self, fbar: torch.Tensor, opts: NewtonOpts | None = None, abar: bool = False) -> dict:
+        """MicroEngine::respond for every engine: pbar [n, 4], abar [n, 16]
+        (Tensor4 storage r + 4c) if requested, iters [n], status [n]."""
+        opts = opts or NewtonOpts()
+        _f64(fbar, (self.n, 4), "fbar")
+        dev = fbar.device
+        pbar = torch.zeros((self.n, 4), dtype=torch.float64, device=dev)
+        ab = torch.zeros((self.n, 16), dtype=torch.float64, device=dev) if abar else None
+        iters = torch.zeros(self.n, dtype=torch.int32, device=dev)
+        status = torch.empty(self.n, dtype=torch.int32, device=dev)
+        oc = opts.c()
+        rc = self.lib.podecm_rom_engines_respond(self.ctx.h, self.ctx.stream(), self.h, _ptr(fbar), C.byref(oc),
+                                                 _ptr(pbar), _ptr(ab), _ptr(iters), _ptr(status))
+        _lib.raise_for(rc, self.ctx.h, "podecm_rom_engines_respond")
+        out = {"pbar": pbar, "iters": iters, "status": status}
+        if abar:
+            out["abar"] = ab
+        return out
+
+    def commit(self) -> None:
+        _lib.raise_for(self.lib.podecm_rom_engines_commit(self.ctx.h, self.ctx.stream(), self.h), self.ctx.h,
+                       "podecm_rom_engines_commit")
+
+    def out_of_range(self) -> torch.Tensor:
+        out = torch.empty(self.n, dtype=torch.int32, device="cuda")
+        _lib.raise_for(self.lib.podecm_rom_engines_out_of_range(self.ctx.h, self.ctx.stream(), self.h, _ptr(out)),
+                       self.ctx.h, "podecm_rom_engines_out_of_range")
+        return out
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.podecm_rom_engines_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass

@@ -46,6 +46,7 @@ constexpr int kInstTile = 8;    // material kernel: instances per CTA
 
 struct RomCtl {
   double tol, resid;
+  double r0, r0max;  // first residual of the current attempt; max over converged sub-steps
   double fstack[kMaxStack][8];  // (F_prev[4], F_target[4]) per pending task
   int dstack[kMaxStack];        // remaining bisection depth per task
   int sp, it, k, iters_acc, cur, active, status, asm_fail;
@@ -74,6 +75,16 @@ struct podecm_rom {
   int64_t last_global_iters = 0;
 };
 
+struct podecm_rom_engines {
+  podecm_rom* rom = nullptr;
+  int64_t n = 0;
+  bool has_bounds = false;
+  double bounds[6] = {0, 0, 0, 0, 0, 0};
+  double *d_geom = nullptr, *d_Sc = nullptr, *d_St = nullptr, *d_ac = nullptr, *d_at = nullptr,
+         *d_fc = nullptr, *d_ft = nullptr, *d_fref = nullptr, *d_ires = nullptr;
+  int32_t *d_ok = nullptr, *d_oor = nullptr, *d_status = nullptr;
+};
+
 namespace {
 
 void free_work(podecm_rom* r) {
@@ -100,7 +111,7 @@ void free_work(podecm_rom* r) {
 __global__ void k_rom_init_points(int64_t n, int Q, int nq, double r0, const int32_t* ids,
                                   const double* nodes, const int32_t* elems, const double* grad,
                                   const double* geom, double* morph, double* S, int64_t cap,
-                                  RomCtl* ctl, double* Sprev) {
+                                  RomCtl* ctl, double* Sprev, const double* S_start) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= n * Q) return;
   const int64_t s = tid / Q;
@@ -121,8 +132,10 @@ __global__ void k_rom_init_points(int64_t n, int Q, int nq, double r0, const int
     ctl[s].status = PODECM_ESOLVE;
     ctl[s].active = 0;
   }
-  double* st = S + (size_t)s * 6 * Q;  // buffer 0 = committed virgin history
-  const double v[6] = {1.0, 0.0, 0.0, 1.0, 1.0, 0.0};
+  double* st = S + (size_t)s * 6 * Q;  // buffer 0 = committed history (virgin or given)
+  double v[6] = {1.0, 0.0, 0.0, 1.0, 1.0, 0.0};
+  if (S_start)
+    for (int t = 0; t < 6; ++t) v[t] = S_start[((size_t)s * 6 + t) * Q + p];
   for (int t = 0; t < 6; ++t) st[(size_t)t * Q + p] = v[t];
   if (Sprev)
     for (int t = 0; t < 6; ++t) Sprev[((size_t)s * 6 + t) * Q + p] = v[t];
@@ -131,7 +144,8 @@ __global__ void k_rom_init_points(int64_t n, int Q, int nq, double r0, const int
 }
 
 __global__ void k_rom_init_inst(int64_t n, int N, int max_bisect, const double* sched, int K,
-                                double* a, double* a0, RomCtl* ctl, int32_t* status) {
+                                double* a, double* a0, RomCtl* ctl, int32_t* status,
+                                const double* fprev, const double* a_start) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   RomCtl c;
@@ -141,11 +155,14 @@ __global__ void k_rom_init_inst(int64_t n, int N, int max_bisect, const double* 
   c.dstack[0] = max_bisect;
   const double I[4] = {1.0, 0.0, 0.0, 1.0};
   for (int t = 0; t < 4; ++t) {
-    c.fstack[0][t] = I[t];
+    c.fstack[0][t] = fprev ? fprev[(size_t)s * 4 + t] : I[t];
     c.fstack[0][4 + t] = sched[((size_t)s * K + 0) * 4 + t];
   }
   ctl[s] = c;
-  for (int i = 0; i < N; ++i) a[(size_t)s * N + i] = a0[(size_t)s * N + i] = 0.0;
+  for (int i = 0; i < N; ++i) {
+    const double v = a_start ? a_start[(size_t)s * N + i] : 0.0;
+    a[(size_t)s * N + i] = a0[(size_t)s * N + i] = v;
+  }
   if (status) status[s] = 0;
 }
 
@@ -524,6 +541,8 @@ struct NewtonArgs {
   const double* S;  // [2][cap][6][Q]
   int64_t cap;
   double* Sprev;  // nullable: committed history at the start of increment K-1
+  const double* force_ref_inst;  // nullable [n]: per-instance force_ref (RomMicroEngine)
+  double* init_res;              // nullable [n][K]: RomStepResult::initial_residual
 };
 
 constexpr int kNW = 4;  // warps (instances) per Newton CTA
@@ -642,7 +661,11 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
   bool conv = false;
   int it = c->it;
   if (!fail) {
-    if (it == 0) c->tol = fmax(g.eps_rel * fmax(r, g.force_ref), g.eps_abs);
+    if (it == 0) {
+      const double fr = g.force_ref_inst ? fmax(g.force_ref, g.force_ref_inst[s]) : g.force_ref;
+      c->tol = fmax(g.eps_rel * fmax(r, fr), g.eps_abs);
+      c->r0 = r;
+    }
     if (r <= c->tol) {
       conv = true;
     } else if (it == g.max_iter) {
@@ -704,10 +727,13 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
     int adv = 0;  // entered the last increment: keep its start history (run_online prev_states)
     if (lane == 0) {
       c->iters_acc += it;
+      c->r0max = fmax(c->r0max, c->r0);  // rom.cpp:173 (failed attempts do not count)
       c->cur ^= 1;  // commit the trial history
       c->sp -= 1;
       c->it = 0;
       if (c->sp == 0) {
+        if (g.init_res) g.init_res[(size_t)s * g.K + c->k] = c->r0max;
+        c->r0max = 0.0;
         if (g.iters) g.iters[(size_t)s * g.K + c->k] = c->iters_acc;
         if (g.resid) g.resid[(size_t)s * g.K + c->k] = r;
         c->iters_acc = 0;
@@ -962,6 +988,74 @@ __global__ void k_rom_sens_combine(int64_t n, double h, const double* geom, cons
   if (status) status[s] = ok ? 0 : PODECM_ESOLVE;
 }
 
+
+// ---- batched RomMicroEngine (twoscale.cpp:53-96) ----------------------------
+struct Bounds {
+  double lo[3], hi[3];
+};
+
+// out_of_range_ (twoscale.cpp:66-74): (F00, F11, F01) outside the training box
+__global__ void k_eng_oor(int64_t n, const double* fbar, Bounds b, int32_t* oor) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const double comp[3] = {fbar[4 * s], fbar[4 * s + 3], fbar[4 * s + 2]};
+  for (int k = 0; k < 3; ++k)
+    if (comp[k] < b.lo[k] || comp[k] > b.hi[k]) {
+      oor[s] += 1;
+      break;
+    }
+}
+
+// successful respond: keep the trial (states, fbar) and raise force_ref
+// (twoscale.cpp:78-82); failed instances keep their previous trial
+__global__ void k_eng_keep(int64_t n, int Q, const int32_t* status, const RomCtl* ctl, const double* S,
+                           int64_t cap, const double* fbar, const double* init_res, double* St, double* ft,
+                           double* fref, int32_t* ok) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= n * Q) return;
+  const int64_t s = tid / Q;
+  const int p = (int)(tid - s * Q);
+  if (status[s] != 0) return;
+  const double* src = S + ((size_t)ctl[s].cur * cap + s) * 6 * Q;
+  for (int t = 0; t < 6; ++t) St[((size_t)s * 6 + t) * Q + p] = src[(size_t)t * Q + p];
+  if (p == 0) {
+    for (int t = 0; t < 4; ++t) ft[4 * s + t] = fbar[4 * s + t];
+    fref[s] = fmax(fref[s], init_res[s]);
+    ok[s] = 1;
+  }
+}
+
+// commit (twoscale.cpp:91-96): only engines that ever produced a trial
+__global__ void k_eng_commit(int64_t n, int Q, int N, const int32_t* ok, const double* St, const double* at,
+                             const double* ft, double* Sc, double* ac, double* fc) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= n * Q) return;
+  const int64_t s = tid / Q;
+  const int p = (int)(tid - s * Q);
+  if (!ok[s]) return;
+  for (int t = 0; t < 6; ++t) Sc[((size_t)s * 6 + t) * Q + p] = St[((size_t)s * 6 + t) * Q + p];
+  for (int i = p; i < N; i += Q) ac[(size_t)s * N + i] = at[(size_t)s * N + i];
+  if (p == 0)
+    for (int t = 0; t < 4; ++t) fc[4 * s + t] = ft[4 * s + t];
+}
+
+__global__ void k_eng_init(int64_t n, int Q, int N, double* Sc, double* ac, double* fc, double* fref,
+                           int32_t* ok, int32_t* oor) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= n * Q) return;
+  const int64_t s = tid / Q;
+  const int p = (int)(tid - s * Q);
+  const double v[6] = {1.0, 0.0, 0.0, 1.0, 1.0, 0.0};
+  for (int t = 0; t < 6; ++t) Sc[((size_t)s * 6 + t) * Q + p] = v[t];
+  for (int i = p; i < N; i += Q) ac[(size_t)s * N + i] = 0.0;
+  if (p == 0) {
+    for (int t = 0; t < 4; ++t) fc[4 * s + t] = v[t];
+    fref[s] = 0.0;
+    ok[s] = 0;
+    oor[s] = 0;
+  }
+}
+
 // register budget of the point kernel (2 or 3 CTAs/SM); PODECM_ROM_POINT_MINB
 int point_minb() {
   static int v = [] {
@@ -1143,9 +1237,21 @@ int check_solve_args(podecm_ctx* ctx, podecm_rom* r, int64_t n_inst, int K, cons
   return PODECM_OK;
 }
 
+// Start of a solve other than rom_solve's virgin one (RomMicroEngine::respond):
+// committed history, reduced coordinates, previous macro gradient and
+// force_ref per instance; initial_residual out.
+struct RomStart {
+  const double* S = nullptr;     // [n][6][Q]
+  const double* a = nullptr;     // [n][N]
+  const double* fprev = nullptr; // [n][4]
+  const double* fref = nullptr;  // [n]
+  double* init_res = nullptr;    // [n][K]
+};
+
 int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst, const double* geom,
                    const double* sched, int K, const podecm_newton* opts, double* pbar, int32_t* iters,
-                   double* resid, double* a_final, int32_t* status, double* abar) {
+                   double* resid, double* a_final, int32_t* status, double* abar,
+                   const RomStart& start = RomStart()) {
   if (int rc = check_solve_args(ctx, r, n_inst, K, opts)) return rc;
   if (n_inst == 0 || K == 0) return PODECM_OK;
   if (!geom || !sched || !pbar) return set_err(ctx, PODECM_ECONFIG, "geom, sched, pbar required");
@@ -1157,10 +1263,11 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
   const int Q = r->Q, N = r->N;
   set_attrs();
   k_rom_init_inst<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, N, opts->max_bisect, sched, K,
-                                                        r->d_a, r->d_a0, r->d_ctl, status);
+                                                        r->d_a, r->d_a0, r->d_ctl, status, start.fprev,
+                                                        start.a);
   k_rom_init_points<<<grid_for(n_inst * Q, 128), 128, 0, s>>>(
       n_inst, Q, rv->n_qp, rv->r0, r->d_ids, rv->d_nodes, rv->d_elems, rv->d_grad, geom,
-      r->d_morph, r->d_S, r->cap, r->d_ctl, abar ? r->d_Sprev : nullptr);
+      r->d_morph, r->d_S, r->cap, r->d_ctl, abar ? r->d_Sprev : nullptr, start.S);
   k_rom_fix_status<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, r->d_ctl, status, ctx->d_fail);
   PODECM_LAUNCHED(ctx, 3);
 
@@ -1196,6 +1303,8 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
   na.S = r->d_S;
   na.cap = r->cap;
   na.Sprev = abar ? r->d_Sprev : nullptr;
+  na.force_ref_inst = start.fref;
+  na.init_res = start.init_res;
   const size_t smem_nt = (size_t)kNW * ((size_t)N * (N + 1) + 2 * N) * sizeof(double);
   const int gnt = (int)((n_inst + kNW - 1) / kNW);
 
@@ -1345,10 +1454,10 @@ int podecm_rom_effective_stiffness_batch(podecm_ctx* ctx, void* stream, podecm_r
   podecm_rve* rv = r->rve;
   set_attrs();
   k_rom_init_inst<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, r->N, 0, fbar, 1, r->d_a, r->d_a0,
-                                                        r->d_ctl, status);
+                                                        r->d_ctl, status, nullptr, nullptr);
   k_rom_init_points<<<grid_for(n_inst * r->Q, 128), 128, 0, s>>>(
       n_inst, r->Q, rv->n_qp, rv->r0, r->d_ids, rv->d_nodes, rv->d_elems, rv->d_grad, geom,
-      r->d_morph, r->d_S, r->cap, r->d_ctl, nullptr);
+      r->d_morph, r->d_S, r->cap, r->d_ctl, nullptr, nullptr);
   k_rom_fix_status<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, r->d_ctl, status, ctx->d_fail);
   PODECM_LAUNCHED(ctx, 3);
   PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(r->d_a, a, (size_t)n_inst * r->N * sizeof(double),
@@ -1388,6 +1497,112 @@ int podecm_rom_sensitivity_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, i
   cudaFreeAsync(pbar4, s);
   cudaFreeAsync(status4, s);
   return rc;
+}
+
+
+int podecm_rom_engines_create(podecm_ctx* ctx, podecm_rom* rom, int64_t n, const double* geom,
+                              const double* stretch_bounds, podecm_rom_engines** out) {
+  if (!ctx || !rom || !out) return PODECM_ECONFIG;
+  *out = nullptr;
+  if (n < 1) return set_err(ctx, PODECM_ECONFIG, "engines: need n >= 1");
+  if (!geom) return set_err(ctx, PODECM_ECONFIG, "engines: geom required");
+  auto* e = new podecm_rom_engines;
+  e->rom = rom;
+  e->n = n;
+  if (stretch_bounds) {
+    e->has_bounds = true;
+    for (int t = 0; t < 6; ++t) e->bounds[t] = stretch_bounds[t];
+  }
+  const size_t Q = rom->Q, N = rom->N;
+  int rc = PODECM_OK;
+  if (!rc) rc = dalloc(ctx, &e->d_geom, (size_t)n * 2);
+  if (!rc) rc = dalloc(ctx, &e->d_Sc, (size_t)n * 6 * Q);
+  if (!rc) rc = dalloc(ctx, &e->d_St, (size_t)n * 6 * Q);
+  if (!rc) rc = dalloc(ctx, &e->d_ac, (size_t)n * N);
+  if (!rc) rc = dalloc(ctx, &e->d_at, (size_t)n * N);
+  if (!rc) rc = dalloc(ctx, &e->d_fc, (size_t)n * 4);
+  if (!rc) rc = dalloc(ctx, &e->d_ft, (size_t)n * 4);
+  if (!rc) rc = dalloc(ctx, &e->d_fref, (size_t)n);
+  if (!rc) rc = dalloc(ctx, &e->d_ires, (size_t)n);
+  if (!rc) rc = dalloc(ctx, &e->d_ok, (size_t)n);
+  if (!rc) rc = dalloc(ctx, &e->d_oor, (size_t)n);
+  if (!rc) rc = dalloc(ctx, &e->d_status, (size_t)n);
+  if (!rc && cudaMemcpy(e->d_geom, geom, (size_t)n * 2 * sizeof(double), cudaMemcpyDefault) != cudaSuccess)
+    rc = set_err(ctx, PODECM_ECUDA, "engines: geom copy failed");
+  if (!rc) {
+    k_eng_init<<<grid_for(n * (int64_t)Q, 128), 128>>>(n, (int)Q, (int)N, e->d_Sc, e->d_ac, e->d_fc, e->d_fref,
+                                                       e->d_ok, e->d_oor);
+    if (cudaDeviceSynchronize() != cudaSuccess) rc = set_err(ctx, PODECM_ECUDA, "engines: init failed");
+  }
+  if (rc) {
+    podecm_rom_engines_destroy(e);
+    return rc;
+  }
+  *out = e;
+  return PODECM_OK;
+}
+
+void podecm_rom_engines_destroy(podecm_rom_engines* e) {
+  if (!e) return;
+  for (double* p : {e->d_geom, e->d_Sc, e->d_St, e->d_ac, e->d_at, e->d_fc, e->d_ft, e->d_fref, e->d_ires})
+    cudaFree(p);
+  for (int32_t* p : {e->d_ok, e->d_oor, e->d_status}) cudaFree(p);
+  delete e;
+}
+
+int podecm_rom_engines_respond(podecm_ctx* ctx, void* stream, podecm_rom_engines* e, const double* fbar,
+                               const podecm_newton* opts, double* pbar, double* abar, int32_t* iters,
+                               int32_t* status) {
+  if (!ctx || !e || !opts) return PODECM_ECONFIG;
+  if (!fbar || !pbar) return set_err(ctx, PODECM_ECONFIG, "engines: fbar and pbar required");
+  auto s = static_cast<cudaStream_t>(stream);
+  podecm_rom* r = e->rom;
+  const int64_t n = e->n;
+  if (e->has_bounds) {
+    Bounds b;
+    for (int k = 0; k < 3; ++k) {
+      b.lo[k] = e->bounds[2 * k];
+      b.hi[k] = e->bounds[2 * k + 1];
+    }
+    k_eng_oor<<<grid_for(n, 128), 128, 0, s>>>(n, fbar, b, e->d_oor);
+    PODECM_LAUNCHED(ctx, 1);
+  }
+  int32_t* st = status ? status : e->d_status;
+  RomStart start;
+  start.S = e->d_Sc;
+  start.a = e->d_ac;
+  start.fprev = e->d_fc;
+  start.fref = e->d_fref;
+  start.init_res = e->d_ires;
+  if (int rc = rom_solve_impl(ctx, stream, r, n, e->d_geom, fbar, 1, opts, pbar, iters, nullptr, e->d_at, st,
+                              nullptr, start))
+    return rc;
+  k_eng_keep<<<grid_for(n * r->Q, 128), 128, 0, s>>>(n, r->Q, st, r->d_ctl, r->d_S, r->cap, fbar, e->d_ires,
+                                                     e->d_St, e->d_ft, e->d_fref, e->d_ok);
+  PODECM_LAUNCHED(ctx, 1);
+  if (abar) {  // rom_effective_stiffness(states_ committed, fbar, a_trial) (twoscale.cpp:85-88)
+    if (int rc = ensure_abar(r, n, false)) return rc;
+    return abar_stage(ctx, s, r, n, e->d_Sc, fbar, 4, abar, st);
+  }
+  return PODECM_OK;
+}
+
+int podecm_rom_engines_commit(podecm_ctx* ctx, void* stream, podecm_rom_engines* e) {
+  if (!ctx || !e) return PODECM_ECONFIG;
+  auto s = static_cast<cudaStream_t>(stream);
+  podecm_rom* r = e->rom;
+  k_eng_commit<<<grid_for(e->n * r->Q, 128), 128, 0, s>>>(e->n, r->Q, r->N, e->d_ok, e->d_St, e->d_at, e->d_ft,
+                                                          e->d_Sc, e->d_ac, e->d_fc);
+  PODECM_LAUNCHED(ctx, 1);
+  return PODECM_OK;
+}
+
+int podecm_rom_engines_out_of_range(podecm_ctx* ctx, void* stream, const podecm_rom_engines* e,
+                                    int32_t* counts) {
+  if (!ctx || !e || !counts) return PODECM_ECONFIG;
+  PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(counts, e->d_oor, (size_t)e->n * sizeof(int32_t),
+                                       cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)));
+  return PODECM_OK;
 }
 
 }  // extern "C"

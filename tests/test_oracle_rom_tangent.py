@@ -65,3 +65,19 @@ def test_sensitivity_definition(small):
     pl = o.rom_solve(m["ids"], m["weights"], m["mode_grads"], lo, sched)["pbar"][:, -1]
     ph = o.rom_solve(m["ids"], m["weights"], m["mode_grads"], hi, sched)["pbar"][:, -1]
     assert np.array_equal(g[:, k], (ph - pl) / (2.0 * step)[:, None])
+
+
+def test_engine_first_response_equals_rom_solve(small):
+    """RomMicroEngine::respond from the virgin state is rom_solve_step_adaptive
+    from (I, a = 0): the first response equals a one-increment rom_solve, and
+    responding twice without commit gives the same answer (twoscale.cpp:65-89)."""
+    import oracle
+    o, m = small
+    geom, sched = synth.rom_instances(3, 1, 8, 0.15)
+    e = oracle.RomEngines(o, m["ids"], m["weights"], m["mode_grads"], geom)
+    r1 = e.respond(sched[:, 0], abar=True)
+    r2 = e.respond(sched[:, 0], abar=True)
+    rs = o.rom_solve(m["ids"], m["weights"], m["mode_grads"], geom, sched, abar=True)
+    assert np.array_equal(r1["pbar"], rs["pbar"][:, 0]) and np.array_equal(r1["abar"], rs["abar"])
+    assert np.array_equal(r1["iters"], rs["iters"][:, 0])
+    assert np.array_equal(r1["pbar"], r2["pbar"])
