@@ -545,7 +545,7 @@ struct NewtonArgs {
   double* init_res;              // nullable [n][K]: RomStepResult::initial_residual
 };
 
-constexpr int kNW = 4;  // warps (instances) per Newton CTA
+constexpr int kNW = 1;  // warps (instances) per Newton CTA (SMEM-bound: 10 per SM)
 
 // Dense LU with partial pivoting (Eigen PartialPivLU semantics: pivot = first
 // row of max |a_ik|, rows swapped whole, unit-lower L) of the column-major
