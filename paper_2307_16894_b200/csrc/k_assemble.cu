@@ -1,18 +1,18 @@
 // K2 — batched full-order assembly of the Q4 RVE (BASELINE configs 0 and 2).
 //
 // Two kernels per chunk of instances, no atomics, bitwise reproducible:
-//   k_asm_qp     one thread per (instance, quadrature point): analytic morph
-//                (derive), F = Fbar + grad(w) Fmu^-1, the material point
-//                (P, FD tangent, history), then the 64 K-terms
-//                wq * gt_a . A . gt_b and 8 f-terms of that point
-//                (microfem.cpp:76-123) into an element-blocked scratch
-//                [e][term][k] that stays L2-resident for the chunk;
-//   k_asm_gather one thread per (instance, CSR slot or residual row): sums its
-//                terms in the reference's triplet order — exactly the order
-//                Eigen's setFromTriplets collapses duplicates in
-//                (microfem.cpp:125-128) — through the precomputed map.
-// Per chunk the scratch holds 72 doubles per qp; chunk size is chosen so it
-// fits comfortably in the 126 MB L2.
+//   k_asm_qp2    one thread per (instance, quadrature point), a quad of lanes
+//                per element: analytic morph (derive), F = Fbar + grad(w)
+//                Fmu^-1, the material point (P, FD tangent, history), then
+//                the element sums of the 64 K-terms wq * gt_a . A . gt_b and
+//                8 f-terms (microfem.cpp:76-123), written to their
+//                slot-ordered scratch positions;
+//   k_asm_gather_fused  one thread per (instance, CSR slot or residual row):
+//                a contiguous run of element sums added in element order.
+// Exact mode (PODECM_ASM_EXACT=1: k_asm_qp + k_asm_gather) stores every
+// per-qp term and sums each slot in the reference's triplet order — exactly
+// the order Eigen's setFromTriplets collapses duplicates in
+// (microfem.cpp:125-128).
 #include <algorithm>
 #include <cstdlib>
 
@@ -71,21 +71,17 @@ __device__ __forceinline__ void quad_reduce8(const double v[8], int k, double ou
   }
 }
 
-// FUSED = true (default): per-element sums of the 4 qp contributions are
-// formed in registers (quad butterfly) and the gather adds element sums in
-// element order: K and f are deterministic and differ from the reference's
-// strict triplet order only in the association inside one element (ulp
-// level).  FUSED = false (PODECM_ASM_EXACT=1): every per-qp term is stored and
-// the gather replays Eigen's setFromTriplets order exactly.
-template <bool FUSED, int MINB>
+// Exact mode (PODECM_ASM_EXACT=1): every per-qp term is stored element-
+// blocked and the gather replays Eigen's setFromTriplets order exactly.  The
+// default (k_asm_qp2 below) sums the 4 qp contributions of an element first
+// (quad butterfly), so K and f differ from the strict triplet order only in
+// the association inside one element (ulp level) and stay deterministic.
+template <int MINB>
 __global__ void __launch_bounds__(128, MINB) k_asm_qp(AsmArgs g, MatTable tab) {
-  const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)g.n_inst * g.n_qp;
-  const bool valid = tid0 < total;
-  if (!FUSED && !valid) return;
-  // FUSED: lanes past the end (whole quads, n_qp % 4 == 0) compute on a clamped
-  // index so the quad shuffles stay converged, and never store.
-  const int64_t tid = valid ? tid0 : total - 1;
+  const bool valid = tid < total;
+  if (!valid) return;
   const int c = (int)(tid / g.n_qp);
   const int q = (int)(tid - (int64_t)c * g.n_qp);
   const int64_t inst = g.inst0 + c;
@@ -175,7 +171,7 @@ __global__ void __launch_bounds__(128, MINB) k_asm_qp(AsmArgs g, MatTable tab) {
 #pragma unroll
     for (int j = 0; j < 2; ++j) gt[a][j] = gq[2 * a] * fmi[2 * j] + gq[2 * a + 1] * fmi[1 + 2 * j];
 
-  if (!FUSED) {
+  {
     // element-blocked scratch: [c][e][72][4], entry (term, k)
     double* sc = g.scratch + ((size_t)c * (nq >> 2) + e) * 72 * 4 + k;
 #pragma unroll
@@ -210,64 +206,187 @@ __global__ void __launch_bounds__(128, MINB) k_asm_qp(AsmArgs g, MatTable tab) {
       };
       ok = fd_tangent<false>(p, z, F, 1e-7, sink);
     }
-  } else {
-    // element sums go to their slot-ordered position: [c][n_groups]
-    double* sc = g.scratch + (size_t)c * g.n_groups;
-    const int32_t* ps = g.pos + (size_t)e * 72;
-    {
-      double v[8], o[2];
+  }
+  if (!ok && valid) {
+    if (g.status) g.status[inst] = PODECM_ESOLVE;
+    atomicAdd(g.fail, 1u);
+  }
+}
+
+
+// per-qp SMEM planes of the two-phase kernel: A (16), P (4), gt (8), wq (1)
+constexpr int kQPlanes = 29;
+
+// ---- default kernel: two phases per thread ------------------------------------
+// Phase 1 is the material point; its FD loop only streams tangent columns
+// into this thread's SMEM row (as the C1 kernel streams them to HBM), so no
+// element accumulator is live across the material evaluations.  Phase 2
+// reads the thread's A, P, gt, wq back and forms the element sums with the
+// quad butterfly.  Lanes past the end (whole quads, n_qp % 4 == 0) compute on
+// a clamped index so the shuffles stay converged, and never store.
+// (Measured on C2: 25.8 ms vs 30.6 ms for the single-phase kernel that
+// contracted each tangent column into element terms inside the FD loop.)
+constexpr int kQ2Thr = 128;
+
+template <int MINB>
+__global__ void __launch_bounds__(kQ2Thr, MINB) k_asm_qp2(AsmArgs g, MatTable tab) {
+  __shared__ double sq[kQPlanes * kQ2Thr];  // [plane][thread]
+  const int lt = threadIdx.x;
+  const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)g.n_inst * g.n_qp;
+  const bool valid = tid0 < total;
+  const int64_t tid = valid ? tid0 : total - 1;  // whole quads stay converged
+  const int c = (int)(tid / g.n_qp);
+  const int q = (int)(tid - (int64_t)c * g.n_qp);
+  const int64_t inst = g.inst0 + c;
+  const int e = q >> 2, k = q & 3;
+  const int nq = g.n_qp;
+  bool ok = true;
+  {
+    double gq[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) gq[t] = __ldg(g.grad + (size_t)q * 8 + t);
+    int node[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) node[a] = __ldg(g.elems + 4 * e + a);
+    double fmi[4], det;
+    if (g.morph) {
+      const double* mo = g.morph + (size_t)inst * 5 * nq;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) fmi[t] = __ldg(mo + (size_t)t * nq + q);
+      det = __ldg(mo + (size_t)4 * nq + q);
+    } else {
+      const double ka = __ldg(g.geom + 2 * inst) / g.r0 - 1.0;
+      const double kb = __ldg(g.geom + 2 * inst + 1) / g.r0 - 1.0;
+      double d[4][2];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) v[a * 2 + i] = wq * (P[i] * gt[a][0] + P[i + 2] * gt[a][1]);
-      quad_reduce8(v, k, o);
-      const int u0 = 4 * (k & 1) + 2 * ((k >> 1) & 1);
-      if (valid) {
-        const int p0 = __ldg(ps + 64 + u0), p1 = __ldg(ps + 64 + u0 + 1);
-        if (p0 >= 0) sc[p0] = o[0];
-        if (p1 >= 0) sc[p1] = o[1];
-      }
+        morph_d(__ldg(g.nodes + 2 * node[a]), __ldg(g.nodes + 2 * node[a] + 1), ka, kb, g.r0, d[a][0],
+                d[a][1]);
+      det = derive_qp(d, gq, fmi);
     }
+    const double* wr = g.w_red + (size_t)inst * g.n_red;
+    double wn[4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int dof = __ldg(g.node_dof + node[a]);
+      wn[a][0] = dof >= 0 ? __ldg(wr + dof) : 0.0;
+      wn[a][1] = dof >= 0 ? __ldg(wr + dof + 1) : 0.0;
+    }
+    double gw[4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        double sm = 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) sm = sm + wn[a][i] * gq[2 * a + j];
+        gw[i + 2 * j] = sm;
+      }
+    double F[4];
+    const double* fb = g.fbar + 4 * inst;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        F[i + 2 * j] = __ldg(fb + i + 2 * j) + (gw[i] * fmi[2 * j] + gw[i + 2] * fmi[1 + 2 * j]);
+    sq[28 * kQ2Thr + lt] = __ldg(g.w + q) * det;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        sq[(20 + 2 * a + j) * kQ2Thr + lt] = gq[2 * a] * fmi[2 * j] + gq[2 * a + 1] * fmi[1 + 2 * j];
+    const MatConst& p = tab.m[__ldg(g.regions + e)];
+    const double* s0 = g.st0 + (size_t)inst * 6 * nq;
+    double fp[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) fp[t] = __ldg(s0 + (size_t)t * nq + q);
+    Frozen z;
+    freeze(fp, __ldg(s0 + (size_t)4 * nq + q), __ldg(s0 + (size_t)5 * nq + q), z);
+    double P[4];
+    FullOut fo;
+    ok = lsu_eval<true>(p, z, F, P, &fo);
+    if (g.st1 && valid) {
+      double* s1 = g.st1 + (size_t)inst * 6 * nq;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) s1[(size_t)t * nq + q] = fo.fp[t];
+      s1[(size_t)4 * nq + q] = fo.fpzz;
+      s1[(size_t)5 * nq + q] = fo.xi;
+    }
+    if (g.p_field && valid) {
+      double* pf = g.p_field + (size_t)inst * 4 * nq;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) pf[(size_t)t * nq + q] = P[t];
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) sq[(16 + t) * kQ2Thr + lt] = P[t];
     if (g.tangent) {
-      double cd[2][4];
       auto sink = [&](int ecol, const double col[4]) {
-        const int d = ecol >> 1, j = ecol & 1;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          cd[0][r] = d == 0 ? col[r] : cd[0][r];
-          cd[1][r] = d == 1 ? col[r] : cd[1][r];
-        }
-        if (d == 0) return;
-        const int u0 = 4 * (k & 1) + 2 * ((k >> 1) & 1);
-        // T[i][c][b] = sum_d A(i,c,j,d) gt_bd, then K(a i, b j) = sum_c (wq gt_ac) T[i][c][b]
-        double T[2][2][4];
+        for (int r = 0; r < 4; ++r) sq[(r + 4 * ecol) * kQ2Thr + lt] = col[r];
+      };
+      const bool ok2 = fd_tangent<false>(p, z, F, 1e-7, sink);
+      ok = ok && ok2;
+    }
+  }
+  // ---- phase 2: element sums from this thread's SMEM row
+  const double wq = sq[28 * kQ2Thr + lt];
+  double gt[4][2], P[4];
 #pragma unroll
-        for (int i = 0; i < 2; ++i)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int cc = 0; cc < 2; ++cc)
+    for (int j = 0; j < 2; ++j) gt[a][j] = sq[(20 + 2 * a + j) * kQ2Thr + lt];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) T[i][cc][b] = fma(cd[1][i + 2 * cc], gt[b][1], cd[0][i + 2 * cc] * gt[b][0]);
+  for (int t = 0; t < 4; ++t) P[t] = sq[(16 + t) * kQ2Thr + lt];
+  double* sc = g.scratch + (size_t)c * g.n_groups;
+  const int32_t* ps = g.pos + (size_t)e * 72;
+  const int u0 = 4 * (k & 1) + 2 * ((k >> 1) & 1);
+  {
+    double v[8], o[2];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          double v[8], o[2];
-          const double w0 = wq * gt[a][0], w1 = wq * gt[a][1];
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b)
+      for (int i = 0; i < 2; ++i) v[a * 2 + i] = wq * (P[i] * gt[a][0] + P[i + 2] * gt[a][1]);
+    quad_reduce8(v, k, o);
+    if (valid) {
+      const int p0 = __ldg(ps + 64 + u0), p1 = __ldg(ps + 64 + u0 + 1);
+      if (p0 >= 0) sc[p0] = o[0];
+      if (p1 >= 0) sc[p1] = o[1];
+    }
+  }
+  if (g.tangent) {
+#pragma unroll 1
+    for (int j = 0; j < 2; ++j) {
+      double cd[2][4];
 #pragma unroll
-            for (int i = 0; i < 2; ++i) v[b * 2 + i] = fma(w1, T[i][1][b], w0 * T[i][0][b]);
-          quad_reduce8(v, k, o);
-          if (valid) {
+      for (int dd = 0; dd < 2; ++dd)
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int u = u0 + h, b = u >> 1, i = u & 1;
-              const int pp = __ldg(ps + a * 16 + b * 4 + i * 2 + j);
-              if (pp >= 0) sc[pp] = o[h];
-            }
+        for (int r = 0; r < 4; ++r) cd[dd][r] = sq[(r + 4 * (j + 2 * dd)) * kQ2Thr + lt];
+      double T[2][2][4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) T[i][cc][b] = fma(cd[1][i + 2 * cc], gt[b][1], cd[0][i + 2 * cc] * gt[b][0]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        double v[8], o[2];
+        const double w0 = wq * gt[a][0], w1 = wq * gt[a][1];
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) v[b * 2 + i] = fma(w1, T[i][1][b], w0 * T[i][0][b]);
+        quad_reduce8(v, k, o);
+        if (valid) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int u = u0 + h, b = u >> 1, i = u & 1;
+            const int pp = __ldg(ps + a * 16 + b * 4 + i * 2 + j);
+            if (pp >= 0) sc[pp] = o[h];
           }
         }
-      };
-      const bool ok2 = fd_tangent<false>(p, z, F, 1e-7, sink);  // all quad lanes run it
-      ok = ok && ok2;
+      }
     }
   }
   if (!ok && valid) {
@@ -292,14 +411,13 @@ struct GatherArgs {
 
 // One thread per (instance, item): items [0, nnz) are CSR slots (if kvals),
 // items [nnz, nnz + n_red) residual rows.
-template <bool FUSED>
 __global__ void __launch_bounds__(256) k_asm_gather(GatherArgs g) {
   const int64_t n_items = (g.kvals ? g.nnz : 0) + g.n_red;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= n_items * g.n_inst) return;
   const int c = (int)(tid / n_items);
   const int64_t it = tid - (int64_t)c * n_items;
-  const double* sc = g.scratch + (size_t)c * g.n_elems * 72 * (FUSED ? 1 : 4);
+  const double* sc = g.scratch + (size_t)c * g.n_elems * 72 * 4;
   const int64_t inst = g.inst0 + c;
   if (g.kvals && it < g.nnz) {
     const int b0 = __ldg(g.slot_gptr + it), b1 = __ldg(g.slot_gptr + it + 1);
@@ -307,11 +425,6 @@ __global__ void __launch_bounds__(256) k_asm_gather(GatherArgs g) {
     for (int m = b0; m < b1; ++m) {
       const int grp = __ldg(g.slot_grp + m);  // e*64 + tl
       const int e = grp >> 6, tl = grp & 63;
-      if (FUSED) {  // element sums, added in element order
-        const double v = sc[(size_t)e * 72 + tl];
-        s = (m == b0) ? v : s + v;
-        continue;
-      }
       const double4 t = *reinterpret_cast<const double4*>(sc + ((size_t)e * 72 + tl) * 4);
       if (m == b0) {
         s = t.x;  // setFromTriplets: first duplicate is copied, the rest added
@@ -330,10 +443,6 @@ __global__ void __launch_bounds__(256) k_asm_gather(GatherArgs g) {
     for (int m = b0; m < b1; ++m) {
       const int grp = __ldg(g.frow_grp + m);  // e*8 + fl
       const int e = grp >> 3, fl = grp & 7;
-      if (FUSED) {
-        s = s + sc[(size_t)e * 72 + 64 + fl];
-        continue;
-      }
       const double4 t = *reinterpret_cast<const double4*>(sc + ((size_t)e * 72 + 64 + fl) * 4);
       s = s + t.x;
       s = s + t.y;
@@ -344,7 +453,7 @@ __global__ void __launch_bounds__(256) k_asm_gather(GatherArgs g) {
   }
 }
 
-// FUSED gather: the element sums already sit in slot order, so every CSR
+// Default gather: the element sums already sit in slot order, so every CSR
 // slot / residual row is a contiguous run scratch[gptr[i] .. gptr[i+1]) summed
 // in element order (first term copied for K, setFromTriplets style; 0 + ...
 // for f).  One thread per (instance, item): a streaming segmented reduction.
@@ -430,8 +539,15 @@ int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t 
     return e ? atoi(e) : 4;
   }();
   const size_t per_inst = (exact ? (size_t)r->n_elems * 72 * 4 : (size_t)r->n_groups) * sizeof(double);
-  // chunk: scratch <= ~48 MB (L2-resident), at least one instance
-  int64_t chunk = std::max<int64_t>(1, (int64_t)(48ull << 20) / (int64_t)per_inst);
+  // Chunk of instances per (qp kernel, gather) pair: the scratch budget
+  // (PODECM_ASM_CHUNK_MB, default 768 MB; 81 instances of 128^2).  Large grids
+  // beat L2 residency here: 48 MB chunks (5 instances, 3.5 waves of the qp
+  // kernel) cost 36 ms per C2 step against 30 ms at 768 MB.
+  static const int64_t chunk_mb = [] {
+    const char* e = getenv("PODECM_ASM_CHUNK_MB");
+    return (int64_t)(e ? std::max(1, atoi(e)) : 768);
+  }();
+  int64_t chunk = std::max<int64_t>(1, (chunk_mb << 20) / (int64_t)per_inst);
   chunk = std::min<int64_t>(chunk, n_inst);
   if (r->scratch_inst < chunk) {
     cudaFree(r->d_scratch);
@@ -469,14 +585,15 @@ int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t 
     a.fail = ctx->d_fail;
     a.tangent = kvals != nullptr;
     const int64_t nthr = (int64_t)nc * r->n_qp;
-    {
+    if (exact) {
       KTimer kt(ctx, s, "k_asm_qp");
-      if (exact)
-        k_asm_qp<false, 5><<<grid_for(nthr, 128), 128, 0, s>>>(a, r->mats);
-      else if (minb == 4)
-        k_asm_qp<true, 4><<<grid_for(nthr, 128), 128, 0, s>>>(a, r->mats);
+      k_asm_qp<5><<<grid_for(nthr, 128), 128, 0, s>>>(a, r->mats);
+    } else {
+      KTimer kt(ctx, s, "k_asm_qp2");
+      if (minb == 5)
+        k_asm_qp2<5><<<grid_for(nthr, kQ2Thr), kQ2Thr, 0, s>>>(a, r->mats);
       else
-        k_asm_qp<true, 5><<<grid_for(nthr, 128), 128, 0, s>>>(a, r->mats);
+        k_asm_qp2<4><<<grid_for(nthr, kQ2Thr), kQ2Thr, 0, s>>>(a, r->mats);
     }
     GatherArgs gg;
     gg.n_red = r->n_red;
@@ -495,7 +612,7 @@ int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t 
     {
       KTimer kt(ctx, s, "k_asm_gather");
       if (exact)
-        k_asm_gather<false><<<grid_for(nitems, 256), 256, 0, s>>>(gg);
+        k_asm_gather<<<grid_for(nitems, 256), 256, 0, s>>>(gg);
       else
         k_asm_gather_fused<<<dim3(grid_for(nitems / nc, 256), nc), 256, 0, s>>>(gg, r->d_gptr_all, r->n_groups);
     }
