@@ -430,6 +430,7 @@ def run_c3(args, ws, rank, local, ctx, n_inst, steps, warmup, fp64):
            "mean_assemblies_per_solve": round(assemblies, 2), "global_iterations": gi,
            "failed_instances": n_fail, "launches_per_step": launches / steps,
            "kernels_ms_per_step": {k: round(v[0] / steps, 3) for k, v in tk.items()},
+           "kernel_calls_per_step": {k: round(v[1] / steps, 1) for k, v in tk.items()},
            "roofline": {"bound": "fp64-tensor (DMMA)", "kernel": "k_rom_contract",
                         "achieved": round(ach_tf, 2) if ach_tf else None,
                         "peak": fp64.get("dmma") if fp64 else None, "unit": "TFLOP/s",
@@ -519,11 +520,20 @@ def run_c4(args, ws, rank, local, ctx, steps, warmup, fp64):
            "ms_per_step": ms / steps, "pod_stage_s": round(res["pod_s"], 4), "ecm_greedy_s": round(res["ecm_s"], 4),
            "ecm_iterations": res["it"], "ecm_residual_rel": res["rel"],
            "kernels_ms_per_step": {k: round(v[0] / steps, 3) for k, v in tk.items()},
+           "kernel_calls_per_step": {k: round(v[1] / steps, 1) for k, v in tk.items()},
            "roofline": {"bound": "fp64-tensor (DMMA)",
                         "gram_and_mode_gemm_tflops": round((gram_flop + 2.0 * n_dof * L * N) / (kg[0] / steps * 1e-3) / 1e12, 2) if kg[0] else None,
                         "ecm_score_tflops": round(score_flop * ks[1] / steps / (ks[0] / steps * 1e-3) / 1e12, 2) if ks[0] else None,
                         "peak": fp64.get("dmma"), "unit": "TFLOP/s",
                         "peak_source": "DMMA probe measured in this run"}}
+    kgc = tk.get("k_ecm_gram_col", (0.0, 0))
+    if kgc[1]:
+        hbm, src = _hbm_peak()
+        wbytes = float(L) * rve.n_qp * 4 * 8  # one streaming pass over W per selected point
+        gbs = wbytes * kgc[1] / (kgc[0] * 1e-3) / 1e9
+        out["roofline"]["ecm_gram_col"] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+                                           "frac": round(gbs / hbm, 4), "bytes_per_launch": wbytes,
+                                           "peak_source": src}
     if rank == 0 and ws == 1 and not args.no_cpu:
         # CPU baseline on a bounded sample: the POD stage (Gram + eigh, LAPACK,
         # all threads) in full, and one greedy scoring pass (J^T r) over the

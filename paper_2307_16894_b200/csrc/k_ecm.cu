@@ -126,7 +126,7 @@ constexpr int kSQ = 16, kSC = 64, kSK = 16, kSLD = kSK + 4;
 __global__ void __launch_bounds__(224) k_ecm_score(int64_t L, int nq, int N, const double* r,
                                                    const double* r_vol_p, const double* H, const double* W,
                                                    const double* cn, const uint8_t* unavailable,
-                                                   double* cta_best, int* cta_idx) {
+                                                   double* cta_best, int* cta_idx, double* corr_out) {
   __shared__ double sR[2][56][kSLD];
   __shared__ double sW[2][kSC][kSLD];
   __shared__ double red[7][kSQ];
@@ -194,6 +194,7 @@ __global__ void __launch_bounds__(224) k_ecm_score(int64_t L, int nq, int N, con
       double corr = 0.0;
       for (int w = 0; w < 7; ++w) corr += red[w][tid];
       if (r_vol_p) corr += *r_vol_p;
+      if (corr_out) corr_out[q] = corr;
       const double sc = corr / cn[q];
       if (sc > 0.0) {
         best = sc;
@@ -213,6 +214,104 @@ __global__ void __launch_bounds__(224) k_ecm_score(int64_t L, int nq, int N, con
       cta_best[blockIdx.x] = best;
       cta_idx[blockIdx.x] = bi;
     }
+  }
+}
+
+
+// Gram-updated scoring.  With r = rhs - J_sel x,
+//   corr = J^T r = J^T rhs - sum_k x_k (J^T J_{s_k}),
+// and column s of J^T J factors through the 4x4 blocks of the integrand:
+//   (J^T J)[q, s] = sum_{c,d} (H_q^T H_s)[c,d] (W_q^T W_s)[c,d] + vol,
+// H_q = H[q] (N x 4), W_q = W[:, q, :] (L x 4).  One new column per selected
+// point costs one streaming pass over W with 16 FMAs per 32 bytes (HBM-bound)
+// instead of the N L 4 n_qp DMMA GEMM of a direct J^T r pass.
+constexpr int kGramSplit = 4;  // L-range splits (partials summed in fixed order)
+
+__global__ void __launch_bounds__(256) k_ecm_gram_col(int64_t L, int nq, int N, int sel, const double* H,
+                                                      const double* W, double* gpart) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const int sp = blockIdx.y;
+  const int64_t l0 = L * sp / kGramSplit, l1 = L * (sp + 1) / kGramSplit;
+  double mw[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) mw[t] = 0.0;
+  const double2* Wq = reinterpret_cast<const double2*>(W) + 2 * (int64_t)q;
+  const double2* Ws = reinterpret_cast<const double2*>(W) + 2 * (int64_t)sel;
+#pragma unroll 4
+  for (int64_t l = l0; l < l1; ++l) {
+    const double2 a0 = __ldcs(Wq + 2 * l * nq), a1 = __ldcs(Wq + 2 * l * nq + 1);
+    const double2 b0 = __ldg(Ws + 2 * l * nq), b1 = __ldg(Ws + 2 * l * nq + 1);
+    const double av[4] = {a0.x, a0.y, a1.x, a1.y}, bv[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int d = 0; d < 4; ++d) mw[c * 4 + d] = fma(av[c], bv[d], mw[c * 4 + d]);
+  }
+  double mh[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) mh[t] = 0.0;
+  for (int i = 0; i < N; ++i) {
+    const double* hq = H + ((int64_t)q * N + i) * 4;
+    const double* hs = H + ((int64_t)sel * N + i) * 4;
+    const double av[4] = {hq[0], hq[1], hq[2], hq[3]};
+    const double bv[4] = {__ldg(hs), __ldg(hs + 1), __ldg(hs + 2), __ldg(hs + 3)};
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int d = 0; d < 4; ++d) mh[c * 4 + d] = fma(av[c], bv[d], mh[c * 4 + d]);
+  }
+  double g = 0.0;
+#pragma unroll
+  for (int t = 0; t < 16; ++t) g = fma(mh[t], mw[t], g);
+  gpart[(int64_t)sp * nq + q] = g;
+}
+
+// G[k][q] = sum of the split partials (+ vol)
+__global__ void k_ecm_gram_finish(int nq, const double* gpart, int vol, double* gcol) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  double g = vol ? 1.0 : 0.0;
+  for (int sp = 0; sp < kGramSplit; ++sp) g += gpart[(int64_t)sp * nq + q];
+  gcol[q] = g;
+}
+
+// corr_q = c0_q - sum_k x_k G[k][q]; score = corr / ||J_q||; CTA argmax
+__global__ void __launch_bounds__(256) k_ecm_score_gram(int nq, int k, const double* c0, const double* G,
+                                                        const double* x, const double* cn,
+                                                        const uint8_t* unavailable, double* cta_best,
+                                                        int* cta_idx) {
+  __shared__ double sb[256];
+  __shared__ int si[256];
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  double best = 0.0;
+  int bi = -1;
+  if (q < nq && !unavailable[q] && cn[q] != 0.0) {
+    double corr = c0[q];
+    for (int j = 0; j < k; ++j) corr = fma(-x[j], G[(int64_t)j * nq + q], corr);
+    const double sc = corr / cn[q];
+    if (sc > 0.0) {
+      best = sc;
+      bi = q;
+    }
+  }
+  sb[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double ob = sb[threadIdx.x + o];
+      const int oi = si[threadIdx.x + o];
+      if (oi >= 0 && (si[threadIdx.x] < 0 || ob > sb[threadIdx.x] || (ob == sb[threadIdx.x] && oi < si[threadIdx.x]))) {
+        sb[threadIdx.x] = ob;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    cta_best[blockIdx.x] = sb[0];
+    cta_idx[blockIdx.x] = si[0];
   }
 }
 
@@ -265,22 +364,6 @@ __global__ void k_ecm_column(int64_t L, int nq, int N, int q, const double* H, c
   }
 }
 
-// out[j] = sum_r A[j*m + r] * v[r] for j < k (one CTA per j, fixed-tree sum)
-__global__ void __launch_bounds__(256) k_dots(int64_t m, int k, const double* A, const double* v, double* out) {
-  __shared__ double red[256];
-  const int j = blockIdx.x;
-  if (j >= k) return;
-  double p = 0.0;
-  for (int64_t r = threadIdx.x; r < m; r += blockDim.x) p = fma(A[(int64_t)j * m + r], v[r], p);
-  red[threadIdx.x] = p;
-  __syncthreads();
-  for (int o = 128; o > 0; o >>= 1) {
-    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) out[j] = red[0];
-}
-
 // v -= sum_j A[:,j] h[j]  (j < k)
 __global__ void k_axpy_cols(int64_t m, int k, const double* A, const double* h, double* v) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -319,41 +402,126 @@ __global__ void __launch_bounds__(256) k_resid(int64_t m, int k, const double* A
 }
 
 
-// QR column finish (one CTA): R[:, k] = h1 + h2, r_kk = ||v||, Q[:, k] = v / r_kk,
-// qtb[k] = Q[:, k] . rhs — fixed-tree block reductions (deterministic).
-__global__ void __launch_bounds__(1024) k_qr_finish(int64_t m, int k, int kmax, const double* v,
-                                                    const double* h1, const double* h2,
-                                                    const double* rhs, double* qcol, double* R,
-                                                    double* qtb) {
-  __shared__ double red[1024];
-  const int t = threadIdx.x;
-  for (int j = t; j < k; j += blockDim.x) R[(size_t)k * kmax + j] = (0.0 + h1[j]) + h2[j];
+
+// Hw[i][(q,c)] = w_q H[q][i][c] (the full-quadrature weights folded into H)
+__global__ void k_ecm_hw(int nq, int N, const double* H, const double* w, double* Hw) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nq * N * 4) return;
+  const int c = (int)(t & 3);
+  const int64_t qi = t >> 2;
+  const int q = (int)(qi / N), i = (int)(qi - (int64_t)q * N);
+  Hw[(int64_t)i * 4 * nq + (int64_t)q * 4 + c] = w[q] * H[t];
+}
+
+// Multi-CTA building blocks of the incremental QR (all reductions are
+// two-stage with a fixed order: deterministic).
+constexpr int kQrBlocks = 296;  // 2 CTAs per SM
+
+// part[b][j] = sum over rows of slab b of A[j*m + r] v[r], j < k.  Each warp
+// takes 4 columns at a time (4 independent accumulators, 5 loads in flight per
+// lane per row step), lanes over rows; a fixed shuffle tree per column.
+__global__ void __launch_bounds__(256) k_dots_part(int64_t m, int k, const double* A, const double* v,
+                                                   double* part) {
+  const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r0 = m * b / gridDim.x, r1 = m * (b + 1) / gridDim.x;
+  for (int j0 = warp * 4; j0 < k; j0 += 32) {
+    const int nj = min(4, k - j0);
+    const double* a0 = A + (int64_t)j0 * m;
+    const double* a1 = nj > 1 ? a0 + m : a0;
+    const double* a2 = nj > 2 ? a0 + 2 * m : a0;
+    const double* a3 = nj > 3 ? a0 + 3 * m : a0;
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
+#pragma unroll 2
+    for (int64_t r = r0 + lane; r < r1; r += 32) {
+      const double x = v[r];
+      p0 = fma(a0[r], x, p0);
+      p1 = fma(a1[r], x, p1);
+      p2 = fma(a2[r], x, p2);
+      p3 = fma(a3[r], x, p3);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+      p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+      p2 += __shfl_xor_sync(0xffffffffu, p2, o);
+      p3 += __shfl_xor_sync(0xffffffffu, p3, o);
+    }
+    if (lane == 0) {
+      double* out = part + (int64_t)b * k + j0;
+      out[0] = p0;
+      if (nj > 1) out[1] = p1;
+      if (nj > 2) out[2] = p2;
+      if (nj > 3) out[3] = p3;
+    }
+  }
+}
+
+// sum of x[b * stride], b < nb, by one warp: lanes stride b, fixed shuffle tree
+__device__ __forceinline__ double warp_sum_strided(const double* x, int nb, int64_t stride, int lane) {
+  double s = 0.0;
+  for (int b = lane; b < nb; b += 32) s += x[(int64_t)b * stride];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+// out[j] = sum_b part[b][j] (one warp per column, fixed order)
+__global__ void __launch_bounds__(256) k_dots_finish(int nb, int k, const double* part, double* out) {
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (j >= k) return;
+  const double s = warp_sum_strided(part + j, nb, k, lane);
+  if (lane == 0) out[j] = s;
+}
+
+// part[b] = sum over slab b of x[r] y[r]
+__global__ void __launch_bounds__(256) k_dot_part(int64_t m, const double* x, const double* y, double* part) {
+  __shared__ double red[256];
+  const int64_t r0 = m * blockIdx.x / gridDim.x, r1 = m * (blockIdx.x + 1) / gridDim.x;
   double p = 0.0;
-  for (int64_t r = t; r < m; r += blockDim.x) p = fma(v[r], v[r], p);
-  red[t] = p;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) p = fma(x[r], y[r], p);
+  red[threadIdx.x] = p;
   __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (t < o) red[t] += red[t + o];
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
-  const double nrm = sqrt(red[0]);
-  __syncthreads();
-  double q = 0.0;
-  for (int64_t r = t; r < m; r += blockDim.x) {
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+// R[:, k] = h1 + h2, r_kk = sqrt(sum part) (one thread block)
+__global__ void k_qr_rcol(int nb, int k, int kmax, const double* part, const double* h1, const double* h2,
+                          double* R) {
+  for (int j = threadIdx.x; j < k; j += blockDim.x) R[(size_t)k * kmax + j] = (0.0 + h1[j]) + h2[j];
+  if (threadIdx.x < 32) {
+    const double s = warp_sum_strided(part, nb, 1, threadIdx.x);
+    if (threadIdx.x == 0) R[(size_t)k * kmax + k] = sqrt(s);
+  }
+}
+
+// qcol = v / r_kk; part[b] = sum over slab of qcol[r] rhs[r]
+__global__ void __launch_bounds__(256) k_qr_scale_dot(int64_t m, const double* v, const double* rkk,
+                                                      const double* rhs, double* qcol, double* part) {
+  __shared__ double red[256];
+  const double nrm = *rkk;
+  const int64_t r0 = m * blockIdx.x / gridDim.x, r1 = m * (blockIdx.x + 1) / gridDim.x;
+  double p = 0.0;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
     const double x = v[r] / nrm;
     qcol[r] = x;
-    q = fma(x, rhs[r], q);
+    p = fma(x, rhs[r], p);
   }
-  red[t] = q;
+  red[threadIdx.x] = p;
   __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (t < o) red[t] += red[t + o];
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
-  if (t == 0) {
-    R[(size_t)k * kmax + k] = nrm;
-    qtb[k] = red[0];
-  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+__global__ void k_sum_to(int nb, const double* part, double* out) {
+  const double s = warp_sum_strided(part, nb, 1, threadIdx.x);
+  if (threadIdx.x == 0) *out = s;
 }
 
 // Incremental QR of the selected integrand columns (classical Gram-Schmidt
@@ -368,23 +536,34 @@ struct Ecm {
   int kmax;
   double *Jsel, *Q, *tmp, *h1, *h2, *R, *qtb;
   const double* rhs;
+  double* part;  // [kQrBlocks][kmax] partial sums
   int k = 0;
-  std::vector<double> hR, hq;  // host mirrors (column-major kmax x kmax, kmax)
+  double *hR, *hq;  // pinned host mirrors (column-major kmax x kmax, kmax)
 
   void append() {  // append column Jsel[:, k]
     double* v = tmp;
     cudaMemcpyAsync(v, Jsel + (int64_t)k * m, sizeof(double) * m, cudaMemcpyDeviceToDevice, s);
     if (k > 0) {
-      k_dots<<<k, 256, 0, s>>>(m, k, Q, v, h1);
-      k_axpy_cols<<<grid_for(m, 256), 256, 0, s>>>(m, k, Q, h1, v);
-      k_dots<<<k, 256, 0, s>>>(m, k, Q, v, h2);
-      k_axpy_cols<<<grid_for(m, 256), 256, 0, s>>>(m, k, Q, h2, v);
+      for (int pass = 0; pass < 2; ++pass) {  // CGS2: project twice
+        double* h = pass ? h2 : h1;
+        {
+          KTimer kt(ctx, s, "ecm_qr_dots");
+          k_dots_part<<<kQrBlocks, 256, 0, s>>>(m, k, Q, v, part);
+          k_dots_finish<<<grid_for(k, 8), 256, 0, s>>>(kQrBlocks, k, part, h);
+        }
+        KTimer kt(ctx, s, "ecm_qr_axpy");
+        k_axpy_cols<<<grid_for(m, 256), 256, 0, s>>>(m, k, Q, h, v);
+      }
     }
-    k_qr_finish<<<1, 1024, 0, s>>>(m, k, kmax, v, h1, h2, rhs, Q + (int64_t)k * m, R, qtb);
-    cudaMemcpyAsync(hR.data() + (size_t)k * kmax, R + (size_t)k * kmax, sizeof(double) * (k + 1),
+    KTimer kt(ctx, s, "ecm_qr_finish");
+    k_dot_part<<<kQrBlocks, 256, 0, s>>>(m, v, v, part);
+    k_qr_rcol<<<1, 256, 0, s>>>(kQrBlocks, k, kmax, part, h1, h2, R);
+    k_qr_scale_dot<<<kQrBlocks, 256, 0, s>>>(m, v, R + (size_t)k * kmax + k, rhs, Q + (int64_t)k * m, part);
+    k_sum_to<<<1, 32, 0, s>>>(kQrBlocks, part, qtb + k);
+    cudaMemcpyAsync(hR + (size_t)k * kmax, R + (size_t)k * kmax, sizeof(double) * (k + 1),
                     cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(hq.data() + k, qtb + k, sizeof(double), cudaMemcpyDeviceToHost, s);
-    ctx->launches += k > 0 ? 5 : 1;
+    cudaMemcpyAsync(hq + k, qtb + k, sizeof(double), cudaMemcpyDeviceToHost, s);
+    ctx->launches += k > 0 ? 10 : 4;
     ++k;
   }
 
@@ -478,6 +657,23 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
   alloc(&pss, n_rb);
   alloc(&pmx, n_rb);
   alloc(&unav, nq);
+  // Gram-updated scoring (default; PODECM_ECM_SCORE=direct runs a J^T r DMMA
+  // pass every iteration instead)
+  static const bool gram = [] {
+    const char* e = getenv("PODECM_ECM_SCORE");
+    return !(e && !strcmp(e, "direct"));
+  }();
+  double *c0 = nullptr, *Gsel = nullptr, *gpart = nullptr;
+  const int n_cta_g = grid_for(nq, 256);
+  if (gram) {
+    alloc(&c0, nq);
+    alloc(&Gsel, (size_t)kq * nq);
+    alloc(&gpart, (size_t)kGramSplit * nq);
+  }
+  double* cta_bg = nullptr;
+  int* cta_ig = nullptr;
+  alloc(&cta_bg, n_cta_g);
+  alloc(&cta_ig, n_cta_g);
   std::vector<int> selected;
   std::vector<double> x;
   double rhs_norm = 0.0, rnorm = 0.0;
@@ -485,14 +681,7 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
   if (!rc) {
     cudaMemsetAsync(unav, 0, nq, s);
     // rhs = J w: Hw[i][(q,c)] = w_q H[q][i][c]; rhs[(i,s)] = sum_k Hw[i][k] W[s][k]
-    std::vector<double> hH((size_t)nq * N * 4), hHw((size_t)N * 4 * nq);
-    cudaMemcpyAsync(hH.data(), H, sizeof(double) * hH.size(), cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    for (int q = 0; q < nq; ++q)
-      for (int i = 0; i < N; ++i)
-        for (int c = 0; c < 4; ++c)
-          hHw[(size_t)i * 4 * nq + (size_t)q * 4 + c] = rve->w[q] * hH[((size_t)q * N + i) * 4 + c];
-    cudaMemcpyAsync(Hw, hHw.data(), sizeof(double) * hHw.size(), cudaMemcpyHostToDevice, s);
+    k_ecm_hw<<<grid_for((int64_t)nq * N * 4, 256), 256, 0, s>>>(nq, N, H, rve->d_w, Hw);
     GemmArgs a{};
     a.M = N;
     a.N = L;
@@ -534,8 +723,26 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
     for (double v : hr) rmax = std::max(rmax, std::fabs(v));
   }
   if (!rc) cudaMemsetAsync(h2buf, 0, sizeof(double) * kq, s);
-  Ecm qr{ctx, s, m, kq, Jsel, Q, tmp, hbuf, h2buf, Rdev, qtbdev, rhs, 0,
-         std::vector<double>((size_t)kq * kq, 0.0), std::vector<double>(kq, 0.0)};
+  double* qpart = nullptr;
+  alloc(&qpart, (size_t)kQrBlocks * kq);
+  // pinned host staging for the per-iteration round trips: R mirror, Q^T b,
+  // residual partials, x, the argmax index and the 'unavailable' flag
+  double* pin = nullptr;
+  const size_t n_pin = (size_t)kq * kq + 2 * (size_t)kq + 2 * (size_t)n_rb + 2;
+  if (!rc && cudaMallocHost(&pin, n_pin * sizeof(double)) != cudaSuccess)
+    rc = fail(PODECM_ECUDA, "ecm: pinned allocation failed");
+  double* pR = pin;
+  double* pq = pR + (size_t)kq * kq;
+  double* px = pq + kq;
+  double* ps = px + kq;
+  double* pm = ps + n_rb;
+  int* pbest = reinterpret_cast<int*>(pm + n_rb);
+  uint8_t* pone = reinterpret_cast<uint8_t*>(pm + n_rb + 1);
+  if (pin) {
+    std::fill(pR, pR + (size_t)kq * kq, 0.0);
+    *pone = 1;
+  }
+  Ecm qr{ctx, s, m, kq, Jsel, Q, tmp, hbuf, h2buf, Rdev, qtbdev, rhs, qpart, 0, pR, pq};
   auto converged = [&]() {
     if (rhs_norm == 0.0) return true;
     return rnorm <= opts->eps * rhs_norm && rmax <= row_tol;
@@ -555,26 +762,43 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
       break;
     }
     // corr = J^T r ; argmax of corr / ||J_q|| over available columns
-    {
-      KTimer kt(ctx, s, "k_ecm_score");
-      k_ecm_score<<<n_cta, 224, 0, s>>>(L, nq, N, r, vol ? r + m - 1 : nullptr, H, W, cn, unav, cta_b, cta_i);
+    if (gram && iters > 0) {
+      {
+        KTimer kt(ctx, s, "k_ecm_score_gram");
+        k_ecm_score_gram<<<n_cta_g, 256, 0, s>>>(nq, (int)x.size(), c0, Gsel, xdev, cn, unav, cta_bg, cta_ig);
+      }
+      k_ecm_argmax<<<1, 1024, 0, s>>>(n_cta_g, cta_bg, cta_ig, best_b, best_i);
+    } else {
+      {
+        KTimer kt(ctx, s, "k_ecm_score");
+        k_ecm_score<<<n_cta, 224, 0, s>>>(L, nq, N, r, vol ? r + m - 1 : nullptr, H, W, cn, unav, cta_b, cta_i,
+                                          gram ? c0 : nullptr);  // first pass: r = rhs, keep J^T rhs
+      }
+      k_ecm_argmax<<<1, 1024, 0, s>>>(n_cta, cta_b, cta_i, best_b, best_i);
     }
-    k_ecm_argmax<<<1, 1024, 0, s>>>(n_cta, cta_b, cta_i, best_b, best_i);
     ctx->launches += 2;
-    int best = -1;
-    cudaMemcpyAsync(&best, best_i, sizeof(int), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(pbest, best_i, sizeof(int), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
+    const int best = *pbest;
     if (best < 0) {
       rc = fail(PODECM_ESOLVE, "cubature stalled: no remaining point improves the residual");
       break;
     }
     selected.push_back(best);
-    const uint8_t one = 1;
-    cudaMemcpyAsync(unav + best, &one, 1, cudaMemcpyHostToDevice, s);
+    cudaMemcpyAsync(unav + best, pone, 1, cudaMemcpyHostToDevice, s);
     x.push_back(0.0);
     // materialise the new column and extend the QR
-    k_ecm_column<<<grid_for(m, 256), 256, 0, s>>>(L, nq, N, best, H, W, vol, Jsel + (int64_t)qr.k * m);
+    {
+      KTimer kt(ctx, s, "k_ecm_column");
+      k_ecm_column<<<grid_for(m, 256), 256, 0, s>>>(L, nq, N, best, H, W, vol, Jsel + (int64_t)qr.k * m);
+    }
     ctx->launches += 1;
+    if (gram) {  // column (J^T J)[:, best] for the scores of the next iterations
+      KTimer kt(ctx, s, "k_ecm_gram_col");
+      k_ecm_gram_col<<<dim3(n_cta_g, kGramSplit), 256, 0, s>>>(L, nq, N, best, H, W, gpart);
+      k_ecm_gram_finish<<<n_cta_g, 256, 0, s>>>(nq, gpart, vol, Gsel + (int64_t)qr.k * nq);
+      ctx->launches += 2;
+    }
     qr.append();
     // restore_feasible (ecm.cpp:56-90)
     while (!selected.empty()) {
@@ -605,9 +829,13 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
         }
       // compact Jsel columns and rebuild the QR of the kept set
       for (size_t k = 0; k < keep_pos.size(); ++k)
-        if (keep_pos[k] != (int)k)
+        if (keep_pos[k] != (int)k) {
           cudaMemcpyAsync(Jsel + (int64_t)k * m, Jsel + (int64_t)keep_pos[k] * m, sizeof(double) * m,
                           cudaMemcpyDeviceToDevice, s);
+          if (gram)
+            cudaMemcpyAsync(Gsel + (int64_t)k * nq, Gsel + (int64_t)keep_pos[k] * nq, sizeof(double) * nq,
+                            cudaMemcpyDeviceToDevice, s);
+        }
       selected = keep_ids;
       x = keep_x;
       qr.k = 0;
@@ -615,18 +843,21 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
     }
     ++iters;
     // resid = rhs - J_sel x
-    cudaMemcpyAsync(xdev, x.data(), sizeof(double) * x.size(), cudaMemcpyHostToDevice, s);
-    k_resid<<<n_rb, 256, 0, s>>>(m, (int)x.size(), Jsel, xdev, rhs, r, pss, pmx);
+    std::copy(x.begin(), x.end(), px);
+    cudaMemcpyAsync(xdev, px, sizeof(double) * x.size(), cudaMemcpyHostToDevice, s);
+    {
+      KTimer kt(ctx, s, "k_resid");
+      k_resid<<<n_rb, 256, 0, s>>>(m, (int)x.size(), Jsel, xdev, rhs, r, pss, pmx);
+    }
     ctx->launches += 1;
-    std::vector<double> hs(n_rb), hm(n_rb);
-    cudaMemcpyAsync(hs.data(), pss, sizeof(double) * n_rb, cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(hm.data(), pmx, sizeof(double) * n_rb, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(ps, pss, sizeof(double) * n_rb, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(pm, pmx, sizeof(double) * n_rb, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     double ss = 0.0;
     rmax = 0.0;
     for (int b = 0; b < n_rb; ++b) {
-      ss += hs[b];
-      rmax = std::max(rmax, hm[b]);
+      ss += ps[b];
+      rmax = std::max(rmax, pm[b]);
     }
     rnorm = std::sqrt(ss);
   }
@@ -663,6 +894,13 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
   cudaFree(pss);
   cudaFree(pmx);
   cudaFree(unav);
+  cudaFree(qpart);
+  if (pin) cudaFreeHost(pin);
+  cudaFree(c0);
+  cudaFree(Gsel);
+  cudaFree(gpart);
+  cudaFree(cta_bg);
+  cudaFree(cta_ig);
   return rc;
 }
 
