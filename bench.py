@@ -46,6 +46,19 @@ def _hbm_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def _ncu_traffic(kernel: str, points: int):
+    """dram__bytes_read + dram__bytes_write per launch of `kernel` from the
+    committed ncu --set full capture (profiles/ncu_traffic.json), scaled to
+    this launch size; None if there is no capture."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        d = json.loads(p.read_text())[kernel]
+        b = d["dram_bytes_read"] + d["dram_bytes_write"]
+        return round(b * points / d["points_per_launch"]) if "points_per_launch" in d else b
+    except Exception:
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -533,6 +546,7 @@ def run_c4(args, ws, rank, local, ctx, steps, warmup, fp64):
         gbs = wbytes * kgc[1] / (kgc[0] * 1e-3) / 1e9
         out["roofline"]["ecm_gram_col"] = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
                                            "frac": round(gbs / hbm, 4), "bytes_per_launch": wbytes,
+                                           "traffic": _ncu_traffic("k_ecm_gram_col", 0),
                                            "peak_source": src}
     if rank == 0 and ws == 1 and not args.no_cpu:
         # CPU baseline on a bounded sample: the POD stage (Gram + eigh, LAPACK,
@@ -646,7 +660,8 @@ def main():
                            "l2": "1.2 GB touched per step > 126 MB L2 (no flush needed)",
                            "plastic_fraction": round(r["plastic_frac"], 4)},
                 "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
-                             "frac": round(ach / peak, 4), "traffic": None, "peak_source": src,
+                             "frac": round(ach / peak, 4), "traffic": _ncu_traffic("k_material_batch", n),
+                             "peak_source": src,
                              "kernel": "k_material_batch", "algorithmic_bytes_per_point": C1_BYTES_PER_POINT,
                              "kernel_ms": round(r["kern_ms"], 4),
                              "note": "FP64-issue bound (9 evaluations/point); see fp64 block"},
