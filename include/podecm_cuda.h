@@ -40,6 +40,8 @@ extern "C" {
 #define PODECM_ECONFIG 2
 #define PODECM_ESOLVE 3
 #define PODECM_ECUDA 4
+#define PODECM_EIO 5     /* IoError (types.hpp:50-53); the reference CLI exits 2 */
+#define PODECM_EFORMAT 6 /* FormatError (types.hpp:55-58); the reference CLI exits 2 */
 
 typedef struct podecm_ctx podecm_ctx;
 typedef struct podecm_rve podecm_rve;
@@ -195,6 +197,28 @@ int podecm_rom_engines_commit(podecm_ctx* ctx, void* stream, podecm_rom_engines*
 /* RomMicroEngine::out_of_range per engine -> counts [n] (device). */
 int podecm_rom_engines_out_of_range(podecm_ctx* ctx, void* stream, const podecm_rom_engines* eng,
                                     int32_t* counts);
+
+/* ---- interchange formats ----------------------------
+ * PODECM1 named-array container (store.cpp:127-238) holding a RomModel
+ * (rom.cpp:265-327).  Host arrays only; no context or device needed.
+ * Errors: 5 IoError, 6 FormatError (message: podecm_store_last_error). */
+const char* podecm_store_last_error(void);
+/* FNV-1a 64-bit (store.hpp:52-54); seed 14695981039346656037 for a fresh hash. */
+uint64_t podecm_fnv1a64(const void* data, uint64_t n, uint64_t seed);
+/* Mesh::fingerprint (mesh.cpp:158-180) of the Q4 cell: element-kind byte 2
+ * (the reference knows Tri6 = 0 and Quad8 = 1), no boundary tags. */
+uint64_t podecm_rve_fingerprint(const podecm_rve* rve);
+/* RomModel::save: modes column-major [N][n_dof] (Eigen MatX storage),
+ * ids [Q], weights [Q], mode_grads [Q][N][4]. */
+int podecm_rom_model_save(const char* path, uint64_t mesh_tag, int32_t kind, int32_t n_stress_modes,
+                          double ecm_eps, int64_t n_dof, int32_t N, const double* modes, int32_t Q,
+                          const int32_t* ids, const double* weights, const double* mode_grads);
+/* RomModel::load in two calls: the shapes and scalars, then the arrays
+ * (each output nullable; layouts as for podecm_rom_model_save). */
+int podecm_rom_model_info(const char* path, int64_t* n_dof, int32_t* N, int32_t* Q, uint64_t* mesh_tag,
+                          int32_t* kind, int32_t* n_stress_modes, double* ecm_eps);
+int podecm_rom_model_read(const char* path, double* modes, int32_t* ids, double* weights,
+                          double* mode_grads);
 
 /* ---- (iv) offline POD / ECM (BASELINE config 4) -------------------------
  * Replaces pod_impl / pod_diag (podkit.cpp:43-72, 117-127):

@@ -23,7 +23,7 @@ ORACLE_DIR = ROOT / "oracle"
 ORACLE_LIB = ORACLE_DIR / "liboracle.so"
 
 CU_SOURCES = ["k_material.cu", "rve_host.cu", "k_assemble.cu", "k_rom.cu", "k_pod.cu", "k_ecm.cu",
-              "k_probe.cu"]
+              "k_probe.cu", "store.cpp"]
 HOST_CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 
 
@@ -53,7 +53,7 @@ def _stale(target: Path, deps: list[Path]) -> bool:
 
 def build_product(force: bool = False, verbose: bool = False) -> Path:
     srcs = [CSRC / s for s in CU_SOURCES if (CSRC / s).exists()]
-    deps = srcs + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "podecm_cuda.h"]
+    deps = srcs + list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "podecm_cuda.h"]
     if not force and not _stale(LIB, deps):
         return LIB
     objdir = ROOT / "build" / "obj"

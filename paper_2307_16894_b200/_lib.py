@@ -74,6 +74,13 @@ _SIGS = {
     "podecm_rom_engines_respond": (C.c_int, [P, P, P, P, C.POINTER(podecm_newton), P, P, P, P]),
     "podecm_rom_engines_commit": (C.c_int, [P, P, P]),
     "podecm_rom_engines_out_of_range": (C.c_int, [P, P, P, P]),
+    "podecm_store_last_error": (C.c_char_p, []),
+    "podecm_fnv1a64": (C.c_uint64, [P, C.c_uint64, C.c_uint64]),
+    "podecm_rve_fingerprint": (C.c_uint64, [P]),
+    "podecm_rom_model_save": (C.c_int, [C.c_char_p, C.c_uint64, I32, I32, D, I64, I32, P, I32, P, P, P]),
+    "podecm_rom_model_info": (C.c_int, [C.c_char_p, C.POINTER(I64), C.POINTER(I32), C.POINTER(I32),
+                                        C.POINTER(C.c_uint64), C.POINTER(I32), C.POINTER(I32), C.POINTER(D)]),
+    "podecm_rom_model_read": (C.c_int, [C.c_char_p, P, P, P, P]),
 }
 
 # every symbol include/podecm_cuda.h declares (checked by tests on CPU)
@@ -94,6 +101,14 @@ class SolveError(PodecmError):
 
 class CudaError(PodecmError):
     """C-ABI code 4."""
+
+
+class IoError(PodecmError):
+    """Reference IoError (types.hpp:50-53); C-ABI code 5."""
+
+
+class FormatError(PodecmError):
+    """Reference FormatError (types.hpp:55-58); C-ABI code 6."""
 
 
 def load(path: Path | str | None = None):
@@ -128,4 +143,8 @@ def raise_for(rc: int, ctx=None, what: str = "") -> None:
         raise SolveError(msg)
     if rc == 4:
         raise CudaError(msg)
+    if rc in (5, 6):
+        m = load().podecm_store_last_error()
+        msg = f"{what}: {m.decode() if m else ''}"
+        raise (IoError if rc == 5 else FormatError)(msg)
     raise PodecmError(f"{msg} (code {rc})")

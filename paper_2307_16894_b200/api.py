@@ -197,6 +197,10 @@ class Rve:
                                                                 "slot_ptr", "slot_terms")))
         return t
 
+    def fingerprint(self) -> int:
+        """Mesh::fingerprint (mesh.cpp:158-180) of this cell (Q4 kind byte 2)."""
+        return int(self.lib.podecm_rve_fingerprint(self.h))
+
     def morph(self, geom: torch.Tensor):
         """Analytic morph at every qp: (fmu_inv [n,4,nqp], det [n,nqp], status)."""
         n = geom.shape[0]
@@ -471,3 +475,56 @@ class RomEngines:
                 self.h = None
         except Exception:
             pass
+
+
+# ---- interchange formats --------------------------------
+FNV_SEED = 14695981039346656037
+
+
+def rom_model_save(path, model: dict) -> None:
+    """RomModel::save (rom.cpp:265-289) into a PODECM1 container.  ``model``:
+    modes [n_dof, N] (numpy), ids [Q], weights [Q], mode_grads [Q, N, 4],
+    optional mesh_tag, kind, n_stress_modes, ecm_eps."""
+    import numpy as np
+    lib = _lib.load()
+    modes = np.asfortranarray(model["modes"], dtype=np.float64)
+    ids = np.ascontiguousarray(model["ids"], dtype=np.int32)
+    w = np.ascontiguousarray(model["weights"], dtype=np.float64)
+    mg = np.ascontiguousarray(model["mode_grads"], dtype=np.float64)
+    n_dof, N = modes.shape
+    Q = ids.shape[0]
+    if mg.shape != (Q, N, 4) or w.shape != (Q,):
+        raise ConfigError("rom_model_save: inconsistent ids/weights/mode_grads shapes")
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+    rc = lib.podecm_rom_model_save(str(path).encode(), int(model.get("mesh_tag", 0)), int(model.get("kind", 0)),
+                                   int(model.get("n_stress_modes", 0)), float(model.get("ecm_eps", 0.0)), n_dof, N,
+                                   p(modes), Q, p(ids), p(w), p(mg))
+    _lib.raise_for(rc, None, "rom_model_save")
+
+
+def rom_model_load(path) -> dict:
+    """RomModel::load (rom.cpp:291-327): the arrays of rom_model_save plus
+    mesh_tag, kind, n_stress_modes, ecm_eps.  Raises IoError / FormatError
+    like the reference."""
+    import numpy as np
+    lib = _lib.load()
+    n_dof, N, Q = C.c_int64(), C.c_int32(), C.c_int32()
+    tag, kind, nsm, eps = C.c_uint64(), C.c_int32(), C.c_int32(), C.c_double()
+    rc = lib.podecm_rom_model_info(str(path).encode(), C.byref(n_dof), C.byref(N), C.byref(Q), C.byref(tag),
+                                   C.byref(kind), C.byref(nsm), C.byref(eps))
+    _lib.raise_for(rc, None, "rom_model_load")
+    modes = np.empty((N.value, n_dof.value))  # column-major image
+    ids = np.empty(Q.value, np.int32)
+    w = np.empty(Q.value)
+    mg = np.empty((Q.value, N.value, 4))
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+    rc = lib.podecm_rom_model_read(str(path).encode(), p(modes), p(ids), p(w), p(mg))
+    _lib.raise_for(rc, None, "rom_model_load")
+    return {"modes": modes.T, "ids": ids, "weights": w, "mode_grads": mg, "mesh_tag": tag.value,
+            "kind": kind.value, "n_stress_modes": nsm.value, "ecm_eps": eps.value}
+
+
+def fnv1a64(data: bytes, seed: int = FNV_SEED) -> int:
+    """FNV-1a 64 (store.hpp:52-54) as the library computes it."""
+    buf = C.create_string_buffer(bytes(data), len(data))
+    return int(_lib.load().podecm_fnv1a64(buf, len(data), seed))

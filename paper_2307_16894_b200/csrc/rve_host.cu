@@ -338,4 +338,29 @@ int podecm_rve_export(const podecm_rve* r, double* nodes, int32_t* elems, int32_
   return PODECM_OK;
 }
 
+uint64_t podecm_rve_fingerprint(const podecm_rve* r) {
+  if (!r) return 0;
+  uint64_t h = podecm_fnv1a64(nullptr, 0, 14695981039346656037ull);
+  const uint8_t kind = 2;  // Q4 (reference: Tri6 = 0, Quad8 = 1)
+  h = podecm_fnv1a64(&kind, 1, h);
+  const int64_t counts[3] = {r->n_nodes, r->n_elems, 0};
+  h = podecm_fnv1a64(counts, sizeof(counts), h);
+  std::vector<double> cm(2 * (size_t)r->n_nodes);  // Eigen n x 2 column-major
+  for (int n = 0; n < r->n_nodes; ++n) {
+    cm[n] = r->nodes[2 * (size_t)n];
+    cm[(size_t)r->n_nodes + n] = r->nodes[2 * (size_t)n + 1];
+  }
+  h = podecm_fnv1a64(cm.data(), sizeof(double) * cm.size(), h);
+  for (int e = 0; e < r->n_elems; ++e)
+    for (int a = 0; a < 4; ++a) {
+      const int64_t v = r->elems[4 * (size_t)e + a];
+      h = podecm_fnv1a64(&v, sizeof(v), h);
+    }
+  for (int e = 0; e < r->n_elems; ++e) {
+    const int64_t v = r->regions[e];
+    h = podecm_fnv1a64(&v, sizeof(v), h);
+  }
+  return h;
+}
+
 }  // extern "C"
