@@ -198,6 +198,22 @@ int podecm_rom_engines_commit(podecm_ctx* ctx, void* stream, podecm_rom_engines*
 int podecm_rom_engines_out_of_range(podecm_ctx* ctx, void* stream, const podecm_rom_engines* eng,
                                     int32_t* counts);
 
+/* ---- full-order Newton ------------------------------
+ * solve_rve with solve_step_adaptive (microfem.cpp:142-238) for a batch of
+ * instances around the batched assembly; the sparse solves are one batched
+ * LU refactorisation per Newton round (symbolic analysis once per pattern). */
+typedef struct podecm_fe podecm_fe;
+int podecm_fe_create(podecm_ctx* ctx, podecm_rve* rve, podecm_fe** out);
+void podecm_fe_destroy(podecm_fe* fe);
+/* Batch-wide Newton rounds of the last solve. */
+int64_t podecm_fe_global_iterations(const podecm_fe* fe);
+/* geom [n][2]; sched [n][K][4] -> pbar [n][K][4] (RveSolution::steps[k].pbar),
+ * iters [n][K], resid [n][K] (nullable), w_final [n][n_red] (nullable),
+ * status [n] (nullable; 3 = SolveError). */
+int podecm_fe_solve_batch(podecm_ctx* ctx, void* stream, podecm_fe* fe, int64_t n, const double* geom,
+                          const double* sched, int K, const podecm_newton* opts, double* pbar,
+                          int32_t* iters, double* resid, double* w_final, int32_t* status);
+
 /* ---- interchange formats ----------------------------
  * PODECM1 named-array container (store.cpp:127-238) holding a RomModel
  * (rom.cpp:265-327).  Host arrays only; no context or device needed.

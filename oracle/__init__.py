@@ -52,6 +52,8 @@ def lib(libm: str = "glibc"):
         l.orc_rom_solve.argtypes = [P, I, I, P, P, P, L, P, P, I, D, D, I, I, P, P, P, P, P, P, I]
         l.orc_rom_effective_stiffness.restype = L
         l.orc_rom_effective_stiffness.argtypes = [P, I, I, P, P, P, L, P, P, P, P, P, P, I]
+        l.orc_fe_solve.restype = L
+        l.orc_fe_solve.argtypes = [P, L, P, P, I, D, D, I, I, P, P, P, P, P, I]
         l.orc_rom_engines_create.restype = P
         l.orc_rom_engines_create.argtypes = [P, I, I, P, P, P, L, P, P, D, D, I, I]
         l.orc_rom_engines_destroy.argtypes = [P]
@@ -187,6 +189,21 @@ class Rve:
         if abar:
             out["abar"] = ab
         return out
+
+    def fe_solve(self, geom, sched, eps_rel=1e-8, eps_abs=1e-12, max_iter=25, max_bisect=5, nthreads=0):
+        """Full-order solve_rve (microfem.cpp:213-238) per instance: pbar
+        [n, K, 4], iters [n, K], resid [n, K], w_final [n, n_red], status [n]."""
+        geom = np.ascontiguousarray(geom, dtype=np.float64)
+        sched = np.ascontiguousarray(sched, dtype=np.float64)
+        n, K = sched.shape[0], sched.shape[1]
+        pbar = np.empty((n, K, 4))
+        iters = np.empty((n, K), np.int32)
+        resid = np.empty((n, K))
+        wf = np.empty((n, self.n_red))
+        status = np.empty(n, np.int32)
+        self.L.orc_fe_solve(self.h, n, _p(geom), _p(sched), K, eps_rel, eps_abs, max_iter, max_bisect, _p(pbar),
+                            _p(iters), _p(resid), _p(wf), _p(status), nthreads)
+        return {"pbar": pbar, "iters": iters, "resid": resid, "w_final": wf, "status": status}
 
     def rom_effective_stiffness(self, ids, weights, mode_grads, geom, st0, fbar, a, nthreads=0):
         """rom_effective_stiffness (rom.cpp:202-241): abar [n, 16] (Tensor4

@@ -385,6 +385,46 @@ void orc_rom_engines_out_of_range(void* eh, int* out) {
   for (size_t s = 0; s < e->eng.size(); ++s) out[s] = e->eng[s].out_of_range;
 }
 
+// Full-order solve_rve per instance (microfem.cpp:213-238): geom[n][2],
+// sched[n][K][4] -> pbar[n][K][4], iters[n][K], resid[n][K], w_final[n][n_red],
+// status 0/3.
+long orc_fe_solve(void* hp, long n_inst, const double* geom, const double* sched, int K, double eps_rel,
+                  double eps_abs, int max_iter, int max_bisect, double* pbar, int* iters, double* resid,
+                  double* w_final, int* status, int nthreads) {
+  set_threads(nthreads);
+  auto* h = static_cast<OrcRve*>(hp);
+  const RveProblem& prob = h->prob;
+  NewtonOpts o;
+  o.eps_rel = eps_rel;
+  o.eps_abs = eps_abs;
+  o.max_iter = max_iter;
+  const int nr = prob.dofs.n_red;
+  long fails = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : fails)
+  for (long s = 0; s < n_inst; ++s) {
+    try {
+      const Morph mo = derive(prob.mesh, prob.cache,
+                              analytic_morph_d(prob.mesh, geom[2 * s], geom[2 * s + 1], h->r0));
+      std::vector<Mat2> sc(K);
+      for (int k = 0; k < K; ++k)
+        for (int c = 0; c < 4; ++c) sc[k].a[c] = sched[((size_t)s * K + k) * 4 + c];
+      std::vector<double> wf;
+      const auto recs = fe_solve(prob, mo, sc, o, max_bisect, &wf);
+      for (int k = 0; k < K; ++k) {
+        for (int c = 0; c < 4; ++c) pbar[((size_t)s * K + k) * 4 + c] = recs[k].pbar.a[c];
+        if (iters) iters[(size_t)s * K + k] = recs[k].iters;
+        if (resid) resid[(size_t)s * K + k] = recs[k].residual;
+      }
+      if (w_final) std::memcpy(w_final + (size_t)s * nr, wf.data(), nr * sizeof(double));
+      if (status) status[s] = 0;
+    } catch (const SolveError&) {
+      if (status) status[s] = 3;
+      ++fails;
+    }
+  }
+  return fails;
+}
+
 // Weighted stress snapshots for ECM (ecm.cpp:10-18 on the parent cell):
 // W[s][q][c] = flatten(P Fmu^-T det) with P from large_strain_update at
 // F = I + grad u_s (assemble's F with Fbar = I, identity morph) from a virgin

@@ -195,6 +195,12 @@ std::vector<RomStepRecord> rom_solve(const RveProblem& prob, const RomModel& mod
                                      const std::vector<Mat2>& schedule, const NewtonOpts& opts,
                                      int max_bisect, std::vector<double>* a_final,
                                      std::vector<PlasticState>* prev_states = nullptr);
+// microfem.cpp:213-238 (solve_rve) with solve_step_adaptive (:190-211);
+// dense LU in place of Eigen::SparseLU.  Throws SolveError.
+std::vector<RomStepRecord> fe_solve(const RveProblem& prob, const Morph& mo, const std::vector<Mat2>& schedule,
+                                    const NewtonOpts& o, int max_bisect, std::vector<double>* w_final);
+// Eigen PartialPivLU restated (dense, column-major k n x n); returns k^-1 rhs.
+std::vector<double> lu_solve(std::vector<double> k, int n, std::vector<double> rhs);
 // rom.cpp:202-241; out[r + 4c] (Tensor4 storage).  Throws SolveError.
 void rom_effective_stiffness(const RveProblem& prob, const RomModel& model,
                              const std::vector<Mat2>& fmi, const std::vector<double>& det,

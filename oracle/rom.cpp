@@ -80,40 +80,6 @@ Mat2 rom_effective_stress(const RveProblem& prob, const RomModel& model,
   return pbar;
 }
 
-// Eigen PartialPivLU (unblocked restatement): pivot = first row of maximal
-// |a_ik|, rows swapped whole, unit-lower L, then forward/back substitution.
-std::vector<double> lu_solve(std::vector<double> k, int n, std::vector<double> rhs) {
-  std::vector<int> perm(n);
-  for (int c = 0; c < n; ++c) {
-    int piv = c;
-    double best = std::abs(k[(size_t)c * n + c]);
-    for (int r = c + 1; r < n; ++r)
-      if (std::abs(k[(size_t)c * n + r]) > best) {
-        best = std::abs(k[(size_t)c * n + r]);
-        piv = r;
-      }
-    perm[c] = piv;
-    if (piv != c)
-      for (int j = 0; j < n; ++j) std::swap(k[(size_t)j * n + c], k[(size_t)j * n + piv]);
-    if (best != 0.0) {
-      const double d = k[(size_t)c * n + c];
-      for (int r = c + 1; r < n; ++r) k[(size_t)c * n + r] /= d;
-    }
-    for (int j = c + 1; j < n; ++j) {
-      const double u = k[(size_t)j * n + c];
-      for (int r = c + 1; r < n; ++r) k[(size_t)j * n + r] -= k[(size_t)c * n + r] * u;
-    }
-  }
-  for (int c = 0; c < n; ++c) std::swap(rhs[c], rhs[perm[c]]);
-  for (int c = 0; c < n; ++c)
-    for (int r = c + 1; r < n; ++r) rhs[r] -= k[(size_t)c * n + r] * rhs[c];
-  for (int c = n - 1; c >= 0; --c) {
-    rhs[c] /= k[(size_t)c * n + c];
-    for (int r = 0; r < c; ++r) rhs[r] -= k[(size_t)c * n + r] * rhs[c];
-  }
-  return rhs;
-}
-
 double norm2(const std::vector<double>& v) {
   double s = 0;
   for (double x : v) s += x * x;
@@ -178,6 +144,40 @@ StepOut rom_step_adaptive(const RveProblem& prob, const RomModel& model,
 }
 
 }  // namespace
+
+// Eigen PartialPivLU (unblocked restatement): pivot = first row of maximal
+// |a_ik|, rows swapped whole, unit-lower L, then forward/back substitution.
+std::vector<double> lu_solve(std::vector<double> k, int n, std::vector<double> rhs) {
+  std::vector<int> perm(n);
+  for (int c = 0; c < n; ++c) {
+    int piv = c;
+    double best = std::abs(k[(size_t)c * n + c]);
+    for (int r = c + 1; r < n; ++r)
+      if (std::abs(k[(size_t)c * n + r]) > best) {
+        best = std::abs(k[(size_t)c * n + r]);
+        piv = r;
+      }
+    perm[c] = piv;
+    if (piv != c)
+      for (int j = 0; j < n; ++j) std::swap(k[(size_t)j * n + c], k[(size_t)j * n + piv]);
+    if (best != 0.0) {
+      const double d = k[(size_t)c * n + c];
+      for (int r = c + 1; r < n; ++r) k[(size_t)c * n + r] /= d;
+    }
+    for (int j = c + 1; j < n; ++j) {
+      const double u = k[(size_t)j * n + c];
+      for (int r = c + 1; r < n; ++r) k[(size_t)j * n + r] -= k[(size_t)c * n + r] * u;
+    }
+  }
+  for (int c = 0; c < n; ++c) std::swap(rhs[c], rhs[perm[c]]);
+  for (int c = 0; c < n; ++c)
+    for (int r = c + 1; r < n; ++r) rhs[r] -= k[(size_t)c * n + r] * rhs[c];
+  for (int c = n - 1; c >= 0; --c) {
+    rhs[c] /= k[(size_t)c * n + c];
+    for (int r = 0; r < c; ++r) rhs[r] -= k[(size_t)c * n + r] * rhs[c];
+  }
+  return rhs;
+}
 
 // rom.cpp:177-200.  prev_states (nullable): the history committed at the
 // start of the last increment (run_online's prev_states, pipeline.cpp:456-468).

@@ -23,7 +23,7 @@ ORACLE_DIR = ROOT / "oracle"
 ORACLE_LIB = ORACLE_DIR / "liboracle.so"
 
 CU_SOURCES = ["k_material.cu", "rve_host.cu", "k_assemble.cu", "k_rom.cu", "k_pod.cu", "k_ecm.cu",
-              "k_probe.cu", "store.cpp"]
+              "k_probe.cu", "k_fe.cu", "store.cpp"]
 HOST_CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 
 
@@ -70,7 +70,7 @@ def build_product(force: bool = False, verbose: bool = False) -> Path:
         objs.append(str(o))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-ccbin", HOST_CXX,
-           "-o", str(tmp), *objs, "-lcudart", "-lcusolver"]
+           "-o", str(tmp), *objs, "-lcudart", "-lcusolver", "-lcusparse"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -74,6 +74,10 @@ _SIGS = {
     "podecm_rom_engines_respond": (C.c_int, [P, P, P, P, C.POINTER(podecm_newton), P, P, P, P]),
     "podecm_rom_engines_commit": (C.c_int, [P, P, P]),
     "podecm_rom_engines_out_of_range": (C.c_int, [P, P, P, P]),
+    "podecm_fe_create": (C.c_int, [P, P, C.POINTER(P)]),
+    "podecm_fe_destroy": (None, [P]),
+    "podecm_fe_global_iterations": (I64, [P]),
+    "podecm_fe_solve_batch": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton), P, P, P, P, P]),
     "podecm_store_last_error": (C.c_char_p, []),
     "podecm_fnv1a64": (C.c_uint64, [P, C.c_uint64, C.c_uint64]),
     "podecm_rve_fingerprint": (C.c_uint64, [P]),

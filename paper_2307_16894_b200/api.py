@@ -477,6 +477,47 @@ class RomEngines:
             pass
 
 
+class FullOrder:
+    """Full-order solve_rve (microfem.cpp:142-238) on the GPU for a batch of
+    instances of one Rve: batched assembly + batched sparse LU refactorisation."""
+
+    def __init__(self, rve: Rve):
+        self.rve = rve
+        self.ctx = rve.ctx
+        self.lib = rve.lib
+        h = C.c_void_p()
+        _lib.raise_for(self.lib.podecm_fe_create(self.ctx.h, rve.h, C.byref(h)), self.ctx.h, "podecm_fe_create")
+        self.h = h
+
+    def solve(self, geom: torch.Tensor, sched: torch.Tensor, opts: NewtonOpts | None = None) -> dict:
+        """pbar [n, K, 4], iters [n, K], resid [n, K], w_final [n, n_red], status [n]."""
+        opts = opts or NewtonOpts()
+        n, K = sched.shape[0], sched.shape[1]
+        dev = sched.device
+        _f64(geom, (n, 2), "geom")
+        _f64(sched, (n, K, 4), "sched")
+        pbar = torch.zeros((n, K, 4), dtype=torch.float64, device=dev)
+        iters = torch.zeros((n, K), dtype=torch.int32, device=dev)
+        resid = torch.zeros((n, K), dtype=torch.float64, device=dev)
+        wf = torch.zeros((n, self.rve.n_red), dtype=torch.float64, device=dev)
+        status = torch.zeros(n, dtype=torch.int32, device=dev)
+        oc = opts.c()
+        rc = self.lib.podecm_fe_solve_batch(self.ctx.h, self.ctx.stream(), self.h, n, _ptr(geom), _ptr(sched), K,
+                                            C.byref(oc), _ptr(pbar), _ptr(iters), _ptr(resid), _ptr(wf),
+                                            _ptr(status))
+        _lib.raise_for(rc, self.ctx.h, "podecm_fe_solve_batch")
+        self.global_iterations = int(self.lib.podecm_fe_global_iterations(self.h))
+        return {"pbar": pbar, "iters": iters, "resid": resid, "w_final": wf, "status": status}
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.podecm_fe_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 # ---- interchange formats (SURVEY 8(f) item 4) --------------------------------
 FNV_SEED = 14695981039346656037
 

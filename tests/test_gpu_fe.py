@@ -1,0 +1,77 @@
+"""§8(f) item 3: full-order Newton on the GPU (solve_rve + solve_step_adaptive,
+microfem.cpp:142-238) vs the CPU oracle restatement (dense LU in place of
+Eigen::SparseLU).  Homogenised stress histories within 1e-8, Newton
+iteration counts and statuses equal; the bisection path is exercised with a
+tight max_iter; the exact-limit ROM (full basis, full quadrature) matches the
+GPU full-order model (test_rom.cpp:105-124 on the device)."""
+import numpy as np
+import pytest
+
+from paper_2307_16894_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _mats():
+    from paper_2307_16894_b200.api import inclusion_params, matrix_params
+    return [matrix_params(), inclusion_params()]
+
+
+def _T(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _check(rg, ro, tol=1e-8):
+    assert np.array_equal(rg["status"], ro["status"]), (rg["status"], ro["status"])
+    ok = ro["status"] == 0
+    d = np.linalg.norm(rg["pbar"][ok] - ro["pbar"][ok], axis=-1)
+    rel = d / np.maximum(np.linalg.norm(ro["pbar"][ok], axis=-1), 1e-14)
+    mism = int((rg["iters"][ok] != ro["iters"][ok]).sum())
+    print(f"FE pbar max rel {rel.max(initial=0):.3e}; iteration mismatches {mism}/{rg['iters'][ok].size}; "
+          f"iters {ro['iters'][ok].sum(1)}")
+    assert rel.max(initial=0) <= tol
+    assert mism == 0
+
+
+@pytest.mark.parametrize("cells,n,K,seed,hm,kw", [
+    (8, 4, 3, 11, 0.15, dict(eps_rel=1e-10, eps_abs=1e-12, max_iter=25)),
+    (16, 3, 4, 12, 0.2, dict(eps_rel=1e-10, eps_abs=1e-12, max_iter=25)),
+    (8, 4, 1, 13, 0.2, dict(eps_rel=1e-10, eps_abs=1e-12, max_iter=4, max_bisect=5)),  # bisection
+    (8, 4, 1, 13, 0.1, dict(eps_rel=1e-10, eps_abs=1e-12, max_iter=3, max_bisect=5)),  # some exhaust it
+])
+def test_fe_vs_oracle(orc, cells, n, K, seed, hm, kw):
+    from paper_2307_16894_b200 import api
+    g = api.Rve(cells, _mats())
+    o = orc.Rve(cells, _mats())
+    geom, sched = synth.rom_instances(n, K, seed, hm)
+    fe = api.FullOrder(g)
+    rg = fe.solve(_T(geom), _T(sched), api.NewtonOpts(**kw))
+    rg = {k: v.cpu().numpy() for k, v in rg.items()}
+    ro = o.fe_solve(geom, sched, **kw)
+    ok = ro["status"] == 0
+    if kw["max_iter"] < 25:
+        assert ok.any() and ro["iters"][ok].max() > kw["max_iter"]  # bisection happened
+    _check(rg, ro)
+    ok = ro["status"] == 0
+    dw = np.linalg.norm(rg["w_final"][ok] - ro["w_final"][ok]) / max(np.linalg.norm(ro["w_final"][ok]), 1e-30)
+    assert dw <= 1e-8
+
+
+def test_exact_limit_rom_equals_full_order_on_gpu(orc):
+    import torch
+    from paper_2307_16894_b200 import api
+    from oracle.fe import exact_limit_model
+    o = orc.Rve(4, _mats())
+    t = o.export()
+    ids, wts, mg = exact_limit_model(o, t)
+    g = api.Rve(4, _mats())
+    geom = np.array([[0.3, 0.2], [0.22, 0.31]])
+    H = np.array([0.06, 0.02, -0.03, -0.04])
+    sched = np.array([[[1, 0, 0, 1] + (k / 6) * H for k in range(1, 7)]] * 2)
+    opts = api.NewtonOpts(eps_rel=1e-12, eps_abs=1e-14)
+    fe = api.FullOrder(g).solve(_T(geom), _T(sched), opts)
+    rom = api.Rom(g, ids, wts, mg).solve(_T(geom), _T(sched), opts)
+    rel = (torch.linalg.norm(fe["pbar"] - rom["pbar"], dim=-1) / torch.linalg.norm(fe["pbar"], dim=-1)).max().item()
+    print(f"exact limit on the GPU: ROM vs FE max rel {rel:.2e}")
+    assert rel <= 1e-8

@@ -81,3 +81,18 @@ def test_engine_first_response_equals_rom_solve(small):
     assert np.array_equal(r1["pbar"], rs["pbar"][:, 0]) and np.array_equal(r1["abar"], rs["abar"])
     assert np.array_equal(r1["iters"], rs["iters"][:, 0])
     assert np.array_equal(r1["pbar"], r2["pbar"])
+
+
+def test_oracle_full_order_newton_matches_dense_python(orc):
+    """oracle fe_solve (C++, microfem.cpp:142-238 with bisection) agrees with
+    the independent Python Newton of oracle/fe.py on a case without bisection."""
+    from oracle.fe import fe_newton_pbar
+    from paper_2307_16894_b200.api import inclusion_params, matrix_params
+    o = orc.Rve(8, [matrix_params(), inclusion_params()])
+    t = o.export()
+    geom, sched = synth.rom_instances(2, 3, 5, 0.15)
+    r = o.fe_solve(geom, sched, eps_rel=1e-10)
+    assert np.all(r["status"] == 0)
+    for s in range(2):
+        ref = fe_newton_pbar(o, t, tuple(geom[s]), sched[s])
+        assert np.abs(r["pbar"][s] - ref).max() <= 1e-12 * np.abs(ref).max()
