@@ -132,6 +132,14 @@ int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* rve, int64_
                           const double* w_red, const double* st0, double* st1, double* f,
                           double* kvals, double* p_field, int32_t* status);
 
+/* podecm_assemble_batch plus AssemblyOpts::store_tangent_field
+ * (microfem.hpp:58-69): a_field [n_inst][16][n_qp] (plane r + 4c, the FD
+ * tangent of every qp; requires kvals). */
+int podecm_assemble_batch_ex(podecm_ctx* ctx, void* stream, podecm_rve* rve, int64_t n_inst,
+                             const double* geom, const double* morph, const double* fbar,
+                             const double* w_red, const double* st0, double* st1, double* f,
+                             double* kvals, double* p_field, int32_t* status, double* a_field);
+
 /* ---- (iii) hyper-reduced online stage ------------------------------------
  * RomModel (rom.hpp:15-30) restricted to what the online solve reads:
  * host arrays ids [Q] ascending, weights [Q], mode_grads [Q][N][4]
@@ -213,6 +221,12 @@ int64_t podecm_fe_global_iterations(const podecm_fe* fe);
 int podecm_fe_solve_batch(podecm_ctx* ctx, void* stream, podecm_fe* fe, int64_t n, const double* geom,
                           const double* sched, int K, const podecm_newton* opts, double* pbar,
                           int32_t* iters, double* resid, double* w_final, int32_t* status);
+/* effective_stiffness (microfem.cpp:240-313) for n instances: geom [n][2],
+ * st0 [n][6][n_qp], fbar [n][4], w [n][n_red] -> abar [n][16] (Tensor4
+ * storage r + 4c), status [n] (nullable). */
+int podecm_fe_effective_stiffness_batch(podecm_ctx* ctx, void* stream, podecm_fe* fe, int64_t n,
+                                        const double* geom, const double* st0, const double* fbar,
+                                        const double* w, double* abar, int32_t* status);
 
 /* ---- interchange formats ----------------------------
  * PODECM1 named-array container (store.cpp:127-238) holding a RomModel

@@ -54,6 +54,8 @@ def lib(libm: str = "glibc"):
         l.orc_rom_effective_stiffness.argtypes = [P, I, I, P, P, P, L, P, P, P, P, P, P, I]
         l.orc_fe_solve.restype = L
         l.orc_fe_solve.argtypes = [P, L, P, P, I, D, D, I, I, P, P, P, P, P, I]
+        l.orc_fe_effective_stiffness.restype = L
+        l.orc_fe_effective_stiffness.argtypes = [P, L, P, P, P, P, P, P, I]
         l.orc_rom_engines_create.restype = P
         l.orc_rom_engines_create.argtypes = [P, I, I, P, P, P, L, P, P, D, D, I, I]
         l.orc_rom_engines_destroy.argtypes = [P]
@@ -204,6 +206,16 @@ class Rve:
         self.L.orc_fe_solve(self.h, n, _p(geom), _p(sched), K, eps_rel, eps_abs, max_iter, max_bisect, _p(pbar),
                             _p(iters), _p(resid), _p(wf), _p(status), nthreads)
         return {"pbar": pbar, "iters": iters, "resid": resid, "w_final": wf, "status": status}
+
+    def fe_effective_stiffness(self, geom, st0, fbar, w, nthreads=0):
+        """effective_stiffness (microfem.cpp:240-313): abar [n, 16], status [n]."""
+        geom, st0, fbar, w = (np.ascontiguousarray(x, dtype=np.float64) for x in (geom, st0, fbar, w))
+        n = geom.shape[0]
+        abar = np.zeros((n, 16))
+        status = np.empty(n, np.int32)
+        self.L.orc_fe_effective_stiffness(self.h, n, _p(geom), _p(st0), _p(fbar), _p(w), _p(abar), _p(status),
+                                          nthreads)
+        return abar, status
 
     def rom_effective_stiffness(self, ids, weights, mode_grads, geom, st0, fbar, a, nthreads=0):
         """rom_effective_stiffness (rom.cpp:202-241): abar [n, 16] (Tensor4

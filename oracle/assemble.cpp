@@ -76,7 +76,8 @@ inline double A4(const double* m, int i, int j, int k, int l) {
 
 void assemble(const RveProblem& prob, const Morph& morph, const std::vector<PlasticState>& s0,
               std::vector<PlasticState>* s1, const Mat2& fbar, const std::vector<double>& w_red,
-              bool tangent, std::vector<double>& f, Csr* K, std::vector<double>* p_field) {
+              bool tangent, std::vector<double>& f, Csr* K, std::vector<double>* p_field,
+              std::vector<double>* a_field) {
   const Mesh& mesh = prob.mesh;
   const QuadCache& cache = prob.cache;
   const int nqp = cache.n_qp();
@@ -90,6 +91,7 @@ void assemble(const RveProblem& prob, const Morph& morph, const std::vector<Plas
   }
   f.assign(prob.dofs.n_red, 0.0);
   if (p_field) p_field->assign(4 * (size_t)nqp, 0.0);
+  if (a_field) a_field->assign(16 * (size_t)nqp, 0.0);
   if (s1) s1->resize(nqp);
   std::vector<Trip> trips;
   if (tangent) trips.reserve((size_t)nqp * 64);
@@ -126,6 +128,8 @@ void assemble(const RveProblem& prob, const Morph& morph, const std::vector<Plas
     if (!tangent) continue;
     double a4[16];
     large_strain_tangent(mat, s0[q], F, 1e-7, a4);
+    if (a_field)  // AssemblyOpts::store_tangent_field (microfem.hpp:62)
+      for (int k = 0; k < 16; ++k) (*a_field)[16 * (size_t)q + k] = a4[k];
     for (int a = 0; a < 4; ++a) {
       const int ra = prob.dofs.node_dof[mesh.elems[4 * e + a]];
       if (ra < 0) continue;

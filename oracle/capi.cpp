@@ -425,6 +425,40 @@ long orc_fe_solve(void* hp, long n_inst, const double* geom, const double* sched
   return fails;
 }
 
+// effective_stiffness (microfem.cpp:240-313) per instance: geom[n][2],
+// st0[n][6][nqp], fbar[n][4], w[n][n_red] -> abar[n][16]; status 0/3.
+long orc_fe_effective_stiffness(void* hp, long n_inst, const double* geom, const double* st0, const double* fbar,
+                                const double* w, double* abar, int* status, int nthreads) {
+  set_threads(nthreads);
+  auto* h = static_cast<OrcRve*>(hp);
+  const RveProblem& prob = h->prob;
+  const int nq = prob.cache.n_qp(), nr = prob.dofs.n_red;
+  long fails = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : fails)
+  for (long s = 0; s < n_inst; ++s) {
+    try {
+      const Morph mo = derive(prob.mesh, prob.cache,
+                              analytic_morph_d(prob.mesh, geom[2 * s], geom[2 * s + 1], h->r0));
+      std::vector<PlasticState> s0(nq);
+      const double* sp = st0 + (size_t)s * 6 * nq;
+      for (int q = 0; q < nq; ++q) {
+        for (int k = 0; k < 4; ++k) s0[q].Fp.a[k] = sp[(size_t)k * nq + q];
+        s0[q].Fp_zz = sp[(size_t)4 * nq + q];
+        s0[q].xi = sp[(size_t)5 * nq + q];
+      }
+      Mat2 fb;
+      for (int k = 0; k < 4; ++k) fb.a[k] = fbar[4 * s + k];
+      std::vector<double> wv(w + (size_t)s * nr, w + (size_t)(s + 1) * nr);
+      fe_effective_stiffness(prob, mo, s0, fb, wv, abar + 16 * (size_t)s);
+      if (status) status[s] = 0;
+    } catch (const SolveError&) {
+      if (status) status[s] = 3;
+      ++fails;
+    }
+  }
+  return fails;
+}
+
 // Weighted stress snapshots for ECM (ecm.cpp:10-18 on the parent cell):
 // W[s][q][c] = flatten(P Fmu^-T det) with P from large_strain_update at
 // F = I + grad u_s (assemble's F with Fbar = I, identity morph) from a virgin

@@ -14,6 +14,9 @@ namespace orc {
 
 namespace {
 
+// A(i, j, k, l) of a Tensor4 stored as m[r + 4c], r = i + 2j, c = k + 2l
+inline double A4(const double* m, int i, int j, int k, int l) { return m[(i + 2 * j) + 4 * (k + 2 * l)]; }
+
 struct FeStep {
   std::vector<double> w;
   std::vector<PlasticState> states;
@@ -111,6 +114,77 @@ std::vector<RomStepRecord> fe_solve(const RveProblem& prob, const Morph& mo, con
   }
   if (w_final) *w_final = w;
   return recs;
+}
+
+// microfem.cpp:240-313: tangent assembly with the tangent field, one
+// factorisation, four unit macro perturbations E_kl (k outer, l inner).
+void fe_effective_stiffness(const RveProblem& prob, const Morph& mo, const std::vector<PlasticState>& s0,
+                            const Mat2& fbar, const std::vector<double>& w, double out[16]) {
+  const Mesh& mesh = prob.mesh;
+  const QuadCache& cache = prob.cache;
+  const int nqp = cache.n_qp(), n = prob.dofs.n_red;
+  std::vector<double> f, pf, af;
+  Csr K;
+  assemble(prob, mo, s0, nullptr, fbar, w, true, f, &K, nullptr, &af);
+  std::vector<double> dense((size_t)n * n, 0.0);
+  for (int r = 0; r < n; ++r)
+    for (int k = K.row_ptr[r]; k < K.row_ptr[r + 1]; ++k) dense[(size_t)K.col[k] * n + r] = K.val[k];
+  std::vector<double> rhs((size_t)n * 4, 0.0);  // column-major n x 4
+  for (int q = 0; q < nqp; ++q) {
+    const int e = cache.elem_of[q];
+    const double* g = &cache.grad[(size_t)q * 8];
+    const Mat2& fmi = mo.fmu_inv[q];
+    const double wq = cache.w[q] * mo.det[q];
+    double gt[4][2];
+    for (int a = 0; a < 4; ++a)
+      for (int j = 0; j < 2; ++j) gt[a][j] = g[2 * a] * fmi(0, j) + g[2 * a + 1] * fmi(1, j);
+    const double* a4 = &af[16 * (size_t)q];
+    for (int a = 0; a < 4; ++a) {
+      const int ra = prob.dofs.node_dof[mesh.elems[4 * e + a]];
+      if (ra < 0) continue;
+      for (int k = 0; k < 2; ++k)
+        for (int l = 0; l < 2; ++l) {
+          const int col = k + 2 * l;
+          for (int i = 0; i < 2; ++i)
+            rhs[(size_t)col * n + ra + i] -= wq * (A4(a4, i, 0, k, l) * gt[a][0] + A4(a4, i, 1, k, l) * gt[a][1]);
+        }
+    }
+  }
+  double abar[16] = {0};
+  for (int k = 0; k < 2; ++k)
+    for (int l = 0; l < 2; ++l) {
+      const int col = k + 2 * l;
+      const std::vector<double> qk = lu_solve(dense, n, std::vector<double>(rhs.begin() + (size_t)col * n,
+                                                                          rhs.begin() + (size_t)(col + 1) * n));
+      std::vector<double> qf(2 * (size_t)mesh.n_nodes, 0.0);  // DofMap::expand
+      for (int i = 0; i < mesh.n_nodes; ++i) {
+        const int d = prob.dofs.node_dof[i];
+        if (d < 0) continue;
+        qf[2 * i] = qk[d];
+        qf[2 * i + 1] = qk[d + 1];
+      }
+      for (int q = 0; q < nqp; ++q) {
+        const int e = cache.elem_of[q];
+        const double* g = &cache.grad[(size_t)q * 8];
+        const Mat2& fmi = mo.fmu_inv[q];
+        const double wq = cache.w[q] * mo.det[q];
+        const double* a4 = &af[16 * (size_t)q];
+        Mat2 gq;
+        for (int a = 0; a < 4; ++a) {
+          const int node = mesh.elems[4 * e + a];
+          for (int i = 0; i < 2; ++i)
+            for (int j = 0; j < 2; ++j) gq(i, j) += qf[2 * node + i] * g[2 * a + j];
+        }
+        Mat2 df = mul(gq, fmi);
+        df(k, l) += 1.0;
+        for (int r = 0; r < 4; ++r) {  // contract: m * flatten(df)
+          double c = 0.0;
+          for (int t = 0; t < 4; ++t) c += a4[r + 4 * t] * df.a[t];
+          abar[r + 4 * col] += wq * c;
+        }
+      }
+    }
+  for (int t = 0; t < 16; ++t) out[t] = abar[t] / prob.cell_volume;
 }
 
 }  // namespace orc

@@ -168,7 +168,8 @@ struct RveProblem {
 // tangent=false skips K.
 void assemble(const RveProblem& prob, const Morph& morph, const std::vector<PlasticState>& s0,
               std::vector<PlasticState>* s1, const Mat2& fbar, const std::vector<double>& w_red,
-              bool tangent, std::vector<double>& f, Csr* K, std::vector<double>* p_field);
+              bool tangent, std::vector<double>& f, Csr* K, std::vector<double>* p_field,
+              std::vector<double>* a_field = nullptr);
 
 // ------------------------------------------------------------------ rom ----
 struct RomModel {
@@ -199,6 +200,9 @@ std::vector<RomStepRecord> rom_solve(const RveProblem& prob, const RomModel& mod
 // dense LU in place of Eigen::SparseLU.  Throws SolveError.
 std::vector<RomStepRecord> fe_solve(const RveProblem& prob, const Morph& mo, const std::vector<Mat2>& schedule,
                                     const NewtonOpts& o, int max_bisect, std::vector<double>* w_final);
+// microfem.cpp:240-313 (effective_stiffness); out[r + 4c] Tensor4 storage.
+void fe_effective_stiffness(const RveProblem& prob, const Morph& mo, const std::vector<PlasticState>& s0,
+                            const Mat2& fbar, const std::vector<double>& w, double out[16]);
 // Eigen PartialPivLU restated (dense, column-major k n x n); returns k^-1 rhs.
 std::vector<double> lu_solve(std::vector<double> k, int n, std::vector<double> rhs);
 // rom.cpp:202-241; out[r + 4c] (Tensor4 storage).  Throws SolveError.

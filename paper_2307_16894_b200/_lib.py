@@ -74,6 +74,8 @@ _SIGS = {
     "podecm_rom_engines_respond": (C.c_int, [P, P, P, P, C.POINTER(podecm_newton), P, P, P, P]),
     "podecm_rom_engines_commit": (C.c_int, [P, P, P]),
     "podecm_rom_engines_out_of_range": (C.c_int, [P, P, P, P]),
+    "podecm_assemble_batch_ex": (C.c_int, [P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P]),
+    "podecm_fe_effective_stiffness_batch": (C.c_int, [P, P, P, I64, P, P, P, P, P, P]),
     "podecm_fe_create": (C.c_int, [P, P, C.POINTER(P)]),
     "podecm_fe_destroy": (None, [P]),
     "podecm_fe_global_iterations": (I64, [P]),

@@ -216,9 +216,10 @@ class Rve:
     def assemble(self, fbar: torch.Tensor, w_red: torch.Tensor, st0: torch.Tensor,
                  geom: torch.Tensor | None = None, morph: torch.Tensor | None = None,
                  tangent: bool = True, states1: bool = True, store_stress: bool = False,
-                 out: dict | None = None) -> dict:
+                 out: dict | None = None, store_tangent_field: bool = False) -> dict:
         """Batched assemble (microfem.cpp:56-130): f [n, n_red], K values
-        [n, nnz] (CSR pattern of :meth:`export`), st1 [n, 6, nqp], p_field."""
+        [n, nnz] (CSR pattern of :meth:`export`), st1 [n, 6, nqp], p_field,
+        and with store_tangent_field the FD tangent per qp, a_field [n, 16, nqp]."""
         n = fbar.shape[0]
         dev = fbar.device
         _f64(fbar, (n, 4), "fbar")
@@ -235,11 +236,15 @@ class Rve:
         S1 = mk("st1", (n, 6, self.n_qp)) if states1 else None
         PF = mk("p_field", (n, 4, self.n_qp)) if store_stress else None
         status = o["status"] if o.get("status") is not None else torch.empty(n, dtype=torch.int32, device=dev)
-        rc = self.lib.podecm_assemble_batch(self.ctx.h, self.ctx.stream(), self.h, n, _ptr(geom),
-                                            _ptr(morph), _ptr(fbar), _ptr(w_red), _ptr(st0), _ptr(S1),
-                                            _ptr(f), _ptr(K), _ptr(PF), _ptr(status))
+        AF = mk("a_field", (n, 16, self.n_qp)) if store_tangent_field else None
+        rc = self.lib.podecm_assemble_batch_ex(self.ctx.h, self.ctx.stream(), self.h, n, _ptr(geom),
+                                               _ptr(morph), _ptr(fbar), _ptr(w_red), _ptr(st0), _ptr(S1),
+                                               _ptr(f), _ptr(K), _ptr(PF), _ptr(status), _ptr(AF))
         _lib.raise_for(rc, self.ctx.h, "podecm_assemble_batch")
-        return {"f": f, "K": K, "st1": S1, "p_field": PF, "status": status}
+        r = {"f": f, "K": K, "st1": S1, "p_field": PF, "status": status}
+        if store_tangent_field:
+            r["a_field"] = AF
+        return r
 
     def __del__(self):
         try:
@@ -508,6 +513,23 @@ class FullOrder:
         _lib.raise_for(rc, self.ctx.h, "podecm_fe_solve_batch")
         self.global_iterations = int(self.lib.podecm_fe_global_iterations(self.h))
         return {"pbar": pbar, "iters": iters, "resid": resid, "w_final": wf, "status": status}
+
+    def effective_stiffness(self, geom: torch.Tensor, st0: torch.Tensor, fbar: torch.Tensor,
+                            w: torch.Tensor) -> dict:
+        """effective_stiffness (microfem.cpp:240-313): history st0 [n, 6, n_qp],
+        fbar [n, 4], fluctuation w [n, n_red] -> abar [n, 16] (Tensor4 storage
+        r + 4c), status [n]."""
+        n = geom.shape[0]
+        _f64(geom, (n, 2), "geom")
+        _f64(st0, (n, 6, self.rve.n_qp), "st0")
+        _f64(fbar, (n, 4), "fbar")
+        _f64(w, (n, self.rve.n_red), "w")
+        abar = torch.zeros((n, 16), dtype=torch.float64, device=geom.device)
+        status = torch.zeros(n, dtype=torch.int32, device=geom.device)
+        rc = self.lib.podecm_fe_effective_stiffness_batch(self.ctx.h, self.ctx.stream(), self.h, n, _ptr(geom),
+                                                          _ptr(st0), _ptr(fbar), _ptr(w), _ptr(abar), _ptr(status))
+        _lib.raise_for(rc, self.ctx.h, "podecm_fe_effective_stiffness_batch")
+        return {"abar": abar, "status": status}
 
     def __del__(self):
         try:

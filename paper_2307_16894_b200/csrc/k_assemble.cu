@@ -48,6 +48,9 @@ struct AsmArgs {
   int32_t* status;
   unsigned int* fail;
   bool tangent;
+  double* a_field;  // nullable [n][16][n_qp] (AssemblyOpts::store_tangent_field)
+  const double* field;  // field-rows mode: [n][16][n_qp] tangent field, column `field_col`
+  int field_col;
 };
 
 // 4-lane butterfly over the quad of lanes holding the 4 qps of one element:
@@ -187,6 +190,9 @@ __global__ void __launch_bounds__(128, MINB) k_asm_qp(AsmArgs g, MatTable tab) {
       double cd[2][4];
       auto sink = [&](int ecol, const double col[4]) {
         const int d = ecol >> 1, j = ecol & 1;
+        if (g.a_field)
+#pragma unroll
+          for (int r = 0; r < 4; ++r) g.a_field[((size_t)inst * 16 + r + 4 * ecol) * nq + q] = col[r];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           cd[0][r] = d == 0 ? col[r] : cd[0][r];
@@ -329,6 +335,9 @@ __global__ void __launch_bounds__(kQ2Thr, MINB) k_asm_qp2(AsmArgs g, MatTable ta
       ok = ok && ok2;
     }
   }
+  if (g.a_field && g.tangent && valid)
+#pragma unroll
+    for (int t = 0; t < 16; ++t) g.a_field[((size_t)inst * 16 + t) * nq + q] = sq[t * kQ2Thr + lt];
   // ---- phase 2: element sums from this thread's SMEM row
   const double wq = sq[28 * kQ2Thr + lt];
   double gt[4][2], P[4];
@@ -392,6 +401,65 @@ __global__ void __launch_bounds__(kQ2Thr, MINB) k_asm_qp2(AsmArgs g, MatTable ta
   if (!ok && valid) {
     if (g.status) g.status[inst] = PODECM_ESOLVE;
     atomicAdd(g.fail, 1u);
+  }
+}
+
+
+// Residual-row sums of a 2x2 "stress" taken from a stored tangent field:
+// Pc = A(:, :, k, l) with column c = k + 2l of A, i.e. the element terms
+// wq (Pc(i,0) gt_a0 + Pc(i,1) gt_a1) of effective_stiffness's right-hand
+// sides (microfem.cpp:262-281), summed exactly like the residual.
+__global__ void __launch_bounds__(256) k_asm_field_terms(AsmArgs g) {
+  const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)g.n_inst * g.n_qp;
+  const bool valid = tid0 < total;
+  const int64_t tid = valid ? tid0 : total - 1;
+  const int c = (int)(tid / g.n_qp);
+  const int q = (int)(tid - (int64_t)c * g.n_qp);
+  const int64_t inst = g.inst0 + c;
+  const int e = q >> 2, k = q & 3;
+  const int nq = g.n_qp;
+  double gq[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) gq[t] = __ldg(g.grad + (size_t)q * 8 + t);
+  double fmi[4], det;
+  if (g.morph) {
+    const double* mo = g.morph + (size_t)inst * 5 * nq;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) fmi[t] = __ldg(mo + (size_t)t * nq + q);
+    det = __ldg(mo + (size_t)4 * nq + q);
+  } else {
+    const double ka = __ldg(g.geom + 2 * inst) / g.r0 - 1.0;
+    const double kb = __ldg(g.geom + 2 * inst + 1) / g.r0 - 1.0;
+    double d[4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int nd = __ldg(g.elems + 4 * e + a);
+      morph_d(__ldg(g.nodes + 2 * nd), __ldg(g.nodes + 2 * nd + 1), ka, kb, g.r0, d[a][0], d[a][1]);
+    }
+    det = derive_qp(d, gq, fmi);
+  }
+  const double wq = __ldg(g.w + q) * det;
+  double gt[4][2], P[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) gt[a][j] = gq[2 * a] * fmi[2 * j] + gq[2 * a + 1] * fmi[1 + 2 * j];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) P[t] = g.field[((size_t)inst * 16 + t + 4 * g.field_col) * nq + q];
+  double v[8], o[2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) v[a * 2 + i] = wq * (P[i] * gt[a][0] + P[i + 2] * gt[a][1]);
+  quad_reduce8(v, k, o);
+  if (valid) {
+    double* sc = g.scratch + (size_t)c * g.n_groups;
+    const int32_t* ps = g.pos + (size_t)e * 72;
+    const int u0 = 4 * (k & 1) + 2 * ((k >> 1) & 1);
+    const int p0 = __ldg(ps + 64 + u0), p1 = __ldg(ps + 64 + u0 + 1);
+    if (p0 >= 0) sc[p0] = o[0];
+    if (p1 >= 0) sc[p1] = o[1];
   }
 }
 
@@ -505,35 +573,26 @@ __global__ void k_morph(int64_t n_inst, int nq, double r0, const double* nodes, 
 
 }  // namespace
 
-extern "C" {
+namespace podecm_impl {
 
-int podecm_rve_morph(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst,
-                     const double* geom, double* fmu_inv, double* det, int32_t* status) {
-  if (!ctx || !r || !geom || !fmu_inv || !det) return set_err(ctx, PODECM_ECONFIG, "null argument");
-  if (n_inst <= 0) return PODECM_OK;
-  auto s = static_cast<cudaStream_t>(stream);
-  if (status) PODECM_CUDA_TRY(ctx, cudaMemsetAsync(status, 0, n_inst * sizeof(int32_t), s));
-  const int64_t total = n_inst * r->n_qp;
-  k_morph<<<grid_for(total, 256), 256, 0, s>>>(n_inst, r->n_qp, r->r0, r->d_nodes, r->d_elems,
-                                               r->d_grad, geom, fmu_inv, det, status, ctx->d_fail);
-  PODECM_LAUNCHED(ctx, 1);
-  return PODECM_OK;
-}
-
-int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst,
-                          const double* geom, const double* morph, const double* fbar,
-                          const double* w_red, const double* st0, double* st1, double* f,
-                          double* kvals, double* p_field, int32_t* status) {
+// field != nullptr: field-rows mode (f = residual-row sums of the stored
+// tangent field's column field_col, see k_asm_field_terms); else the assembly.
+int assemble_impl(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst, const double* geom,
+                  const double* morph, const double* fbar, const double* w_red, const double* st0, double* st1,
+                  double* f, double* kvals, double* p_field, int32_t* status, double* a_field,
+                  const double* field, int field_col) {
   if (!ctx || !r) return PODECM_ECONFIG;
   if (n_inst < 0) return set_err(ctx, PODECM_ECONFIG, "negative instance count");
   if (n_inst == 0) return PODECM_OK;
-  if ((!geom && !morph) || !fbar || !w_red || !st0 || !f)
+  if ((!geom && !morph) || !f || (!field && (!fbar || !w_red || !st0)))
     return set_err(ctx, PODECM_ECONFIG, "geom|morph, fbar, w_red, st0 and f are required");
   auto s = static_cast<cudaStream_t>(stream);
-  static const bool exact = [] {
+  static const bool exact_env = [] {
     const char* e = getenv("PODECM_ASM_EXACT");
     return e && atoi(e) != 0;
   }();
+  const bool exact = exact_env && !field;
+  if (field) kvals = nullptr;
   static const int minb = [] {
     const char* e = getenv("PODECM_ASM_MINB");
     return e ? atoi(e) : 4;
@@ -555,7 +614,7 @@ int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t 
     PODECM_CUDA_TRY(ctx, cudaMalloc(&r->d_scratch, per_inst * chunk));
     r->scratch_inst = chunk;
   }
-  if (status) PODECM_CUDA_TRY(ctx, cudaMemsetAsync(status, 0, n_inst * sizeof(int32_t), s));
+  if (status && !field) PODECM_CUDA_TRY(ctx, cudaMemsetAsync(status, 0, n_inst * sizeof(int32_t), s));
   for (int64_t i0 = 0; i0 < n_inst; i0 += chunk) {
     const int nc = (int)std::min<int64_t>(chunk, n_inst - i0);
     AsmArgs a;
@@ -584,8 +643,14 @@ int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t 
     a.status = status;
     a.fail = ctx->d_fail;
     a.tangent = kvals != nullptr;
+    a.a_field = a_field;
+    a.field = field;
+    a.field_col = field_col;
     const int64_t nthr = (int64_t)nc * r->n_qp;
-    if (exact) {
+    if (field) {
+      KTimer kt(ctx, s, "k_asm_field_terms");
+      k_asm_field_terms<<<grid_for(nthr, 256), 256, 0, s>>>(a);
+    } else if (exact) {
       KTimer kt(ctx, s, "k_asm_qp");
       k_asm_qp<5><<<grid_for(nthr, 128), 128, 0, s>>>(a, r->mats);
     } else {
@@ -619,6 +684,47 @@ int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t 
     PODECM_LAUNCHED(ctx, 2);
   }
   return PODECM_OK;
+}
+
+
+int assemble_field_rows(podecm_ctx* ctx, cudaStream_t s, podecm_rve* r, int64_t n, const double* geom,
+                        const double* morph, const double* field, int col, double* out) {
+  return assemble_impl(ctx, s, r, n, geom, morph, nullptr, nullptr, nullptr, nullptr, out, nullptr, nullptr,
+                       nullptr, nullptr, field, col);
+}
+
+}  // namespace podecm_impl
+
+extern "C" {
+
+int podecm_rve_morph(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst,
+                     const double* geom, double* fmu_inv, double* det, int32_t* status) {
+  if (!ctx || !r || !geom || !fmu_inv || !det) return set_err(ctx, PODECM_ECONFIG, "null argument");
+  if (n_inst <= 0) return PODECM_OK;
+  auto s = static_cast<cudaStream_t>(stream);
+  if (status) PODECM_CUDA_TRY(ctx, cudaMemsetAsync(status, 0, n_inst * sizeof(int32_t), s));
+  const int64_t total = n_inst * r->n_qp;
+  k_morph<<<grid_for(total, 256), 256, 0, s>>>(n_inst, r->n_qp, r->r0, r->d_nodes, r->d_elems,
+                                               r->d_grad, geom, fmu_inv, det, status, ctx->d_fail);
+  PODECM_LAUNCHED(ctx, 1);
+  return PODECM_OK;
+}
+
+int podecm_assemble_batch(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst,
+                          const double* geom, const double* morph, const double* fbar,
+                          const double* w_red, const double* st0, double* st1, double* f,
+                          double* kvals, double* p_field, int32_t* status) {
+  return assemble_impl(ctx, stream, r, n_inst, geom, morph, fbar, w_red, st0, st1, f, kvals, p_field, status,
+                       nullptr, nullptr, 0);
+}
+
+int podecm_assemble_batch_ex(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst,
+                             const double* geom, const double* morph, const double* fbar,
+                             const double* w_red, const double* st0, double* st1, double* f,
+                             double* kvals, double* p_field, int32_t* status, double* a_field) {
+  if (a_field && !kvals) return set_err(ctx, PODECM_ECONFIG, "a_field requires the tangent (kvals)");
+  return assemble_impl(ctx, stream, r, n_inst, geom, morph, fbar, w_red, st0, st1, f, kvals, p_field, status,
+                       a_field, nullptr, 0);
 }
 
 }  // extern "C"

@@ -115,6 +115,73 @@ __global__ void k_fe_virgin(int64_t n, int nq, double* S) {
   for (int k = 0; k < 6; ++k) S[(s * 6 + k) * nq + q] = v[k];
 }
 
+
+// effective_stiffness (microfem.cpp:283-308): for each unit perturbation
+// E_kl (column c = k + 2l) with fluctuation response x_c,
+//   Abar(:, c) = sum_q wq A_q (grad(x_c) Fmu^-1 + E_kl)
+// one CTA per instance, fixed-order block tree over the qps.
+__global__ void __launch_bounds__(256) k_fe_abar(int nq, int n_red, int64_t n, const int32_t* elems,
+                                                 const int32_t* node_dof, const double* grad, const double* w,
+                                                 const double* fmi, const double* det, const double* af,
+                                                 const double* x, double* abar) {
+  __shared__ double red[16][256];
+  const int64_t s = blockIdx.x;
+  double acc[16];
+#pragma unroll
+  for (int t = 0; t < 16; ++t) acc[t] = 0.0;
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) {
+    const int e = q >> 2;
+    double g[8], m[4], A[16];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) g[t] = grad[(size_t)q * 8 + t];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) m[t] = fmi[((size_t)s * 4 + t) * nq + q];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) A[t] = af[((size_t)s * 16 + t) * nq + q];
+    const double wq = w[q] * det[(size_t)s * nq + q];
+    int dof[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) dof[a] = node_dof[elems[4 * e + a]];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double* xs = x + ((size_t)c * n + s) * n_red;
+      double gq[4];  // (i + 2j)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          double v = 0.0;
+#pragma unroll
+          for (int a = 0; a < 4; ++a) v = v + (dof[a] >= 0 ? xs[dof[a] + i] : 0.0) * g[2 * a + j];
+          gq[i + 2 * j] = v;
+        }
+      double df[4];
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) df[i + 2 * j] = gq[i] * m[2 * j] + gq[i + 2] * m[1 + 2 * j];
+      df[c] = df[c] + 1.0;  // E_kl, k + 2l = c
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        double cr = 0.0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) cr = cr + A[r + 4 * t] * df[t];
+        acc[r + 4 * c] = acc[r + 4 * c] + wq * cr;
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 16; ++t) red[t][threadIdx.x] = acc[t];
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+#pragma unroll
+      for (int t = 0; t < 16; ++t) red[t][threadIdx.x] += red[t][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x < 16) abar[s * 16 + threadIdx.x] = red[threadIdx.x][0] / 1.0;  // cell_volume
+}
+
 struct Frame {
   double fp[4], ft[4];
   int depth;
@@ -144,6 +211,8 @@ struct podecm_fe {
   int32_t *d_astat = nullptr, *d_mask = nullptr, *d_mstat = nullptr;
   double* h_pin = nullptr;  // pinned: norms, pbar, fbar, masks
   int64_t global_iters = 0;
+  double *d_af = nullptr, *d_rhs = nullptr;  // effective stiffness: tangent field, 4 right-hand sides
+  int64_t af_cap = 0;
 };
 
 namespace {
@@ -329,6 +398,8 @@ void podecm_fe_destroy(podecm_fe* e) {
   if (!e) return;
   for (cusolverRfHandle_t h : e->rf) cusolverRfDestroy(h);
   fe_free(e);
+  cudaFree(e->d_af);
+  cudaFree(e->d_rhs);
   cudaFree(e->d_row);
   cudaFree(e->d_col);
   cudaFree(e->d_P);
@@ -562,6 +633,87 @@ int podecm_fe_solve_batch(podecm_ctx* ctx, void* stream, podecm_fe* e, int64_t n
   if (w_final)
     PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(w_final, e->d_w, sizeof(double) * n * nr, cudaMemcpyDeviceToDevice, s));
   if (nfail) {  // context-wide failure count (podecm_check reports SolveError)
+    k_fe_addfail<<<1, 1, 0, s>>>(ctx->d_fail, nfail);
+    PODECM_LAUNCHED(ctx, 1);
+  }
+  PODECM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  return PODECM_OK;
+}
+
+
+int podecm_fe_effective_stiffness_batch(podecm_ctx* ctx, void* stream, podecm_fe* e, int64_t n,
+                                        const double* geom, const double* st0, const double* fbar,
+                                        const double* w, double* abar, int32_t* status) {
+  if (!ctx || !e) return PODECM_ECONFIG;
+  if (n < 0) return set_err(ctx, PODECM_ECONFIG, "negative batch size");
+  if (n == 0) return PODECM_OK;
+  if (!geom || !st0 || !fbar || !w || !abar)
+    return set_err(ctx, PODECM_ECONFIG, "geom, st0, fbar, w, abar required");
+  if (int rc = fe_alloc(e, n)) return rc;
+  podecm_rve* r = e->rve;
+  const int nr = r->n_red, nq = r->n_qp;
+  const int64_t nnz = r->nnz;
+  auto s = static_cast<cudaStream_t>(stream);
+  if (e->af_cap < n) {
+    cudaFree(e->d_af);
+    cudaFree(e->d_rhs);
+    e->d_af = e->d_rhs = nullptr;
+    e->af_cap = 0;
+    PODECM_CUDA_TRY(ctx, cudaMalloc(&e->d_af, sizeof(double) * (size_t)n * 16 * nq));
+    PODECM_CUDA_TRY(ctx, cudaMalloc(&e->d_rhs, sizeof(double) * (size_t)n * 4 * nr));
+    e->af_cap = n;
+  }
+  if (int rc = podecm_rve_morph(ctx, stream, r, n, geom, e->d_fmi, e->d_det, e->d_mstat)) return rc;
+  // tangent assembly with the tangent field (microfem.cpp:247-251)
+  if (int rc = podecm_assemble_batch_ex(ctx, stream, r, n, geom, nullptr, fbar, w, st0, nullptr, e->d_f, e->d_K,
+                                        nullptr, e->d_astat, e->d_af))
+    return rc;
+  // right-hand sides (microfem.cpp:262-281): rhs_c = -(row sums of A(:, :, c))
+  for (int c = 0; c < 4; ++c)
+    if (int rc = assemble_field_rows(ctx, s, r, n, geom, nullptr, e->d_af, c, e->d_rhs + (size_t)c * n * nr))
+      return rc;
+  k_fe_negate<<<grid_for(4 * n * nr, 256), 256, 0, s>>>(4 * n * nr, e->d_rhs, e->d_rhs);
+  PODECM_LAUNCHED(ctx, 1);
+  if (int rc = rf_setup(e, s, n)) return rc;
+  std::vector<int32_t> ast(n), mst(n);
+  PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(ast.data(), e->d_astat, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(mst.data(), e->d_mstat, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
+  PODECM_CUDA_TRY(ctx, cudaStreamSynchronize(s));  // Rf runs on the legacy stream
+  std::vector<int32_t> hst(n, 0);
+  bool ok = true;
+  std::string msg;
+  {
+    KTimer kt(ctx, s, "rf_refactor_solve");
+    for (int64_t i = 0; ok && i < n; ++i) {
+      if (ast[i] || mst[i]) {  // material or morph SolveError
+        hst[i] = PODECM_ESOLVE;
+        continue;
+      }
+      cusolverRfHandle_t h = e->rf[i];
+      FE_SP(cusolverRfResetValues(nr, (int)nnz, e->d_row, e->d_col, e->d_K + (size_t)i * nnz, e->d_P, e->d_Q, h),
+            "Rf reset values");
+      if (!ok) break;
+      const cusolverStatus_t rs = cusolverRfRefactor(h);
+      if (rs == CUSOLVER_STATUS_ZERO_PIVOT) {  // "tangent factorization failed" (microfem.cpp:254-255)
+        hst[i] = PODECM_ESOLVE;
+        continue;
+      }
+      FE_SP(rs, "Rf refactor");
+      for (int c = 0; ok && c < 4; ++c)
+        FE_SP(cusolverRfSolve(h, e->d_P, e->d_Q, 1, e->d_tmp, nr, e->d_rhs + ((size_t)c * n + i) * nr, nr),
+              "Rf solve");
+    }
+    cudaDeviceSynchronize();
+  }
+  if (!ok) return set_err(ctx, PODECM_ESOLVE, std::string("fe: ") + msg);
+  k_fe_abar<<<(unsigned)n, 256, 0, s>>>(nq, nr, n, r->d_elems, r->d_node_dof, r->d_grad, r->d_w, e->d_fmi, e->d_det,
+                                        e->d_af, e->d_rhs, abar);
+  PODECM_LAUNCHED(ctx, 1);
+  unsigned int nfail = 0;
+  for (int64_t i = 0; i < n; ++i) nfail += hst[i] != 0;
+  if (status)
+    PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(status, hst.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+  if (nfail) {
     k_fe_addfail<<<1, 1, 0, s>>>(ctx->d_fail, nfail);
     PODECM_LAUNCHED(ctx, 1);
   }

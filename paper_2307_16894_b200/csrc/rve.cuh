@@ -74,3 +74,10 @@ __device__ __forceinline__ double derive_qp(const double d[4][2], const double g
 }
 
 }  // namespace podecm_dev
+
+namespace podecm_impl {
+// Residual-row sums of column `col` of a stored tangent field [n][16][n_qp]
+// (effective_stiffness right-hand sides, microfem.cpp:262-281), k_assemble.cu.
+int assemble_field_rows(podecm_ctx* ctx, cudaStream_t s, podecm_rve* r, int64_t n, const double* geom,
+                        const double* morph, const double* field, int col, double* out);
+}  // namespace podecm_impl

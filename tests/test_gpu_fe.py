@@ -75,3 +75,51 @@ def test_exact_limit_rom_equals_full_order_on_gpu(orc):
     rel = (torch.linalg.norm(fe["pbar"] - rom["pbar"], dim=-1) / torch.linalg.norm(fe["pbar"], dim=-1)).max().item()
     print(f"exact limit on the GPU: ROM vs FE max rel {rel:.2e}")
     assert rel <= 1e-8
+
+
+def test_fe_effective_stiffness_vs_oracle(orc):
+    """effective_stiffness (microfem.cpp:240-313) at a converged first
+    increment from a virgin history: GPU vs oracle within 1e-8."""
+    from paper_2307_16894_b200 import api
+    g = api.Rve(8, _mats())
+    o = orc.Rve(8, _mats())
+    geom, sched = synth.rom_instances(3, 1, 21, 0.15)
+    kw = dict(eps_rel=1e-12, eps_abs=1e-14)
+    ro = o.fe_solve(geom, sched, **kw)
+    nq = g.n_qp
+    st0 = np.zeros((3, 6, nq))
+    st0[:, 0] = st0[:, 3] = st0[:, 4] = 1.0
+    ab_o, st_o = o.fe_effective_stiffness(geom, st0, sched[:, -1], ro["w_final"])
+    r = api.FullOrder(g).effective_stiffness(_T(geom), _T(st0), _T(sched[:, -1].copy()), _T(ro["w_final"]))
+    ab = r["abar"].cpu().numpy()
+    assert np.array_equal(r["status"].cpu().numpy(), st_o) and np.all(st_o == 0)
+    rel = np.linalg.norm(ab - ab_o, axis=-1) / np.linalg.norm(ab_o, axis=-1)
+    print(f"FE effective stiffness rel {rel.max():.3e}")
+    assert rel.max() <= 1e-8
+
+
+def test_exact_limit_effective_stiffness_on_gpu(orc):
+    """test_rom.cpp:127-156 on the device: the full-basis ROM tangent equals
+    the full-order effective stiffness (reference tolerance 1e-6)."""
+    import torch
+    from paper_2307_16894_b200 import api
+    from oracle.fe import exact_limit_model
+    o = orc.Rve(4, _mats())
+    t = o.export()
+    ids, wts, mg = exact_limit_model(o, t)
+    g = api.Rve(4, _mats())
+    geom = np.array([[0.3, 0.2]])
+    sched = np.array([[[1.02, 0.01, -0.005, 0.97]]])
+    opts = api.NewtonOpts(eps_rel=1e-12, eps_abs=1e-14)
+    fe = api.FullOrder(g)
+    rf = fe.solve(_T(geom), _T(sched), opts)
+    st0 = torch.zeros((1, 6, g.n_qp), dtype=torch.float64, device="cuda")
+    st0[:, 0] = st0[:, 3] = st0[:, 4] = 1.0
+    fb = _T(sched[:, -1].copy())
+    ab_fe = fe.effective_stiffness(_T(geom), st0, fb, rf["w_final"])["abar"]
+    rom = api.Rom(g, ids, wts, mg)
+    rr = rom.solve(_T(geom), _T(sched), opts, abar=True)
+    ab_rom = rr["abar"]
+    rel = (torch.linalg.norm(ab_fe - ab_rom) / torch.linalg.norm(ab_fe)).item()
+    print(f"exact-limit effective stiffness: ROM vs FE rel {rel:.2e}")
+    assert rel <= 1e-6
