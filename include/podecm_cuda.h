@@ -221,6 +221,18 @@ int64_t podecm_fe_global_iterations(const podecm_fe* fe);
 int podecm_fe_solve_batch(podecm_ctx* ctx, void* stream, podecm_fe* fe, int64_t n, const double* geom,
                           const double* sched, int K, const podecm_newton* opts, double* pbar,
                           int32_t* iters, double* resid, double* w_final, int32_t* status);
+/* podecm_fe_solve_batch plus the per-increment snapshots of collect_snapshots
+ * (pipeline.cpp:157-188): w_hist [n][K][n_red] converged fluctuations,
+ * p_hist [n][K][4][n_qp] stress fields (each nullable). */
+int podecm_fe_solve_batch_ex(podecm_ctx* ctx, void* stream, podecm_fe* fe, int64_t n, const double* geom,
+                             const double* sched, int K, const podecm_newton* opts, double* pbar,
+                             int32_t* iters, double* resid, double* w_final, int32_t* status,
+                             double* w_hist, double* p_hist);
+/* weighted_stress_field (ecm.cpp:10-18) on the analytic morph of each
+ * instance: p_field [n][4][n_qp] -> W [n][n_qp][4] = P Fmu^-T det (the
+ * ECM snapshot layout of podecm_ecm_select). */
+int podecm_weighted_stress_field(podecm_ctx* ctx, void* stream, podecm_rve* rve, int64_t n,
+                                 const double* geom, const double* p_field, double* W);
 /* effective_stiffness (microfem.cpp:240-313) for n instances: geom [n][2],
  * st0 [n][6][n_qp], fbar [n][4], w [n][n_red] -> abar [n][16] (Tensor4
  * storage r + 4c), status [n] (nullable). */

@@ -53,7 +53,7 @@ def lib(libm: str = "glibc"):
         l.orc_rom_effective_stiffness.restype = L
         l.orc_rom_effective_stiffness.argtypes = [P, I, I, P, P, P, L, P, P, P, P, P, P, I]
         l.orc_fe_solve.restype = L
-        l.orc_fe_solve.argtypes = [P, L, P, P, I, D, D, I, I, P, P, P, P, P, I]
+        l.orc_fe_solve.argtypes = [P, L, P, P, I, D, D, I, I, P, P, P, P, P, P, P, I]
         l.orc_fe_effective_stiffness.restype = L
         l.orc_fe_effective_stiffness.argtypes = [P, L, P, P, P, P, P, P, I]
         l.orc_rom_engines_create.restype = P
@@ -192,7 +192,8 @@ class Rve:
             out["abar"] = ab
         return out
 
-    def fe_solve(self, geom, sched, eps_rel=1e-8, eps_abs=1e-12, max_iter=25, max_bisect=5, nthreads=0):
+    def fe_solve(self, geom, sched, eps_rel=1e-8, eps_abs=1e-12, max_iter=25, max_bisect=5, nthreads=0,
+                 history=False):
         """Full-order solve_rve (microfem.cpp:213-238) per instance: pbar
         [n, K, 4], iters [n, K], resid [n, K], w_final [n, n_red], status [n]."""
         geom = np.ascontiguousarray(geom, dtype=np.float64)
@@ -203,9 +204,14 @@ class Rve:
         resid = np.empty((n, K))
         wf = np.empty((n, self.n_red))
         status = np.empty(n, np.int32)
+        wh = np.zeros((n, K, self.n_red)) if history else None
+        ph = np.zeros((n, K, 4, self.n_qp)) if history else None
         self.L.orc_fe_solve(self.h, n, _p(geom), _p(sched), K, eps_rel, eps_abs, max_iter, max_bisect, _p(pbar),
-                            _p(iters), _p(resid), _p(wf), _p(status), nthreads)
-        return {"pbar": pbar, "iters": iters, "resid": resid, "w_final": wf, "status": status}
+                            _p(iters), _p(resid), _p(wf), _p(status), _p(wh), _p(ph), nthreads)
+        out = {"pbar": pbar, "iters": iters, "resid": resid, "w_final": wf, "status": status}
+        if history:
+            out.update(w_hist=wh, p_hist=ph)
+        return out
 
     def fe_effective_stiffness(self, geom, st0, fbar, w, nthreads=0):
         """effective_stiffness (microfem.cpp:240-313): abar [n, 16], status [n]."""

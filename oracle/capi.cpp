@@ -390,7 +390,7 @@ void orc_rom_engines_out_of_range(void* eh, int* out) {
 // status 0/3.
 long orc_fe_solve(void* hp, long n_inst, const double* geom, const double* sched, int K, double eps_rel,
                   double eps_abs, int max_iter, int max_bisect, double* pbar, int* iters, double* resid,
-                  double* w_final, int* status, int nthreads) {
+                  double* w_final, int* status, double* w_hist, double* p_hist, int nthreads) {
   set_threads(nthreads);
   auto* h = static_cast<OrcRve*>(hp);
   const RveProblem& prob = h->prob;
@@ -408,8 +408,15 @@ long orc_fe_solve(void* hp, long n_inst, const double* geom, const double* sched
       std::vector<Mat2> sc(K);
       for (int k = 0; k < K; ++k)
         for (int c = 0; c < 4; ++c) sc[k].a[c] = sched[((size_t)s * K + k) * 4 + c];
-      std::vector<double> wf;
-      const auto recs = fe_solve(prob, mo, sc, o, max_bisect, &wf);
+      std::vector<double> wf, wh, ph;
+      const auto recs = fe_solve(prob, mo, sc, o, max_bisect, &wf, &wh, &ph);
+      const int nq = prob.cache.n_qp();
+      if (w_hist) std::memcpy(w_hist + (size_t)s * K * nr, wh.data(), wh.size() * sizeof(double));
+      if (p_hist)  // [s][k][4][nq] from [k][q][4]
+        for (int k = 0; k < K; ++k)
+          for (int q = 0; q < nq; ++q)
+            for (int c = 0; c < 4; ++c)
+              p_hist[(((size_t)s * K + k) * 4 + c) * nq + q] = ph[((size_t)k * nq + q) * 4 + c];
       for (int k = 0; k < K; ++k) {
         for (int c = 0; c < 4; ++c) pbar[((size_t)s * K + k) * 4 + c] = recs[k].pbar.a[c];
         if (iters) iters[(size_t)s * K + k] = recs[k].iters;

@@ -18,7 +18,7 @@ namespace {
 inline double A4(const double* m, int i, int j, int k, int l) { return m[(i + 2 * j) + 4 * (k + 2 * l)]; }
 
 struct FeStep {
-  std::vector<double> w;
+  std::vector<double> w, pf;  // pf: converged p_field [q][4]
   std::vector<PlasticState> states;
   Mat2 pbar;
   int iters = 0;
@@ -60,6 +60,7 @@ FeStep solve_step(const RveProblem& prob, const Morph& mo, const std::vector<Pla
       res.iters = it;
       res.residual = rn;
       res.pbar = effective_stress(prob, pf, mo);
+      res.pf = std::move(pf);
       return res;
     }
     if (it == o.max_iter) break;
@@ -96,7 +97,8 @@ FeStep solve_step_adaptive(const RveProblem& prob, const Morph& mo, const std::v
 
 // microfem.cpp:213-238 (solve_rve)
 std::vector<RomStepRecord> fe_solve(const RveProblem& prob, const Morph& mo, const std::vector<Mat2>& schedule,
-                                    const NewtonOpts& o, int max_bisect, std::vector<double>* w_final) {
+                                    const NewtonOpts& o, int max_bisect, std::vector<double>* w_final,
+                                    std::vector<double>* w_hist, std::vector<double>* p_hist) {
   std::vector<PlasticState> committed(prob.cache.n_qp());
   std::vector<double> w(prob.dofs.n_red, 0.0);
   Mat2 fprev = Mat2::identity();
@@ -106,6 +108,8 @@ std::vector<RomStepRecord> fe_solve(const RveProblem& prob, const Morph& mo, con
     fprev = fbar;
     committed = st.states;
     w = st.w;
+    if (w_hist) w_hist->insert(w_hist->end(), st.w.begin(), st.w.end());
+    if (p_hist) p_hist->insert(p_hist->end(), st.pf.begin(), st.pf.end());
     RomStepRecord r;
     r.pbar = st.pbar;
     r.iters = st.iters;

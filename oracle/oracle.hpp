@@ -199,7 +199,8 @@ std::vector<RomStepRecord> rom_solve(const RveProblem& prob, const RomModel& mod
 // microfem.cpp:213-238 (solve_rve) with solve_step_adaptive (:190-211);
 // dense LU in place of Eigen::SparseLU.  Throws SolveError.
 std::vector<RomStepRecord> fe_solve(const RveProblem& prob, const Morph& mo, const std::vector<Mat2>& schedule,
-                                    const NewtonOpts& o, int max_bisect, std::vector<double>* w_final);
+                                    const NewtonOpts& o, int max_bisect, std::vector<double>* w_final,
+                                    std::vector<double>* w_hist = nullptr, std::vector<double>* p_hist = nullptr);
 // microfem.cpp:240-313 (effective_stiffness); out[r + 4c] Tensor4 storage.
 void fe_effective_stiffness(const RveProblem& prob, const Morph& mo, const std::vector<PlasticState>& s0,
                             const Mat2& fbar, const std::vector<double>& w, double out[16]);

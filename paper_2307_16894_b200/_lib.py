@@ -75,6 +75,9 @@ _SIGS = {
     "podecm_rom_engines_commit": (C.c_int, [P, P, P]),
     "podecm_rom_engines_out_of_range": (C.c_int, [P, P, P, P]),
     "podecm_assemble_batch_ex": (C.c_int, [P, P, P, I64, P, P, P, P, P, P, P, P, P, P, P]),
+    "podecm_fe_solve_batch_ex": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton), P, P, P, P, P,
+                                           P, P]),
+    "podecm_weighted_stress_field": (C.c_int, [P, P, P, I64, P, P, P]),
     "podecm_fe_effective_stiffness_batch": (C.c_int, [P, P, P, I64, P, P, P, P, P, P]),
     "podecm_fe_create": (C.c_int, [P, P, C.POINTER(P)]),
     "podecm_fe_destroy": (None, [P]),

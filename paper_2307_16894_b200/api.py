@@ -494,25 +494,58 @@ class FullOrder:
         _lib.raise_for(self.lib.podecm_fe_create(self.ctx.h, rve.h, C.byref(h)), self.ctx.h, "podecm_fe_create")
         self.h = h
 
-    def solve(self, geom: torch.Tensor, sched: torch.Tensor, opts: NewtonOpts | None = None) -> dict:
-        """pbar [n, K, 4], iters [n, K], resid [n, K], w_final [n, n_red], status [n]."""
+    def solve(self, geom: torch.Tensor, sched: torch.Tensor, opts: NewtonOpts | None = None,
+              history: bool = False) -> dict:
+        """pbar [n, K, 4], iters [n, K], resid [n, K], w_final [n, n_red], status [n];
+        history=True adds w_hist [n, K, n_red] and p_hist [n, K, 4, n_qp]."""
         opts = opts or NewtonOpts()
         n, K = sched.shape[0], sched.shape[1]
         dev = sched.device
         _f64(geom, (n, 2), "geom")
         _f64(sched, (n, K, 4), "sched")
-        pbar = torch.zeros((n, K, 4), dtype=torch.float64, device=dev)
-        iters = torch.zeros((n, K), dtype=torch.int32, device=dev)
-        resid = torch.zeros((n, K), dtype=torch.float64, device=dev)
-        wf = torch.zeros((n, self.rve.n_red), dtype=torch.float64, device=dev)
-        status = torch.zeros(n, dtype=torch.int32, device=dev)
+        z = lambda shape, dt=torch.float64: torch.zeros(shape, dtype=dt, device=dev)
+        pbar, iters, resid = z((n, K, 4)), z((n, K), torch.int32), z((n, K))
+        wf, status = z((n, self.rve.n_red)), z(n, torch.int32)
+        wh = z((n, K, self.rve.n_red)) if history else None
+        ph = z((n, K, 4, self.rve.n_qp)) if history else None
         oc = opts.c()
-        rc = self.lib.podecm_fe_solve_batch(self.ctx.h, self.ctx.stream(), self.h, n, _ptr(geom), _ptr(sched), K,
-                                            C.byref(oc), _ptr(pbar), _ptr(iters), _ptr(resid), _ptr(wf),
-                                            _ptr(status))
+        rc = self.lib.podecm_fe_solve_batch_ex(self.ctx.h, self.ctx.stream(), self.h, n, _ptr(geom), _ptr(sched), K,
+                                               C.byref(oc), _ptr(pbar), _ptr(iters), _ptr(resid), _ptr(wf),
+                                               _ptr(status), _ptr(wh), _ptr(ph))
         _lib.raise_for(rc, self.ctx.h, "podecm_fe_solve_batch")
         self.global_iterations = int(self.lib.podecm_fe_global_iterations(self.h))
-        return {"pbar": pbar, "iters": iters, "resid": resid, "w_final": wf, "status": status}
+        out = {"pbar": pbar, "iters": iters, "resid": resid, "w_final": wf, "status": status}
+        if history:
+            out.update(w_hist=wh, p_hist=ph)
+        return out
+
+    def collect_snapshots(self, geom: torch.Tensor, sched: torch.Tensor, opts: NewtonOpts | None = None) -> dict:
+        """collect_snapshots (pipeline.cpp:157-188) for the training samples
+        geom [S, 2] with schedules sched [S, K, 4]: disp [2 n_nodes, S K]
+        (expanded fluctuations, sample-major columns), stress [4 n_qp, S K]
+        (weighted_stress_field, column entries q*4 + c), newton_iters [S K],
+        steps_per_sample [S].  A failed sample raises SolveError like the
+        reference."""
+        r = self.solve(geom, sched, opts, history=True)
+        if int((r["status"] != 0).sum().item()):
+            bad = int(torch.nonzero(r["status"] != 0)[0].item())
+            raise SolveError(f"training sample {bad}: cell Newton did not converge")
+        S, K = sched.shape[0], sched.shape[1]
+        rv = self.rve
+        nd = torch.as_tensor(rv.export()["node_dof"], device=geom.device, dtype=torch.int64)
+        w = r["w_hist"].reshape(S * K, rv.n_red)
+        disp = torch.zeros((S * K, rv.n_nodes, 2), dtype=torch.float64, device=geom.device)
+        m = nd >= 0  # DofMap::expand (mesh.cpp:390-400): the anchor stays zero
+        disp[:, m, 0] = w[:, nd[m]]
+        disp[:, m, 1] = w[:, nd[m] + 1]
+        geom_k = geom.repeat_interleave(K, dim=0).contiguous()
+        W = torch.empty((S * K, rv.n_qp, 4), dtype=torch.float64, device=geom.device)
+        pf = r["p_hist"].reshape(S * K, 4, rv.n_qp).contiguous()
+        rc = self.lib.podecm_weighted_stress_field(self.ctx.h, self.ctx.stream(), rv.h, S * K, _ptr(geom_k),
+                                                   _ptr(pf), _ptr(W))
+        _lib.raise_for(rc, self.ctx.h, "podecm_weighted_stress_field")
+        return {"disp": disp.reshape(S * K, 2 * rv.n_nodes).T, "stress": W.reshape(S * K, 4 * rv.n_qp).T,
+                "newton_iters": r["iters"].reshape(-1), "steps_per_sample": torch.full((S,), K, dtype=torch.int64)}
 
     def effective_stiffness(self, geom: torch.Tensor, st0: torch.Tensor, fbar: torch.Tensor,
                             w: torch.Tensor) -> dict:

@@ -182,6 +182,25 @@ __global__ void __launch_bounds__(256) k_fe_abar(int nq, int n_red, int64_t n, c
   if (threadIdx.x < 16) abar[s * 16 + threadIdx.x] = red[threadIdx.x][0] / 1.0;  // cell_volume
 }
 
+
+// weighted_stress_field (ecm.cpp:10-18): W_q = P_q Fmu_q^-T det_q, [n][nq][4]
+__global__ void k_fe_wstress(int64_t n, int nq, const double* fmi, const double* det, const double* pf,
+                             double* W) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * nq) return;
+  const int64_t s = t / nq;
+  const int q = (int)(t - s * nq);
+  double P[4], m[4];
+  for (int k = 0; k < 4; ++k) {
+    P[k] = pf[(s * 4 + k) * nq + q];
+    m[k] = fmi[(s * 4 + k) * nq + q];
+  }
+  const double d = det[s * nq + q];
+  for (int j = 0; j < 2; ++j)
+    for (int i = 0; i < 2; ++i)  // (P Fmi^T)(i,j) = P(i,0) Fmi(j,0) + P(i,1) Fmi(j,1)
+      W[(s * nq + q) * 4 + i + 2 * j] = (P[i] * m[j] + P[i + 2] * m[j + 2]) * d;
+}
+
 struct Frame {
   double fp[4], ft[4];
   int depth;
@@ -409,9 +428,10 @@ void podecm_fe_destroy(podecm_fe* e) {
 
 int64_t podecm_fe_global_iterations(const podecm_fe* e) { return e ? e->global_iters : 0; }
 
-int podecm_fe_solve_batch(podecm_ctx* ctx, void* stream, podecm_fe* e, int64_t n, const double* geom,
-                          const double* sched, int K, const podecm_newton* opts, double* pbar, int32_t* iters,
-                          double* resid, double* w_final, int32_t* status) {
+int podecm_fe_solve_batch_ex(podecm_ctx* ctx, void* stream, podecm_fe* e, int64_t n, const double* geom,
+                             const double* sched, int K, const podecm_newton* opts, double* pbar,
+                             int32_t* iters, double* resid, double* w_final, int32_t* status, double* w_hist,
+                             double* p_hist) {
   if (!ctx || !e || !opts) return PODECM_ECONFIG;
   if (n < 0 || K < 0) return set_err(ctx, PODECM_ECONFIG, "negative batch or schedule size");
   if (n == 0 || K == 0) return PODECM_OK;
@@ -529,6 +549,13 @@ int podecm_fe_solve_batch(podecm_ctx* ctx, void* stream, podecm_fe* e, int64_t n
         c.it = 0;
         if (c.stack.empty()) {  // increment done (solve_rve, microfem.cpp:221-236)
           for (int t = 0; t < 4; ++t) hpbar[((size_t)i * K + c.k) * 4 + t] = h_pb[4 * i + t];
+          if (w_hist)  // RveSolution::Step::w_red (snapshot collection, pipeline.cpp:167-175)
+            PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(w_hist + ((size_t)i * K + c.k) * nr, e->d_w + (size_t)i * nr,
+                                                 sizeof(double) * nr, cudaMemcpyDeviceToDevice, s));
+          if (p_hist)  // RveSolution::Step::p_field
+            PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(p_hist + ((size_t)i * K + c.k) * 4 * nq,
+                                                 e->d_pf + (size_t)i * 4 * nq, sizeof(double) * 4 * nq,
+                                                 cudaMemcpyDeviceToDevice, s));
           hit[(size_t)i * K + c.k] = c.iters_acc;
           hres[(size_t)i * K + c.k] = h_norm[i];
           c.iters_acc = 0;
@@ -719,6 +746,34 @@ int podecm_fe_effective_stiffness_batch(podecm_ctx* ctx, void* stream, podecm_fe
   }
   PODECM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
   return PODECM_OK;
+}
+
+
+int podecm_fe_solve_batch(podecm_ctx* ctx, void* stream, podecm_fe* e, int64_t n, const double* geom,
+                          const double* sched, int K, const podecm_newton* opts, double* pbar, int32_t* iters,
+                          double* resid, double* w_final, int32_t* status) {
+  return podecm_fe_solve_batch_ex(ctx, stream, e, n, geom, sched, K, opts, pbar, iters, resid, w_final, status,
+                                  nullptr, nullptr);
+}
+
+int podecm_weighted_stress_field(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n, const double* geom,
+                                 const double* p_field, double* W) {
+  if (!ctx || !r || !geom || !p_field || !W) return PODECM_ECONFIG;
+  if (n <= 0) return PODECM_OK;
+  auto s = static_cast<cudaStream_t>(stream);
+  const int nq = r->n_qp;
+  double *fmi = nullptr, *det = nullptr;
+  PODECM_CUDA_TRY(ctx, cudaMallocAsync(&fmi, sizeof(double) * (size_t)n * 4 * nq, s));
+  PODECM_CUDA_TRY(ctx, cudaMallocAsync(&det, sizeof(double) * (size_t)n * nq, s));
+  int rc = podecm_rve_morph(ctx, stream, r, n, geom, fmi, det, nullptr);
+  if (!rc) {
+    k_fe_wstress<<<grid_for(n * nq, 256), 256, 0, s>>>(n, nq, fmi, det, p_field, W);
+    rc = cudaGetLastError() == cudaSuccess ? PODECM_OK : set_err(ctx, PODECM_ECUDA, "launch");
+    if (!rc) ctx->launches += 1;
+  }
+  cudaFreeAsync(fmi, s);
+  cudaFreeAsync(det, s);
+  return rc;
 }
 
 }  // extern "C"

@@ -123,3 +123,40 @@ def test_exact_limit_effective_stiffness_on_gpu(orc):
     rel = (torch.linalg.norm(ab_fe - ab_rom) / torch.linalg.norm(ab_fe)).item()
     print(f"exact-limit effective stiffness: ROM vs FE rel {rel:.2e}")
     assert rel <= 1e-6
+
+
+def test_collect_snapshots_vs_oracle(orc):
+    """collect_snapshots (pipeline.cpp:157-188): expanded displacement and
+    weighted stress snapshots of FE training solves, GPU vs oracle."""
+    from paper_2307_16894_b200 import api
+    g = api.Rve(8, _mats())
+    o = orc.Rve(8, _mats())
+    geom, sched = synth.rom_instances(3, 2, 23, 0.12)
+    kw = dict(eps_rel=1e-10, eps_abs=1e-12)
+    snap = api.FullOrder(g).collect_snapshots(_T(geom), _T(sched), api.NewtonOpts(**kw))
+    ro = o.fe_solve(geom, sched, history=True, **kw)
+    t = o.export()
+    nd = t["node_dof"]
+    disp = np.zeros((2 * g.n_nodes, 6))
+    stress = np.zeros((4 * g.n_qp, 6))
+    col = 0
+    for s in range(3):
+        fmi, det, _ = o.morph(*geom[s])
+        for k in range(2):
+            w = ro["w_hist"][s, k]
+            for n in range(g.n_nodes):
+                if nd[n] >= 0:
+                    disp[2 * n:2 * n + 2, col] = w[nd[n]:nd[n] + 2]
+            P = ro["p_hist"][s, k]  # [4][nq]
+            Wq = np.zeros((g.n_qp, 4))
+            for j in range(2):
+                for i in range(2):
+                    Wq[:, i + 2 * j] = (P[i] * fmi[j] + P[i + 2] * fmi[j + 2]) * det
+            stress[:, col] = Wq.reshape(-1)
+            col += 1
+    gd, gs = snap["disp"].cpu().numpy(), snap["stress"].cpu().numpy()
+    ed = np.linalg.norm(gd - disp) / np.linalg.norm(disp)
+    es = np.linalg.norm(gs - stress) / np.linalg.norm(stress)
+    print(f"snapshots: disp rel {ed:.2e}, stress rel {es:.2e}")
+    assert ed <= 1e-8 and es <= 1e-8
+    assert np.array_equal(snap["newton_iters"].cpu().numpy(), ro["iters"].reshape(-1))
