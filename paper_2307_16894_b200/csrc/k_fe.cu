@@ -763,16 +763,17 @@ int podecm_weighted_stress_field(podecm_ctx* ctx, void* stream, podecm_rve* r, i
   auto s = static_cast<cudaStream_t>(stream);
   const int nq = r->n_qp;
   double *fmi = nullptr, *det = nullptr;
-  PODECM_CUDA_TRY(ctx, cudaMallocAsync(&fmi, sizeof(double) * (size_t)n * 4 * nq, s));
-  PODECM_CUDA_TRY(ctx, cudaMallocAsync(&det, sizeof(double) * (size_t)n * nq, s));
-  int rc = podecm_rve_morph(ctx, stream, r, n, geom, fmi, det, nullptr);
+  cudaError_t ce = cudaMallocAsync(&fmi, sizeof(double) * (size_t)n * 4 * nq, s);
+  if (ce == cudaSuccess) ce = cudaMallocAsync(&det, sizeof(double) * (size_t)n * nq, s);
+  int rc = ce == cudaSuccess ? podecm_rve_morph(ctx, stream, r, n, geom, fmi, det, nullptr)
+                             : cuda_err(ctx, ce, "weighted_stress_field: allocation");
   if (!rc) {
     k_fe_wstress<<<grid_for(n * nq, 256), 256, 0, s>>>(n, nq, fmi, det, p_field, W);
     rc = cudaGetLastError() == cudaSuccess ? PODECM_OK : set_err(ctx, PODECM_ECUDA, "launch");
     if (!rc) ctx->launches += 1;
   }
-  cudaFreeAsync(fmi, s);
-  cudaFreeAsync(det, s);
+  if (fmi) cudaFreeAsync(fmi, s);
+  if (det) cudaFreeAsync(det, s);
   return rc;
 }
 

@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <type_traits>
 #include <vector>
 
@@ -1110,9 +1111,15 @@ int ensure_abar(podecm_rom* r, int64_t n, bool sprev) {
   return rc;
 }
 
+// Opt-in dynamic SMEM limits are per device: set them once for every device
+// a context of this process launches on.
 void set_attrs() {
-  static bool attr_set = false;
-  if (attr_set) return;
+  static std::mutex mu;
+  static uint64_t done = 0;  // bit d: device d configured
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 64 && (done >> dev) & 1u) return;
   cudaFuncSetAttribute(k_rom_F, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   cudaFuncSetAttribute(k_rom_newton, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_rom_abar, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1123,7 +1130,7 @@ void set_attrs() {
   cudaFuncSetAttribute(k_rom_contract<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<5>());
   cudaFuncSetAttribute(k_rom_contract<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<6>());
   cudaFuncSetAttribute(k_rom_contract<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<7>());
-  attr_set = true;
+  if (dev < 64) done |= uint64_t(1) << dev;
 }
 
 PointArgs point_args(podecm_rom* r, int64_t n) {
@@ -1478,24 +1485,25 @@ int podecm_rom_sensitivity_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, i
   const int64_t n4 = 4 * n_inst;
   double *geom4 = nullptr, *sched4 = nullptr, *pbar4 = nullptr;
   int32_t* status4 = nullptr;
-  PODECM_CUDA_TRY(ctx, cudaMallocAsync(&geom4, (size_t)n4 * 2 * sizeof(double), s));
-  PODECM_CUDA_TRY(ctx, cudaMallocAsync(&sched4, (size_t)n4 * K * 4 * sizeof(double), s));
-  PODECM_CUDA_TRY(ctx, cudaMallocAsync(&pbar4, (size_t)n4 * K * 4 * sizeof(double), s));
-  PODECM_CUDA_TRY(ctx, cudaMallocAsync(&status4, (size_t)n4 * sizeof(int32_t), s));
-  k_rom_sens_prep<<<grid_for(n4, 128), 128, 0, s>>>(n_inst, h, geom, sched, K, geom4, sched4);
-  PODECM_LAUNCHED(ctx, 1);
-  int rc = rom_solve_impl(ctx, stream, r, n4, geom4, sched4, K, opts, pbar4, nullptr, nullptr, nullptr,
-                          status4, nullptr);
+  cudaError_t ce = cudaMallocAsync(&geom4, (size_t)n4 * 2 * sizeof(double), s);
+  if (ce == cudaSuccess) ce = cudaMallocAsync(&sched4, (size_t)n4 * K * 4 * sizeof(double), s);
+  if (ce == cudaSuccess) ce = cudaMallocAsync(&pbar4, (size_t)n4 * K * 4 * sizeof(double), s);
+  if (ce == cudaSuccess) ce = cudaMallocAsync(&status4, (size_t)n4 * sizeof(int32_t), s);
+  int rc = ce == cudaSuccess ? PODECM_OK : cuda_err(ctx, ce, "rom_sensitivity: allocation");
+  if (!rc) {
+    k_rom_sens_prep<<<grid_for(n4, 128), 128, 0, s>>>(n_inst, h, geom, sched, K, geom4, sched4);
+    ctx->launches += 1;
+    rc = rom_solve_impl(ctx, stream, r, n4, geom4, sched4, K, opts, pbar4, nullptr, nullptr, nullptr, status4,
+                        nullptr);
+  }
   if (!rc) {
     k_rom_sens_combine<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, h, geom, pbar4, K, status4, grad,
                                                              status);
     rc = cudaGetLastError() == cudaSuccess ? PODECM_OK : set_err(ctx, PODECM_ECUDA, "launch");
     if (!rc) PODECM_LAUNCHED(ctx, 1);
   }
-  cudaFreeAsync(geom4, s);
-  cudaFreeAsync(sched4, s);
-  cudaFreeAsync(pbar4, s);
-  cudaFreeAsync(status4, s);
+  for (void* ptr : {(void*)geom4, (void*)sched4, (void*)pbar4, (void*)status4})
+    if (ptr) cudaFreeAsync(ptr, s);
   return rc;
 }
 
