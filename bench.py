@@ -230,14 +230,14 @@ def run_c1(args, ws, rank, local, ctx, clk):
 
     # e2e through the public API with pinned host buffers; H2D and D2H of every
     # step's inputs / results inside the timed region, pipelined over 3 streams
-    n_chunks = 8
+    n_chunks = int(os.environ.get("PODECM_E2E_CHUNKS", "8"))
     cs = n // n_chunks
     hF = [torch.from_numpy(np.ascontiguousarray(F_np[:, c * cs:(c + 1) * cs])).pin_memory() for c in range(n_chunks)]
     hS = [torch.from_numpy(np.ascontiguousarray(st_np[:, c * cs:(c + 1) * cs])).pin_memory() for c in range(n_chunks)]
     oP = [torch.empty((4, cs), dtype=torch.float64).pin_memory() for _ in range(n_chunks)]
     oA = [torch.empty((16, cs), dtype=torch.float64).pin_memory() for _ in range(n_chunks)]
     oS = [torch.empty((6, cs), dtype=torch.float64).pin_memory() for _ in range(n_chunks)]
-    streams = [torch.cuda.Stream(dev) for _ in range(3)]
+    streams = [torch.cuda.Stream(dev) for _ in range(int(os.environ.get("PODECM_E2E_STREAMS", "3")))]
     dF = [torch.empty((4, cs), dtype=torch.float64, device=dev) for _ in streams]
     dS = [torch.empty((6, cs), dtype=torch.float64, device=dev) for _ in streams]
     dout = [{"P": torch.empty((4, cs), dtype=torch.float64, device=dev),
