@@ -59,6 +59,29 @@ def _ncu_traffic(kernel: str, points: int):
         return None
 
 
+def _fp64_issue_roofline(points_per_s: float, clk):
+    """The C1 kernel's binding roofline: FP64 pipe issue.  FP64 thread
+    instructions per point (DFMA + DMUL + DADD, committed ncu capture) x the
+    live point rate, against the pipe's peak of 64 FP64 thread-instructions
+    per clock per SM (B200: 148 SMs) at the sampled SM clock."""
+    try:
+        d = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())["k_material_batch"]
+        c = d["fp64_thread_inst_per_point"]
+        per_pt = c["dfma"] + c["dmul"] + c["dadd"]
+    except Exception:
+        return None
+    mhz = None
+    if clk is not None:
+        mhz = clk.summary().get("sm_mhz")
+    mhz = mhz or 1965.0
+    peak = 148 * 64 * mhz * 1e6
+    ach = per_pt * points_per_s
+    return {"bound": "fp64-pipe", "achieved": round(ach / 1e12, 3), "peak": round(peak / 1e12, 3),
+            "unit": "T FP64 thread-instructions/s", "frac": round(ach / peak, 4),
+            "fp64_inst_per_point": per_pt, "sm_mhz": mhz,
+            "note": "DMUL and DADD occupy the FP64 pipe like DFMA; cf. ncu sm__pipe_fp64_cycles_active 62 %"}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -664,8 +687,9 @@ def main():
                              "peak_source": src,
                              "kernel": "k_material_batch", "algorithmic_bytes_per_point": C1_BYTES_PER_POINT,
                              "kernel_ms": round(r["kern_ms"], 4),
-                             "note": "FP64-issue bound (9 evaluations/point); see fp64 block"},
+                             "note": "FP64-issue bound (9 evaluations/point); see the fp64_issue block"},
                 "fp64": {"probe_peak_tflops": fp64},
+                "fp64_issue": _fp64_issue_roofline(n / (r["kern_ms"] * 1e-3), clk),
                 "e2e": {"value": ws * n / (r["e2e_ms"] * 1e-3), "unit": "points/s",
                         "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
                         "matches_resident_path": r["e2e_same"],
