@@ -160,3 +160,19 @@ def test_collect_snapshots_vs_oracle(orc):
     print(f"snapshots: disp rel {ed:.2e}, stress rel {es:.2e}")
     assert ed <= 1e-8 and es <= 1e-8
     assert np.array_equal(snap["newton_iters"].cpu().numpy(), ro["iters"].reshape(-1))
+
+
+def test_fe_folding_morph_fails_only_its_instance(orc):
+    from paper_2307_16894_b200 import api
+    g = api.Rve(8, _mats())
+    o = orc.Rve(8, _mats())
+    geom, sched = synth.rom_instances(3, 2, 43, 0.1)
+    geom[2] = (0.49, 0.49)
+    kw = dict(eps_rel=1e-10, eps_abs=1e-12)
+    rg = api.FullOrder(g).solve(_T(geom), _T(sched), api.NewtonOpts(**kw))
+    rg = {k: v.cpu().numpy() for k, v in rg.items()}
+    ro = o.fe_solve(geom, sched, **kw)
+    assert list(ro["status"]) == [0, 0, 3]
+    _check(rg, ro)
+    with pytest.raises(api.SolveError):
+        g.ctx.check()

@@ -104,3 +104,24 @@ def test_exact_limit_gpu_equals_full_order(orc):
     err = np.abs(r["pbar"][0].cpu().numpy() - fe).max() / np.abs(fe).max()
     print(f"exact limit: GPU ROM vs FE max rel {err:.2e}")
     assert err <= 1e-8
+
+
+def test_folding_morph_fails_only_its_instance(setup):
+    """A geometry whose morph folds the mesh (det Fmu <= 0) raises SolveError
+    in MorphOperator::derive (morph.cpp:116-119): that instance fails, the
+    others are unaffected and match the oracle."""
+    import torch
+    from paper_2307_16894_b200 import api
+    g, o, model, rom = setup
+    geom, sched = synth.rom_instances(3, 3, 41, 0.1)
+    geom[1] = (0.49, 0.49)  # folds the transition ring
+    opts = api.NewtonOpts(eps_rel=1e-10, eps_abs=1e-12)
+    T = lambda a: torch.from_numpy(a).cuda()
+    rg = rom.solve(T(geom), T(sched), opts)
+    rg = {k: v.cpu().numpy() for k, v in rg.items()}
+    ro = o.rom_solve(model["ids"], model["weights"], model["mode_grads"], geom, sched, eps_rel=1e-10,
+                     eps_abs=1e-12)
+    assert list(ro["status"]) == [0, 3, 0]
+    _check(rg, ro)
+    with pytest.raises(api.SolveError):
+        rom.ctx.check()
