@@ -30,6 +30,7 @@
 #include <cstring>
 #include <mutex>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "rve.cuh"
@@ -41,7 +42,8 @@ namespace {
 
 constexpr int kMaxStack = 8;    // max_bisect + 1 frames (max_bisect <= 7)
 constexpr int kPC = 8;          // points per contraction chunk (32 k-rows)
-constexpr int kIPC = 2;         // instances per contraction CTA
+constexpr int kIPC = 2;         // instances per contraction CTA (NT <= 7)
+constexpr int kMaxNT = 15;      // contraction column tiles: N + 1 <= 120 (N <= 119 modes)
 constexpr int kPtsTile = 32;    // material kernel: points per CTA
 constexpr int kInstTile = 8;    // material kernel: instances per CTA
 
@@ -378,14 +380,20 @@ template <int NT>
 __host__ __device__ constexpr int contract_ld() {
   return NT * 8 + 4;
 }
+// instances per CTA: two for the usual tile widths, one for wide ones (SMEM)
+template <int NT>
+__host__ __device__ constexpr int contract_ipc() {
+  return NT <= 7 ? kIPC : 1;
+}
 template <int NT>
 constexpr size_t contract_smem_bytes() {
-  return sizeof(double) * (2 * (kPC * 4) * contract_ld<NT>() + 2 * kIPC * (kPC * 4) * contract_ld<NT>() +
-                           2 * kIPC * kPC * 20);
+  return sizeof(double) * (2 * (kPC * 4) * contract_ld<NT>() +
+                           2 * contract_ipc<NT>() * (kPC * 4) * contract_ld<NT>() + 2 * contract_ipc<NT>() * kPC * 20);
 }
 
 template <int NT>
-__global__ void __launch_bounds__(32 * NT * kIPC) k_rom_contract(ContractArgs g) {
+__global__ void __launch_bounds__(32 * NT * contract_ipc<NT>()) k_rom_contract(ContractArgs g) {
+  constexpr int kIPC = contract_ipc<NT>();
   constexpr int NP = NT * 8;
   constexpr int LDY = contract_ld<NT>();
   constexpr int KR = kPC * 4;  // k-rows per chunk
@@ -848,10 +856,11 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_abar(AbarArgs g) {
   }
   const double* mo = g.morph + (size_t)s * 5 * Q;
   const double* CA = g.CA + (size_t)s * Q * 16;
-  // rhs[c][i] = -sum_p sum_r G_p[i][r] X_p[r][c]; lanes over modes i
-  double acc[2][4];
+  // rhs[c][i] = -sum_p sum_r G_p[i][r] X_p[r][c]; lanes over modes i = lane + 32 h
+  constexpr int kRowsPerLane = 4;  // N <= 128
+  double acc[kRowsPerLane][4];
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
+  for (int h = 0; h < kRowsPerLane; ++h)
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) acc[h][cc] = 0.0;
   for (int p0 = 0; p0 < Q; p0 += 32) {
@@ -875,21 +884,23 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_abar(AbarArgs g) {
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const double* gr = g.G + ((size_t)(p0 + pl) * 4 + r) * g.NP;
-        const double g0 = lane < N ? gr[lane] : 0.0, g1 = lane + 32 < N ? gr[lane + 32] : 0.0;
+        double gv[kRowsPerLane];
+#pragma unroll
+        for (int h = 0; h < kRowsPerLane; ++h) gv[h] = lane + 32 * h < N ? gr[lane + 32 * h] : 0.0;
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
           const double x = sX[pl * 17 + r + 4 * cc];
-          acc[0][cc] = fma(g0, x, acc[0][cc]);
-          acc[1][cc] = fma(g1, x, acc[1][cc]);
+#pragma unroll
+          for (int h = 0; h < kRowsPerLane; ++h) acc[h][cc] = fma(gv[h], x, acc[h][cc]);
         }
       }
     __syncwarp();
   }
 #pragma unroll
-  for (int cc = 0; cc < 4; ++cc) {
-    if (lane < N) rhs[cc * N + lane] = -acc[0][cc];
-    if (lane + 32 < N) rhs[cc * N + lane + 32] = -acc[1][cc];
-  }
+  for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+    for (int h = 0; h < kRowsPerLane; ++h)
+      if (lane + 32 * h < N) rhs[cc * N + lane + 32 * h] = -acc[h][cc];
   __syncwarp();
   warp_lu_solve<4>(Ks, LD, N, rhs, lane);
   // Abar(:, cc) = sum_p CA_p (e_cc + R_p^T (G_p^T q_cc)); lanes over points
@@ -1111,6 +1122,14 @@ int ensure_abar(podecm_rom* r, int64_t n, bool sprev) {
   return rc;
 }
 
+template <int... I>
+void set_contract_attrs(std::integer_sequence<int, I...>) {
+  (..., (I > 0 ? (void)cudaFuncSetAttribute(k_rom_contract<(I > 0 ? I : 1)>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)contract_smem_bytes<(I > 0 ? I : 1)>())
+               : (void)0));
+}
+
 // Opt-in dynamic SMEM limits are per device: set them once for every device
 // a context of this process launches on.
 void set_attrs() {
@@ -1120,16 +1139,10 @@ void set_attrs() {
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
   if (dev < 64 && (done >> dev) & 1u) return;
-  cudaFuncSetAttribute(k_rom_F, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(k_rom_F, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  set_contract_attrs(std::make_integer_sequence<int, kMaxNT + 1>{});
   cudaFuncSetAttribute(k_rom_newton, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_rom_abar, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_rom_contract<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<1>());
-  cudaFuncSetAttribute(k_rom_contract<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<2>());
-  cudaFuncSetAttribute(k_rom_contract<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<3>());
-  cudaFuncSetAttribute(k_rom_contract<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<4>());
-  cudaFuncSetAttribute(k_rom_contract<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<5>());
-  cudaFuncSetAttribute(k_rom_contract<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<6>());
-  cudaFuncSetAttribute(k_rom_contract<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<7>());
   if (dev < 64) done |= uint64_t(1) << dev;
 }
 
@@ -1178,18 +1191,21 @@ void launch_F(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, const PointArgs& p
   k_rom_F<<<gpt, 256, smem_pt, s>>>(pa);
 }
 
+template <int NT>
+void launch_contract_nt(cudaStream_t s, const ContractArgs& ca) {
+  constexpr int ipc = contract_ipc<NT>();
+  const int gct = (int)((ca.n + ipc - 1) / ipc);
+  k_rom_contract<NT><<<gct, 32 * NT * ipc, contract_smem_bytes<NT>(), s>>>(ca);
+}
+
+template <int... I>
+void launch_contract_sw(int nt, cudaStream_t s, const ContractArgs& ca, std::integer_sequence<int, I...>) {
+  (..., (nt == I + 1 ? launch_contract_nt<I + 1>(s, ca) : (void)0));
+}
+
 void launch_contract(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, const ContractArgs& ca) {
   KTimer kt(ctx, s, "k_rom_contract");
-  const int gct = (int)((ca.n + kIPC - 1) / kIPC);
-  switch (r->NT) {
-    case 1: k_rom_contract<1><<<gct, 32 * 1 * kIPC, contract_smem_bytes<1>(), s>>>(ca); break;
-    case 2: k_rom_contract<2><<<gct, 32 * 2 * kIPC, contract_smem_bytes<2>(), s>>>(ca); break;
-    case 3: k_rom_contract<3><<<gct, 32 * 3 * kIPC, contract_smem_bytes<3>(), s>>>(ca); break;
-    case 4: k_rom_contract<4><<<gct, 32 * 4 * kIPC, contract_smem_bytes<4>(), s>>>(ca); break;
-    case 5: k_rom_contract<5><<<gct, 32 * 5 * kIPC, contract_smem_bytes<5>(), s>>>(ca); break;
-    case 6: k_rom_contract<6><<<gct, 32 * 6 * kIPC, contract_smem_bytes<6>(), s>>>(ca); break;
-    default: k_rom_contract<7><<<gct, 32 * 7 * kIPC, contract_smem_bytes<7>(), s>>>(ca); break;
-  }
+  launch_contract_sw(r->NT, s, ca, std::make_integer_sequence<int, kMaxNT>{});
 }
 
 // Effective-stiffness stage over n instances whose morph slice (d_morph),
@@ -1240,7 +1256,7 @@ int check_solve_args(podecm_ctx* ctx, podecm_rom* r, int64_t n_inst, int K, cons
   if (opts->max_bisect < 0 || opts->max_bisect + 1 > kMaxStack)
     return set_err(ctx, PODECM_ECONFIG, "max_bisect must lie in [0, 7]");
   if (opts->max_iter < 0) return set_err(ctx, PODECM_ECONFIG, "max_iter must be >= 0");
-  if (r->NT > 7) return set_err(ctx, PODECM_ECONFIG, "rom: N > 55 exceeds the contraction tile");
+  if (r->NT > kMaxNT) return set_err(ctx, PODECM_ECONFIG, "rom: N > 119 exceeds the contraction tile");
   return PODECM_OK;
 }
 
@@ -1360,7 +1376,7 @@ int podecm_rom_create(podecm_ctx* ctx, podecm_rve* rve, int N, int Q, const int3
                       const double* weights, const double* mode_grads, podecm_rom** out) {
   if (!ctx || !rve || !out) return PODECM_ECONFIG;
   *out = nullptr;
-  if (N < 1 || N > 55) return set_err(ctx, PODECM_ECONFIG, "rom: need 1 <= N <= 55 modes");
+  if (N < 1 || N > 8 * kMaxNT - 1) return set_err(ctx, PODECM_ECONFIG, "rom: need 1 <= N <= 119 modes");
   if (Q < 1) return set_err(ctx, PODECM_ECONFIG, "rom: empty cubature rule");
   if (!ids || !weights || !mode_grads) return set_err(ctx, PODECM_ECONFIG, "rom: null model arrays");
   for (int p = 0; p < Q; ++p) {
@@ -1454,7 +1470,7 @@ int podecm_rom_effective_stiffness_batch(podecm_ctx* ctx, void* stream, podecm_r
   if (n_inst == 0) return PODECM_OK;
   if (!geom || !st0 || !fbar || !a || !abar)
     return set_err(ctx, PODECM_ECONFIG, "geom, st0, fbar, a, abar required");
-  if (r->NT > 7) return set_err(ctx, PODECM_ECONFIG, "rom: N > 55 exceeds the contraction tile");
+  if (r->NT > kMaxNT) return set_err(ctx, PODECM_ECONFIG, "rom: N > 119 exceeds the contraction tile");
   if (int rc = ensure_cap(r, n_inst)) return rc;
   if (int rc = ensure_abar(r, n_inst, false)) return rc;
   auto s = static_cast<cudaStream_t>(stream);

@@ -125,3 +125,27 @@ def test_folding_morph_fails_only_its_instance(setup):
     _check(rg, ro)
     with pytest.raises(api.SolveError):
         rom.ctx.check()
+
+
+@pytest.mark.parametrize("N", [80, 119])
+def test_wide_bases(orc, N):
+    """Bases wider than the one-CTA-pair tile (N + 1 > 56 columns): the
+    contraction runs one instance per CTA with up to 15 column tiles; the warp
+    LU, the effective stiffness and the Newton logic are generic in N."""
+    import torch
+    from paper_2307_16894_b200 import api
+    g = api.Rve(16, _mats())
+    o = orc.Rve(16, _mats())
+    model = synth.rom_model(g.export(), g.n_red, N=N, Q=150, seed=2040 + N)
+    rom = api.Rom(g, model["ids"], model["weights"], model["mode_grads"])
+    geom, sched = synth.rom_instances(3, 2, 2041, 0.12)
+    opts = api.NewtonOpts(eps_rel=1e-10, eps_abs=1e-12)
+    T = lambda a: torch.from_numpy(a).cuda()
+    rg = rom.solve(T(geom), T(sched), opts, abar=True)
+    rg = {k: v.cpu().numpy() for k, v in rg.items()}
+    ro = o.rom_solve(model["ids"], model["weights"], model["mode_grads"], geom, sched, eps_rel=1e-10,
+                     eps_abs=1e-12, abar=True)
+    _check(rg, ro)
+    rel = np.linalg.norm(rg["abar"] - ro["abar"], axis=-1) / np.maximum(1.0, np.linalg.norm(ro["abar"], axis=-1))
+    print(f"N={N}: abar rel {rel.max():.2e}")
+    assert rel.max() <= 1e-8
