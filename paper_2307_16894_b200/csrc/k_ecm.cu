@@ -123,10 +123,13 @@ __global__ void k_ecm_colnorm(int64_t L, int nq, int N, const double* H, const d
 // CTA: 16 qps (64 columns of T), 7 warps x 8 rows (N <= 56), K-loop over s.
 constexpr int kSQ = 16, kSC = 64, kSK = 16, kSLD = kSK + 4;
 
+// Bases wider than 56 modes run in row blocks: N rows of r starting at the
+// block, H rows strided by ldH, and corr_out accumulated (accumulate != 0).
 __global__ void __launch_bounds__(224) k_ecm_score(int64_t L, int nq, int N, const double* r,
                                                    const double* r_vol_p, const double* H, const double* W,
                                                    const double* cn, const uint8_t* unavailable,
-                                                   double* cta_best, int* cta_idx, double* corr_out) {
+                                                   double* cta_best, int* cta_idx, double* corr_out, int ldH,
+                                                   int accumulate) {
   __shared__ double sR[2][56][kSLD];
   __shared__ double sW[2][kSC][kSLD];
   __shared__ double red[7][kSQ];
@@ -172,7 +175,7 @@ __global__ void __launch_bounds__(224) k_ecm_score(int64_t L, int nq, int N, con
     const int q = q0 + ql;
     double v = 0.0;
     if (i < N && q < nq) {
-      const double* h = H + ((int64_t)q * N + i) * 4;
+      const double* h = H + ((int64_t)q * ldH + i) * 4;
       const int c0 = 2 * (tig & 1);
       v = h[c0] * acc[ct][0] + h[c0 + 1] * acc[ct][1];
     }
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(224) k_ecm_score(int64_t L, int nq, int N, con
       double corr = 0.0;
       for (int w = 0; w < 7; ++w) corr += red[w][tid];
       if (r_vol_p) corr += *r_vol_p;
-      if (corr_out) corr_out[q] = corr;
+      if (corr_out) corr_out[q] = accumulate ? corr_out[q] + corr : corr;
       const double sc = corr / cn[q];
       if (sc > 0.0) {
         best = sc;
@@ -614,7 +617,13 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
                       const double* W, int64_t L, const podecm_ecm_opts* opts, int32_t* ids,
                       double* weights, int* n_sel, double* resid_rel, int* iterations) {
   if (!ctx || !rve || !H || !W || !opts || !ids || !weights || !n_sel) return PODECM_ECONFIG;
-  if (N < 1 || N > 56) return set_err(ctx, PODECM_ECONFIG, "ecm: need 1 <= N <= 56 displacement modes");
+  static const bool gram_env = [] {
+    const char* e = getenv("PODECM_ECM_SCORE");
+    return !(e && !strcmp(e, "direct"));
+  }();
+  if (N < 1 || N > (gram_env ? 1024 : 56))
+    return set_err(ctx, PODECM_ECONFIG, gram_env ? "ecm: need 1 <= N <= 1024 displacement modes"
+                                                 : "ecm: the direct scoring mode needs 1 <= N <= 56");
   auto s = static_cast<cudaStream_t>(stream);
   const int nq = rve->n_qp;
   const int vol = opts->volume_row ? 1 : 0;
@@ -769,12 +778,22 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
       }
       k_ecm_argmax<<<1, 1024, 0, s>>>(n_cta_g, cta_bg, cta_ig, best_b, best_i);
     } else {
-      {
+      if (N <= 56) {
         KTimer kt(ctx, s, "k_ecm_score");
         k_ecm_score<<<n_cta, 224, 0, s>>>(L, nq, N, r, vol ? r + m - 1 : nullptr, H, W, cn, unav, cta_b, cta_i,
-                                          gram ? c0 : nullptr);  // first pass: r = rhs, keep J^T rhs
+                                          gram ? c0 : nullptr, N, 0);  // first pass: r = rhs, keep J^T rhs
+        k_ecm_argmax<<<1, 1024, 0, s>>>(n_cta, cta_b, cta_i, best_b, best_i);
+      } else {  // wide basis (Gram mode only): c0 = J^T rhs in row blocks of 56 modes, then score it
+        KTimer kt(ctx, s, "k_ecm_score");
+        for (int i0 = 0; i0 < N; i0 += 56) {
+          const int nb = std::min(56, N - i0);
+          k_ecm_score<<<n_cta, 224, 0, s>>>(L, nq, nb, r + (int64_t)i0 * L, (vol && i0 == 0) ? r + m - 1 : nullptr,
+                                            H + (int64_t)i0 * 4, W, cn, unav, cta_b, cta_i, c0, N, i0 > 0);
+          ctx->launches += 1;
+        }
+        k_ecm_score_gram<<<n_cta_g, 256, 0, s>>>(nq, 0, c0, Gsel, xdev, cn, unav, cta_bg, cta_ig);
+        k_ecm_argmax<<<1, 1024, 0, s>>>(n_cta_g, cta_bg, cta_ig, best_b, best_i);
       }
-      k_ecm_argmax<<<1, 1024, 0, s>>>(n_cta, cta_b, cta_i, best_b, best_i);
     }
     ctx->launches += 2;
     cudaMemcpyAsync(pbest, best_i, sizeof(int), cudaMemcpyDeviceToHost, s);

@@ -110,3 +110,22 @@ def test_ecm_budget_exhaustion_raises(case):
     with pytest.raises(api.SolveError):
         api.ecm_select(g, torch.from_numpy(H).cuda(), torch.from_numpy(W).cuda(),
                        api.EcmOpts(eps=1e-12, max_points=5))
+
+
+def test_ecm_wide_basis_ids_bit_exact(case):
+    """N = 80 displacement modes (> 56 rows of the DMMA scoring tile): the
+    first J^T rhs pass runs in row blocks, later iterations use the Gram
+    update; ids still bit-exact vs the oracle."""
+    import torch
+    from oracle import pod_ecm
+    from paper_2307_16894_b200 import api
+    g, o, t, U, modes, lam, W, H = case
+    modes80, _ = pod_ecm.pod_diag(U, None, 80)
+    H80 = pod_ecm.mode_grads(t, modes80)
+    Ws = np.ascontiguousarray(W[:40])
+    ids_o, w_o, rel_o, it_o = pod_ecm.ecm_select(H80, Ws, t["w"], 1e-8, max_points=40, stop_at_count=True)
+    ids_g, w_g, rel_g, it_g = api.ecm_select(g, torch.from_numpy(H80).cuda(), torch.from_numpy(Ws).cuda(),
+                                             api.EcmOpts(eps=1e-8, max_points=40, stop_at_count=True))
+    print(f"N=80: ids equal {np.array_equal(ids_g, ids_o)}; resid {rel_g:.6e} vs {rel_o:.6e}")
+    assert np.array_equal(ids_g, ids_o) and it_g == it_o
+    assert np.abs(w_g - w_o).max() <= 1e-8 * np.abs(w_o).max()
