@@ -206,6 +206,30 @@ int podecm_rom_engines_commit(podecm_ctx* ctx, void* stream, podecm_rom_engines*
 int podecm_rom_engines_out_of_range(podecm_ctx* ctx, void* stream, const podecm_rom_engines* eng,
                                     int32_t* counts);
 
+/* ---- FE2 macro driver (twoscale.hpp:82-118) -----------
+ * MacroConfig: nx x ny Quad8 plate of width x height, bottom edge clamped,
+ * parabolic top traction ramped to peak and back over `steps` steps. */
+typedef struct podecm_macro_cfg {
+  int32_t nx, ny;
+  double width, height, peak_traction;
+  int32_t steps;
+  podecm_newton newton; /* macro Newton (eps_rel, eps_abs, max_iter used) */
+} podecm_macro_cfg;
+/* out = n_nodes, n_elems, n_qp (4 per element, quadrature order), n_red. */
+int podecm_macro_info(const podecm_macro_cfg* cfg, int64_t out[4]);
+/* Reference positions of the macro Gauss points (host [n_qp][2]): the
+ * engine factory's argument (twoscale.cpp:149-152). */
+int podecm_macro_qp_positions(const podecm_macro_cfg* cfg, double* x);
+/* run_twoscale (twoscale.cpp:131-242).  eng: the batched ROM micro engines
+ * of the n_qp macro Gauss points (quadrature order; micro_opts for their
+ * responds), or NULL for LinearElasticEngine(E, nu) at every point.  Host
+ * outputs (each nullable): load_factor, compliance, iters [steps]; u_final
+ * [2 n_nodes]; residual_norm; micro_evals. */
+int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* cfg, podecm_rom_engines* eng,
+                        const podecm_newton* micro_opts, double E, double nu, double* load_factor,
+                        double* compliance, int32_t* iters, double* u_final, double* residual_norm,
+                        int64_t* micro_evals);
+
 /* ---- full-order Newton ------------------------------
  * solve_rve with solve_step_adaptive (microfem.cpp:142-238) for a batch of
  * instances around the batched assembly; the sparse solves are one batched

@@ -56,6 +56,10 @@ def lib(libm: str = "glibc"):
         l.orc_fe_solve.argtypes = [P, L, P, P, I, D, D, I, I, P, P, P, P, P, P, P, I]
         l.orc_fe_effective_stiffness.restype = L
         l.orc_fe_effective_stiffness.argtypes = [P, L, P, P, P, P, P, P, I]
+        l.orc_macro_qp_positions.restype = L
+        l.orc_macro_qp_positions.argtypes = [I, I, D, D, P]
+        l.orc_twoscale_run.restype = I
+        l.orc_twoscale_run.argtypes = [P, I, I, D, D, D, I, D, D, I, D, D, P, P, P, P, P]
         l.orc_rom_engines_create.restype = P
         l.orc_rom_engines_create.argtypes = [P, I, I, P, P, P, L, P, P, D, D, I, I]
         l.orc_rom_engines_destroy.argtypes = [P]
@@ -311,3 +315,24 @@ class RomEngines:
                 self.h = None
         except Exception:
             pass
+
+
+def macro_qp_positions(nx, ny, width=2.0, height=1.0):
+    n = lib().orc_macro_qp_positions(nx, ny, width, height, None)
+    x = np.empty((n, 2))
+    lib().orc_macro_qp_positions(nx, ny, width, height, _p(x))
+    return x
+
+
+def run_twoscale(nx=5, ny=3, width=2.0, height=1.0, peak=0.2, steps=50, eps_rel=1e-8, eps_abs=1e-12, max_iter=25,
+                 engines: "RomEngines | None" = None, E=1.0, nu=0.3):
+    """run_twoscale (twoscale.cpp:131-242) with the oracle's RomMicroEngines or
+    LinearElasticEngine(E, nu).  Returns the result dict and the status (0/3)."""
+    n_nodes = (2 * nx + 1) * (2 * ny + 1) - nx * ny
+    lf, comp, uf = np.zeros(steps), np.zeros(steps), np.zeros(2 * n_nodes)
+    it = np.zeros(steps, np.int32)
+    rn = C.c_double()
+    L = engines.rve.L if engines is not None else lib()
+    st = L.orc_twoscale_run(engines.h if engines is not None else None, nx, ny, width, height, peak, steps, eps_rel,
+                            eps_abs, max_iter, E, nu, _p(lf), _p(comp), _p(it), _p(uf), C.byref(rn))
+    return {"load_factor": lf, "compliance": comp, "iters": it, "u_final": uf, "residual_norm": rn.value}, st

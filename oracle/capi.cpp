@@ -466,6 +466,78 @@ long orc_fe_effective_stiffness(void* hp, long n_inst, const double* geom, const
   return fails;
 }
 
+// Macro Gauss point positions (host [n_qp][2]); returns n_qp.
+long orc_macro_qp_positions(int nx, int ny, double w, double h, double* x) {
+  const auto p = macro_qp_positions(nx, ny, w, h);
+  if (x)
+    for (size_t q = 0; q < p.size(); ++q) {
+      x[2 * q] = p[q][0];
+      x[2 * q + 1] = p[q][1];
+    }
+  return (long)p.size();
+}
+
+// run_twoscale with the oracle's RomMicroEngines (eh, one per macro qp) or
+// LinearElasticEngine(E, nu) when eh is null; returns 0 or 3 (SolveError).
+int orc_twoscale_run(void* eh, int nx, int ny, double width, double height, double peak, int steps, double eps_rel,
+                     double eps_abs, int max_iter, double E, double nu, double* load_factor, double* compliance,
+                     int* iters, double* u_final, double* residual_norm) {
+  MacroCfg cfg;
+  cfg.nx = nx;
+  cfg.ny = ny;
+  cfg.width = width;
+  cfg.height = height;
+  cfg.peak = peak;
+  cfg.steps = steps;
+  cfg.eps_rel = eps_rel;
+  cfg.eps_abs = eps_abs;
+  cfg.max_iter = max_iter;
+  auto* e = static_cast<OrcEngines*>(eh);
+  PlasticityParams lp;
+  lp.E = E;
+  lp.nu = nu;
+  const double la = lp.lambda(), mu = lp.mu();
+  double d[16];
+  for (int i = 0; i < 2; ++i)  // elastic_tangent_2d (material.cpp:69-78)
+    for (int j = 0; j < 2; ++j)
+      for (int k = 0; k < 2; ++k)
+        for (int l = 0; l < 2; ++l)
+          d[(i + 2 * j) + 4 * (k + 2 * l)] = la * (i == j) * (k == l) + mu * ((i == k) * (j == l) + (i == l) * (j == k));
+  auto respond = [&](int q, const double* F, double* pb, double* ab) {
+    if (e) {
+      Mat2 fb, p;
+      for (int k = 0; k < 4; ++k) fb.a[k] = F[k];
+      e->eng[q].respond(fb, &p, ab, nullptr);
+      for (int k = 0; k < 4; ++k) pb[k] = p.a[k];
+    } else {  // LinearElasticEngine::respond (twoscale.cpp:17-20)
+      const double b[4] = {F[0] - 1.0, F[1] - 0.0, F[2] - 0.0, F[3] - 1.0};
+      for (int r = 0; r < 4; ++r) {
+        double v = 0.0;
+        for (int t = 0; t < 4; ++t) v += d[r + 4 * t] * b[t];
+        pb[r] = v;
+      }
+      for (int k = 0; k < 16; ++k) ab[k] = d[k];
+    }
+  };
+  auto commit = [&]() {
+    if (e)
+      for (auto& g : e->eng) g.commit();
+  };
+  try {
+    const TwoscaleResult r = twoscale(cfg, respond, commit);
+    for (int k = 0; k < steps; ++k) {
+      if (load_factor) load_factor[k] = r.load_factor[k];
+      if (compliance) compliance[k] = r.compliance[k];
+      if (iters) iters[k] = r.iters[k];
+    }
+    if (u_final) std::copy(r.u_final.begin(), r.u_final.end(), u_final);
+    if (residual_norm) *residual_norm = r.residual_norm;
+    return 0;
+  } catch (const SolveError&) {
+    return 3;
+  }
+}
+
 // Weighted stress snapshots for ECM (ecm.cpp:10-18 on the parent cell):
 // W[s][q][c] = flatten(P Fmu^-T det) with P from large_strain_update at
 // F = I + grad u_s (assemble's F with Fbar = I, identity morph) from a virgin

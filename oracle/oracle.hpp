@@ -21,6 +21,8 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <array>
+#include <functional>
 #include <vector>
 
 namespace orc {
@@ -211,6 +213,25 @@ void rom_effective_stiffness(const RveProblem& prob, const RomModel& model,
                              const std::vector<Mat2>& fmi, const std::vector<double>& det,
                              const std::vector<PlasticState>& s0, const Mat2& fbar,
                              const std::vector<double>& a, double out[16]);
+
+// twoscale.hpp:82-118 (MacroConfig / TwoscaleResult) and run_twoscale
+// (twoscale.cpp:131-242) over caller-supplied MicroEngine callbacks.
+struct MacroCfg {
+  int nx = 5, ny = 3;
+  double width = 2.0, height = 1.0, peak = 0.2;
+  int steps = 50;
+  double eps_rel = 1e-8, eps_abs = 1e-12;
+  int max_iter = 25;
+};
+struct TwoscaleResult {
+  std::vector<double> load_factor, compliance, u_final;
+  std::vector<int> iters;
+  double residual_norm = 0;
+};
+std::vector<std::array<double, 2>> macro_qp_positions(int nx, int ny, double w, double h);
+TwoscaleResult twoscale(const MacroCfg& cfg,
+                        const std::function<void(int, const double*, double*, double*)>& respond,
+                        const std::function<void()>& commit);
 
 // twoscale.hpp:55-80 (RomMicroEngine): per-engine committed history,
 // reduced coordinates, macro gradient and force_ref.

@@ -23,7 +23,7 @@ ORACLE_DIR = ROOT / "oracle"
 ORACLE_LIB = ORACLE_DIR / "liboracle.so"
 
 CU_SOURCES = ["k_material.cu", "rve_host.cu", "k_assemble.cu", "k_rom.cu", "k_pod.cu", "k_ecm.cu",
-              "k_probe.cu", "k_fe.cu", "store.cpp"]
+              "k_probe.cu", "k_fe.cu", "twoscale.cu", "store.cpp"]
 HOST_CXX = "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else "g++"
 
 

@@ -33,6 +33,11 @@ class podecm_newton(C.Structure):
                 ("max_bisect", I32)]
 
 
+class podecm_macro_cfg(C.Structure):
+    _fields_ = [("nx", I32), ("ny", I32), ("width", D), ("height", D), ("peak_traction", D), ("steps", I32),
+                ("newton", podecm_newton)]
+
+
 _SIGS = {
     "podecm_ctx_create": (C.c_int, [C.c_int, C.POINTER(P)]),
     "podecm_ctx_destroy": (None, [P]),
@@ -83,6 +88,10 @@ _SIGS = {
     "podecm_fe_destroy": (None, [P]),
     "podecm_fe_global_iterations": (I64, [P]),
     "podecm_fe_solve_batch": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton), P, P, P, P, P]),
+    "podecm_macro_info": (C.c_int, [C.POINTER(podecm_macro_cfg), C.POINTER(I64)]),
+    "podecm_macro_qp_positions": (C.c_int, [C.POINTER(podecm_macro_cfg), P]),
+    "podecm_twoscale_run": (C.c_int, [P, P, C.POINTER(podecm_macro_cfg), P, C.POINTER(podecm_newton), D, D, P, P,
+                                      P, P, C.POINTER(D), C.POINTER(I64)]),
     "podecm_store_last_error": (C.c_char_p, []),
     "podecm_fnv1a64": (C.c_uint64, [P, C.c_uint64, C.c_uint64]),
     "podecm_rve_fingerprint": (C.c_uint64, [P]),

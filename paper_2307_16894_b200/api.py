@@ -573,6 +573,61 @@ class FullOrder:
             pass
 
 
+# ---- FE2 macro driver -------------------------------------
+@dataclass
+class MacroConfig:
+    """MacroConfig (twoscale.hpp:82-94): nx x ny Quad8 plate, bottom clamped,
+    parabolic top traction ramped up to peak over steps/2 and back."""
+    nx: int = 5
+    ny: int = 3
+    width: float = 2.0
+    height: float = 1.0
+    peak_traction: float = 0.2
+    steps: int = 50
+    newton: NewtonOpts | None = None
+
+    def c(self) -> _lib.podecm_macro_cfg:
+        nw = (self.newton or NewtonOpts()).c()
+        return _lib.podecm_macro_cfg(self.nx, self.ny, self.width, self.height, self.peak_traction, self.steps, nw)
+
+    def info(self) -> dict:
+        out = (C.c_int64 * 4)()
+        cc = self.c()
+        _lib.raise_for(_lib.load().podecm_macro_info(C.byref(cc), out), None, "podecm_macro_info")
+        return dict(zip(("n_nodes", "n_elems", "n_qp", "n_red"), (int(v) for v in out)))
+
+    def qp_positions(self):
+        import numpy as np
+        x = np.empty((self.info()["n_qp"], 2))
+        cc = self.c()
+        _lib.raise_for(_lib.load().podecm_macro_qp_positions(C.byref(cc), x.ctypes.data_as(C.c_void_p)), None,
+                       "podecm_macro_qp_positions")
+        return x
+
+
+def run_twoscale(cfg: MacroConfig, engines: "RomEngines | None" = None, micro_opts: NewtonOpts | None = None,
+                 E: float = 1.0, nu: float = 0.3, ctx: Context | None = None) -> dict:
+    """run_twoscale (twoscale.cpp:131-242) with the batched ROM engines of the
+    macro Gauss points, or LinearElasticEngine(E, nu) when engines is None.
+    Returns load_factor, compliance, iters [steps], u_final [2 n_nodes],
+    residual_norm, micro_evals."""
+    import numpy as np
+    ctx = engines.ctx if engines is not None else (ctx or Context.default())
+    inf = cfg.info()
+    lf, comp = np.zeros(cfg.steps), np.zeros(cfg.steps)
+    it = np.zeros(cfg.steps, np.int32)
+    uf = np.zeros(2 * inf["n_nodes"])
+    rn, ev = C.c_double(), C.c_int64()
+    cc = cfg.c()
+    mo = (micro_opts or NewtonOpts()).c()
+    p = lambda a: a.ctypes.data_as(C.c_void_p)
+    rc = ctx.lib.podecm_twoscale_run(ctx.h, ctx.stream(), C.byref(cc), engines.h if engines is not None else None,
+                                     C.byref(mo), E, nu, p(lf), p(comp), p(it), p(uf), C.byref(rn), C.byref(ev))
+    _lib.raise_for(rc, ctx.h, "podecm_twoscale_run")
+    return {"load_factor": lf, "compliance": comp, "iters": it, "u_final": uf, "residual_norm": rn.value,
+            "micro_evals": ev.value}
+
+
 # ---- interchange formats (SURVEY 8(f) item 4) --------------------------------
 FNV_SEED = 14695981039346656037
 

@@ -96,3 +96,16 @@ def test_oracle_full_order_newton_matches_dense_python(orc):
     for s in range(2):
         ref = fe_newton_pbar(o, t, tuple(geom[s]), sched[s])
         assert np.abs(r["pbar"][s] - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_oracle_twoscale_linear_engine_is_single_scale(orc):
+    """test_twoscale.cpp:93-134: with the linear engine the FE2 driver is the
+    single-scale linear problem, so compliance = factor^2 x const and the
+    unloaded plate returns to u = 0."""
+    r, st = orc.run_twoscale(nx=2, ny=1, steps=10, peak=0.02, E=1.0, nu=0.3)
+    assert st == 0
+    lf = r["load_factor"]
+    ratio = r["compliance"][lf > 0] / lf[lf > 0] ** 2
+    assert np.abs(ratio / ratio[0] - 1.0).max() <= 1e-10
+    assert r["residual_norm"] <= 1e-12
+    assert np.all(r["iters"] == 1)
