@@ -385,15 +385,15 @@ template <int NT>
 __host__ __device__ constexpr int contract_ipc() {
   return NT <= 7 ? kIPC : 1;
 }
-template <int NT>
+template <int NT, int IPC = contract_ipc<NT>()>
 constexpr size_t contract_smem_bytes() {
-  return sizeof(double) * (2 * (kPC * 4) * contract_ld<NT>() +
-                           2 * contract_ipc<NT>() * (kPC * 4) * contract_ld<NT>() + 2 * contract_ipc<NT>() * kPC * 20);
+  return sizeof(double) * (2 * (kPC * 4) * contract_ld<NT>() + 2 * IPC * (kPC * 4) * contract_ld<NT>() +
+                           2 * IPC * kPC * 20);
 }
 
-template <int NT>
-__global__ void __launch_bounds__(32 * NT * contract_ipc<NT>()) k_rom_contract(ContractArgs g) {
-  constexpr int kIPC = contract_ipc<NT>();
+template <int NT, int IPC = contract_ipc<NT>()>
+__global__ void __launch_bounds__(32 * NT * IPC) k_rom_contract(ContractArgs g) {
+  constexpr int kIPC = IPC;
   constexpr int NP = NT * 8;
   constexpr int LDY = contract_ld<NT>();
   constexpr int KR = kPC * 4;  // k-rows per chunk
@@ -1128,6 +1128,10 @@ void set_contract_attrs(std::integer_sequence<int, I...>) {
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)contract_smem_bytes<(I > 0 ? I : 1)>())
                : (void)0));
+  (..., (I > 0 && I <= 7 ? (void)cudaFuncSetAttribute(k_rom_contract<(I > 0 && I <= 7 ? I : 1), 1>,
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)contract_smem_bytes<(I > 0 && I <= 7 ? I : 1), 1>())
+                         : (void)0));
 }
 
 // Opt-in dynamic SMEM limits are per device: set them once for every device
@@ -1191,9 +1195,17 @@ void launch_F(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, const PointArgs& p
   k_rom_F<<<gpt, 256, smem_pt, s>>>(pa);
 }
 
+// Small batches (e.g. the FE2 engines: 800 instances = 1.35 waves of
+// two-instance CTAs) run one instance per CTA for twice the CTAs.
+constexpr int64_t kSmallBatch = 4096;
+
 template <int NT>
 void launch_contract_nt(cudaStream_t s, const ContractArgs& ca) {
   constexpr int ipc = contract_ipc<NT>();
+  if (ipc > 1 && ca.n < kSmallBatch) {
+    k_rom_contract<NT, 1><<<(int)ca.n, 32 * NT, contract_smem_bytes<NT, 1>(), s>>>(ca);
+    return;
+  }
   const int gct = (int)((ca.n + ipc - 1) / ipc);
   k_rom_contract<NT><<<gct, 32 * NT * ipc, contract_smem_bytes<NT>(), s>>>(ca);
 }
