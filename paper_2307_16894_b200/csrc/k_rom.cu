@@ -23,6 +23,17 @@
 //                   partial pivoting (Eigen PartialPivLU semantics) and the
 //                   update, or the adaptive bisection / commit logic.
 //
+// Default ("lazy tangent") order of one global iteration: k_rom_F, k_rom_point
+// MODE 1 (P, Pt, trial history), k_rom_check (f = Gm^T Pt by DMMA, residual
+// test; converged / failed instances finish here, the rest are compacted into
+// a list), k_rom_point MODE 2 (FD tangent for the listed instances only),
+// k_rom_contract over the list, k_rom_solve (LU + update).  A quarter of the
+// assemblies are the final convergence checks, which never need K, so this
+// skips a quarter of the tangents and contractions.  One deviation: an FD
+// failure at an assembly that already satisfies the tolerance is not seen
+// (the reference would fail that attempt); PODECM_ROM_LAZY=0 restores the
+// fused order.
+//
 // Summation order of the contractions differs from Eigen's; the stated
 // tolerance for the homogenised stress history is 1e-8 (BASELINE north star).
 #include <algorithm>
@@ -73,8 +84,9 @@ struct podecm_rom {
   double* d_CA = nullptr;     // effective stiffness: c_p A_p [cap][Q][16] (lazy)
   double* d_Sprev = nullptr;  // effective stiffness: history at the start of the last increment
   int64_t abar_cap = 0;
-  int* d_nactive = nullptr;
+  int* d_nactive = nullptr;  // [0] active instances, [1] lazy-tangent list length
   int* h_nactive = nullptr;
+  int* d_list = nullptr;  // lazy tangent: compacted instances that need K [cap]
   int64_t last_global_iters = 0;
 };
 
@@ -101,12 +113,14 @@ void free_work(podecm_rom* r) {
   cudaFree(r->d_a0);
   cudaFree(r->d_Fb);
   cudaFree(r->d_ctl);
+  cudaFree(r->d_list);
   cudaFree(r->d_CA);
   cudaFree(r->d_Sprev);
   r->d_CA = r->d_Sprev = nullptr;
   r->abar_cap = 0;
   r->d_morph = r->d_S = r->d_At = r->d_P = r->d_K = r->d_f = r->d_a = r->d_a0 = r->d_Fb = nullptr;
   r->d_ctl = nullptr;
+  r->d_list = nullptr;
   r->cap = 0;
 }
 
@@ -197,6 +211,8 @@ struct PointArgs {
   RomCtl* ctl;
   const double* S0;  // effective-stiffness stage: frozen history [n][6][Q]
   double* CA;        // effective-stiffness stage: c_p A_p [n][Q][16]
+  const int* list;   // lazy tangent: instances that need K (MODE 2)
+  const int* count;
 };
 
 // F at every ECM point: F = Fbar + R(Fmu^-1)^T (G_p^T a) (rom.cpp:48-50).  CTA =
@@ -271,12 +287,23 @@ __global__ void __launch_bounds__(256) k_rom_F(PointArgs g) {
 // budget): P, FD tangent, trial history, then the mapped operators
 // At = c R A R^T and Pt = c R P.  ABAR (rom_effective_stiffness,
 // rom.cpp:206-207): history from g.S0, no trial history, and c A kept too.
-template <int MINB, bool ABAR = false>
+// MODE (lazy-tangent pipeline): 0 everything, 1 P / Pt / trial history only,
+// 2 the tangent only, for the instances g.list[0 .. *g.count).
+template <int MINB, bool ABAR = false, int MODE = 0>
 __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable tab) {
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= g.n * g.Q) return;
-  const int64_t s = tid / g.Q;
-  const int p = tid - (int)s * g.Q;
+  int64_t s;
+  int p;
+  if (MODE == 2) {
+    const int j = tid / g.Q;
+    if (j >= *g.count) return;
+    s = g.list[j];
+    p = tid - j * g.Q;
+  } else {
+    s = tid / g.Q;
+    p = tid - (int)s * g.Q;
+  }
   RomCtl* c = g.ctl + s;
   if (!c->active) return;
   const double* mo = g.morph + (size_t)s * 5 * g.Q;
@@ -296,27 +323,30 @@ __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable t
   for (int t = 0; t < 4; ++t) fp[t] = s0p[(size_t)t * g.Q + p];
   Frozen z;
   freeze(fp, s0p[(size_t)4 * g.Q + p], s0p[(size_t)5 * g.Q + p], z);
-  double P[4];
-  FullOut fo;
-  bool ok = lsu_eval<true>(pm, z, F, P, &fo);
-  if (!ABAR) {
-#pragma unroll
-    for (int t = 0; t < 4; ++t) s1p[(size_t)t * g.Q + p] = fo.fp[t];
-    s1p[(size_t)4 * g.Q + p] = fo.fpzz;
-    s1p[(size_t)5 * g.Q + p] = fo.xi;
-  }
-  double* Pp = g.P + ((size_t)s * g.Q + p) * 4;
-#pragma unroll
-  for (int t = 0; t < 4; ++t) Pp[t] = P[t];
   const double cw = g.w[p] * det;  // rom.cpp:56
   double* at = g.At + ((size_t)s * g.Qpad + p) * 20;
-  // Pt = c R P : (R P)[i + 2j] = sum_l m(j,l) P[i + 2l]
+  bool ok = true;
+  if (MODE != 2) {
+    double P[4];
+    FullOut fo;
+    ok = lsu_eval<true>(pm, z, F, P, &fo);
+    if (!ABAR) {
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
-    const int i = r & 1, j = r >> 1;
-    at[16 + r] = cw * (m[j] * P[i] + m[j + 2] * P[i + 2]);
+      for (int t = 0; t < 4; ++t) s1p[(size_t)t * g.Q + p] = fo.fp[t];
+      s1p[(size_t)4 * g.Q + p] = fo.fpzz;
+      s1p[(size_t)5 * g.Q + p] = fo.xi;
+    }
+    double* Pp = g.P + ((size_t)s * g.Q + p) * 4;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) Pp[t] = P[t];
+    // Pt = c R P : (R P)[i + 2j] = sum_l m(j,l) P[i + 2l]
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = r & 1, j = r >> 1;
+      at[16 + r] = cw * (m[j] * P[i] + m[j + 2] * P[i + 2]);
+    }
   }
-  if (ok) {
+  if (ok && MODE != 1) {
     // At = c R A R^T streamed per column pair: columns e = (s&1) + 2l' arrive
     // in the order 0, 2, 1, 3, so after each pair the four entries of both
     // output columns s in {e&1, (e&1)+2} are final.  T = R col:
@@ -361,6 +391,8 @@ struct ContractArgs {
   double* K;         // [n][N][N]
   double* f;         // [n][N]
   const RomCtl* ctl;
+  const int* list;   // nullable: CTA slots index this compacted instance list
+  const int* count;
 };
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
@@ -391,8 +423,15 @@ constexpr size_t contract_smem_bytes() {
                            2 * IPC * kPC * 20);
 }
 
-template <int NT, int IPC = contract_ipc<NT>()>
-__global__ void __launch_bounds__(32 * NT * IPC) k_rom_contract(ContractArgs g) {
+// two-instance CTAs: 2 resident per SM when the SMEM allows, as a register
+// bound too, so a register-hungrier variant cannot silently halve occupancy
+template <int NT, int IPC>
+constexpr int contract_minb() {
+  return IPC > 1 && (228 * 1024) / (contract_smem_bytes<NT, IPC>() + 1024) >= 2 ? 2 : 1;
+}
+
+template <int NT, int IPC = contract_ipc<NT>(), bool LIST = false>
+__global__ void __launch_bounds__(32 * NT * IPC, (contract_minb<NT, IPC>())) k_rom_contract(ContractArgs g) {
   constexpr int kIPC = IPC;
   constexpr int NP = NT * 8;
   constexpr int LDY = contract_ld<NT>();
@@ -407,9 +446,22 @@ __global__ void __launch_bounds__(32 * NT * IPC) k_rom_contract(ContractArgs g) 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int si = warp / NT, trow = warp - si * NT;
   const int64_t sbase = (int64_t)blockIdx.x * kIPC;
+  // LIST: CTA slots index the compacted instance list (lazy tangent)
+  int64_t sid[kIPC];
+  if constexpr (LIST) {
+    const int64_t lim = *g.count;
+#pragma unroll
+    for (int q = 0; q < kIPC; ++q) sid[q] = sbase + q < lim ? (int64_t)g.list[sbase + q] : -1;
+  }
   bool any = false;
-  for (int q = 0; q < kIPC; ++q)
-    if (sbase + q < g.n && g.ctl[sbase + q].active) any = true;
+  if constexpr (LIST) {
+#pragma unroll
+    for (int q = 0; q < kIPC; ++q)
+      if (sid[q] >= 0) any = true;
+  } else {
+    for (int q = 0; q < kIPC; ++q)
+      if (sbase + q < g.n && g.ctl[sbase + q].active) any = true;
+  }
   if (!any) return;
   const int gid = lane >> 2, tig = lane & 3;
   double acc[NT][2];
@@ -431,8 +483,16 @@ __global__ void __launch_bounds__(32 * NT * IPC) k_rom_contract(ContractArgs g) 
       rA[k] = 0.0;
       if (t < kIPC * kPC * 20) {
         const int q = t / (kPC * 20), rem = t - q * kPC * 20;
-        const int64_t sq = sbase + q;
-        if (sq < g.n) rA[k] = g.At[((size_t)sq * g.Qpad + (size_t)c * kPC) * 20 + rem];
+        if constexpr (LIST) {
+          int64_t sq = sid[0];
+#pragma unroll
+          for (int u = 1; u < kIPC; ++u)
+            if (q == u) sq = sid[u];
+          if (sq >= 0) rA[k] = g.At[((size_t)sq * g.Qpad + (size_t)c * kPC) * 20 + rem];
+        } else {
+          const int64_t sq = sbase + q;
+          if (sq < g.n) rA[k] = g.At[((size_t)sq * g.Qpad + (size_t)c * kPC) * 20 + rem];
+        }
       }
     }
   };
@@ -510,8 +570,16 @@ __global__ void __launch_bounds__(32 * NT * IPC) k_rom_contract(ContractArgs g) 
     if (c + 2 < nch) gstore(cur);
     __syncthreads();
   }
-  const int64_t s = sbase + si;
-  if (s >= g.n || !g.ctl[s].active) return;
+  int64_t s = sbase + si;
+  if constexpr (LIST) {
+    s = sid[0];
+#pragma unroll
+    for (int u = 1; u < kIPC; ++u)
+      if (si == u) s = sid[u];
+    if (s < 0) return;
+  } else {
+    if (s >= g.n || !g.ctl[s].active) return;
+  }
   const int i = trow * 8 + gid;
   if (i >= g.N) return;
 #pragma unroll
@@ -552,6 +620,13 @@ struct NewtonArgs {
   double* Sprev;  // nullable: committed history at the start of increment K-1
   const double* force_ref_inst;  // nullable [n]: per-instance force_ref (RomMicroEngine)
   double* init_res;              // nullable [n][K]: RomStepResult::initial_residual
+  // lazy-tangent pipeline (k_rom_check / k_rom_solve)
+  const double* G;   // Gm [Qpad*4][NP]
+  const double* At;  // Pt_p at At[(s, p)][16 + r]
+  int Qpad, NP;
+  double* f_out;
+  int* list;
+  int* count;
 };
 
 constexpr int kNW = 1;  // warps (instances) per Newton CTA (SMEM-bound: 10 per SM)
@@ -647,6 +722,166 @@ __device__ __forceinline__ void warp_lu_solve(double* Ks, int LD, int N, double*
   }
 }
 
+// The three outcomes of one Newton check (rom.cpp:129-150 with the adaptive
+// wrapper :152-175), shared by the fused and the lazy-tangent pipelines.
+__device__ __forceinline__ void rom_converged(const NewtonArgs& g, RomCtl* c, int64_t s, int lane, double r, int it) {
+  const int N = g.N;
+  // rom_effective_stress at the converged state (rom.cpp:68-76)
+  const bool last_sub = c->sp == 1;
+  if (last_sub) {  // lanes over points, fixed shuffle tree
+    double pb[4] = {0.0, 0.0, 0.0, 0.0};
+    const double* mo = g.morph + (size_t)s * 5 * g.Q;
+    for (int p = lane; p < g.Q; p += 32) {
+      const double cw = g.w[p] * mo[(size_t)4 * g.Q + p];
+      const double4 P4 = *reinterpret_cast<const double4*>(g.P + ((size_t)s * g.Q + p) * 4);
+      pb[0] += cw * P4.x;
+      pb[1] += cw * P4.y;
+      pb[2] += cw * P4.z;
+      pb[3] += cw * P4.w;
+    }
+#pragma unroll
+    for (int c4 = 0; c4 < 4; ++c4)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) pb[c4] += __shfl_xor_sync(0xffffffffu, pb[c4], o);
+    if (lane == 0)
+      for (int c4 = 0; c4 < 4; ++c4) g.pbar[((size_t)s * g.K + c->k) * 4 + c4] = pb[c4] / 1.0;
+  }
+  for (int i = lane; i < N; i += 32) g.a0[(size_t)s * N + i] = g.a[(size_t)s * N + i];
+  __syncwarp();
+  int adv = 0;  // entered the last increment: keep its start history (run_online prev_states)
+  if (lane == 0) {
+    c->iters_acc += it;
+    c->r0max = fmax(c->r0max, c->r0);  // rom.cpp:173 (failed attempts do not count)
+    c->cur ^= 1;  // commit the trial history
+    c->sp -= 1;
+    c->it = 0;
+    if (c->sp == 0) {
+      if (g.init_res) g.init_res[(size_t)s * g.K + c->k] = c->r0max;
+      c->r0max = 0.0;
+      if (g.iters) g.iters[(size_t)s * g.K + c->k] = c->iters_acc;
+      if (g.resid) g.resid[(size_t)s * g.K + c->k] = r;
+      c->iters_acc = 0;
+      c->k += 1;
+      if (c->k == g.K) {
+        c->active = 0;
+      } else {
+        for (int t = 0; t < 4; ++t) {
+          c->fstack[0][t] = g.sched[((size_t)s * g.K + c->k - 1) * 4 + t];
+          c->fstack[0][4 + t] = g.sched[((size_t)s * g.K + c->k) * 4 + t];
+        }
+        c->dstack[0] = g.max_bisect;
+        c->sp = 1;
+        adv = c->k == g.K - 1;
+      }
+    }
+  }
+  __syncwarp();
+  adv = __shfl_sync(0xffffffffu, adv, 0);
+  if (adv && g.Sprev) {
+    const double* src = g.S + ((size_t)c->cur * g.cap + s) * 6 * g.Q;
+    double* dst = g.Sprev + (size_t)s * 6 * g.Q;
+    for (int t = lane; t < 6 * g.Q; t += 32) dst[t] = src[t];
+  }
+  if (!c->active && g.a_final)
+    for (int i = lane; i < N; i += 32) g.a_final[(size_t)s * N + i] = g.a[(size_t)s * N + i];
+}
+
+__device__ __forceinline__ void rom_failed(const NewtonArgs& g, RomCtl* c, int64_t s, int lane) {
+  const int N = g.N;
+  for (int i = lane; i < N; i += 32) g.a[(size_t)s * N + i] = g.a0[(size_t)s * N + i];
+  __syncwarp();
+  if (lane == 0) {
+    c->asm_fail = 0;
+    c->it = 0;
+    const int top = c->sp - 1;
+    if (c->dstack[top] <= 0 || c->sp + 1 > kMaxStack) {
+      c->active = 0;  // rom.cpp:159: rethrow -> SolveError for this instance
+      c->status = PODECM_ESOLVE;
+      if (g.status) g.status[s] = PODECM_ESOLVE;
+      atomicAdd(g.fail, 1u);
+    } else {
+      double fp[4], ft[4], mid[4];
+      for (int t = 0; t < 4; ++t) {
+        fp[t] = c->fstack[top][t];
+        ft[t] = c->fstack[top][4 + t];
+        mid[t] = 0.5 * (fp[t] + ft[t]);
+      }
+      const int d = c->dstack[top] - 1;
+      for (int t = 0; t < 4; ++t) {  // second half below, first half on top
+        c->fstack[top][t] = mid[t];
+        c->fstack[top][4 + t] = ft[t];
+        c->fstack[top + 1][t] = fp[t];
+        c->fstack[top + 1][4 + t] = mid[t];
+      }
+      c->dstack[top] = d;
+      c->dstack[top + 1] = d;
+      c->sp += 1;
+    }
+  }
+  __syncwarp();
+}
+
+// K da = -f (dense LU, partial pivoting: first row of max |a_ik|), a += da
+__device__ __forceinline__ void rom_update(const NewtonArgs& g, RomCtl* c, int64_t s, int lane, double* Ks,
+                                           double* rhs, int it) {
+  const int N = g.N, LD = N + 1;
+  {  // K row-major [i][j] -> Ks column-major; 8 loads in flight per lane
+    const double* src = g.Kg + (size_t)s * N * N;
+    const int NN = N * N;
+    for (int t0 = 0; t0 < NN; t0 += 32 * 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u * 32 + lane;
+        v[u] = t < NN ? __ldcs(src + t) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u * 32 + lane;
+        if (t < NN) {
+          const int i = t / N, j = t - i * N;
+          Ks[j * LD + i] = v[u];
+        }
+      }
+    }
+  }
+  for (int i = lane; i < N; i += 32) rhs[i] = -g.f[(size_t)s * N + i];
+  __syncwarp();
+  warp_lu_solve<1>(Ks, LD, N, rhs, lane);
+  for (int i = lane; i < N; i += 32) g.a[(size_t)s * N + i] += rhs[i];
+  if (lane == 0) c->it = it + 1;
+}
+
+// residual norm and the reference's convergence test (tolerance frozen at
+// iteration 0); returns 0 solve, 1 converged, 2 failed
+__device__ __forceinline__ int rom_decide(const NewtonArgs& g, RomCtl* c, int64_t s, int lane, double ss,
+                                          double* r_out) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const double r = sqrt(ss);
+  *r_out = r;
+  int out = 0;
+  if (c->asm_fail != 0) {
+    out = 2;
+  } else {
+    const int it = c->it;
+    if (it == 0) {
+      const double fr = g.force_ref_inst ? fmax(g.force_ref, g.force_ref_inst[s]) : g.force_ref;
+      const double tol = fmax(g.eps_rel * fmax(r, fr), g.eps_abs);
+      __syncwarp();
+      if (lane == 0) {
+        c->tol = tol;
+        c->r0 = r;
+      }
+      out = r <= tol ? 1 : (it == g.max_iter ? 2 : 0);
+    } else {
+      out = r <= c->tol ? 1 : (it == g.max_iter ? 2 : 0);
+    }
+  }
+  __syncwarp();
+  return out;
+}
+
 __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
   extern __shared__ double smn[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -657,153 +892,134 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
   if (s >= g.n) return;
   RomCtl* c = g.ctl + s;
   if (!c->active) return;
-  // residual norm
+  const int it = c->it;
   double ss = 0.0;
   for (int i = lane; i < N; i += 32) {
     const double v = g.f[(size_t)s * N + i];
     ss = fma(v, v, ss);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-  const double r = sqrt(ss);
-  bool fail = c->asm_fail != 0;
-  bool conv = false;
-  int it = c->it;
-  if (!fail) {
-    if (it == 0) {
-      const double fr = g.force_ref_inst ? fmax(g.force_ref, g.force_ref_inst[s]) : g.force_ref;
-      c->tol = fmax(g.eps_rel * fmax(r, fr), g.eps_abs);
-      c->r0 = r;
-    }
-    if (r <= c->tol) {
-      conv = true;
-    } else if (it == g.max_iter) {
-      fail = true;
-    }
-  }
-  __syncwarp();
-  if (!fail && !conv) {
-    // K da = -f  (dense LU, partial pivoting: first row of max |a_ik|)
-    {  // K row-major [i][j] -> Ks column-major; 8 loads in flight per lane
-      const double* src = g.Kg + (size_t)s * N * N;
-      const int NN = N * N;
-      for (int t0 = 0; t0 < NN; t0 += 32 * 8) {
-        double v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int t = t0 + u * 32 + lane;
-          v[u] = t < NN ? __ldcs(src + t) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int t = t0 + u * 32 + lane;
-          if (t < NN) {
-            const int i = t / N, j = t - i * N;
-            Ks[j * LD + i] = v[u];
-          }
-        }
-      }
-    }
-    for (int i = lane; i < N; i += 32) rhs[i] = -g.f[(size_t)s * N + i];
-    __syncwarp();
-    warp_lu_solve<1>(Ks, LD, N, rhs, lane);
-    for (int i = lane; i < N; i += 32) g.a[(size_t)s * N + i] += rhs[i];
-    if (lane == 0) c->it = it + 1;
-  }
-  if (conv) {
-    // rom_effective_stress at the converged state (rom.cpp:68-76)
-    const bool last_sub = c->sp == 1;
-    if (last_sub) {  // lanes over points, fixed shuffle tree
-      double pb[4] = {0.0, 0.0, 0.0, 0.0};
-      const double* mo = g.morph + (size_t)s * 5 * g.Q;
-      for (int p = lane; p < g.Q; p += 32) {
-        const double cw = g.w[p] * mo[(size_t)4 * g.Q + p];
-        const double4 P4 = *reinterpret_cast<const double4*>(g.P + ((size_t)s * g.Q + p) * 4);
-        pb[0] += cw * P4.x;
-        pb[1] += cw * P4.y;
-        pb[2] += cw * P4.z;
-        pb[3] += cw * P4.w;
-      }
-#pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) pb[c4] += __shfl_xor_sync(0xffffffffu, pb[c4], o);
-      if (lane == 0)
-        for (int c4 = 0; c4 < 4; ++c4) g.pbar[((size_t)s * g.K + c->k) * 4 + c4] = pb[c4] / 1.0;
-    }
-    for (int i = lane; i < N; i += 32) g.a0[(size_t)s * N + i] = g.a[(size_t)s * N + i];
-    __syncwarp();
-    int adv = 0;  // entered the last increment: keep its start history (run_online prev_states)
-    if (lane == 0) {
-      c->iters_acc += it;
-      c->r0max = fmax(c->r0max, c->r0);  // rom.cpp:173 (failed attempts do not count)
-      c->cur ^= 1;  // commit the trial history
-      c->sp -= 1;
-      c->it = 0;
-      if (c->sp == 0) {
-        if (g.init_res) g.init_res[(size_t)s * g.K + c->k] = c->r0max;
-        c->r0max = 0.0;
-        if (g.iters) g.iters[(size_t)s * g.K + c->k] = c->iters_acc;
-        if (g.resid) g.resid[(size_t)s * g.K + c->k] = r;
-        c->iters_acc = 0;
-        c->k += 1;
-        if (c->k == g.K) {
-          c->active = 0;
-        } else {
-          for (int t = 0; t < 4; ++t) {
-            c->fstack[0][t] = g.sched[((size_t)s * g.K + c->k - 1) * 4 + t];
-            c->fstack[0][4 + t] = g.sched[((size_t)s * g.K + c->k) * 4 + t];
-          }
-          c->dstack[0] = g.max_bisect;
-          c->sp = 1;
-          adv = c->k == g.K - 1;
-        }
-      }
-    }
-    __syncwarp();
-    adv = __shfl_sync(0xffffffffu, adv, 0);
-    if (adv && g.Sprev) {
-      const double* src = g.S + ((size_t)c->cur * g.cap + s) * 6 * g.Q;
-      double* dst = g.Sprev + (size_t)s * 6 * g.Q;
-      for (int t = lane; t < 6 * g.Q; t += 32) dst[t] = src[t];
-    }
-    if (!c->active && g.a_final)
-      for (int i = lane; i < N; i += 32) g.a_final[(size_t)s * N + i] = g.a[(size_t)s * N + i];
-  }
-  if (fail) {
-    for (int i = lane; i < N; i += 32) g.a[(size_t)s * N + i] = g.a0[(size_t)s * N + i];
-    __syncwarp();
-    if (lane == 0) {
-      c->asm_fail = 0;
-      c->it = 0;
-      const int top = c->sp - 1;
-      if (c->dstack[top] <= 0 || c->sp + 1 > kMaxStack) {
-        c->active = 0;  // rom.cpp:159: rethrow -> SolveError for this instance
-        c->status = PODECM_ESOLVE;
-        if (g.status) g.status[s] = PODECM_ESOLVE;
-        atomicAdd(g.fail, 1u);
-      } else {
-        double fp[4], ft[4], mid[4];
-        for (int t = 0; t < 4; ++t) {
-          fp[t] = c->fstack[top][t];
-          ft[t] = c->fstack[top][4 + t];
-          mid[t] = 0.5 * (fp[t] + ft[t]);
-        }
-        const int d = c->dstack[top] - 1;
-        for (int t = 0; t < 4; ++t) {  // second half below, first half on top
-          c->fstack[top][t] = mid[t];
-          c->fstack[top][4 + t] = ft[t];
-          c->fstack[top + 1][t] = fp[t];
-          c->fstack[top + 1][4 + t] = mid[t];
-        }
-        c->dstack[top] = d;
-        c->dstack[top + 1] = d;
-        c->sp += 1;
-      }
-    }
-  }
+  double r;
+  const int d = rom_decide(g, c, s, lane, ss, &r);
+  if (d == 0) rom_update(g, c, s, lane, Ks, rhs, it);
+  if (d == 1) rom_converged(g, c, s, lane, r, it);
+  if (d == 2) rom_failed(g, c, s, lane);
   __syncwarp();
   if (lane == 0 && c->active) atomicAdd(g.nactive, 1);
+}
+
+// Lazy-tangent pipeline, step 1: f = Gm^T Pt for kCI instances per CTA as
+// one DMMA GEMM (M = instances, N = modes, K = the 4Q point rows; Gm staged
+// through SMEM 32 rows at a time and shared by the CTA's instances), then the
+// Newton decision, one warp per instance.  Converged and failed instances
+// finish here without ever needing K; the rest are appended to g.list for the
+// tangent pass, the contraction and k_rom_solve.
+constexpr int kCI = 16;     // instances (and warps) per k_rom_check CTA
+constexpr int kCRows = 32;  // Gm rows per SMEM stage (kPC points)
+constexpr int kCLdp = kCRows + 4;
+
+__host__ __device__ constexpr size_t check_smem_doubles(int NP) {
+  return (size_t)kCRows * (NP + 4) + (size_t)kCI * kCLdp + (size_t)kCI * NP;
+}
+
+__global__ void __launch_bounds__(32 * kCI) k_rom_check(NewtonArgs g) {
+  extern __shared__ double smk[];
+  const int NP = g.NP, LDG = NP + 4, N = g.N;
+  double* sG = smk;                                // [kCRows][LDG]
+  double* sPt = sG + (size_t)kCRows * LDG;         // [kCI][kCLdp]
+  double* sF = sPt + (size_t)kCI * kCLdp;          // [kCI][NP]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int64_t s0 = (int64_t)blockIdx.x * kCI;
+  const int64_t s = s0 + warp;
+  const bool act = s < g.n && g.ctl[s].active;
+  if (!__syncthreads_or(act)) return;
+  const int NTt = NP / 8;
+  // jobs: (m-tile, n-tile) = (j & 1, j >> 1), two per warp at most (NT <= 15)
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  const int R = g.Qpad * 4;  // padding rows of Gm and Pt are zero
+  constexpr int kGPT = kCRows * 128 / (32 * kCI);  // Gm doubles per thread per stage (NP <= 128)
+  double rG[kGPT], rP;
+  auto load = [&](int r0) {  // next stage into registers (in flight during the DMMAs)
+#pragma unroll
+    for (int k = 0; k < kGPT; ++k) {
+      const int t = tid + k * 32 * kCI;
+      rG[k] = t < kCRows * NP ? g.G[(size_t)r0 * NP + t] : 0.0;
+    }
+    const int row = r0 + lane;
+    rP = act ? g.At[((size_t)s * g.Qpad + (row >> 2)) * 20 + 16 + (row & 3)] : 0.0;
+  };
+  load(0);
+  for (int r0 = 0; r0 < R; r0 += kCRows) {
+#pragma unroll
+    for (int k = 0; k < kGPT; ++k) {
+      const int t = tid + k * 32 * kCI;
+      if (t < kCRows * NP) {
+        const int rr = t / NP, i = t - rr * NP;
+        sG[rr * LDG + i] = rG[k];
+      }
+    }
+    sPt[warp * kCLdp + lane] = rP;
+    __syncthreads();
+    if (r0 + kCRows < R) load(r0 + kCRows);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int j = warp + u * kCI;
+      if (j < 2 * NTt) {
+        const int mt = j & 1, nt = j >> 1;
+#pragma unroll
+        for (int ks = 0; ks < kCRows / 4; ++ks) {
+          const double afr = sPt[(mt * 8 + gid) * kCLdp + ks * 4 + tig];
+          const double bfr = sG[(ks * 4 + tig) * LDG + nt * 8 + gid];
+          dmma(acc[u][0], acc[u][1], afr, bfr);
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int j = warp + u * kCI;
+    if (j < 2 * NTt) {
+      const int mt = j & 1, nt = j >> 1;
+      sF[(mt * 8 + gid) * NP + nt * 8 + 2 * tig] = acc[u][0];
+      sF[(mt * 8 + gid) * NP + nt * 8 + 2 * tig + 1] = acc[u][1];
+    }
+  }
+  __syncthreads();
+  if (!act) return;
+  RomCtl* c = g.ctl + s;
+  double ss = 0.0;
+  for (int i = lane; i < N; i += 32) {
+    const double v = sF[warp * NP + i];
+    g.f_out[(size_t)s * N + i] = v;
+    ss = fma(v, v, ss);
+  }
+  const int it = c->it;
+  double r;
+  const int d = rom_decide(g, c, s, lane, ss, &r);
+  if (d == 1) rom_converged(g, c, s, lane, r, it);
+  if (d == 2) rom_failed(g, c, s, lane);
+  if (d == 0 && lane == 0) g.list[atomicAdd(g.count, 1)] = (int)s;
+  __syncwarp();
+  if (lane == 0 && c->active) atomicAdd(g.nactive, 1);
+}
+
+// Lazy-tangent pipeline, step 2 (after the tangent pass and the contraction
+// over g.list): a tangent failure fails the attempt (bisection), otherwise
+// the Newton update K da = -f.
+__global__ void __launch_bounds__(32) k_rom_solve(NewtonArgs g) {
+  extern __shared__ double smn[];
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x;
+  if (j >= *g.count) return;
+  const int64_t s = g.list[j];
+  RomCtl* c = g.ctl + s;
+  double* Ks = smn;
+  double* rhs = Ks + g.N * (g.N + 1);
+  if (c->asm_fail != 0)
+    rom_failed(g, c, s, lane);
+  else
+    rom_update(g, c, s, lane, Ks, rhs, c->it);
 }
 
 
@@ -1069,6 +1285,17 @@ __global__ void k_eng_init(int64_t n, int Q, int N, double* Sc, double* ac, doub
 }
 
 // register budget of the point kernel (2 or 3 CTAs/SM); PODECM_ROM_POINT_MINB
+// Lazy tangent (default): the FD tangent and the contraction run only for
+// the instances the residual check sends to a Newton update.  PODECM_ROM_LAZY=0
+// restores the fused pipeline (tangent at every point every iteration).
+bool rom_lazy() {
+  static bool v = [] {
+    const char* e = getenv("PODECM_ROM_LAZY");
+    return !(e && atoi(e) == 0);
+  }();
+  return v;
+}
+
 int point_minb() {
   static int v = [] {
     const char* e = getenv("PODECM_ROM_POINT_MINB");
@@ -1099,6 +1326,7 @@ int ensure_cap(podecm_rom* r, int64_t n) {
   if (!rc) rc = dalloc(ctx, &r->d_a0, (size_t)n * N);
   if (!rc) rc = dalloc(ctx, &r->d_Fb, (size_t)n * 4 * Q);
   if (!rc) rc = dalloc(ctx, &r->d_ctl, (size_t)n);
+  if (!rc) rc = dalloc(ctx, &r->d_list, (size_t)n);
   if (rc) {
     free_work(r);
     return rc;
@@ -1122,13 +1350,13 @@ int ensure_abar(podecm_rom* r, int64_t n, bool sprev) {
   return rc;
 }
 
-template <int... I>
+template <bool LIST, int... I>
 void set_contract_attrs(std::integer_sequence<int, I...>) {
-  (..., (I > 0 ? (void)cudaFuncSetAttribute(k_rom_contract<(I > 0 ? I : 1)>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)contract_smem_bytes<(I > 0 ? I : 1)>())
+  (..., (I > 0 ? (void)cudaFuncSetAttribute(
+                     k_rom_contract<(I > 0 ? I : 1), contract_ipc<(I > 0 ? I : 1)>(), LIST>,
+                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)contract_smem_bytes<(I > 0 ? I : 1)>())
                : (void)0));
-  (..., (I > 0 && I <= 7 ? (void)cudaFuncSetAttribute(k_rom_contract<(I > 0 && I <= 7 ? I : 1), 1>,
+  (..., (I > 0 && I <= 7 ? (void)cudaFuncSetAttribute(k_rom_contract<(I > 0 && I <= 7 ? I : 1), 1, LIST>,
                                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                      (int)contract_smem_bytes<(I > 0 && I <= 7 ? I : 1), 1>())
                          : (void)0));
@@ -1144,7 +1372,10 @@ void set_attrs() {
   std::lock_guard<std::mutex> lock(mu);
   if (dev < 64 && (done >> dev) & 1u) return;
   cudaFuncSetAttribute(k_rom_F, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  set_contract_attrs(std::make_integer_sequence<int, kMaxNT + 1>{});
+  set_contract_attrs<false>(std::make_integer_sequence<int, kMaxNT + 1>{});
+  set_contract_attrs<true>(std::make_integer_sequence<int, kMaxNT + 1>{});
+  cudaFuncSetAttribute(k_rom_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_rom_check, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_rom_newton, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_rom_abar, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (dev < 64) done |= uint64_t(1) << dev;
@@ -1169,6 +1400,8 @@ PointArgs point_args(podecm_rom* r, int64_t n) {
   pa.ctl = r->d_ctl;
   pa.S0 = nullptr;
   pa.CA = nullptr;
+  pa.list = nullptr;
+  pa.count = nullptr;
   return pa;
 }
 
@@ -1185,6 +1418,8 @@ ContractArgs contract_args(podecm_rom* r, int64_t n) {
   ca.K = r->d_K;
   ca.f = r->d_f;
   ca.ctl = r->d_ctl;
+  ca.list = nullptr;
+  ca.count = nullptr;
   return ca;
 }
 
@@ -1199,20 +1434,23 @@ void launch_F(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, const PointArgs& p
 // two-instance CTAs) run one instance per CTA for twice the CTAs.
 constexpr int64_t kSmallBatch = 4096;
 
-template <int NT>
+template <int NT, bool LIST>
 void launch_contract_nt(cudaStream_t s, const ContractArgs& ca) {
   constexpr int ipc = contract_ipc<NT>();
   if (ipc > 1 && ca.n < kSmallBatch) {
-    k_rom_contract<NT, 1><<<(int)ca.n, 32 * NT, contract_smem_bytes<NT, 1>(), s>>>(ca);
+    k_rom_contract<NT, 1, LIST><<<(int)ca.n, 32 * NT, contract_smem_bytes<NT, 1>(), s>>>(ca);
     return;
   }
   const int gct = (int)((ca.n + ipc - 1) / ipc);
-  k_rom_contract<NT><<<gct, 32 * NT * ipc, contract_smem_bytes<NT>(), s>>>(ca);
+  k_rom_contract<NT, ipc, LIST><<<gct, 32 * NT * ipc, contract_smem_bytes<NT>(), s>>>(ca);
 }
 
 template <int... I>
 void launch_contract_sw(int nt, cudaStream_t s, const ContractArgs& ca, std::integer_sequence<int, I...>) {
-  (..., (nt == I + 1 ? launch_contract_nt<I + 1>(s, ca) : (void)0));
+  if (ca.list)
+    (..., (nt == I + 1 ? launch_contract_nt<I + 1, true>(s, ca) : (void)0));
+  else
+    (..., (nt == I + 1 ? launch_contract_nt<I + 1, false>(s, ca) : (void)0));
 }
 
 void launch_contract(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, const ContractArgs& ca) {
@@ -1340,12 +1578,55 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
   na.Sprev = abar ? r->d_Sprev : nullptr;
   na.force_ref_inst = start.fref;
   na.init_res = start.init_res;
+  na.G = r->d_G;
+  na.At = r->d_At;
+  na.Qpad = r->Qpad;
+  na.NP = r->NP;
+  na.f_out = r->d_f;
+  na.list = r->d_list;
+  na.count = r->d_nactive + 1;
+  const bool lazy = rom_lazy();
+  PointArgs pl = pa;
+  pl.list = r->d_list;
+  pl.count = r->d_nactive + 1;
+  ContractArgs cl = ca;
+  cl.list = r->d_list;
+  cl.count = r->d_nactive + 1;
+  const size_t smem_ck = check_smem_doubles(r->NP) * sizeof(double);
   const size_t smem_nt = (size_t)kNW * ((size_t)N * (N + 1) + 2 * N) * sizeof(double);
   const int gnt = (int)((n_inst + kNW - 1) / kNW);
 
   const int64_t max_global = (int64_t)K * (opts->max_iter + 1) * (2ll << opts->max_bisect) + 8;
   for (int64_t it = 0; it < max_global; ++it) {
     launch_F(ctx, s, r, pa);
+    if (lazy) {
+      const int gp = grid_for(n_inst * Q, 128);
+      {
+        KTimer kt(ctx, s, "k_rom_point_p");
+        if (point_minb() == 4)
+          k_rom_point<4, false, 1><<<gp, 128, 0, s>>>(pa, rv->mats);
+        else
+          k_rom_point<5, false, 1><<<gp, 128, 0, s>>>(pa, rv->mats);
+      }
+      PODECM_CUDA_TRY(ctx, cudaMemsetAsync(r->d_nactive, 0, 2 * sizeof(int), s));
+      {
+        KTimer kt(ctx, s, "k_rom_check");
+        k_rom_check<<<(int)((n_inst + kCI - 1) / kCI), 32 * kCI, smem_ck, s>>>(na);
+      }
+      {
+        KTimer kt(ctx, s, "k_rom_point_tangent");
+        if (point_minb() == 4)
+          k_rom_point<4, false, 2><<<gp, 128, 0, s>>>(pl, rv->mats);
+        else
+          k_rom_point<5, false, 2><<<gp, 128, 0, s>>>(pl, rv->mats);
+      }
+      launch_contract(ctx, s, r, cl);
+      {
+        KTimer kt(ctx, s, "k_rom_solve");
+        k_rom_solve<<<(int)n_inst, 32, (size_t)((size_t)N * (N + 1) + 2 * N) * sizeof(double), s>>>(na);
+      }
+      PODECM_LAUNCHED(ctx, 6);
+    } else {
     {
       KTimer kt(ctx, s, "k_rom_point");
       const int gp = grid_for(n_inst * Q, 128);
@@ -1361,6 +1642,7 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
       k_rom_newton<<<gnt, 32 * kNW, smem_nt, s>>>(na);
     }
     PODECM_LAUNCHED(ctx, 4);
+    }
     if ((it & 3) == 3) {
       PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(r->h_nactive, r->d_nactive, sizeof(int),
                                            cudaMemcpyDeviceToHost, s));
@@ -1431,7 +1713,7 @@ int podecm_rom_create(podecm_ctx* ctx, podecm_rve* rve, int N, int Q, const int3
   up(&r->d_w, hw);
   up(&r->d_G, G);
   up(&r->d_Gt, Gt);
-  if (!rc && cudaMalloc(&r->d_nactive, sizeof(int)) != cudaSuccess) rc = PODECM_ECUDA;
+  if (!rc && cudaMalloc(&r->d_nactive, 2 * sizeof(int)) != cudaSuccess) rc = PODECM_ECUDA;
   if (!rc && cudaMallocHost(&r->h_nactive, sizeof(int)) != cudaSuccess) rc = PODECM_ECUDA;
   if (rc) {
     podecm_rom_destroy(r);

@@ -149,3 +149,21 @@ def test_wide_bases(orc, N):
     rel = np.linalg.norm(rg["abar"] - ro["abar"], axis=-1) / np.maximum(1.0, np.linalg.norm(ro["abar"], axis=-1))
     print(f"N={N}: abar rel {rel.max():.2e}")
     assert rel.max() <= 1e-8
+
+
+def test_fused_pipeline_variant():
+    """The default pipeline evaluates the FD tangent and the contraction only
+    for instances the residual check sends to a Newton update (k_rom_check /
+    k_rom_solve).  PODECM_ROM_LAZY=0 selects the fused one (tangent at every
+    point every iteration, k_rom_newton); the library reads the variable once
+    per process, so this module runs again in a child process under it."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, PODECM_ROM_LAZY="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", str(Path(__file__)), "-x", "-q", "-m", "gpu",
+                        "-k", "not fused_pipeline_variant", "-p", "no:cacheprovider"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
