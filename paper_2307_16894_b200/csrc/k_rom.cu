@@ -722,6 +722,105 @@ __device__ __forceinline__ void warp_lu_solve(double* Ks, int LD, int N, double*
   }
 }
 
+// The same factorisation and solve (identical pivots and per-element FMA
+// sequence) on a row-major A[i * N + j] as it arrives from global memory in
+// one bulk copy: lanes over columns in the rank-1 update (conflict-free rows,
+// the multipliers are warp broadcasts), one right-hand side.
+__device__ __forceinline__ void warp_lu_solve_rm(double* A, int N, double* rhs, int lane) {
+  for (int k = 0; k < N; ++k) {
+    double best = -1.0;
+    int bi = N;
+    for (int i = k + lane; i < N; i += 32) {
+      const double v = fabs(A[i * N + k]);
+      if (v > best) {
+        best = v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (bi != k) {
+      for (int j = lane; j < N; j += 32) {
+        const double t0 = A[k * N + j];
+        A[k * N + j] = A[bi * N + j];
+        A[bi * N + j] = t0;
+      }
+      if (lane == 0) {
+        const double t0 = rhs[k];
+        rhs[k] = rhs[bi];
+        rhs[bi] = t0;
+      }
+    }
+    __syncwarp();
+    const double d = A[k * N + k];
+    if (best != 0.0) {
+      const double rd = __drcp_rn(d);  // correctly rounded: div_rcp == '/'
+      for (int i = k + 1 + lane; i < N; i += 32) A[i * N + k] = div_rcp(A[i * N + k], d, rd);
+    }
+    __syncwarp();
+    const double bk = rhs[k];
+    for (int j = k + 1 + lane; j < N; j += 32) {
+      const double u = A[k * N + j];
+      int i = k + 1;
+      for (; i + 3 < N; i += 4) {
+        const double l0 = A[i * N + k], l1 = A[(i + 1) * N + k];
+        const double l2 = A[(i + 2) * N + k], l3 = A[(i + 3) * N + k];
+        const double a0 = A[i * N + j], a1 = A[(i + 1) * N + j];
+        const double a2 = A[(i + 2) * N + j], a3 = A[(i + 3) * N + j];
+        A[i * N + j] = fma(-l0, u, a0);
+        A[(i + 1) * N + j] = fma(-l1, u, a1);
+        A[(i + 2) * N + j] = fma(-l2, u, a2);
+        A[(i + 3) * N + j] = fma(-l3, u, a3);
+      }
+      for (; i < N; ++i) A[i * N + j] = fma(-A[i * N + k], u, A[i * N + j]);
+    }
+    for (int i = k + 1 + lane; i < N; i += 32) rhs[i] = fma(-A[i * N + k], bk, rhs[i]);
+    __syncwarp();
+  }
+  for (int k = N - 1; k >= 0; --k) {  // back substitution with U, lanes over rows
+    const double ukk = A[k * N + k];
+    const double xk = div_rcp(rhs[k], ukk, __drcp_rn(ukk));
+    __syncwarp();
+    if (lane == 0) rhs[k] = xk;
+    for (int i = lane; i < k; i += 32) rhs[i] = fma(-A[i * N + k], xk, rhs[i]);
+    __syncwarp();
+  }
+}
+
+// One cp.async.bulk global -> shared copy completing on an mbarrier (bytes
+// and both addresses 16-byte aligned), issued and awaited by one warp.
+__device__ __forceinline__ void warp_bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* mbar,
+                                               int lane) {
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(mbar);
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  if (lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    asm volatile("fence.proxy.async.shared::cta;\n" ::);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes));
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(d),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+  }
+  __syncwarp();
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar)
+      : "memory");
+}
+
 // The three outcomes of one Newton check (rom.cpp:129-150 with the adaptive
 // wrapper :152-175), shared by the fused and the lazy-tangent pipelines.
 __device__ __forceinline__ void rom_converged(const NewtonArgs& g, RomCtl* c, int64_t s, int lane, double r, int it) {
@@ -821,13 +920,18 @@ __device__ __forceinline__ void rom_failed(const NewtonArgs& g, RomCtl* c, int64
   __syncwarp();
 }
 
-// K da = -f (dense LU, partial pivoting: first row of max |a_ik|), a += da
+// K da = -f (dense LU, partial pivoting: first row of max |a_ik|), a += da.
+// SMEM per warp: K row-major [N][N], rhs [N], the mbarrier (fits the
+// N (N + 1) + 2N doubles the launches reserve).
 __device__ __forceinline__ void rom_update(const NewtonArgs& g, RomCtl* c, int64_t s, int lane, double* Ks,
-                                           double* rhs, int it) {
-  const int N = g.N, LD = N + 1;
-  {  // K row-major [i][j] -> Ks column-major; 8 loads in flight per lane
-    const double* src = g.Kg + (size_t)s * N * N;
-    const int NN = N * N;
+                                           double*, int it) {
+  const int N = g.N, NN = N * N;
+  double* rhs = Ks + NN;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(rhs + N);
+  const double* src = g.Kg + (size_t)s * NN;
+  if ((NN & 1) == 0) {  // 16-byte aligned rows of the batch: one bulk copy
+    warp_bulk_load(Ks, src, (unsigned)NN * 8u, mbar, lane);
+  } else {
     for (int t0 = 0; t0 < NN; t0 += 32 * 8) {
       double v[8];
 #pragma unroll
@@ -838,16 +942,13 @@ __device__ __forceinline__ void rom_update(const NewtonArgs& g, RomCtl* c, int64
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int t = t0 + u * 32 + lane;
-        if (t < NN) {
-          const int i = t / N, j = t - i * N;
-          Ks[j * LD + i] = v[u];
-        }
+        if (t < NN) Ks[t] = v[u];
       }
     }
   }
   for (int i = lane; i < N; i += 32) rhs[i] = -g.f[(size_t)s * N + i];
   __syncwarp();
-  warp_lu_solve<1>(Ks, LD, N, rhs, lane);
+  warp_lu_solve_rm(Ks, N, rhs, lane);
   for (int i = lane; i < N; i += 32) g.a[(size_t)s * N + i] += rhs[i];
   if (lane == 0) c->it = it + 1;
 }
