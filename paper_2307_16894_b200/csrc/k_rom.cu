@@ -79,7 +79,8 @@ struct podecm_rom {
   double* d_Gt = nullptr;  // [N][4][Qpad]: G_p[i][r], p fastest (material kernel)
   int64_t cap = 0;
   double *d_morph = nullptr, *d_S = nullptr, *d_At = nullptr, *d_P = nullptr, *d_K = nullptr,
-         *d_f = nullptr, *d_a = nullptr, *d_a0 = nullptr, *d_Fb = nullptr;
+         *d_f = nullptr, *d_a = nullptr, *d_a0 = nullptr, *d_Fb = nullptr,
+         *d_Pt = nullptr;  // lazy tangent: compact Pt [cap][Qpad][4]
   RomCtl* d_ctl = nullptr;
   double* d_CA = nullptr;     // effective stiffness: c_p A_p [cap][Q][16] (lazy)
   double* d_Sprev = nullptr;  // effective stiffness: history at the start of the last increment
@@ -112,13 +113,14 @@ void free_work(podecm_rom* r) {
   cudaFree(r->d_a);
   cudaFree(r->d_a0);
   cudaFree(r->d_Fb);
+  cudaFree(r->d_Pt);
   cudaFree(r->d_ctl);
   cudaFree(r->d_list);
   cudaFree(r->d_CA);
   cudaFree(r->d_Sprev);
   r->d_CA = r->d_Sprev = nullptr;
   r->abar_cap = 0;
-  r->d_morph = r->d_S = r->d_At = r->d_P = r->d_K = r->d_f = r->d_a = r->d_a0 = r->d_Fb = nullptr;
+  r->d_morph = r->d_S = r->d_At = r->d_P = r->d_K = r->d_f = r->d_a = r->d_a0 = r->d_Fb = r->d_Pt = nullptr;
   r->d_ctl = nullptr;
   r->d_list = nullptr;
   r->cap = 0;
@@ -208,6 +210,7 @@ struct PointArgs {
   double* At;  // [n][Qpad][20]
   double* P;   // [n][Q][4]
   double* Fb;  // [n][4][Q]
+  double* Pt;  // MODE 1: compact Pt [n][Qpad][4]
   RomCtl* ctl;
   const double* S0;  // effective-stiffness stage: frozen history [n][6][Q]
   double* CA;        // effective-stiffness stage: c_p A_p [n][Q][16]
@@ -340,11 +343,17 @@ __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable t
 #pragma unroll
     for (int t = 0; t < 4; ++t) Pp[t] = P[t];
     // Pt = c R P : (R P)[i + 2j] = sum_l m(j,l) P[i + 2l]
+    double pt[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int i = r & 1, j = r >> 1;
-      at[16 + r] = cw * (m[j] * P[i] + m[j + 2] * P[i + 2]);
+      pt[r] = cw * (m[j] * P[i] + m[j + 2] * P[i + 2]);
     }
+    if (MODE == 1)  // read back by k_rom_check only (32 B per point, not a 160 B At row)
+      *reinterpret_cast<double4*>(g.Pt + ((size_t)s * g.Qpad + p) * 4) = make_double4(pt[0], pt[1], pt[2], pt[3]);
+    else
+#pragma unroll
+      for (int r = 0; r < 4; ++r) at[16 + r] = pt[r];
   }
   if (ok && MODE != 1) {
     // At = c R A R^T streamed per column pair: columns e = (s&1) + 2l' arrive
@@ -589,7 +598,7 @@ __global__ void __launch_bounds__(32 * NT * IPC, (contract_minb<NT, IPC>())) k_r
       const int j = ct * 8 + 2 * tig + h;
       if (j < g.N)
         g.K[((size_t)s * g.N + i) * g.N + j] = acc[ct][h];
-      else if (j == g.N)
+      else if (j == g.N && !LIST)  // LIST: f comes from k_rom_check (the Pt column is stale here)
         g.f[(size_t)s * g.N + i] = acc[ct][h];
     }
 }
@@ -622,7 +631,7 @@ struct NewtonArgs {
   double* init_res;              // nullable [n][K]: RomStepResult::initial_residual
   // lazy-tangent pipeline (k_rom_check / k_rom_solve)
   const double* G;   // Gm [Qpad*4][NP]
-  const double* At;  // Pt_p at At[(s, p)][16 + r]
+  const double* Pt;  // compact Pt [n][Qpad][4] (k_rom_point MODE 1)
   int Qpad, NP;
   double* f_out;
   int* list;
@@ -1047,7 +1056,7 @@ __global__ void __launch_bounds__(32 * kCI) k_rom_check(NewtonArgs g) {
       rG[k] = t < kCRows * NP ? g.G[(size_t)r0 * NP + t] : 0.0;
     }
     const int row = r0 + lane;
-    rP = act ? g.At[((size_t)s * g.Qpad + (row >> 2)) * 20 + 16 + (row & 3)] : 0.0;
+    rP = act ? g.Pt[((size_t)s * g.Qpad) * 4 + row] : 0.0;
   };
   load(0);
   for (int r0 = 0; r0 < R; r0 += kCRows) {
@@ -1426,14 +1435,16 @@ int ensure_cap(podecm_rom* r, int64_t n) {
   if (!rc) rc = dalloc(ctx, &r->d_a, (size_t)n * N);
   if (!rc) rc = dalloc(ctx, &r->d_a0, (size_t)n * N);
   if (!rc) rc = dalloc(ctx, &r->d_Fb, (size_t)n * 4 * Q);
+  if (!rc) rc = dalloc(ctx, &r->d_Pt, (size_t)n * r->Qpad * 4);
   if (!rc) rc = dalloc(ctx, &r->d_ctl, (size_t)n);
   if (!rc) rc = dalloc(ctx, &r->d_list, (size_t)n);
   if (rc) {
     free_work(r);
     return rc;
   }
-  // padding rows of At (p >= Q) stay zero forever
+  // padding rows of At and Pt (p >= Q) stay zero forever
   PODECM_CUDA_TRY(ctx, cudaMemset(r->d_At, 0, (size_t)n * r->Qpad * 20 * sizeof(double)));
+  PODECM_CUDA_TRY(ctx, cudaMemset(r->d_Pt, 0, (size_t)n * r->Qpad * 4 * sizeof(double)));
   r->cap = n;
   return PODECM_OK;
 }
@@ -1498,6 +1509,7 @@ PointArgs point_args(podecm_rom* r, int64_t n) {
   pa.At = r->d_At;
   pa.P = r->d_P;
   pa.Fb = r->d_Fb;
+  pa.Pt = r->d_Pt;
   pa.ctl = r->d_ctl;
   pa.S0 = nullptr;
   pa.CA = nullptr;
@@ -1680,7 +1692,7 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
   na.force_ref_inst = start.fref;
   na.init_res = start.init_res;
   na.G = r->d_G;
-  na.At = r->d_At;
+  na.Pt = r->d_Pt;
   na.Qpad = r->Qpad;
   na.NP = r->NP;
   na.f_out = r->d_f;
