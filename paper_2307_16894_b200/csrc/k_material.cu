@@ -61,18 +61,74 @@ __global__ void __launch_bounds__(128, MINB) k_material_batch(
   }
 }
 
-// Variant table (FD pairing x register budget); the default was chosen by
-// measurement on B200, PODECM_K1_VARIANT overrides it.
+// Slab variant: the point's operands sit in a shared-memory slab column
+// (material.cuh, SlabSrc) instead of registers across the 9 evaluations.
+template <int MINB>
+__global__ void __launch_bounds__(128, MINB) k_material_slab(
+    int64_t n, MatTable tab, int n_mats, const int32_t* __restrict__ region,
+    const double* __restrict__ F, const double* __restrict__ st, double* __restrict__ P,
+    double* __restrict__ A, double* __restrict__ st_out, int32_t* __restrict__ status,
+    unsigned int* __restrict__ fail, double h_rel) {
+  constexpr int S = 128;
+  __shared__ double slab[kSlabSlots * S];
+  volatile double* c = slab + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    int r = region ? __ldg(region + i) : 0;
+    r = (r < 0 || r >= n_mats) ? 0 : r;
+    const MatConst& p = tab.m[r];
+    {
+      double f[4], fp[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) f[k] = __ldg(F + k * n + i);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) fp[k] = __ldg(st + k * n + i);
+      slab_load<S>(c, f, fp, __ldg(st + 4 * n + i), __ldg(st + 5 * n + i));
+    }
+    bool ok;
+    {
+      double pv[4];
+      FullOut fo;
+      ok = lsu_eval_src<true>(p, SlabSrc<S>{c}, pv, &fo);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) __stcs(P + k * n + i, pv[k]);
+      if (st_out) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) __stcs(st_out + k * n + i, fo.fp[k]);
+        __stcs(st_out + 4 * n + i, fo.fpzz);
+        __stcs(st_out + 5 * n + i, fo.xi);
+      }
+    }
+    if (ok && A) {
+      auto sink = [&](int e, const double col[4]) {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) __stcs(A + (int64_t)(r + 4 * e) * n + i, col[r]);
+      };
+      ok = fd_tangent_slab<S>(p, c, h_rel, sink);
+    }
+    if (status) status[i] = ok ? 0 : PODECM_ESOLVE;
+    if (!ok) atomicAdd(fail, 1u);
+  }
+}
+
+// Variant table (FD pairing x register budget, register- or slab-resident
+// operands); the default was chosen by measurement on B200:
+// the slab kernel at 7 CTAs/SM (71 registers) runs 1.074 ms per config-1
+// step against 1.146 ms for the best register-resident one (<false, 5>).
+// PODECM_K1_VARIANT overrides it.
 using KFn = void (*)(int64_t, MatTable, int, const int32_t*, const double*, const double*, double*,
                      double*, double*, int32_t*, unsigned int*, double);
 const KFn kVariants[] = {k_material_batch<true, 3>, k_material_batch<true, 4>,
-                         k_material_batch<false, 4>, k_material_batch<false, 5>};
+                         k_material_batch<false, 4>, k_material_batch<false, 5>,
+                         k_material_slab<6>,         k_material_slab<7>,
+                         k_material_slab<8>};
+constexpr int kNVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 
 int k1_variant() {
   static int v = [] {
     const char* e = getenv("PODECM_K1_VARIANT");
-    int x = e ? atoi(e) : 3;
-    return (x >= 0 && x < 4) ? x : 3;
+    int x = e ? atoi(e) : 5;
+    return (x >= 0 && x < kNVariants) ? x : 5;
   }();
   return v;
 }

@@ -292,8 +292,12 @@ __global__ void __launch_bounds__(256) k_rom_F(PointArgs g) {
 // rom.cpp:206-207): history from g.S0, no trial history, and c A kept too.
 // MODE (lazy-tangent pipeline): 0 everything, 1 P / Pt / trial history only,
 // 2 the tangent only, for the instances g.list[0 .. *g.count).
-template <int MINB, bool ABAR = false, int MODE = 0>
+// SLAB: the FD loop runs over a shared-memory slab column (material.cuh,
+// SlabSrc), which frees the registers for more resident warps.
+template <int MINB, bool ABAR = false, int MODE = 0, bool SLAB = false>
 __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable tab) {
+  constexpr int kSlabS = 128;
+  __shared__ double slab[(SLAB && MODE != 1) ? kSlabSlots * kSlabS : 1];
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= g.n * g.Q) return;
   int64_t s;
@@ -329,10 +333,16 @@ __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable t
   const double cw = g.w[p] * det;  // rom.cpp:56
   double* at = g.At + ((size_t)s * g.Qpad + p) * 20;
   bool ok = true;
+  constexpr bool kSlab = SLAB && MODE != 1;
+  volatile double* sc = slab + threadIdx.x;
+  if constexpr (kSlab) slab_put<kSlabS>(sc, F, z);
   if (MODE != 2) {
     double P[4];
     FullOut fo;
-    ok = lsu_eval<true>(pm, z, F, P, &fo);
+    if constexpr (kSlab)
+      ok = lsu_eval_src<true>(pm, SlabSrc<kSlabS>{sc}, P, &fo);
+    else
+      ok = lsu_eval<true>(pm, z, F, P, &fo);
     if (!ABAR) {
 #pragma unroll
       for (int t = 0; t < 4; ++t) s1p[(size_t)t * g.Q + p] = fo.fp[t];
@@ -386,7 +396,11 @@ __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable t
         for (int r = 0; r < 4; ++r) at[r + 4 * sc] = cw * fma(Tc[r], m[js + 2], T0[r] * m[js]);
       }
     };
-    ok = fd_tangent<false>(pm, z, F, 1e-7, sink);
+    if constexpr (kSlab) {
+      ok = fd_tangent_slab<kSlabS>(pm, sc, 1e-7, sink);
+    } else {
+      ok = fd_tangent<false>(pm, z, F, 1e-7, sink);
+    }
   }
   if (!ok) c->asm_fail = 1;  // SolveError inside rom_assemble -> attempt fails
 }
@@ -1406,12 +1420,27 @@ bool rom_lazy() {
   return v;
 }
 
+// Material-point kernel variant: 4 / 5 = register-resident operands at that
+// many CTAs per SM, 6 / 7 = slab-resident (PODECM_ROM_POINT_MINB).  Default 6
+// (measured, C3 at 16,384 instances: k_rom_point_tangent 99.6 ms against
+// 117.6 ms for 5; 7 is within noise of 6).
 int point_minb() {
   static int v = [] {
     const char* e = getenv("PODECM_ROM_POINT_MINB");
-    return (e && atoi(e) == 4) ? 4 : 5;
+    const int x = e ? atoi(e) : 6;
+    return (x >= 4 && x <= 7) ? x : 6;
   }();
   return v;
+}
+
+template <bool ABAR, int MODE>
+void launch_point(int grid, cudaStream_t s, const PointArgs& a, const MatTable& mats) {
+  switch (point_minb()) {
+    case 4: k_rom_point<4, ABAR, MODE><<<grid, 128, 0, s>>>(a, mats); break;
+    case 6: k_rom_point<6, ABAR, MODE, true><<<grid, 128, 0, s>>>(a, mats); break;
+    case 7: k_rom_point<7, ABAR, MODE, true><<<grid, 128, 0, s>>>(a, mats); break;
+    default: k_rom_point<5, ABAR, MODE><<<grid, 128, 0, s>>>(a, mats); break;
+  }
 }
 
 template <class T>
@@ -1584,10 +1613,7 @@ int abar_stage(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, int64_t n, const 
   {
     KTimer kt(ctx, s, "k_rom_point_abar");
     const int gp = grid_for(n * r->Q, 128);
-    if (point_minb() == 4)
-      k_rom_point<4, true><<<gp, 128, 0, s>>>(pa, r->rve->mats);
-    else
-      k_rom_point<5, true><<<gp, 128, 0, s>>>(pa, r->rve->mats);
+    launch_point<true, 0>(gp, s, pa, r->rve->mats);
   }
   launch_contract(ctx, s, r, contract_args(r, n));
   AbarArgs aa;
@@ -1716,10 +1742,7 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
       const int gp = grid_for(n_inst * Q, 128);
       {
         KTimer kt(ctx, s, "k_rom_point_p");
-        if (point_minb() == 4)
-          k_rom_point<4, false, 1><<<gp, 128, 0, s>>>(pa, rv->mats);
-        else
-          k_rom_point<5, false, 1><<<gp, 128, 0, s>>>(pa, rv->mats);
+        launch_point<false, 1>(gp, s, pa, rv->mats);
       }
       PODECM_CUDA_TRY(ctx, cudaMemsetAsync(r->d_nactive, 0, 2 * sizeof(int), s));
       {
@@ -1728,10 +1751,7 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
       }
       {
         KTimer kt(ctx, s, "k_rom_point_tangent");
-        if (point_minb() == 4)
-          k_rom_point<4, false, 2><<<gp, 128, 0, s>>>(pl, rv->mats);
-        else
-          k_rom_point<5, false, 2><<<gp, 128, 0, s>>>(pl, rv->mats);
+        launch_point<false, 2>(gp, s, pl, rv->mats);
       }
       launch_contract(ctx, s, r, cl);
       {
@@ -1743,10 +1763,7 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
     {
       KTimer kt(ctx, s, "k_rom_point");
       const int gp = grid_for(n_inst * Q, 128);
-      if (point_minb() == 4)
-        k_rom_point<4><<<gp, 128, 0, s>>>(pa, rv->mats);
-      else
-        k_rom_point<5><<<gp, 128, 0, s>>>(pa, rv->mats);
+      launch_point<false, 0>(gp, s, pa, rv->mats);
     }
     launch_contract(ctx, s, r, ca);
     PODECM_CUDA_TRY(ctx, cudaMemsetAsync(r->d_nactive, 0, sizeof(int), s));
