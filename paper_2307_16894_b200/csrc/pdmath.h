@@ -92,14 +92,11 @@ PDM_HD double fma_(double a, double b, double c) {
 #endif
 }
 
-PDM_HD double exp(double x) {
-  if (!(x > -700.0 && x < 700.0)) {
-#ifdef __CUDA_ARCH__
-    return ::exp(x);
-#else
-    return std::exp(x);
-#endif
-  }
+PDM_HD bool exp_fast_ok(double x) { return x > -700.0 && x < 700.0; }
+
+// Fast path only (callers check exp_fast_ok); on an out-of-range input it
+// returns garbage without faulting (saturating conversions, masked index).
+PDM_HD double exp_core(double x) {
   const double shift = 0x1.8p52;
   double kd = fma_(x, pdm_k[kInvLn2N], shift);
   kd = kd - shift;                       // round(256 x / ln2), exact integer
@@ -116,16 +113,25 @@ PDM_HD double exp(double x) {
   return res * from_bits((uint64_t)(e + 1023) << 52);  // exact power-of-two scale
 }
 
-PDM_HD double log(double x) {
-  const uint64_t ix = bits(x);
-  const uint32_t top = (uint32_t)(ix >> 52);
-  if (top - 1u >= 0x7feu) {  // x <= 0, subnormal, inf, nan (sign bit set => top >= 0x800)
+PDM_HD double exp(double x) {
+  if (!exp_fast_ok(x)) {
 #ifdef __CUDA_ARCH__
-    return ::log(x);
+    return ::exp(x);
 #else
-    return std::log(x);
+    return std::exp(x);
 #endif
   }
+  return exp_core(x);
+}
+
+// x > 0 normal and finite (otherwise: x <= 0, subnormal, inf, nan; a set
+// sign bit makes top >= 0x800)
+PDM_HD bool log_fast_ok(double x) { return (uint32_t)(bits(x) >> 52) - 1u < 0x7feu; }
+
+// Fast path only (callers check log_fast_ok); garbage but no fault otherwise.
+PDM_HD double log_core(double x) {
+  const uint64_t ix = bits(x);
+  const uint32_t top = (uint32_t)(ix >> 52);
   int e = (int)top - 1023;
   const int i = (int)((ix >> 45) & 127);
   uint64_t mb = (ix & 0x000fffffffffffffull) | 0x3ff0000000000000ull;  // m in [1, 2)
@@ -154,6 +160,48 @@ PDM_HD double log(double x) {
   const double h_err = (s - hh) + r;     // Fast2Sum, |s| >= |r| or s == 0
   const double lo = ((fma_(ed, pdm_k[kLn2Lo], s_err) + llo) + h_err) + q;
   return hh + lo;
+}
+
+PDM_HD double log(double x) {
+  if (!log_fast_ok(x)) {
+#ifdef __CUDA_ARCH__
+    return ::log(x);
+#else
+    return std::log(x);
+#endif
+  }
+  return log_core(x);
+}
+
+// Two independent evaluations with one range branch: both fast paths are
+// straight-line code the scheduler can interleave (instruction-level
+// parallelism for the FP64 pipe); results are exactly exp(x0), exp(x1).
+PDM_HD void exp_pair(double x0, double x1, double& r0, double& r1) {
+#ifndef __CUDA_ARCH__
+  r0 = pdm::exp(x0);  // host: no speculative fast path (int conversion UB)
+  r1 = pdm::exp(x1);
+  return;
+#endif
+  r0 = exp_core(x0);
+  r1 = exp_core(x1);
+  if (!(exp_fast_ok(x0) && exp_fast_ok(x1))) {
+    r0 = pdm::exp(x0);
+    r1 = pdm::exp(x1);
+  }
+}
+
+PDM_HD void log_pair(double x0, double x1, double& r0, double& r1) {
+#ifndef __CUDA_ARCH__
+  r0 = pdm::log(x0);
+  r1 = pdm::log(x1);
+  return;
+#endif
+  r0 = log_core(x0);
+  r1 = log_core(x1);
+  if (!(log_fast_ok(x0) && log_fast_ok(x1))) {
+    r0 = pdm::log(x0);
+    r1 = pdm::log(x1);
+  }
 }
 
 }  // namespace pdm
