@@ -537,9 +537,19 @@ __global__ void __launch_bounds__(256) k_asm_gather_fused(GatherArgs g, const in
   const int gi = g.kvals ? it : it + (int)g.nnz;  // index into gptr (slots then rows)
   const int b0 = __ldg(gptr + gi), b1 = __ldg(gptr + gi + 1);
   const double* sc = g.scratch + (size_t)c * n_groups;
-  double sm = b1 > b0 ? __ldcs(sc + b0) : 0.0;
+  // runs hold 1-4 element sums on the Q4 cell: all four loads are issued
+  // before the (ordered) additions, so a thread keeps up to 4 in flight
+  const int n = b1 - b0;
+  const double v0 = n > 0 ? __ldcs(sc + b0) : 0.0;
+  const double v1 = n > 1 ? __ldcs(sc + b0 + 1) : 0.0;
+  const double v2 = n > 2 ? __ldcs(sc + b0 + 2) : 0.0;
+  const double v3 = n > 3 ? __ldcs(sc + b0 + 3) : 0.0;
+  double sm = v0;
   if (!is_slot) sm = 0.0 + sm;
-  for (int m = b0 + 1; m < b1; ++m) sm = sm + __ldcs(sc + m);
+  if (n > 1) sm = sm + v1;
+  if (n > 2) sm = sm + v2;
+  if (n > 3) sm = sm + v3;
+  for (int m = b0 + 4; m < b1; ++m) sm = sm + __ldcs(sc + m);
   const int64_t inst = g.inst0 + c;
   if (is_slot)
     g.kvals[(size_t)inst * g.nnz + it] = sm;
