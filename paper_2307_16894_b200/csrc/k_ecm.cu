@@ -372,7 +372,15 @@ __global__ void k_axpy_cols(int64_t m, int k, const double* A, const double* h, 
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= m) return;
   double s = v[r];
-  for (int j = 0; j < k; ++j) s = fma(-A[(int64_t)j * m + r], h[j], s);
+  int j = 0;
+  for (; j + 8 <= k; j += 8) {  // 8 column loads in flight, FMAs in column order
+    double a[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = __ldcs(A + (int64_t)(j + u) * m + r);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s = fma(-a[u], __ldg(h + j + u), s);
+  }
+  for (; j < k; ++j) s = fma(-A[(int64_t)j * m + r], h[j], s);
   v[r] = s;
 }
 
@@ -385,7 +393,15 @@ __global__ void __launch_bounds__(256) k_resid(int64_t m, int k, const double* A
   double v = 0.0;
   if (r < m) {
     v = b[r];
-    for (int j = 0; j < k; ++j) v = v - x[j] * A[(int64_t)j * m + r];
+    int j = 0;
+    for (; j + 8 <= k; j += 8) {  // 8 column loads in flight, updates in column order
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = __ldcs(A + (int64_t)(j + u) * m + r);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v = v - __ldg(x + j + u) * a[u];
+    }
+    for (; j < k; ++j) v = v - x[j] * A[(int64_t)j * m + r];
     out[r] = v;
   }
   s1[threadIdx.x] = v * v;
@@ -434,13 +450,13 @@ __global__ void __launch_bounds__(256) k_dots_part(int64_t m, int k, const doubl
     const double* a2 = nj > 2 ? a0 + 2 * m : a0;
     const double* a3 = nj > 3 ? a0 + 3 * m : a0;
     double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;
-#pragma unroll 2
+#pragma unroll 4
     for (int64_t r = r0 + lane; r < r1; r += 32) {
-      const double x = v[r];
-      p0 = fma(a0[r], x, p0);
-      p1 = fma(a1[r], x, p1);
-      p2 = fma(a2[r], x, p2);
-      p3 = fma(a3[r], x, p3);
+      const double x = __ldg(v + r);
+      p0 = fma(__ldcs(a0 + r), x, p0);
+      p1 = fma(__ldcs(a1 + r), x, p1);
+      p2 = fma(__ldcs(a2 + r), x, p2);
+      p3 = fma(__ldcs(a3 + r), x, p3);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
