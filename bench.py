@@ -79,7 +79,7 @@ def _fp64_issue_roofline(points_per_s: float, clk):
     return {"bound": "fp64-pipe", "achieved": round(ach / 1e12, 3), "peak": round(peak / 1e12, 3),
             "unit": "T FP64 thread-instructions/s", "frac": round(ach / peak, 4),
             "fp64_inst_per_point": per_pt, "sm_mhz": mhz,
-            "note": "DMUL and DADD occupy the FP64 pipe like DFMA; cf. ncu sm__pipe_fp64_cycles_active 68.6 % (profiles/r1_ncu_summary_v6.md)"}
+            "note": "DMUL and DADD occupy the FP64 pipe like DFMA; cf. ncu sm__pipe_fp64_cycles_active 69.0 % (profiles/r1_ncu_summary_v7.md)"}
 
 
 class ClockSampler:
