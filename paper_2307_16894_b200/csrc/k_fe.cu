@@ -384,7 +384,20 @@ int rf_setup(podecm_fe* e, cudaStream_t s, int64_t batch) {
     if (!ok) break;
     e->rf.push_back(h);
     FE_SP(cusolverRfSetNumericProperties(h, 0.0, 0.0), "Rf numeric properties");
-    if (ok) FE_SP(cusolverRfSetAlgs(h, CUSOLVERRF_FACTORIZATION_ALG0, CUSOLVERRF_TRIANGULAR_SOLVE_ALG1), "Rf algs");
+    // Refactorisation ALG1 + triangular solve ALG3: bitwise run-to-run
+    // deterministic (tools/dev/rf_det_probe.sh).  The default ALG0 is not: its
+    // ulp-level jitter flips Newton convergence decisions on ill-conditioned
+    // increments, and a flipped bisection changes the plastic load path
+    // (2.7 % in P-bar on the exact-limit case).  PODECM_RF_ALGS = 10 * factor
+    // alg + solve alg overrides it.
+    static const int rf_algs = [] {
+      const char* v = getenv("PODECM_RF_ALGS");
+      return v ? atoi(v) : 13;
+    }();
+    if (ok)
+      FE_SP(cusolverRfSetAlgs(h, (cusolverRfFactorization_t)(rf_algs / 10),
+                              (cusolverRfTriangularSolve_t)(rf_algs % 10)),
+            "Rf algs");
     if (ok)
       FE_SP(cusolverRfSetMatrixFormat(h, CUSOLVERRF_MATRIX_FORMAT_CSR, CUSOLVERRF_UNIT_DIAGONAL_ASSUMED_L),
             "Rf format");
@@ -452,6 +465,11 @@ int podecm_fe_solve_batch_ex(podecm_ctx* ctx, void* stream, podecm_fe* e, int64_
   double* h_fb = h_pb + 4 * n;
   int32_t* h_mask = reinterpret_cast<int32_t*>(h_fb + 4 * n);  // n ints
   int32_t* h_astat = h_mask + n;                                // n ints (fits in 1 double per 2)
+  // the failed-attempt and Newton-update masks go to the device by async
+  // copies within one global iteration, without a host sync in between: each
+  // needs its own pinned buffer (reusing h_mask raced with the pending copy)
+  int32_t* h_mask_fail = h_astat + n;
+  int32_t* h_mask_solve = h_mask_fail + n;
   // morph (det per qp) and virgin history, w = 0
   if (int rc = podecm_rve_morph(ctx, stream, r, n, geom, e->d_fmi, e->d_det, e->d_mstat)) return rc;
   k_fe_virgin<<<grid_for(n * nq, 256), 256, 0, s>>>(n, nq, e->d_Sc);
@@ -576,8 +594,8 @@ int podecm_fe_solve_batch_ex(podecm_ctx* ctx, void* stream, podecm_fe* e, int64_
     }
     // failed attempts: restore w, bisect (solve_step_adaptive, microfem.cpp:190-211)
     if (any_fail) {
-      for (int64_t i = 0; i < n; ++i) h_mask[i] = act[i] == kFail;
-      PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(e->d_mask, h_mask, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+      for (int64_t i = 0; i < n; ++i) h_mask_fail[i] = act[i] == kFail;
+      PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(e->d_mask, h_mask_fail, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
       k_fe_copy<<<grid_for(n * nr, 256), 256, 0, s>>>(n, nr, e->d_mask, e->d_w0, e->d_w);
       PODECM_LAUNCHED(ctx, 1);
       for (int64_t i = 0; i < n; ++i) {
@@ -605,8 +623,8 @@ int podecm_fe_solve_batch_ex(podecm_ctx* ctx, void* stream, podecm_fe* e, int64_
     // Newton updates: one batched refactorisation + solve for the whole batch
     if (any_solve) {
       if (int rc = rf_setup(e, s, n)) return rc;
-      for (int64_t i = 0; i < n; ++i) h_mask[i] = act[i] == kSolve;
-      PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(e->d_mask, h_mask, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+      for (int64_t i = 0; i < n; ++i) h_mask_solve[i] = act[i] == kSolve;
+      PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(e->d_mask, h_mask_solve, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
       k_fe_negate<<<grid_for(n * nr, 256), 256, 0, s>>>(n * nr, e->d_f, e->d_x);
       PODECM_LAUNCHED(ctx, 1);
       PODECM_CUDA_TRY(ctx, cudaStreamSynchronize(s));  // Rf runs on the legacy stream
@@ -621,7 +639,7 @@ int podecm_fe_solve_batch_ex(podecm_ctx* ctx, void* stream, podecm_fe* e, int64_
           if (!ok) break;
           const cusolverStatus_t rs = cusolverRfRefactor(h);
           if (rs == CUSOLVER_STATUS_ZERO_PIVOT) {  // factorization failed
-            h_mask[i] = 0;
+            h_mask_solve[i] = 0;
             act[i] = kZeroPivot;
             continue;
           }
@@ -632,7 +650,7 @@ int podecm_fe_solve_batch_ex(podecm_ctx* ctx, void* stream, podecm_fe* e, int64_
         FE_DBG("solve ok=%d err=%s\n", (int)ok, cudaGetErrorString(cudaGetLastError()));
       }
       if (!ok) return set_err(ctx, PODECM_ESOLVE, std::string("fe: ") + msg);
-      PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(e->d_mask, h_mask, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+      PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(e->d_mask, h_mask_solve, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
       k_fe_update<<<grid_for(n * nr, 256), 256, 0, s>>>(n, nr, e->d_mask, e->d_x, e->d_w);
       PODECM_LAUNCHED(ctx, 1);
       for (int64_t i = 0; i < n; ++i) {

@@ -82,6 +82,24 @@ def test_exact_limit_rom_equals_full_order_on_gpu(orc):
     assert rel <= 1e-8
 
 
+def test_fe_run_to_run_bitwise(orc):
+    """The full-order solve is bitwise reproducible (a nondeterministic sparse
+    refactorisation once flipped a Newton convergence decision on this
+    ill-conditioned exact-limit case and with it the bisection path)."""
+    import torch
+    from paper_2307_16894_b200 import api
+    g = api.Rve(4, _mats())
+    geom = np.array([[0.3, 0.2], [0.22, 0.31]])
+    H = np.array([0.06, 0.02, -0.03, -0.04])
+    sched = np.array([[[1, 0, 0, 1] + (k / 6) * H for k in range(1, 7)]] * 2)
+    opts = api.NewtonOpts(eps_rel=1e-12, eps_abs=1e-14)
+    fe = api.FullOrder(g)
+    first = fe.solve(_T(geom), _T(sched), opts)
+    for _ in range(12):
+        r = fe.solve(_T(geom), _T(sched), opts)
+        assert torch.equal(r["pbar"], first["pbar"]) and torch.equal(r["iters"], first["iters"])
+
+
 def test_fe_effective_stiffness_vs_oracle(orc):
     """effective_stiffness (microfem.cpp:240-313) at a converged first
     increment from a virgin history: GPU vs oracle within 1e-8."""
