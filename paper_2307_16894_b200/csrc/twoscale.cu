@@ -213,6 +213,26 @@ int podecm_macro_qp_positions(const podecm_macro_cfg* cfg, double* x) {
   return PODECM_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Dense macro tangent from its per-qp contributions: K[ent[e]] = sum of
+// contrib[idx[p]], p in [ptr[e], ptr[e+1]), in the host loop's order (the
+// same additions, from 0, as the column-major host assembly).
+__global__ void k_macro_gather(int n_ent, const int64_t* ent, const int32_t* ptr, const int32_t* idx,
+                               const double* contrib, double* K) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_ent) return;
+  double v = 0.0;
+  for (int p = ptr[e]; p < ptr[e + 1]; ++p) v += contrib[idx[p]];
+  K[ent[e]] = v;
+}
+
+}  // namespace
+
+extern "C" {
+
 int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* cfg, podecm_rom_engines* eng,
                         const podecm_newton* micro_opts, double E, double nu, double* load_factor,
                         double* compliance, int32_t* iters, double* u_final, double* residual_norm,
@@ -268,8 +288,68 @@ int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* c
     cleanup();
     return set_err(ctx, PODECM_ECUDA, "twoscale: getrf workspace");
   }
+  // Macro tangent: the per-qp contributions w v of the host loop below are
+  // gathered into the dense device K (k_macro_gather) instead of a dense host
+  // K that is zero-filled and copied whole (12 MB) every macro iteration.
+  std::vector<int64_t> tgt;
+  for (int q = 0; q < nq; ++q) {
+    const int e = m.elem_of[q];
+    for (int a = 0; a < 8; ++a) {
+      const int da = m.node_dof[m.elems[8 * e + a]];
+      if (da < 0) continue;
+      for (int b = 0; b < 8; ++b) {
+        const int db = m.node_dof[m.elems[8 * e + b]];
+        if (db < 0) continue;
+        for (int r = 0; r < 2; ++r)
+          for (int sc = 0; sc < 2; ++sc) tgt.push_back((int64_t)(db + sc) * n + (da + r));
+      }
+    }
+  }
+  const int64_t n_con = (int64_t)tgt.size();
+  std::vector<int32_t> order(n_con);
+  for (int64_t t = 0; t < n_con; ++t) order[t] = (int32_t)t;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return tgt[x] < tgt[y]; });
+  std::vector<int64_t> ent;
+  std::vector<int32_t> eptr;
+  for (int64_t k = 0; k < n_con; ++k) {
+    if (k == 0 || tgt[order[k]] != tgt[order[k - 1]]) {
+      ent.push_back(tgt[order[k]]);
+      eptr.push_back((int32_t)k);
+    }
+  }
+  eptr.push_back((int32_t)n_con);
+  const int n_ent = (int)ent.size();
+  int64_t* d_ent = nullptr;
+  int32_t *d_eptr = nullptr, *d_eidx = nullptr;
+  double *d_con = nullptr, *h_con = nullptr;
+  {
+    cudaError_t e2 = cudaMalloc(&d_ent, sizeof(int64_t) * std::max(n_ent, 1));
+    if (!e2) e2 = cudaMalloc(&d_eptr, sizeof(int32_t) * (n_ent + 1));
+    if (!e2) e2 = cudaMalloc(&d_eidx, sizeof(int32_t) * std::max<int64_t>(n_con, 1));
+    if (!e2) e2 = cudaMalloc(&d_con, sizeof(double) * std::max<int64_t>(n_con, 1));
+    if (!e2) e2 = cudaMallocHost(&h_con, sizeof(double) * std::max<int64_t>(n_con, 1));
+    if (!e2 && n_ent) e2 = cudaMemcpy(d_ent, ent.data(), sizeof(int64_t) * n_ent, cudaMemcpyHostToDevice);
+    if (!e2) e2 = cudaMemcpy(d_eptr, eptr.data(), sizeof(int32_t) * (n_ent + 1), cudaMemcpyHostToDevice);
+    if (!e2 && n_con) e2 = cudaMemcpy(d_eidx, order.data(), sizeof(int32_t) * n_con, cudaMemcpyHostToDevice);
+    if (e2) {
+      cudaFree(d_ent);
+      cudaFree(d_eptr);
+      cudaFree(d_eidx);
+      cudaFree(d_con);
+      cudaFreeHost(h_con);
+      cleanup();
+      return cuda_err(ctx, e2, "twoscale: macro gather map");
+    }
+  }
+  auto cleanup_map = [&]() {
+    cudaFree(d_ent);
+    cudaFree(d_eptr);
+    cudaFree(d_eidx);
+    cudaFree(d_con);
+    cudaFreeHost(h_con);
+  };
   std::vector<double> u(n, 0.0), ufull(2 * (size_t)m.n_nodes), F(4 * (size_t)nq), P(4 * (size_t)nq),
-      A(16 * (size_t)nq), fint(2 * (size_t)m.n_nodes), res(n), K((size_t)n * n);
+      A(16 * (size_t)nq), fint(2 * (size_t)m.n_nodes), res(n);
   std::vector<int32_t> st(nq);
   int64_t evals = 0;
   const int up = steps / 2;
@@ -329,33 +409,17 @@ int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* c
         }
       }
       evals += nq;
-      // macro residual and tangent (twoscale.cpp:171-204), dense K
+      // macro residual (twoscale.cpp:171-204); the tangent only if Newton goes on
       std::fill(fint.begin(), fint.end(), 0.0);
-      std::fill(K.begin(), K.end(), 0.0);
       for (int q = 0; q < nq; ++q) {
         const int e = m.elem_of[q];
         const double w = m.w[q];
         const double* pb = &P[4 * (size_t)q];
-        const double* ab = &A[16 * (size_t)q];
         for (int a = 0; a < 8; ++a) {
           const int na = m.elems[8 * e + a];
           const double* ga = &m.grad[((size_t)q * 8 + a) * 2];
           fint[2 * (size_t)na] += w * (pb[0] * ga[0] + pb[2] * ga[1]);
           fint[2 * (size_t)na + 1] += w * (pb[1] * ga[0] + pb[3] * ga[1]);
-          const int da = m.node_dof[na];
-          if (da < 0) continue;
-          for (int b = 0; b < 8; ++b) {
-            const int db = m.node_dof[m.elems[8 * e + b]];
-            if (db < 0) continue;
-            const double* gb = &m.grad[((size_t)q * 8 + b) * 2];
-            for (int r = 0; r < 2; ++r)
-              for (int sc = 0; sc < 2; ++sc) {
-                double v = 0.0;
-                for (int c = 0; c < 2; ++c)
-                  for (int d = 0; d < 2; ++d) v += ga[c] * ab[(r + 2 * c) + 4 * (sc + 2 * d)] * gb[d];
-                K[(size_t)(db + sc) * n + (da + r)] += w * v;  // column-major
-              }
-          }
         }
       }
       double rn = 0.0;
@@ -376,8 +440,38 @@ int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* c
         rc = set_err(ctx, PODECM_ESOLVE, "macro Newton did not converge at step " + std::to_string(step));
         break;
       }
+      // dense K (column-major): contributions w v in the host loop order,
+      // summed per entry on the device in that order
+      {
+        int64_t t = 0;
+        for (int q = 0; q < nq; ++q) {
+          const int e = m.elem_of[q];
+          const double w = m.w[q];
+          const double* ab = &A[16 * (size_t)q];
+          for (int a = 0; a < 8; ++a) {
+            const int da = m.node_dof[m.elems[8 * e + a]];
+            if (da < 0) continue;
+            const double* ga = &m.grad[((size_t)q * 8 + a) * 2];
+            for (int b = 0; b < 8; ++b) {
+              const int db = m.node_dof[m.elems[8 * e + b]];
+              if (db < 0) continue;
+              const double* gb = &m.grad[((size_t)q * 8 + b) * 2];
+              for (int r = 0; r < 2; ++r)
+                for (int sc = 0; sc < 2; ++sc) {
+                  double v = 0.0;
+                  for (int c = 0; c < 2; ++c)
+                    for (int d = 0; d < 2; ++d) v += ga[c] * ab[(r + 2 * c) + 4 * (sc + 2 * d)] * gb[d];
+                  h_con[t++] = w * v;
+                }
+            }
+          }
+        }
+      }
       for (int i = 0; i < n; ++i) res[i] = -res[i];
-      cudaMemcpyAsync(d_K, K.data(), sizeof(double) * (size_t)n * n, cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(d_con, h_con, sizeof(double) * n_con, cudaMemcpyHostToDevice, s);
+      cudaMemsetAsync(d_K, 0, sizeof(double) * (size_t)n * n, s);
+      k_macro_gather<<<(n_ent + 255) / 256, 256, 0, s>>>(n_ent, d_ent, d_eptr, d_eidx, d_con, d_K);
+      ctx->launches += 1;
       cudaMemcpyAsync(d_b, res.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s);
       cusolverDnDgetrf(dn, n, n, d_K, n, d_work, d_piv, d_info);
       cusolverDnDgetrs(dn, CUBLAS_OP_N, n, 1, d_K, n, d_piv, d_b, n, d_info);
@@ -409,6 +503,7 @@ int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* c
     if (micro_evals) *micro_evals = evals;
   }
   cudaStreamSynchronize(s);
+  cleanup_map();
   cleanup();
   return rc;
 }
