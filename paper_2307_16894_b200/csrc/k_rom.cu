@@ -1037,7 +1037,7 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
 // Newton decision, one warp per instance.  Converged and failed instances
 // finish here without ever needing K; the rest are appended to g.list for the
 // tangent pass, the contraction and k_rom_solve.
-constexpr int kCI = 16;     // instances (and warps) per k_rom_check CTA
+constexpr int kCI = 32;     // instances (and warps) per k_rom_check CTA (each CTA streams all of Gm once)
 constexpr int kCRows = 32;  // Gm rows per SMEM stage (kPC points)
 constexpr int kCLdp = kCRows + 4;
 
@@ -1058,7 +1058,8 @@ __global__ void __launch_bounds__(32 * kCI) k_rom_check(NewtonArgs g) {
   const bool act = s < g.n && g.ctl[s].active;
   if (!__syncthreads_or(act)) return;
   const int NTt = NP / 8;
-  // jobs: (m-tile, n-tile) = (j & 1, j >> 1), two per warp at most (NT <= 15)
+  constexpr int MT = kCI / 8;  // m-tiles (8 instances each)
+  // jobs: (m-tile, n-tile) = (j % MT, j / MT), two per warp at most (NT <= 15)
   double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
   const int R = g.Qpad * 4;  // padding rows of Gm and Pt are zero
   constexpr int kGPT = kCRows * 128 / (32 * kCI);  // Gm doubles per thread per stage (NP <= 128)
@@ -1088,8 +1089,8 @@ __global__ void __launch_bounds__(32 * kCI) k_rom_check(NewtonArgs g) {
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int j = warp + u * kCI;
-      if (j < 2 * NTt) {
-        const int mt = j & 1, nt = j >> 1;
+      if (j < MT * NTt) {
+        const int mt = j % MT, nt = j / MT;
 #pragma unroll
         for (int ks = 0; ks < kCRows / 4; ++ks) {
           const double afr = sPt[(mt * 8 + gid) * kCLdp + ks * 4 + tig];
@@ -1103,8 +1104,8 @@ __global__ void __launch_bounds__(32 * kCI) k_rom_check(NewtonArgs g) {
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const int j = warp + u * kCI;
-    if (j < 2 * NTt) {
-      const int mt = j & 1, nt = j >> 1;
+    if (j < MT * NTt) {
+      const int mt = j % MT, nt = j / MT;
       sF[(mt * 8 + gid) * NP + nt * 8 + 2 * tig] = acc[u][0];
       sF[(mt * 8 + gid) * NP + nt * 8 + 2 * tig + 1] = acc[u][1];
     }
