@@ -88,6 +88,7 @@ struct podecm_rom {
   int* d_nactive = nullptr;  // [0] active instances, [1] lazy-tangent list length
   int* h_nactive = nullptr;
   int* d_list = nullptr;  // lazy tangent: compacted instances that need K [cap]
+  int* d_alist = nullptr;  // lazy tangent: compacted active instances [cap] (refreshed at host syncs)
   int64_t last_global_iters = 0;
 };
 
@@ -116,6 +117,7 @@ void free_work(podecm_rom* r) {
   cudaFree(r->d_Pt);
   cudaFree(r->d_ctl);
   cudaFree(r->d_list);
+  cudaFree(r->d_alist);
   cudaFree(r->d_CA);
   cudaFree(r->d_Sprev);
   r->d_CA = r->d_Sprev = nullptr;
@@ -123,6 +125,7 @@ void free_work(podecm_rom* r) {
   r->d_morph = r->d_S = r->d_At = r->d_P = r->d_K = r->d_f = r->d_a = r->d_a0 = r->d_Fb = r->d_Pt = nullptr;
   r->d_ctl = nullptr;
   r->d_list = nullptr;
+  r->d_alist = nullptr;
   r->cap = 0;
 }
 
@@ -198,7 +201,8 @@ __global__ void k_rom_fix_status(int64_t n, RomCtl* ctl, int32_t* status, unsign
 
 // ---- material at the ECM points -----------------------------------------
 struct PointArgs {
-  int64_t n;
+  int64_t n;          // instances (or, with alist, entries of alist) this launch covers
+  const int* alist = nullptr;  // nullable: instance of entry k (lazy pipeline: active instances only)
   int N, Q, Qpad;
   int64_t cap;
   const double* Gt;
@@ -222,6 +226,34 @@ struct PointArgs {
 // 32 points x 8 instances sharing one SMEM tile of the mode gradients.
 constexpr int kFInst = 32;  // k_rom_F: instances per CTA (4 per thread)
 
+__device__ __forceinline__ int64_t inst_of(const int* alist, int64_t k) { return alist ? alist[k] : k; }
+
+// Active instances in ascending order (deterministic block scan, one CTA):
+// alist[0 .. alist[cap]) .  The lazy pipeline sizes its grids by this count
+// between host syncs, so finished instances cost no empty CTAs.
+__global__ void __launch_bounds__(1024) k_rom_compact(int64_t n, const RomCtl* ctl, int* alist, int64_t cap) {
+  __shared__ int part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (n + 1023) / 1024, b = t * per, e = b + per < n ? b + per : n;
+  int cnt = 0;
+  for (int64_t i = b; i < e; ++i) cnt += ctl[i].active ? 1 : 0;
+  part[t] = cnt;
+  __syncthreads();
+  if (t == 0) {
+    int acc = 0;
+    for (int k = 0; k < 1024; ++k) {
+      const int v = part[k];
+      part[k] = acc;
+      acc += v;
+    }
+    alist[cap] = acc;
+  }
+  __syncthreads();
+  int o = part[t];
+  for (int64_t i = b; i < e; ++i)
+    if (ctl[i].active) alist[o++] = (int)i;
+}
+
 __global__ void __launch_bounds__(256) k_rom_F(PointArgs g) {
   extern __shared__ double sm[];
   double* sG = sm;                               // [N][4][32]
@@ -233,7 +265,8 @@ __global__ void __launch_bounds__(256) k_rom_F(PointArgs g) {
     __shared__ int any_active;
     if (threadIdx.x == 0) any_active = 0;
     __syncthreads();
-    if (threadIdx.x < kFInst && s0 + threadIdx.x < g.n && g.ctl[s0 + threadIdx.x].active) any_active = 1;
+    if (threadIdx.x < kFInst && s0 + threadIdx.x < g.n && g.ctl[inst_of(g.alist, s0 + threadIdx.x)].active)
+      any_active = 1;
     __syncthreads();
     if (!any_active) return;
   }
@@ -243,7 +276,7 @@ __global__ void __launch_bounds__(256) k_rom_F(PointArgs g) {
   }
   for (int t = threadIdx.x; t < kFInst * g.N; t += blockDim.x) {
     const int si = t / g.N, i = t - si * g.N;
-    sa[t] = (s0 + si < g.n) ? g.a[(size_t)(s0 + si) * g.N + i] : 0.0;
+    sa[t] = (s0 + si < g.n) ? g.a[(size_t)inst_of(g.alist, s0 + si) * g.N + i] : 0.0;
   }
   __syncthreads();
   const int p = p0 + tx;
@@ -267,8 +300,8 @@ __global__ void __launch_bounds__(256) k_rom_F(PointArgs g) {
   }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int64_t s = s0 + ty + 8 * q;
-    if (s >= g.n) break;
+    if (s0 + ty + 8 * q >= g.n) break;
+    const int64_t s = inst_of(g.alist, s0 + ty + 8 * q);
     const RomCtl* c = g.ctl + s;
     if (!c->active) continue;
     // F = Fbar + R(fmi)^T u  (mapped^T a, rom.cpp:48-50)
@@ -308,8 +341,9 @@ __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable t
     s = g.list[j];
     p = tid - j * g.Q;
   } else {
-    s = tid / g.Q;
-    p = tid - (int)s * g.Q;
+    const int64_t k = tid / g.Q;
+    p = tid - (int)k * g.Q;
+    s = inst_of(g.alist, k);
   }
   RomCtl* c = g.ctl + s;
   if (!c->active) return;
@@ -650,6 +684,7 @@ struct NewtonArgs {
   double* f_out;
   int* list;
   int* count;
+  const int* alist = nullptr;  // k_rom_check: instance of entry k (n = entries)
 };
 
 constexpr int kNW = 1;  // warps (instances) per Newton CTA (SMEM-bound: 10 per SM)
@@ -1053,9 +1088,9 @@ __global__ void __launch_bounds__(32 * kCI) k_rom_check(NewtonArgs g) {
   double* sF = sPt + (size_t)kCI * kCLdp;          // [kCI][NP]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const int64_t s0 = (int64_t)blockIdx.x * kCI;
-  const int64_t s = s0 + warp;
-  const bool act = s < g.n && g.ctl[s].active;
+  const int64_t k0 = (int64_t)blockIdx.x * kCI;
+  const int64_t s = k0 + warp < g.n ? inst_of(g.alist, k0 + warp) : g.n;
+  const bool act = k0 + warp < g.n && g.ctl[s].active;
   if (!__syncthreads_or(act)) return;
   const int NTt = NP / 8;
   constexpr int MT = kCI / 8;  // m-tiles (8 instances each)
@@ -1468,6 +1503,7 @@ int ensure_cap(podecm_rom* r, int64_t n) {
   if (!rc) rc = dalloc(ctx, &r->d_Pt, (size_t)n * r->Qpad * 4);
   if (!rc) rc = dalloc(ctx, &r->d_ctl, (size_t)n);
   if (!rc) rc = dalloc(ctx, &r->d_list, (size_t)n);
+  if (!rc) rc = dalloc(ctx, &r->d_alist, (size_t)n + 1);  // [n]: the count
   if (rc) {
     free_work(r);
     return rc;
@@ -1737,30 +1773,66 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
   const int gnt = (int)((n_inst + kNW - 1) / kNW);
 
   const int64_t max_global = (int64_t)K * (opts->max_iter + 1) * (2ll << opts->max_bisect) + 8;
+  // lazy pipeline: grids cover only the instances still active at the last
+  // host sync (k_rom_compact; a superset of the active ones until the next)
+  // (large batches only: a small batch is one short wave either way, and the
+  // extra host sync per call costs more than the trimmed grids save)
+  int64_t n_run = n_inst;
+  const bool use_alist = n_inst >= 8192;
+  auto compact = [&]() -> int {
+    if (use_alist) {
+      k_rom_compact<<<1, 1024, 0, s>>>(n_inst, r->d_ctl, r->d_alist, n_inst);
+      PODECM_LAUNCHED(ctx, 1);
+      PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(r->h_nactive, r->d_alist + n_inst, sizeof(int),
+                                           cudaMemcpyDeviceToHost, s));
+    } else {  // instances k_rom_check left active in the last iteration
+      PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(r->h_nactive, r->d_nactive, sizeof(int), cudaMemcpyDeviceToHost, s));
+    }
+    PODECM_CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    if (use_alist || *r->h_nactive == 0) n_run = *r->h_nactive;
+    return PODECM_OK;
+  };
+  if (lazy && use_alist)
+    if (int rc = compact()) return rc;
   for (int64_t it = 0; it < max_global; ++it) {
-    launch_F(ctx, s, r, pa);
     if (lazy) {
-      const int gp = grid_for(n_inst * Q, 128);
+      if (n_run == 0) break;
+      PointArgs pr = pa;
+      pr.alist = use_alist ? r->d_alist : nullptr;
+      pr.n = n_run;
+      NewtonArgs nr_ = na;
+      nr_.alist = pr.alist;
+      nr_.n = n_run;
+      ContractArgs cr = cl;
+      cr.n = n_run;
+      launch_F(ctx, s, r, pr);
+      const int gp = grid_for(n_run * Q, 128);
       {
         KTimer kt(ctx, s, "k_rom_point_p");
-        launch_point<false, 1>(gp, s, pa, rv->mats);
+        launch_point<false, 1>(gp, s, pr, rv->mats);
       }
       PODECM_CUDA_TRY(ctx, cudaMemsetAsync(r->d_nactive, 0, 2 * sizeof(int), s));
       {
         KTimer kt(ctx, s, "k_rom_check");
-        k_rom_check<<<(int)((n_inst + kCI - 1) / kCI), 32 * kCI, smem_ck, s>>>(na);
+        k_rom_check<<<(int)((n_run + kCI - 1) / kCI), 32 * kCI, smem_ck, s>>>(nr_);
       }
       {
         KTimer kt(ctx, s, "k_rom_point_tangent");
         launch_point<false, 2>(gp, s, pl, rv->mats);
       }
-      launch_contract(ctx, s, r, cl);
+      launch_contract(ctx, s, r, cr);
       {
         KTimer kt(ctx, s, "k_rom_solve");
-        k_rom_solve<<<(int)n_inst, 32, (size_t)((size_t)N * (N + 1) + 2 * N) * sizeof(double), s>>>(na);
+        k_rom_solve<<<(int)n_run, 32, (size_t)((size_t)N * (N + 1) + 2 * N) * sizeof(double), s>>>(na);
       }
       PODECM_LAUNCHED(ctx, 6);
-    } else {
+      r->last_global_iters = it + 1;
+      if ((it & 3) == 3)
+        if (int rc = compact()) return rc;
+      continue;
+    }
+    launch_F(ctx, s, r, pa);
+    {
     {
       KTimer kt(ctx, s, "k_rom_point");
       const int gp = grid_for(n_inst * Q, 128);
