@@ -586,6 +586,7 @@ def run_c4(args, ws, rank, local, ctx, steps, warmup, fp64):
     res = {}
 
     def step():
+        res.clear()  # release the previous step's 8.4 GB W first, so the allocator reuses it
         t0 = time.perf_counter()
         modes_t, ev = api.pod(U_t, N)
         W, st = api.ecm_stress_snapshots(rve, U_t)
