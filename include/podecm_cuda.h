@@ -271,8 +271,8 @@ int podecm_fe_effective_stiffness_batch(podecm_ctx* ctx, void* stream, podecm_fe
 const char* podecm_store_last_error(void);
 /* FNV-1a 64-bit (store.hpp:52-54); seed 14695981039346656037 for a fresh hash. */
 uint64_t podecm_fnv1a64(const void* data, uint64_t n, uint64_t seed);
-/* Mesh::fingerprint (mesh.cpp:158-180) of the Q4 cell: element-kind byte 2
- * (the reference knows Tri6 = 0 and Quad8 = 1), no boundary tags. */
+/* Mesh::fingerprint (mesh.cpp:158-180) of the Q4 cell: element-kind byte 1
+ * (mesh.cpp:160 maps every non-Tri6 kind to 1), no boundary tags. */
 uint64_t podecm_rve_fingerprint(const podecm_rve* rve);
 /* RomModel::save: modes column-major [N][n_dof] (Eigen MatX storage),
  * ids [Q], weights [Q], mode_grads [Q][N][4]. */

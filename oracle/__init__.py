@@ -16,6 +16,11 @@ import numpy as np
 HERE = Path(__file__).resolve().parent
 LIB = HERE / "liboracle.so"          # faithful: glibc exp/log, like the reference
 LIB_PDM = HERE / "liboracle_pdm.so"  # same algorithm with the device's portable exp/log
+# The reference's own material.cpp / rom.cpp / store.cpp / mesh.cpp compiled
+# unchanged against oracle/eigen_shim (oracle/ref/Makefile).  Built only where
+# /root/reference exists (this container); the .so travels to the GPU box.
+REF_LIB = HERE / "_ref" / "libpodecm_ref.so"
+REF_SRC = Path("/root/reference/proj")
 _libs = {}
 
 P = C.c_void_p
@@ -28,7 +33,131 @@ def build() -> Path:
     r = subprocess.run(["make", "-C", str(HERE), "-s"], capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"oracle build failed:\n{r.stdout}\n{r.stderr}")
+    build_ref()
     return LIB
+
+
+def build_ref() -> Path | None:
+    """oracle/_ref from the reference's sources (only where they exist)."""
+    if not (REF_SRC / "src" / "material.cpp").exists():
+        return REF_LIB if REF_LIB.exists() else None
+    r = subprocess.run(["make", "-C", str(HERE / "ref"), "-s", f"REF={REF_SRC}"], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"oracle/_ref build failed:\n{r.stdout}\n{r.stderr}")
+    return REF_LIB
+
+
+_ref = None
+
+
+def ref_available() -> bool:
+    return REF_LIB.exists()
+
+
+def ref_lib():
+    global _ref
+    if _ref is None:
+        l = C.CDLL(str(REF_LIB))
+        l.ref_last_error.restype = C.c_char_p
+        l.ref_material_batch.restype = L
+        l.ref_material_batch.argtypes = [L, P, P, P, P, P, P, P, D, I]
+        l.ref_rom_solve.restype = L
+        l.ref_rom_solve.argtypes = [I, P, P, I, I, I, P, P, P, L, P, P, P, I, D, D, I, P, P, P, P, P, P, I]
+        l.ref_periodic_dof_map.restype = I
+        l.ref_periodic_dof_map.argtypes = [I, P]
+        l.ref_fingerprint.restype = C.c_ulonglong
+        l.ref_fingerprint.argtypes = [I, P]
+        l.ref_rom_model_save.restype = I
+        l.ref_rom_model_save.argtypes = [C.c_char_p, C.c_ulonglong, I, I, D, L, I, P, I, P, P, P]
+        l.ref_rom_model_load.restype = I
+        l.ref_rom_model_load.argtypes = [C.c_char_p, C.POINTER(L), C.POINTER(I), C.POINTER(I),
+                                         C.POINTER(C.c_ulonglong), C.POINTER(I), C.POINTER(I), C.POINTER(D),
+                                         P, P, P, P]
+        _ref = l
+    return _ref
+
+
+def ref_material_batch(F, st, mat, h_rel=1e-7, nthreads=0):
+    """The reference's large_strain_update + large_strain_tangent per point
+    (material.cpp compiled unchanged).  Failed points (status 3) are NaN."""
+    F = np.ascontiguousarray(F, dtype=np.float64)
+    st = np.ascontiguousarray(st, dtype=np.float64)
+    n = F.shape[1]
+    out = {"P": np.full((4, n), np.nan), "A": np.full((16, n), np.nan), "st": np.full((6, n), np.nan),
+           "status": np.empty(n, np.int32)}
+    m = np.array([mat.E, mat.nu, mat.sigma_y0, mat.H], dtype=np.float64)
+    ref_lib().ref_material_batch(n, _p(m), _p(F), _p(st), _p(out["P"]), _p(out["A"]), _p(out["st"]),
+                                 _p(out["status"]), h_rel, nthreads)
+    return out
+
+
+def ref_rom_solve(n_cells, regions, mats, ids, weights, mode_grads, fmi_q, det_q, sched, eps_rel=1e-8,
+                  eps_abs=1e-12, max_iter=25, abar=False, nthreads=0):
+    """The reference's rom_solve (+ rom_effective_stiffness at the last step)
+    on a structured Q4 cell.  fmi_q [n, Q, 4] / det_q [n, Q]: the morph at the
+    ECM points; sched [n, K, 4]."""
+    regions = np.ascontiguousarray(regions, dtype=np.int32)
+    m = _mats(mats)
+    ids = np.ascontiguousarray(ids, dtype=np.int32)
+    weights = np.ascontiguousarray(weights, dtype=np.float64)
+    mg = np.ascontiguousarray(mode_grads, dtype=np.float64)
+    fmi_q = np.ascontiguousarray(fmi_q, dtype=np.float64)
+    det_q = np.ascontiguousarray(det_q, dtype=np.float64)
+    sched = np.ascontiguousarray(sched, dtype=np.float64)
+    Q, N = mg.shape[0], mg.shape[1]
+    n, K = sched.shape[0], sched.shape[1]
+    out = {"pbar": np.zeros((n, K, 4)), "iters": np.zeros((n, K), np.int32), "resid": np.zeros((n, K)),
+           "a_final": np.zeros((n, N)), "status": np.zeros(n, np.int32)}
+    ab = np.zeros((n, 16)) if abar else None
+    ref_lib().ref_rom_solve(n_cells, _p(regions), _p(m), len(mats), N, Q, _p(ids), _p(weights), _p(mg), n,
+                            _p(fmi_q), _p(det_q), _p(sched), K, eps_rel, eps_abs, max_iter, _p(out["pbar"]),
+                            _p(out["iters"]), _p(out["resid"]), _p(out["a_final"]), _p(out["status"]), _p(ab),
+                            nthreads)
+    if abar:
+        out["abar"] = ab
+    return out
+
+
+def ref_periodic_dof_map(n_cells):
+    nd = np.empty((n_cells + 1) ** 2, np.int32)
+    n_red = ref_lib().ref_periodic_dof_map(n_cells, _p(nd))
+    if n_red < 0:
+        raise RuntimeError(ref_lib().ref_last_error().decode())
+    return nd, n_red
+
+
+def ref_fingerprint(n_cells, regions) -> int:
+    regions = np.ascontiguousarray(regions, dtype=np.int32)
+    return int(ref_lib().ref_fingerprint(n_cells, _p(regions)))
+
+
+def ref_rom_model_save(path, model) -> int:
+    modes = np.asfortranarray(model["modes"], dtype=np.float64)
+    ids = np.ascontiguousarray(model["ids"], dtype=np.int32)
+    w = np.ascontiguousarray(model["weights"], dtype=np.float64)
+    mg = np.ascontiguousarray(model["mode_grads"], dtype=np.float64)
+    return ref_lib().ref_rom_model_save(str(path).encode(), int(model.get("mesh_tag", 0)), int(model.get("kind", 0)),
+                                        int(model.get("n_stress_modes", 0)), float(model.get("ecm_eps", 0.0)),
+                                        modes.shape[0], modes.shape[1], modes.ctypes.data_as(C.c_void_p),
+                                        ids.shape[0], _p(ids), _p(w), _p(mg))
+
+
+def ref_rom_model_load(path):
+    """(rc, model dict or error message) via the reference's RomModel::load."""
+    n_dof, N, Q, tag, kind, nsm, eps = L(), I(), I(), C.c_ulonglong(), I(), I(), D()
+    l = ref_lib()
+    args = [str(path).encode(), C.byref(n_dof), C.byref(N), C.byref(Q), C.byref(tag), C.byref(kind), C.byref(nsm),
+            C.byref(eps)]
+    rc = l.ref_rom_model_load(*args, None, None, None, None)
+    if rc != 0:
+        return rc, l.ref_last_error().decode()
+    modes = np.empty((N.value, n_dof.value))  # column-major image
+    ids = np.empty(Q.value, np.int32)
+    w = np.empty(Q.value)
+    mg = np.empty((Q.value, N.value, 4))
+    rc = l.ref_rom_model_load(*args, _p(modes), _p(ids), _p(w), _p(mg))
+    return rc, {"modes": modes.T, "ids": ids, "weights": w, "mode_grads": mg, "mesh_tag": tag.value,
+                "kind": kind.value, "n_stress_modes": nsm.value, "ecm_eps": eps.value}
 
 
 def lib(libm: str = "glibc"):
@@ -71,17 +200,30 @@ def lib(libm: str = "glibc"):
         l.orc_stress_snapshots.argtypes = [P, P, L, P, I]
         l.orc_max_threads.restype = I
         l.orc_libm.argtypes = [I, L, P, P]
+        l.orc_libm_sweep.restype = L
+        l.orc_libm_sweep.argtypes = [I, L, C.c_ulonglong, I, D, D, P]
         _libs[libm] = l
     return _libs[libm]
 
 
 def libm(which: str, x):
-    """Host exp/log: 'exp'/'log' (glibc) or 'pdm_exp'/'pdm_log' (portable)."""
+    """Host exp/log: 'exp'/'log' (glibc), 'pdm_exp'/'pdm_log' (portable
+    variant) or 'gm_exp'/'gm_log' (csrc/gmath.h, the device's restatement of
+    glibc, built for the host)."""
     x = np.ascontiguousarray(x, dtype=np.float64)
     out = np.empty_like(x)
-    code = {"exp": 0, "log": 1, "pdm_exp": 2, "pdm_log": 3}[which]
+    code = {"exp": 0, "log": 1, "pdm_exp": 2, "pdm_log": 3, "gm_exp": 4, "gm_log": 5}[which]
     lib().orc_libm(code, x.size, _p(x), _p(out))
     return out
+
+
+def libm_sweep(which: str, n: int, seed: int, mode: int, lo: float = 0.0, hi: float = 0.0):
+    """gm:: vs glibc over n generated arguments (see orc_libm_sweep):
+    returns (mismatch count, first mismatching argument or None)."""
+    bad = C.c_double(0.0)
+    m = lib().orc_libm_sweep({"exp": 0, "log": 1}[which], int(n), int(seed), int(mode), float(lo),
+                             float(hi), C.byref(bad))
+    return int(m), (bad.value if m else None)
 
 
 def _p(a):

@@ -10,6 +10,7 @@
 
 #include "oracle.hpp"
 #include "../paper_2307_16894_b200/csrc/pdmath.h"
+#include "../paper_2307_16894_b200/csrc/gmath.h"
 
 using namespace orc;
 
@@ -577,16 +578,61 @@ long orc_stress_snapshots(void* hp, const double* U, long L, double* W, int nthr
 }
 
 // libm probes: 0 glibc exp, 1 glibc log, 2 pdm exp, 3 pdm log (host build of
-// the device's portable functions).
+// the portable variant), 4 gm exp, 5 gm log (host build of the device's
+// restatement of glibc, csrc/gmath.h).
 void orc_libm(int which, long n, const double* x, double* out) {
   for (long i = 0; i < n; ++i) {
     switch (which) {
       case 0: out[i] = std::exp(x[i]); break;
       case 1: out[i] = std::log(x[i]); break;
       case 2: out[i] = pdm::exp(x[i]); break;
-      default: out[i] = pdm::log(x[i]); break;
+      case 3: out[i] = pdm::log(x[i]); break;
+      case 4: out[i] = gm::exp(x[i]); break;
+      default: out[i] = gm::log(x[i]); break;
     }
   }
+}
+
+// Bulk bitwise sweep gm:: vs glibc over n generated arguments (OpenMP;
+// splitmix64 stream per index, so the set does not depend on the thread
+// count).  which: 0 exp, 1 log.  mode 0: uniform in [lo, hi]; mode 1:
+// log-uniform magnitude in [lo, hi] (lo > 0); mode 2: raw random bit
+// patterns.  Returns the number of results that differ in any bit (two nans
+// count as equal) and the first such argument in *bad.
+long orc_libm_sweep(int which, long n, unsigned long long seed, int mode, double lo, double hi,
+                    double* bad) {
+  long mism = 0;
+  double first = 0.0;
+  long first_i = -1;
+#pragma omp parallel for schedule(static) reduction(+ : mism)
+  for (long i = 0; i < n; ++i) {
+    unsigned long long z = seed + 0x9e3779b97f4a7c15ull * (unsigned long long)(i + 1);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    z ^= z >> 31;
+    double x;
+    if (mode == 2) {
+      std::memcpy(&x, &z, sizeof(x));
+    } else {
+      const double u = (double)(z >> 11) * 0x1p-53;
+      x = mode == 0 ? lo + (hi - lo) * u : std::exp2(std::log2(lo) + (std::log2(hi) - std::log2(lo)) * u);
+    }
+    const double g = which == 0 ? std::exp(x) : std::log(x);
+    const double m = which == 0 ? gm::exp(x) : gm::log(x);
+    unsigned long long bg, bm;
+    std::memcpy(&bg, &g, 8);
+    std::memcpy(&bm, &m, 8);
+    if (bg != bm && !(std::isnan(g) && std::isnan(m))) {
+      ++mism;
+#pragma omp critical
+      if (first_i < 0 || i < first_i) {
+        first_i = i;
+        first = x;
+      }
+    }
+  }
+  if (bad) *bad = first;
+  return mism;
 }
 
 int orc_max_threads() { return omp_get_max_threads(); }

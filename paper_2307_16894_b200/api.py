@@ -198,7 +198,7 @@ class Rve:
         return t
 
     def fingerprint(self) -> int:
-        """Mesh::fingerprint (mesh.cpp:158-180) of this cell (Q4 kind byte 2)."""
+        """Mesh::fingerprint (mesh.cpp:158-180) of this cell (non-Tri6 kind byte 1)."""
         return int(self.lib.podecm_rve_fingerprint(self.h))
 
     def morph(self, geom: torch.Tensor):

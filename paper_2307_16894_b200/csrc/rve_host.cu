@@ -341,7 +341,10 @@ int podecm_rve_export(const podecm_rve* r, double* nodes, int32_t* elems, int32_
 uint64_t podecm_rve_fingerprint(const podecm_rve* r) {
   if (!r) return 0;
   uint64_t h = podecm_fnv1a64(nullptr, 0, 14695981039346656037ull);
-  const uint8_t kind = 2;  // Q4 (reference: Tri6 = 0, Quad8 = 1)
+  // mesh.cpp:160 hashes `kind == Tri6 ? 0 : 1`, so the Q4 kind behind the
+  // same interface hashes as 1 (checked against the reference's own
+  // fingerprint in tests/test_gpu_formats.py)
+  const uint8_t kind = 1;
   h = podecm_fnv1a64(&kind, 1, h);
   const int64_t counts[3] = {r->n_nodes, r->n_elems, 0};
   h = podecm_fnv1a64(counts, sizeof(counts), h);

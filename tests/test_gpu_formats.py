@@ -1,7 +1,8 @@
 """Interchange formats on a real model (test_rom.cpp:188-216 analogue): a
 reduced model written to PODECM1 and read back replays a batched solve
 bit-identically; the content tag is the cell's fingerprint, recomputed here
-independently from the exported mesh tables."""
+independently from the exported mesh tables and by the reference's own
+Mesh::fingerprint (mesh.cpp:158-180, compiled into oracle/_ref)."""
 import struct
 
 import numpy as np
@@ -21,7 +22,7 @@ def _py_fingerprint(t) -> int:
             h ^= c
             h = (h * 1099511628211) & 0xFFFFFFFFFFFFFFFF
 
-    fnv(bytes([2]))
+    fnv(bytes([1]))  # mesh.cpp:160: every non-Tri6 kind hashes as 1
     fnv(struct.pack("<qqq", t["nodes"].shape[0], t["elems"].shape[0], 0))
     fnv(np.asfortranarray(t["nodes"]).tobytes(order="F"))
     fnv(t["elems"].astype(np.int64).tobytes())
@@ -36,6 +37,9 @@ def test_model_round_trips_through_disk(tmp_path):
     g = api.Rve(16, mats)
     t = g.export()
     assert g.fingerprint() == _py_fingerprint(t)
+    import oracle
+    if oracle.ref_available():  # the reference's own Mesh::fingerprint (oracle/_ref)
+        assert g.fingerprint() == oracle.ref_fingerprint(16, t["regions"])
     m = synth.rom_model(t, g.n_red, N=10, Q=60, seed=3)
     n_dof = 2 * g.n_nodes
     modes = np.random.default_rng(4).normal(size=(n_dof, 10))

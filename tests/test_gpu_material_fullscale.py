@@ -1,33 +1,22 @@
 """K1 parity over the full config-1 population (2^22 points, the bench's own
-inputs).
+inputs), against the faithful oracle (oracle/material.cpp: material.cpp
+restated, glibc exp/log like the reference) and — when it was built here
+from the reference's own source — oracle/_ref (reference material.cpp
+compiled unchanged): the CUDA kernel must reproduce P, the FD tangent A,
+the updated history and the status BIT FOR BIT.
 
-Two references:
-  * oracle with the device's portable exp/log (liboracle_pdm.so): the CUDA
-    kernel must reproduce it BIT FOR BIT — every other operation is
-    correctly rounded and in the reference's order, so this proves the
-    kernel computes exactly the reference algorithm;
-  * the faithful oracle (glibc exp/log, like the reference): stresses and
-    history within 1e-10, tangents within 1e-9 per point normwise.  The FD
-    tangent divides ulp-level libm differences of P by 2h (SURVEY §0 fact
-    5).  glibc's exp/log are not correctly rounded (~0.06 % of calls differ
-    from the correctly rounded value, max 0.52 ulp) and the device's are
-    within 0.504 ulp, so the two disagree by one ulp in ~0.07 % of calls;
-    amplified by 1/(2h) that puts a handful of the 4.2 M tangents just above
-    1e-9 (1.1e-9 measured).  This is the reference's own libm floor — the
-    same gap separates two CPU builds that differ only in the libm — so the
-    tangent bound is asserted on 99.999 % of points (the BASELINE 1e-9) with
-    the libm floor (2e-9) as the hard maximum, and the count is reported.
-"""
+Every device operation is correctly rounded and in the reference's order
+(--fmad=false; sqrt and '/' are IEEE), and exp/log are csrc/gmath.h, the
+device restatement of the host glibc functions (tests/test_gmath.py,
+tests/test_gpu_gmath.py), so bitwise equality is the criterion: it implies
+the BASELINE tolerances (1e-10 stresses / history, 1e-9 tangents) with no
+libm floor left."""
 import numpy as np
 import pytest
 
 from paper_2307_16894_b200 import synth
 
 pytestmark = pytest.mark.gpu
-
-
-def _rel(G, O):
-    return np.sqrt(((G - O) ** 2).sum(0)) / np.maximum(np.sqrt((O ** 2).sum(0)), 1e-14)
 
 
 def test_config1_full_population(orc):
@@ -38,25 +27,13 @@ def test_config1_full_population(orc):
     g = api.material_batch(torch.from_numpy(F).cuda(), torch.from_numpy(st).cuda(), mats)
     G = {k: g[k].cpu().numpy() for k in ("P", "A", "st", "status")}
     del g
-    # 1) algorithmic identity: bit for bit against the same-libm oracle
-    o = orc.material_batch(F, st, mats, libm="pdm")
-    assert np.array_equal(G["status"], o["status"])
-    for k in ("P", "A", "st"):
-        assert np.array_equal(G[k].view(np.int64), o[k].view(np.int64)), k
-    del o
-    # 2) faithful (glibc) oracle: BASELINE tolerances
     o = orc.material_batch(F, st, mats)
     assert np.array_equal(G["status"], o["status"])
-    ok = o["status"] == 0
-    out = {}
-    n_above = 0
-    for k, tol in (("P", 1e-10), ("st", 1e-10), ("A", 1e-9)):
-        rel = _rel(G[k][:, ok], o[k][:, ok])
-        out[k] = (rel.max(), np.quantile(rel, 0.99999), float(np.mean(rel == 0)))
-        if k == "A":
-            n_above = int((rel > 1e-9).sum())
-    print({k: f"max {v[0]:.3e} p99.999 {v[1]:.3e} bitwise {v[2]:.4f}" for k, v in out.items()},
-          f"tangents above 1e-9: {n_above} of {int(ok.sum())}")
-    assert out["P"][0] <= 1e-10 and out["st"][0] <= 1e-10
-    assert out["A"][1] <= 1e-9 and out["A"][0] <= 2e-9
-    assert n_above <= 1e-5 * ok.sum()
+    for k in ("P", "A", "st"):
+        ndiff = int((G[k].view(np.int64) != o[k].view(np.int64)).any(0).sum())
+        print(f"{k}: {ndiff} of {F.shape[1]} points differ from the glibc oracle")
+        assert ndiff == 0, k
+    if orc.ref_available():
+        r = orc.ref_material_batch(F, st, mats[0])
+        for k in ("P", "A", "st"):
+            assert np.array_equal(G[k].view(np.int64), r[k].view(np.int64)), ("oracle/_ref", k)
