@@ -75,9 +75,10 @@ def _J_cols(H, W, q, vol):
     return J
 
 
-def ecm_select(H, W, wq, eps, volume_row=True, max_points=0, stop_at_count=False, trace=None):
+def ecm_select(H, W, wq, eps, volume_row=True, max_points=0, stop_at_count=False, trace=None, stats=None):
     """ecm_select (ecm.cpp:132-204) with restore_feasible (:56-90).
-    Returns (ids ascending, weights, residual_rel, iterations)."""
+    Returns (ids ascending, weights, residual_rel, iterations).  ``stats``
+    (a dict) receives the number of restore_feasible weight drops."""
     nq, N, _ = H.shape
     L = W.shape[0]
     vol = 1 if volume_row else 0
@@ -139,6 +140,9 @@ def ecm_select(H, W, wq, eps, volume_row=True, max_points=0, stop_at_count=False
             x = x + alpha * (z - x)
             zero_tol = 1e-12 * max(np.abs(x).max(), 1e-30)
             keep = x > zero_tol
+            if stats is not None:
+                stats["drops"] = stats.get("drops", 0) + int((~keep).sum())
+                stats["drop_iters"] = stats.get("drop_iters", []) + [iters]
             selected = [s for s, kp in zip(selected, keep) if kp]
             x = x[keep]
         iters += 1

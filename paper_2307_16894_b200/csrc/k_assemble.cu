@@ -597,7 +597,9 @@ int assemble_impl(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst, 
   if ((!geom && !morph) || !f || (!field && (!fbar || !w_red || !st0)))
     return set_err(ctx, PODECM_ECONFIG, "geom|morph, fbar, w_red, st0 and f are required");
   auto s = static_cast<cudaStream_t>(stream);
-  static const bool exact_env = [] {
+  // exact triplet-order mode, read per call (tests/test_gpu_assembly.py runs
+  // both modes in one process)
+  const bool exact_env = [] {
     const char* e = getenv("PODECM_ASM_EXACT");
     return e && atoi(e) != 0;
   }();

@@ -633,7 +633,9 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
                       const double* W, int64_t L, const podecm_ecm_opts* opts, int32_t* ids,
                       double* weights, int* n_sel, double* resid_rel, int* iterations) {
   if (!ctx || !rve || !H || !W || !opts || !ids || !weights || !n_sel) return PODECM_ECONFIG;
-  static const bool gram_env = [] {
+  // scoring mode, read per call: Gram-updated (default) or PODECM_ECM_SCORE=
+  // direct (a J^T r DMMA pass every iteration)
+  const bool gram_env = [] {
     const char* e = getenv("PODECM_ECM_SCORE");
     return !(e && !strcmp(e, "direct"));
   }();
@@ -682,12 +684,7 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
   alloc(&pss, n_rb);
   alloc(&pmx, n_rb);
   alloc(&unav, nq);
-  // Gram-updated scoring (default; PODECM_ECM_SCORE=direct runs a J^T r DMMA
-  // pass every iteration instead)
-  static const bool gram = [] {
-    const char* e = getenv("PODECM_ECM_SCORE");
-    return !(e && !strcmp(e, "direct"));
-  }();
+  const bool gram = gram_env;
   double *c0 = nullptr, *Gsel = nullptr, *gpart = nullptr;
   const int n_cta_g = grid_for(nq, 256);
   if (gram) {

@@ -168,3 +168,20 @@ def test_failed_instance_is_isolated(pair64):
     for s in (0, 2):
         assert np.linalg.norm(rg["f"][s] - ro["f"][s]) <= 1e-10 * np.linalg.norm(ro["f"][s])
         assert np.linalg.norm(rg["K"][s] - ro["K"][s]) <= 1e-9 * np.linalg.norm(ro["K"][s])
+
+
+@pytest.mark.parametrize("n_inst", [1, 3])
+def test_exact_order_mode_bitwise(pair64, monkeypatch, n_inst):
+    """PODECM_ASM_EXACT=1: every qp's 64 K-terms and 8 f-terms in the
+    reference's expression order, each CSR slot and residual row summed in
+    setFromTriplets' order (microfem.cpp:76-128) — with the bitwise material
+    (glibc exp/log on the device) the whole assembly equals the oracle BIT FOR
+    BIT: f, K values, stresses and history (config 0)."""
+    g, o = pair64
+    monkeypatch.setenv("PODECM_ASM_EXACT", "1")
+    rg, ro = _assemble_both(g, o, n_inst, 2026 + n_inst, 0.1, geom_range=(0.15, 0.35) if n_inst > 1 else None)
+    assert np.array_equal(rg["status"], ro["status"])
+    for k, ko in (("f", "f"), ("K", "K"), ("p_field", "p_field"), ("st1", "st1")):
+        ndiff = int((rg[k].view(np.int64) != ro[ko].view(np.int64)).sum())
+        print(f"exact mode, {k}: {ndiff} of {rg[k].size} values differ")
+        assert ndiff == 0, k
