@@ -620,11 +620,13 @@ int assemble_impl(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst, 
   }();
   int64_t chunk = std::max<int64_t>(1, (chunk_mb << 20) / (int64_t)per_inst);
   chunk = std::min<int64_t>(chunk, n_inst);
-  if (r->scratch_inst < chunk) {
+  // scratch_inst counts BYTES: the two modes have different per-instance
+  // footprints and may alternate on one cell
+  if (r->scratch_inst < (int64_t)per_inst * chunk) {
     cudaFree(r->d_scratch);
     r->d_scratch = nullptr;
     PODECM_CUDA_TRY(ctx, cudaMalloc(&r->d_scratch, per_inst * chunk));
-    r->scratch_inst = chunk;
+    r->scratch_inst = (int64_t)per_inst * chunk;
   }
   if (status && !field) PODECM_CUDA_TRY(ctx, cudaMemsetAsync(status, 0, n_inst * sizeof(int32_t), s));
   for (int64_t i0 = 0; i0 < n_inst; i0 += chunk) {

@@ -34,7 +34,7 @@ struct podecm_rve {
           *d_frow_grp = nullptr, *d_pos = nullptr, *d_gptr_all = nullptr;
   // assembly scratch (per-qp K and f terms of a chunk of instances)
   double* d_scratch = nullptr;
-  int64_t scratch_inst = 0;
+  int64_t scratch_inst = 0;  // bytes of d_scratch
 };
 
 namespace podecm_dev {
