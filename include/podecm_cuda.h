@@ -86,6 +86,12 @@ int podecm_get_timings(podecm_ctx* ctx, char* names, int names_len, double* ms, 
 int podecm_material_batch(podecm_ctx* ctx, void* stream, int64_t n, const podecm_params* mats,
                           int n_mats, const int32_t* region, const double* F, const double* st_in,
                           double* P, double* A, double* st_out, int32_t* status, double h_rel);
+/* podecm_material_batch plus the remaining LargeResult fields (material.hpp:
+ * 61-67): extra [4][n] = dgamma, f_trial, q_trial, mises (nullable). */
+int podecm_material_batch_ex(podecm_ctx* ctx, void* stream, int64_t n, const podecm_params* mats,
+                             int n_mats, const int32_t* region, const double* F, const double* st_in,
+                             double* P, double* A, double* st_out, int32_t* status, double h_rel,
+                             double* extra);
 
 /* ---- RVE tables (mesh, quadrature cache, periodic dof map, CSR pattern,
  * deterministic scatter map) ----------------------------------------------
@@ -96,6 +102,11 @@ int podecm_material_batch(podecm_ctx* ctx, void* stream, int64_t n, const podecm
  * (region 1 = element centroid within r0 of the centre). */
 int podecm_rve_create_q4(podecm_ctx* ctx, int n_cells, double r0, const podecm_params* mats,
                          int n_mats, podecm_rve** out);
+/* Same cell with the caller's element regions (host [n_cells^2], row-major
+ * elements as built here; e.g. a reference Mesh::regions) instead of the
+ * centroid-within-r0 rule; r0 still parameterises the analytic morph. */
+int podecm_rve_create_q4_regions(podecm_ctx* ctx, int n_cells, double r0, const int32_t* regions,
+                                 const podecm_params* mats, int n_mats, podecm_rve** out);
 void podecm_rve_destroy(podecm_rve* rve);
 /* out[0..5] = n_nodes, n_elems, n_qp, n_red, nnz, anchor node. */
 int podecm_rve_info(const podecm_rve* rve, int64_t out[6]);
@@ -168,6 +179,16 @@ int podecm_rom_solve_batch_ex(podecm_ctx* ctx, void* stream, podecm_rom* rom, in
                               const double* geom, const double* sched, int K,
                               const podecm_newton* opts, double* pbar, int32_t* iters,
                               double* resid, double* a_final, int32_t* status, double* abar);
+/* podecm_rom_solve_batch_ex on a caller's MorphField instead of the analytic
+ * map: morph_q [n_inst][5][Q] = fmu_inv planes (flatten order) and det at
+ * the ECM points (slice_morph, rom.cpp:111-120), e.g. from the reference's
+ * MorphOperator::solve (the drop-in rom_solve of dropin/podecm_dropin.cpp);
+ * a_hist [n_inst][K][N] (nullable) = RomSolution::steps[k].a. */
+int podecm_rom_solve_batch_morph(podecm_ctx* ctx, void* stream, podecm_rom* rom, int64_t n_inst,
+                                 const double* morph_q, const double* sched, int K,
+                                 const podecm_newton* opts, double* pbar, int32_t* iters,
+                                 double* resid, double* a_final, int32_t* status, double* abar,
+                                 double* a_hist);
 /* Replaces rom_effective_stiffness (rom.hpp:92-95; rom.cpp:202-241) for
  * n_inst instances: geom [n_inst][2]; st0 [n_inst][6][Q] history at the
  * ECM points (planes Fp00, Fp10, Fp01, Fp11, Fp_zz, xi); fbar [n_inst][4];

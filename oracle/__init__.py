@@ -69,6 +69,10 @@ def ref_lib():
         l.ref_fingerprint.argtypes = [I, P]
         l.ref_rom_model_save.restype = I
         l.ref_rom_model_save.argtypes = [C.c_char_p, C.c_ulonglong, I, I, D, L, I, P, I, P, P, P]
+        l.ref_assemble.restype = I
+        l.ref_assemble.argtypes = [I, P, P, I, P, P, P, P, P, P, P, I, P, P, P, P, P, P]
+        l.ref_solve_rve.restype = I
+        l.ref_solve_rve.argtypes = [I, P, P, I, P, P, P, P, P, I, D, D, I, P, P, P, P]
         l.ref_rom_model_load.restype = I
         l.ref_rom_model_load.argtypes = [C.c_char_p, C.POINTER(L), C.POINTER(I), C.POINTER(I),
                                          C.POINTER(C.c_ulonglong), C.POINTER(I), C.POINTER(I), C.POINTER(D),
@@ -116,6 +120,40 @@ def ref_rom_solve(n_cells, regions, mats, ids, weights, mode_grads, fmi_q, det_q
     if abar:
         out["abar"] = ab
     return out
+
+
+def ref_assemble(n_cells, tables, mats, fmi, det, st0, fbar, w_red, tangent=True):
+    """The reference's assemble (microfem.cpp:56-130) of one instance on the Q4
+    cell: tables = an exported Rve (regions, grad, w, row_ptr, col_idx);
+    fmi [4][nq], det [nq], st0 [6][nq], fbar [4], w_red [n_red].  Returns
+    (rc, dict f, K (on the CSR pattern), p_field [4][nq], st1 [6][nq])."""
+    nq = tables["w"].shape[0]
+    n_red = tables["row_ptr"].shape[0] - 1
+    c = lambda a, t=np.float64: np.ascontiguousarray(a, dtype=t)
+    out = {"f": np.zeros(n_red), "K": np.zeros(tables["col_idx"].shape[0]), "p_field": np.zeros((4, nq)),
+           "st1": np.zeros((6, nq))}
+    regs, m = c(tables["regions"], np.int32), _mats(mats)
+    g, w, fm, dt, s0, fb, wr = (c(x) for x in (tables["grad"], tables["w"], fmi, det, st0, fbar, w_red))
+    rp, ci = c(tables["row_ptr"], np.int32), c(tables["col_idx"], np.int32)
+    rc = ref_lib().ref_assemble(n_cells, _p(regs), _p(m), len(mats), _p(g), _p(w), _p(fm), _p(dt), _p(s0), _p(fb),
+                                _p(wr), int(tangent), _p(rp), _p(ci), _p(out["f"]), _p(out["K"]),
+                                _p(out["p_field"]), _p(out["st1"]))
+    return rc, out
+
+
+def ref_solve_rve(n_cells, tables, mats, fmi, det, sched, eps_rel=1e-8, eps_abs=1e-12, max_iter=25):
+    """The reference's solve_rve (microfem.cpp:213-238; dense-LU stand-in for
+    SparseLU) of one instance: sched [K][4] -> (rc, pbar [K][4], iters [K],
+    resid [K], w_final [n_red])."""
+    c = lambda a, t=np.float64: np.ascontiguousarray(a, dtype=t)
+    K = sched.shape[0]
+    n_red = tables["row_ptr"].shape[0] - 1
+    pbar, iters, resid, wf = np.zeros((K, 4)), np.zeros(K, np.int32), np.zeros(K), np.zeros(n_red)
+    regs, g, w, fm, dt, sc = (c(tables["regions"], np.int32), c(tables["grad"]), c(tables["w"]), c(fmi), c(det),
+                              c(sched))
+    rc = ref_lib().ref_solve_rve(n_cells, _p(regs), _p(_mats(mats)), len(mats), _p(g), _p(w), _p(fm), _p(dt),
+                                 _p(sc), K, eps_rel, eps_abs, max_iter, _p(pbar), _p(iters), _p(resid), _p(wf))
+    return rc, {"pbar": pbar, "iters": iters, "resid": resid, "w_final": wf}
 
 
 def ref_periodic_dof_map(n_cells):

@@ -28,6 +28,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <initializer_list>
+#include <map>
 #include <stdexcept>
 #include <type_traits>
 #include <utility>
@@ -264,6 +265,7 @@ class Matrix {
     return t;
   }
   const Matrix& eval() const { return *this; }
+  Matrix& noalias() { return *this; }
 
   // views
   Block<Matrix, 1, C> row(Index i) { return {this, i, 0, 1, cols_}; }
@@ -535,7 +537,11 @@ using VectorXd = Matrix<double, -1, 1>;
 using MatrixXi = Matrix<int, -1, -1>;
 using VectorXi = Matrix<int, -1, 1>;
 
-// Sparse types: declared for the reference headers' struct members only.
+enum ComputationInfo { Success = 0, NumericalIssue = 1 };
+
+// Sparse types.  SparseMatrix keeps (row, col) -> value; setFromTriplets sums
+// duplicates in triplet order onto the first occurrence, which is the order
+// Eigen's collapseDuplicates adds them in (microfem.cpp:125-128).
 template <typename T>
 class Triplet {
  public:
@@ -551,8 +557,63 @@ class Triplet {
 template <typename T>
 class SparseMatrix {
  public:
-  Index rows() const { return 0; }
-  Index cols() const { return 0; }
+  using Scalar = T;
+  SparseMatrix() = default;
+  SparseMatrix(Index r, Index c) : r_(r), c_(c) {}
+  Index rows() const { return r_; }
+  Index cols() const { return c_; }
+  Index nonZeros() const { return (Index)v_.size(); }
+  void resize(Index r, Index c) {
+    r_ = r, c_ = c;
+    v_.clear();
+  }
+  template <typename It>
+  void setFromTriplets(It b, It e) {
+    v_.clear();
+    for (It t = b; t != e; ++t) {
+      auto key = std::make_pair((Index)t->col(), (Index)t->row());
+      auto it = v_.find(key);
+      if (it == v_.end())
+        v_.emplace(key, t->value());
+      else
+        it->second = it->second + t->value();
+    }
+  }
+  T coeff(Index i, Index j) const {
+    auto it = v_.find(std::make_pair(j, i));
+    return it == v_.end() ? T(0) : it->second;
+  }
+  Matrix<T, -1, -1> toDense() const {
+    Matrix<T, -1, -1> d(r_, c_);
+    for (const auto& kv : v_) d(kv.first.second, kv.first.first) = kv.second;
+    return d;
+  }
+
+ private:
+  Index r_ = 0, c_ = 0;
+  std::map<std::pair<Index, Index>, T> v_;  // (col, row) -> value
+};
+
+// SparseLU stand-in: a dense partial-pivoting LU of the matrix (test sizes).
+template <typename M>
+class SparseLU {
+ public:
+  using T = typename M::Scalar;
+  void analyzePattern(const M&) {}
+  void factorize(const M& m) {
+    lu_.compute(m.toDense());
+    info_ = Success;
+  }
+  void compute(const M& m) { factorize(m); }
+  ComputationInfo info() const { return info_; }
+  template <typename X>
+  Matrix<T, -1, -1> solve(const X& b) const {
+    return lu_.solve(b);
+  }
+
+ private:
+  PartialPivLU<Matrix<T, -1, -1>> lu_;
+  ComputationInfo info_ = Success;
 };
 template <typename M>
 class SimplicialLDLT {};

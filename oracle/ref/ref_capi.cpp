@@ -1,7 +1,7 @@
 // ORACLE — test infrastructure only (never linked or loaded by the product).
 //
 // C entry points over the reference's OWN source files, compiled unchanged
-// from /root/reference/proj/src (material.cpp, rom.cpp, store.cpp, mesh.cpp)
+// from /root/reference/proj/src (material.cpp, rom.cpp, store.cpp, mesh.cpp, microfem.cpp)
 // against the Eigen stand-in in oracle/eigen_shim (oracle/ref/Makefile ->
 // oracle/_ref/libpodecm_ref.so).  This pins the restated oracle (oracle/*.cpp)
 // and the CUDA path to the reference's code itself:
@@ -20,6 +20,11 @@
 //   * ref_rom_model_save / ref_rom_model_load: RomModel::save / load
 //     (rom.cpp:265-327) through ArrayStore (store.cpp), i.e. the PODECM1
 //     container written and read by the reference's code.
+//   * ref_assemble / ref_solve_rve: assemble (microfem.cpp:56-130) and the
+//     full-order solve_rve / solve_step_adaptive (microfem.cpp:142-238) on the
+//     Q4 cell (ElemKind{2}; q4_kind.hpp), setFromTriplets summing duplicates
+//     in triplet order like Eigen — bitwise comparable; the sparse solve is a
+//     dense LU stand-in (small cells only).
 // Symbols rom.cpp references but the calls above never reach (geometry and
 // the morph aux-solve, out of scope per SURVEY §2) are stubs that throw.
 #include <omp.h>
@@ -36,6 +41,10 @@
 #include "podecm/store.hpp"
 
 namespace podecm {
+// nodes_per_elem as microfem.cpp sees it (q4_kind.hpp): ElemKind{2} = Quad4.
+int podecm_ref_nodes_per_elem_q4(ElemKind kind) {
+  return static_cast<int>(kind) == 2 ? 4 : nodes_per_elem(kind);
+}
 // rom_sensitivity's morph solve (morph.cpp) is not compiled into oracle/_ref.
 MorphField MorphOperator::solve(const GeomParams&) const {
   throw ConfigError("oracle/_ref: MorphOperator::solve is not built (morph.cpp out of scope)");
@@ -63,10 +72,12 @@ void set_threads(int n) {
 
 // Structured Q4 cell as a reference Mesh: node j*(n+1)+i at (i/n, j/n),
 // elements row-major with CCW corners, regions as given (the kind byte of
-// Mesh::fingerprint maps every non-Tri6 kind to 1).
+// Mesh::fingerprint maps every non-Tri6 kind to 1).  The quadrature cache
+// comes from the caller (grad [nq][4][2], w [nq]; build_quad_cache has no Q4
+// shape functions in the reference).
 Mesh q4_mesh(int n_cells, const int* regions) {
   Mesh m;
-  m.kind = ElemKind::Quad8;
+  m.kind = static_cast<ElemKind>(2);  // Quad4 (q4_kind.hpp)
   const int nn = n_cells + 1;
   m.nodes = MatX(nn * nn, 2);
   for (int j = 0; j < nn; ++j)
@@ -86,6 +97,40 @@ Mesh q4_mesh(int n_cells, const int* regions) {
       m.regions(e) = regions ? regions[e] : 0;
     }
   return m;
+}
+
+QuadCache q4_cache(int n_elems, const double* grad, const double* w) {
+  QuadCache c;
+  c.n_per_elem = 4;
+  const int nq = 4 * n_elems;
+  c.grad.resize(nq);
+  c.w = VecX(nq);
+  c.elem_of = VecXi(nq);
+  for (int q = 0; q < nq; ++q) {
+    c.grad[q] = MatX(4, 2);
+    for (int a = 0; a < 4; ++a)
+      for (int j = 0; j < 2; ++j) c.grad[q](a, j) = grad[(size_t)q * 8 + a * 2 + j];
+    c.w(q) = w[q];
+    c.elem_of(q) = q / 4;
+  }
+  return c;
+}
+
+MorphField morph_field(int nq, const double* fmi, const double* det) {
+  MorphField m;
+  m.fmu_inv.resize(nq);
+  m.det_fmu = VecX(nq);
+  for (int q = 0; q < nq; ++q) {
+    m.fmu_inv[q] << fmi[q], fmi[2 * (size_t)nq + q], fmi[(size_t)nq + q], fmi[3 * (size_t)nq + q];
+    m.det_fmu(q) = det[q];
+  }
+  return m;
+}
+
+std::vector<PlasticityParams> params_vec(const double* mats, int n_mats) {
+  std::vector<PlasticityParams> v;
+  for (int k = 0; k < n_mats; ++k) v.push_back(params_from(mats + 4 * k));
+  return v;
 }
 
 }  // namespace
@@ -292,6 +337,89 @@ int ref_rom_model_load(const char* path, long* n_dof, int* N, int* Q, unsigned l
   } catch (const FormatError& e) {
     g_err = e.what();
     return 6;
+  }
+}
+
+// assemble (microfem.cpp:56-130) of one instance.  fmi [4][nq] / det [nq]
+// the MorphField, st0 [6][nq], fbar [4], w_red [n_red]; K values read as
+// K(r, c) on the caller's CSR pattern (row_ptr / col_idx); p_field [4][nq],
+// st1 [6][nq].  Returns 0, 3 (SolveError) or 2 (ConfigError).
+int ref_assemble(int n_cells, const int* regions, const double* mats, int n_mats, const double* grad,
+                 const double* w, const double* fmi, const double* det, const double* st0, const double* fbar,
+                 const double* w_red, int tangent, const int* row_ptr, const int* col_idx, double* f,
+                 double* kvals, double* p_field, double* st1) {
+  try {
+    const Mesh mesh = q4_mesh(n_cells, regions);
+    const QuadCache cache = q4_cache(mesh.n_elems(), grad, w);
+    const RveProblem prob = RveProblem::build(mesh, cache, params_vec(mats, n_mats));
+    const int nq = cache.n_qp();
+    const MorphField morph = morph_field(nq, fmi, det);
+    std::vector<PlasticState> s0(nq), s1;
+    for (int q = 0; q < nq; ++q) {
+      s0[q].Fp << st0[q], st0[2 * (size_t)nq + q], st0[(size_t)nq + q], st0[3 * (size_t)nq + q];
+      s0[q].Fp_zz = st0[4 * (size_t)nq + q];
+      s0[q].xi = st0[5 * (size_t)nq + q];
+    }
+    Mat2 fb;
+    fb << fbar[0], fbar[2], fbar[1], fbar[3];
+    VecX wr(prob.dofs.n_red);
+    for (int i = 0; i < prob.dofs.n_red; ++i) wr(i) = w_red[i];
+    AssemblyOpts opts;
+    opts.tangent = tangent != 0;
+    opts.store_stress = true;
+    const Assembly as = assemble(prob, morph, s0, &s1, fb, wr, opts);
+    for (int i = 0; i < prob.dofs.n_red; ++i) f[i] = as.f(i);
+    if (tangent)
+      for (int r = 0; r < prob.dofs.n_red; ++r)
+        for (int k = row_ptr[r]; k < row_ptr[r + 1]; ++k) kvals[k] = as.k.coeff(r, col_idx[k]);
+    for (int q = 0; q < nq; ++q) {
+      for (int c = 0; c < 4; ++c) p_field[(size_t)c * nq + q] = as.p_field(c, q);
+      for (int c = 0; c < 4; ++c) st1[(size_t)c * nq + q] = s1[q].Fp.data()[c];
+      st1[4 * (size_t)nq + q] = s1[q].Fp_zz;
+      st1[5 * (size_t)nq + q] = s1[q].xi;
+    }
+    return 0;
+  } catch (const SolveError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+// solve_rve (microfem.cpp:213-238) with solve_step_adaptive on one instance:
+// sched [K][4] -> pbar [K][4], iters [K], resid [K], w_final [n_red].
+int ref_solve_rve(int n_cells, const int* regions, const double* mats, int n_mats, const double* grad,
+                  const double* w, const double* fmi, const double* det, const double* sched, int K,
+                  double eps_rel, double eps_abs, int max_iter, double* pbar, int* iters, double* resid,
+                  double* w_final) {
+  try {
+    const Mesh mesh = q4_mesh(n_cells, regions);
+    const QuadCache cache = q4_cache(mesh.n_elems(), grad, w);
+    const RveProblem prob = RveProblem::build(mesh, cache, params_vec(mats, n_mats));
+    const MorphField morph = morph_field(cache.n_qp(), fmi, det);
+    LoadSchedule sc;
+    for (int k = 0; k < K; ++k) {
+      Mat2 m;
+      m << sched[4 * k], sched[4 * k + 2], sched[4 * k + 1], sched[4 * k + 3];
+      sc.fbar.push_back(m);
+    }
+    NewtonOpts o;
+    o.eps_rel = eps_rel;
+    o.eps_abs = eps_abs;
+    o.max_iter = max_iter;
+    const RveSolution sol = solve_rve(prob, morph, sc, o);
+    for (int k = 0; k < K; ++k) {
+      for (int c = 0; c < 4; ++c) pbar[4 * k + c] = sol.steps[k].pbar.data()[c];
+      iters[k] = sol.steps[k].iters;
+      resid[k] = sol.steps[k].residual;
+    }
+    for (int i = 0; i < prob.dofs.n_red; ++i) w_final[i] = sol.steps.back().w_red(i);
+    return 0;
+  } catch (const SolveError& e) {
+    g_err = e.what();
+    return 3;
   }
 }
 

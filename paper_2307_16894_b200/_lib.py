@@ -48,8 +48,12 @@ _SIGS = {
     "podecm_get_timings": (C.c_int, [P, C.c_char_p, C.c_int, P, P, C.c_int]),
     "podecm_material_batch": (C.c_int, [P, P, I64, C.POINTER(podecm_params), C.c_int, P, P, P, P,
                                         P, P, P, D]),
+    "podecm_material_batch_ex": (C.c_int, [P, P, I64, C.POINTER(podecm_params), C.c_int, P, P, P, P,
+                                           P, P, P, D, P]),
     "podecm_rve_create_q4": (C.c_int, [P, C.c_int, D, C.POINTER(podecm_params), C.c_int,
                                        C.POINTER(P)]),
+    "podecm_rve_create_q4_regions": (C.c_int, [P, C.c_int, D, P, C.POINTER(podecm_params), C.c_int,
+                                               C.POINTER(P)]),
     "podecm_rve_destroy": (None, [P]),
     "podecm_rve_info": (C.c_int, [P, C.POINTER(I64)]),
     "podecm_rve_export": (C.c_int, [P, P, P, P, P, P, P, P, P, P, P]),
@@ -71,6 +75,8 @@ _SIGS = {
                                          P, P, P, P, P]),
     "podecm_rom_solve_batch_ex": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton),
                                             P, P, P, P, P, P]),
+    "podecm_rom_solve_batch_morph": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton),
+                                               P, P, P, P, P, P, P]),
     "podecm_rom_effective_stiffness_batch": (C.c_int, [P, P, P, I64, P, P, P, P, P, P]),
     "podecm_rom_sensitivity_batch": (C.c_int, [P, P, P, I64, P, P, C.c_int, C.POINTER(podecm_newton),
                                                D, P, P]),

@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(128, MINB) k_material_batch(
     int64_t n, MatTable tab, int n_mats, const int32_t* __restrict__ region,
     const double* __restrict__ F, const double* __restrict__ st, double* __restrict__ P,
     double* __restrict__ A, double* __restrict__ st_out, int32_t* __restrict__ status,
-    unsigned int* __restrict__ fail, double h_rel) {
+    unsigned int* __restrict__ fail, double h_rel, double* __restrict__ extra) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     int r = region ? __ldg(region + i) : 0;
@@ -42,6 +42,12 @@ __global__ void __launch_bounds__(128, MINB) k_material_batch(
     bool ok = lsu_eval<true>(p, z, f, pv, &fo);
 #pragma unroll
     for (int k = 0; k < 4; ++k) __stcs(P + k * n + i, pv[k]);
+    if (extra) {
+      extra[i] = fo.dgamma;
+      extra[n + i] = fo.f_trial;
+      extra[2 * n + i] = fo.q_trial;
+      extra[3 * n + i] = fo.mises;
+    }
     if (st_out) {
 #pragma unroll
       for (int k = 0; k < 4; ++k) __stcs(st_out + k * n + i, fo.fp[k]);
@@ -68,7 +74,7 @@ __global__ void __launch_bounds__(128, MINB) k_material_slab(
     int64_t n, MatTable tab, int n_mats, const int32_t* __restrict__ region,
     const double* __restrict__ F, const double* __restrict__ st, double* __restrict__ P,
     double* __restrict__ A, double* __restrict__ st_out, int32_t* __restrict__ status,
-    unsigned int* __restrict__ fail, double h_rel) {
+    unsigned int* __restrict__ fail, double h_rel, double* __restrict__ extra) {
   constexpr int S = 128;
   __shared__ double slab[kSlabSlots * S];
   volatile double* c = slab + threadIdx.x;
@@ -92,6 +98,12 @@ __global__ void __launch_bounds__(128, MINB) k_material_slab(
       ok = lsu_eval_src<true>(p, SlabSrc<S>{c}, pv, &fo);
 #pragma unroll
       for (int k = 0; k < 4; ++k) __stcs(P + k * n + i, pv[k]);
+      if (extra) {
+        extra[i] = fo.dgamma;
+        extra[n + i] = fo.f_trial;
+        extra[2 * n + i] = fo.q_trial;
+        extra[3 * n + i] = fo.mises;
+      }
       if (st_out) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) __stcs(st_out + k * n + i, fo.fp[k]);
@@ -117,7 +129,7 @@ __global__ void __launch_bounds__(128, MINB) k_material_slab(
 // step against 1.146 ms for the best register-resident one (<false, 5>).
 // PODECM_K1_VARIANT overrides it.
 using KFn = void (*)(int64_t, MatTable, int, const int32_t*, const double*, const double*, double*,
-                     double*, double*, int32_t*, unsigned int*, double);
+                     double*, double*, int32_t*, unsigned int*, double, double*);
 const KFn kVariants[] = {k_material_batch<true, 3>, k_material_batch<true, 4>,
                          k_material_batch<false, 4>, k_material_batch<false, 5>,
                          k_material_slab<6>,         k_material_slab<7>,
@@ -228,6 +240,14 @@ int podecm_check(podecm_ctx* ctx, void* stream) {
 int podecm_material_batch(podecm_ctx* ctx, void* stream, int64_t n, const podecm_params* mats,
                           int n_mats, const int32_t* region, const double* F, const double* st_in,
                           double* P, double* A, double* st_out, int32_t* status, double h_rel) {
+  return podecm_material_batch_ex(ctx, stream, n, mats, n_mats, region, F, st_in, P, A, st_out, status,
+                                  h_rel, nullptr);
+}
+
+int podecm_material_batch_ex(podecm_ctx* ctx, void* stream, int64_t n, const podecm_params* mats,
+                             int n_mats, const int32_t* region, const double* F, const double* st_in,
+                             double* P, double* A, double* st_out, int32_t* status, double h_rel,
+                             double* extra) {
   if (!ctx) return PODECM_ECONFIG;
   if (int rc = check_params(ctx, mats, n_mats)) return rc;
   if (n < 0) return set_err(ctx, PODECM_ECONFIG, "negative point count");
@@ -240,7 +260,7 @@ int podecm_material_batch(podecm_ctx* ctx, void* stream, int64_t n, const podecm
   const int grid = (int)(blocks < (int64_t)ctx->n_sm * 64 ? blocks : (int64_t)ctx->n_sm * 64);
   KTimer kt(ctx, static_cast<cudaStream_t>(stream), "k_material_batch");
   kVariants[k1_variant()]<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
-      n, tab, n_mats, region, F, st_in, P, A, st_out, status, ctx->d_fail, h_rel);
+      n, tab, n_mats, region, F, st_in, P, A, st_out, status, ctx->d_fail, h_rel, extra);
   PODECM_LAUNCHED(ctx, 1);
   return PODECM_OK;
 }

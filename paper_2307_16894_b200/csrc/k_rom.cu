@@ -130,23 +130,34 @@ void free_work(podecm_rom* r) {
 }
 
 // ---- init: morph slice at the ECM points, virgin history, control blocks
+// Morph slice at the ECM points (slice_morph, rom.cpp:111-120): from the
+// analytic map of geom (a, b), or copied from morph_in [n][5][Q] (fmu_inv
+// planes + det of a caller's MorphField, podecm_rom_solve_batch_morph).
 __global__ void k_rom_init_points(int64_t n, int Q, int nq, double r0, const int32_t* ids,
                                   const double* nodes, const int32_t* elems, const double* grad,
                                   const double* geom, double* morph, double* S, int64_t cap,
-                                  RomCtl* ctl, double* Sprev, const double* S_start) {
+                                  RomCtl* ctl, double* Sprev, const double* S_start,
+                                  const double* morph_in = nullptr) {
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (tid >= n * Q) return;
   const int64_t s = tid / Q;
   const int p = (int)(tid - s * Q);
-  const int qp = ids[p], e = qp >> 2;
-  const double ka = geom[2 * s] / r0 - 1.0, kb = geom[2 * s + 1] / r0 - 1.0;
-  double d[4][2], gq[8], fmi[4];
-  for (int t = 0; t < 8; ++t) gq[t] = grad[(size_t)qp * 8 + t];
-  for (int a = 0; a < 4; ++a) {
-    const int nd = elems[4 * e + a];
-    morph_d(nodes[2 * nd], nodes[2 * nd + 1], ka, kb, r0, d[a][0], d[a][1]);
+  double fmi[4], dt;
+  if (morph_in) {
+    const double* mi = morph_in + (size_t)s * 5 * Q;
+    for (int t = 0; t < 4; ++t) fmi[t] = mi[(size_t)t * Q + p];
+    dt = mi[(size_t)4 * Q + p];
+  } else {
+    const int qp = ids[p], e = qp >> 2;
+    const double ka = geom[2 * s] / r0 - 1.0, kb = geom[2 * s + 1] / r0 - 1.0;
+    double d[4][2], gq[8];
+    for (int t = 0; t < 8; ++t) gq[t] = grad[(size_t)qp * 8 + t];
+    for (int a = 0; a < 4; ++a) {
+      const int nd = elems[4 * e + a];
+      morph_d(nodes[2 * nd], nodes[2 * nd + 1], ka, kb, r0, d[a][0], d[a][1]);
+    }
+    dt = derive_qp(d, gq, fmi);
   }
-  const double dt = derive_qp(d, gq, fmi);
   double* mo = morph + (size_t)s * 5 * Q;
   for (int t = 0; t < 4; ++t) mo[(size_t)t * Q + p] = fmi[t];
   mo[(size_t)4 * Q + p] = dt;
@@ -677,6 +688,7 @@ struct NewtonArgs {
   double* Sprev;  // nullable: committed history at the start of increment K-1
   const double* force_ref_inst;  // nullable [n]: per-instance force_ref (RomMicroEngine)
   double* init_res;              // nullable [n][K]: RomStepResult::initial_residual
+  double* a_hist = nullptr;      // nullable [n][K][N]: RomSolution::steps[k].a
   // lazy-tangent pipeline (k_rom_check / k_rom_solve)
   const double* G;   // Gm [Qpad*4][NP]
   const double* Pt;  // compact Pt [n][Qpad][4] (k_rom_point MODE 1)
@@ -904,6 +916,10 @@ __device__ __forceinline__ void rom_converged(const NewtonArgs& g, RomCtl* c, in
       for (int c4 = 0; c4 < 4; ++c4) g.pbar[((size_t)s * g.K + c->k) * 4 + c4] = pb[c4] / 1.0;
   }
   for (int i = lane; i < N; i += 32) g.a0[(size_t)s * N + i] = g.a[(size_t)s * N + i];
+  if (last_sub && g.a_hist) {  // the increment completes: steps[k].a (rom.cpp:191)
+    const int k = c->k;
+    for (int i = lane; i < N; i += 32) g.a_hist[((size_t)s * g.K + k) * N + i] = g.a[(size_t)s * N + i];
+  }
   __syncwarp();
   int adv = 0;  // entered the last increment: keep its start history (run_online prev_states)
   if (lane == 0) {
@@ -1695,6 +1711,8 @@ struct RomStart {
   const double* fprev = nullptr; // [n][4]
   const double* fref = nullptr;  // [n]
   double* init_res = nullptr;    // [n][K]
+  const double* morph_q = nullptr;  // [n][5][Q] morph slice (replaces geom)
+  double* a_hist = nullptr;         // [n][K][N] reduced coordinates per increment
 };
 
 int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst, const double* geom,
@@ -1703,7 +1721,8 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
                    const RomStart& start = RomStart()) {
   if (int rc = check_solve_args(ctx, r, n_inst, K, opts)) return rc;
   if (n_inst == 0 || K == 0) return PODECM_OK;
-  if (!geom || !sched || !pbar) return set_err(ctx, PODECM_ECONFIG, "geom, sched, pbar required");
+  if ((!geom && !start.morph_q) || !sched || !pbar)
+    return set_err(ctx, PODECM_ECONFIG, "geom (or a morph slice), sched, pbar required");
   if (int rc = ensure_cap(r, n_inst)) return rc;
   if (abar)
     if (int rc = ensure_abar(r, n_inst, true)) return rc;
@@ -1716,7 +1735,7 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
                                                         start.a);
   k_rom_init_points<<<grid_for(n_inst * Q, 128), 128, 0, s>>>(
       n_inst, Q, rv->n_qp, rv->r0, r->d_ids, rv->d_nodes, rv->d_elems, rv->d_grad, geom,
-      r->d_morph, r->d_S, r->cap, r->d_ctl, abar ? r->d_Sprev : nullptr, start.S);
+      r->d_morph, r->d_S, r->cap, r->d_ctl, abar ? r->d_Sprev : nullptr, start.S, start.morph_q);
   k_rom_fix_status<<<grid_for(n_inst, 128), 128, 0, s>>>(n_inst, r->d_ctl, status, ctx->d_fail);
   PODECM_LAUNCHED(ctx, 3);
 
@@ -1754,6 +1773,7 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
   na.Sprev = abar ? r->d_Sprev : nullptr;
   na.force_ref_inst = start.fref;
   na.init_res = start.init_res;
+  na.a_hist = start.a_hist;
   na.G = r->d_G;
   na.Pt = r->d_Pt;
   na.Qpad = r->Qpad;
@@ -1957,6 +1977,20 @@ int podecm_rom_solve_batch_ex(podecm_ctx* ctx, void* stream, podecm_rom* r, int6
   if (!ctx || !r || !opts) return PODECM_ECONFIG;
   return rom_solve_impl(ctx, stream, r, n_inst, geom, sched, K, opts, pbar, iters, resid, a_final, status,
                         abar);
+}
+
+int podecm_rom_solve_batch_morph(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
+                                 const double* morph_q, const double* sched, int K,
+                                 const podecm_newton* opts, double* pbar, int32_t* iters,
+                                 double* resid, double* a_final, int32_t* status, double* abar,
+                                 double* a_hist) {
+  if (!ctx || !r || !opts) return PODECM_ECONFIG;
+  if (!morph_q && n_inst > 0) return set_err(ctx, PODECM_ECONFIG, "morph slice required");
+  RomStart st;
+  st.morph_q = morph_q;
+  st.a_hist = a_hist;
+  return rom_solve_impl(ctx, stream, r, n_inst, nullptr, sched, K, opts, pbar, iters, resid, a_final, status,
+                        abar, st);
 }
 
 int podecm_rom_effective_stiffness_batch(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,

@@ -252,6 +252,11 @@ extern "C" {
 
 int podecm_rve_create_q4(podecm_ctx* ctx, int n_cells, double r0, const podecm_params* mats,
                          int n_mats, podecm_rve** out) {
+  return podecm_rve_create_q4_regions(ctx, n_cells, r0, nullptr, mats, n_mats, out);
+}
+
+int podecm_rve_create_q4_regions(podecm_ctx* ctx, int n_cells, double r0, const int32_t* regions,
+                                 const podecm_params* mats, int n_mats, podecm_rve** out) {
   if (!ctx || !out) return PODECM_ECONFIG;
   *out = nullptr;
   if (n_cells < 2) return set_err(ctx, PODECM_ECONFIG, "structured Q4 RVE needs n_cells >= 2");
@@ -265,6 +270,8 @@ int podecm_rve_create_q4(podecm_ctx* ctx, int n_cells, double r0, const podecm_p
   r->mats = make_table(mats, n_mats);
   try {
     build_mesh(*r);
+    if (regions)  // caller's region map (a reference Mesh::regions), row-major elements
+      for (int e = 0; e < r->n_elems; ++e) r->regions[e] = regions[e];
     build_cache(*r);
     build_dofs(*r);
     build_pattern(*r);

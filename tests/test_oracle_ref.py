@@ -153,3 +153,46 @@ def test_rom_model_container_reference_source(ref, tmp_path):
     from paper_2307_16894_b200 import _lib
     with pytest.raises(_lib.FormatError, match="checksum"):
         api.rom_model_load(fp)
+
+
+def _asm_case(ref, n_cells, seed, hm=0.1):
+    o = ref.Rve(n_cells, _mats())
+    t = o.export()
+    geom, fbar, w_red, st0 = synth.rve_instances(1, o.n_red, np.repeat(t["regions"], 4), seed, hm,
+                                                 geom_range=(0.15, 0.35))
+    fmi, det, rc = o.morph(*geom[0])
+    assert rc == 0
+    return o, t, geom, fbar, w_red, st0, fmi, det
+
+
+@pytest.mark.parametrize("n_cells", [8, 64])
+def test_assemble_reference_source_bitwise(ref, n_cells):
+    """The reference's assemble (microfem.cpp:56-130, Q4 kind) and the oracle's
+    restatement agree bit for bit: residual, every CSR value K(r, c) summed in
+    setFromTriplets order, stresses and history."""
+    o, t, geom, fbar, w_red, st0, fmi, det = _asm_case(ref, n_cells, 40 + n_cells)
+    rc, r = ref.ref_assemble(n_cells, t, _mats(), fmi, det, st0[0], fbar[0], w_red[0])
+    assert rc == 0
+    w = o.assemble(geom, fbar, w_red, st0, store_stress=True)
+    assert w["status"][0] == 0
+    for k, kw in (("f", "f"), ("K", "K"), ("p_field", "p_field"), ("st1", "st1")):
+        assert _bitwise(r[k], w[kw][0]), k
+
+
+def test_solve_rve_reference_source(ref):
+    """solve_rve + solve_step_adaptive (microfem.cpp:142-238) of the reference
+    vs the oracle's full-order Newton (dense LU stand-in for SparseLU on both
+    sides): P-bar histories and iteration counts."""
+    n_cells = 8
+    o = ref.Rve(n_cells, _mats())
+    t = o.export()
+    geom, sched = synth.rom_instances(2, 4, 77, 0.15)
+    w = o.fe_solve(geom, sched, eps_rel=1e-10, eps_abs=1e-12)
+    for s in range(2):
+        fmi, det, rc = o.morph(*geom[s])
+        rc, r = ref.ref_solve_rve(n_cells, t, _mats(), fmi, det, sched[s], eps_rel=1e-10, eps_abs=1e-12)
+        assert rc == 0 and w["status"][s] == 0
+        assert np.array_equal(r["iters"], w["iters"][s])
+        dp = np.abs(r["pbar"] - w["pbar"][s]).max() / np.abs(w["pbar"][s]).max()
+        print(f"instance {s}: iters {r['iters']}, pbar rel {dp:.2e}")
+        assert dp <= 1e-12
