@@ -60,7 +60,7 @@ def ref_lib():
         l = C.CDLL(str(REF_LIB))
         l.ref_last_error.restype = C.c_char_p
         l.ref_material_batch.restype = L
-        l.ref_material_batch.argtypes = [L, P, P, P, P, P, P, P, D, I]
+        l.ref_material_batch.argtypes = [L, P, P, P, P, P, P, P, D, I, P]
         l.ref_rom_solve.restype = L
         l.ref_rom_solve.argtypes = [I, P, P, I, I, I, P, P, P, L, P, P, P, I, D, D, I, P, P, P, P, P, P, I]
         l.ref_periodic_dof_map.restype = I
@@ -88,10 +88,10 @@ def ref_material_batch(F, st, mat, h_rel=1e-7, nthreads=0):
     st = np.ascontiguousarray(st, dtype=np.float64)
     n = F.shape[1]
     out = {"P": np.full((4, n), np.nan), "A": np.full((16, n), np.nan), "st": np.full((6, n), np.nan),
-           "status": np.empty(n, np.int32)}
+           "status": np.empty(n, np.int32), "extra": np.full((4, n), np.nan)}
     m = np.array([mat.E, mat.nu, mat.sigma_y0, mat.H], dtype=np.float64)
     ref_lib().ref_material_batch(n, _p(m), _p(F), _p(st), _p(out["P"]), _p(out["A"]), _p(out["st"]),
-                                 _p(out["status"]), h_rel, nthreads)
+                                 _p(out["status"]), h_rel, nthreads, _p(out["extra"]))
     return out
 
 
@@ -154,6 +154,74 @@ def ref_solve_rve(n_cells, tables, mats, fmi, det, sched, eps_rel=1e-8, eps_abs=
     rc = ref_lib().ref_solve_rve(n_cells, _p(regs), _p(_mats(mats)), len(mats), _p(g), _p(w), _p(fm), _p(dt),
                                  _p(sc), K, eps_rel, eps_abs, max_iter, _p(pbar), _p(iters), _p(resid), _p(wf))
     return rc, {"pbar": pbar, "iters": iters, "resid": resid, "w_final": wf}
+
+
+DROPIN_LIB = HERE / "_ref" / "libpodecm_dropin.so"
+_dropin = None
+
+
+def dropin_available() -> bool:
+    return DROPIN_LIB.exists()
+
+
+def dropin_lib():
+    """The reference-signature drop-in (paper_2307_16894_b200/dropin) built
+    against the reference's headers, with C test drivers (oracle/ref/
+    dropin_check.cpp).  Runs the product's device path: GPU tests only."""
+    global _dropin
+    if _dropin is None:
+        l = C.CDLL(str(DROPIN_LIB))
+        l.dropin_material.argtypes = [L, P, P, P, P, P, P, P, P, I]
+        l.dropin_assemble.restype = I
+        l.dropin_assemble.argtypes = [I, P, P, I, P, P, P, P, P, P, P, P, P, P, P, P, P]
+        l.dropin_rom_solve.argtypes = [I, P, P, I, P, P, I, I, P, P, P, L, P, P, P, I, D, D, I, P, P, P, P, P, I]
+        _dropin = l
+    return _dropin
+
+
+def dropin_material(F, st, mat, per_call):
+    F = np.ascontiguousarray(F, dtype=np.float64)
+    st = np.ascontiguousarray(st, dtype=np.float64)
+    n = F.shape[1]
+    out = {"P": np.full((4, n), np.nan), "A": np.full((16, n), np.nan), "st": np.full((6, n), np.nan),
+           "extra": np.full((4, n), np.nan), "status": np.empty(n, np.int32)}
+    m = np.array([mat.E, mat.nu, mat.sigma_y0, mat.H], dtype=np.float64)
+    dropin_lib().dropin_material(n, _p(m), _p(F), _p(st), _p(out["P"]), _p(out["A"]), _p(out["st"]),
+                                 _p(out["extra"]), _p(out["status"]), int(per_call))
+    return out
+
+
+def dropin_assemble(n_cells, tables, mats, fmi, det, st0, fbar, w_red):
+    nq = tables["w"].shape[0]
+    n_red = tables["row_ptr"].shape[0] - 1
+    c = lambda a, t=np.float64: np.ascontiguousarray(a, dtype=t)
+    out = {"f": np.zeros(n_red), "K": np.zeros(tables["col_idx"].shape[0]), "p_field": np.zeros((4, nq)),
+           "st1": np.zeros((6, nq))}
+    regs, m = c(tables["regions"], np.int32), _mats(mats)
+    g, w, fm, dt, s0, fb, wr = (c(x) for x in (tables["grad"], tables["w"], fmi, det, st0, fbar, w_red))
+    rp, ci = c(tables["row_ptr"], np.int32), c(tables["col_idx"], np.int32)
+    rc = dropin_lib().dropin_assemble(n_cells, _p(regs), _p(m), len(mats), _p(g), _p(w), _p(fm), _p(dt), _p(s0),
+                                      _p(fb), _p(wr), _p(rp), _p(ci), _p(out["f"]), _p(out["K"]),
+                                      _p(out["p_field"]), _p(out["st1"]))
+    return rc, out
+
+
+def dropin_rom_solve(n_cells, tables, mats, ids, weights, mode_grads, fmi_q, det_q, sched, eps_rel=1e-8,
+                     eps_abs=1e-12, max_iter=25, per_call=True):
+    c = lambda a, t=np.float64: np.ascontiguousarray(a, dtype=t)
+    mg = c(mode_grads)
+    Q, N = mg.shape[0], mg.shape[1]
+    n, K = sched.shape[0], sched.shape[1]
+    out = {"pbar": np.zeros((n, K, 4)), "iters": np.zeros((n, K), np.int32), "resid": np.zeros((n, K)),
+           "a_hist": np.zeros((n, K, N)), "status": np.zeros(n, np.int32)}
+    regs, m = c(tables["regions"], np.int32), _mats(mats)
+    g, w, idc, wt, fm, dt, sc = (c(tables["grad"]), c(tables["w"]), c(ids, np.int32), c(weights), c(fmi_q), c(det_q),
+                                 c(sched))
+    dropin_lib().dropin_rom_solve(n_cells, _p(regs), _p(m), len(mats), _p(g), _p(w), N, Q, _p(idc), _p(wt), _p(mg), n,
+                                  _p(fm), _p(dt), _p(sc), K, eps_rel, eps_abs, max_iter, _p(out["pbar"]),
+                                  _p(out["iters"]), _p(out["resid"]), _p(out["a_hist"]), _p(out["status"]),
+                                  int(per_call))
+    return out
 
 
 def ref_periodic_dof_map(n_cells):

@@ -141,9 +141,10 @@ const char* ref_last_error() { return g_err.c_str(); }
 
 // Per point: F[4][n], st_in[6][n] (Fp00, Fp10, Fp01, Fp11, Fp_zz, xi) ->
 // P[4][n], A[16][n] (Tensor4 storage r + 4c), st_out[6][n], status (0 / 3
-// SolveError; outputs of a failed point are left untouched).
+// SolveError; outputs of a failed point are left untouched), extra[4][n]
+// (nullable: dgamma, f_trial, q_trial, mises).
 long ref_material_batch(long n, const double* mat, const double* F, const double* st_in, double* P,
-                        double* A, double* st_out, int* status, double h_rel, int nthreads) {
+                        double* A, double* st_out, int* status, double h_rel, int nthreads, double* extra) {
   set_threads(nthreads);
   const PlasticityParams p = params_from(mat);
   long fails = 0;
@@ -164,6 +165,12 @@ long ref_material_batch(long n, const double* mat, const double* F, const double
       for (int k = 0; k < 4; ++k) st_out[k * n + i] = s1.Fp.data()[k];
       st_out[4 * n + i] = s1.Fp_zz;
       st_out[5 * n + i] = s1.xi;
+      if (extra) {  // the remaining LargeResult fields (material.hpp:61-67)
+        extra[i] = r.dgamma;
+        extra[n + i] = r.f_trial;
+        extra[2 * n + i] = r.q_trial;
+        extra[3 * n + i] = r.mises;
+      }
       status[i] = 0;
     } catch (const SolveError&) {
       status[i] = 3;
