@@ -152,16 +152,70 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def dist_setup():
+def self_launch(args) -> int | None:
+    """`--gpus N` (N > 1) outside a torch.distributed launcher: re-execute this
+    script under `python -m torch.distributed.run` with one process per GPU
+    (127.0.0.1 rendezvous) and return its exit code; None when already
+    launched (WORLD_SIZE set) or N == 1."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    if args.config != "launch-stub":
+        env.setdefault("NCCL_DEBUG", "INFO")  # communicator lines on stderr
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
+
+
+def dist_setup(cpu_only: bool = False):
+    """One process per GPU: NCCL for device tensors, gloo for host tensors
+    (the ECM greedy's host-side exchanges); gloo only for the CPU stub."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
-        import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if cpu_only:
+            dist.init_process_group("gloo")
+        else:
+            import torch
+            torch.cuda.set_device(local)
+            dist.init_process_group("cuda:nccl,cpu:gloo")
     return ws, rank, local
+
+
+def launch_stub(args, ws, rank):
+    """CPU stand-in step for the launcher test (tests/test_multirank_gloo.py):
+    the bench's barrier / max-over-ranks timing around a small host matmul."""
+    import torch
+    import torch.distributed as dist
+    a = np.random.default_rng(rank).standard_normal((256, 256))
+    for _ in range(args.warmup):
+        a @ a
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        a @ a
+    dt = time.perf_counter() - t0
+    ranks = [rank]
+    if ws > 1:
+        t = torch.tensor([dt], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+        got = [None] * ws
+        dist.all_gather_object(got, rank)
+        ranks = sorted(got)
+    if rank == 0:
+        print(json.dumps({"metric": "launcher stub (host matmuls/s)", "value": ws * args.steps / dt, "unit": "1/s",
+                          "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+                          "higher_is_better": True, "scaling": "weak", "config": {"workload": "launch-stub",
+                                                                                    "ranks_seen": ranks}}))
 
 
 def barrier(ws):
@@ -580,20 +634,36 @@ def run_c4(args, ws, rank, local, ctx, steps, warmup, fp64):
     rve = api.Rve(128, mats, ctx=ctx)
     t = rve.export()
     L, N, Q = args.c4_snap, 50, 400
-    U_t = synth.c4_snapshots(t, L=L, n_terms=20, kmax=8, seed=2030 + rank, xp=torch, device=dev)
+    # one reduction problem; with N > 1 ranks it is split: dof
+    # rows of S for the Gram (all-reduce) and candidates for the greedy
+    # (argmax exchange + column broadcast), i.e. strong scaling of this block
+    U_t = synth.c4_snapshots(t, L=L, n_terms=20, kmax=8, seed=2030, xp=torch, device=dev)
     n_dof = U_t.shape[1]
     opts = api.EcmOpts(eps=1e-6, volume_row=True, max_points=Q, stop_at_count=True)
     res = {}
+    from paper_2307_16894_b200 import shard
+    d0, d1 = shard.shard_range(n_dof, rank, ws)
+    q0, q1 = shard.shard_range(rve.n_qp, rank, ws)
+    U_loc = U_t[:, d0:d1].contiguous() if ws > 1 else U_t
 
     def step():
         res.clear()  # release the previous step's 8.4 GB W first, so the allocator reuses it
         t0 = time.perf_counter()
-        modes_t, ev = api.pod(U_t, N)
+        if ws > 1:
+            modes_t, ev = api.pod_sharded(U_loc, N)
+        else:
+            modes_t, ev = api.pod(U_t, N)
         W, st = api.ecm_stress_snapshots(rve, U_t)
         H = api.ecm_mode_grads(rve, modes_t)
+        if ws > 1:
+            W = W[:, q0:q1].contiguous()
+            H = H[q0:q1].contiguous()
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        ids, w, rel, it = api.ecm_select(rve, H, W, opts)
+        if ws > 1:
+            ids, w, rel, it = api.ecm_select_sharded(rve, H, W, q0, opts)
+        else:
+            ids, w, rel, it = api.ecm_select(rve, H, W, opts)
         torch.cuda.synchronize()
         t2 = time.perf_counter()
         res.update(ids=ids, w=w, rel=rel, it=it, pod_s=t1 - t0, ecm_s=t2 - t1, ev=ev[:N].cpu().numpy(),
@@ -612,6 +682,8 @@ def run_c4(args, ws, rank, local, ctx, steps, warmup, fp64):
     ks = tk.get("k_ecm_score", (0.0, 1))
     score_flop = 2.0 * 56 * L * 4 * rve.n_qp  # padded tile rows x L x 4 nqp per iteration
     out = {"n_dof": n_dof, "snapshots": L, "modes": N, "candidates": rve.n_qp, "selected": int(len(res["ids"])),
+           "split": (f"{ws} ranks: dof rows of S (Gram all-reduce) and candidates (argmax exchange + column "
+                     "broadcast); strong scaling of one reduction") if ws > 1 else "single GPU",
            "ms_per_step": ms / steps, "pod_stage_s": round(res["pod_s"], 4), "ecm_greedy_s": round(res["ecm_s"], 4),
            "ecm_iterations": res["it"], "ecm_residual_rel": res["rel"],
            "kernels_ms_per_step": {k: round(v[0] / steps, 3) for k, v in tk.items()},
@@ -697,7 +769,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="all", choices=["all", "c1", "c0", "c2", "c3", "c4", "fe2"])
+    ap.add_argument("--config", default="all", choices=["all", "c1", "c0", "c2", "c3", "c4", "fe2", "launch-stub"])
     ap.add_argument("--points", type=int, default=1 << 22)
     ap.add_argument("--c2-inst", type=int, default=1024)
     ap.add_argument("--c3-inst", type=int, default=65536)
@@ -706,8 +778,13 @@ def main():
     args = ap.parse_args()
     if args.impl == "ours":
         args.warmup = max(args.warmup, 3)
-
-    ws, rank, local = dist_setup()
+        rc = self_launch(args)
+        if rc is not None:
+            sys.exit(rc)
+    ws, rank, local = dist_setup(cpu_only=args.config == "launch-stub")
+    if args.config == "launch-stub":
+        launch_stub(args, ws, rank)
+        return
     workload = (f"config1: {args.points} independent plane-strain material points per GPU "
                 "(finite-strain J2 + central-FD consistent tangent + history), matrix material "
                 "E=1 nu=0.3 sigma_y=0.01 H=0.1")

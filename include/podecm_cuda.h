@@ -322,6 +322,17 @@ int podecm_pod_modes(podecm_ctx* ctx, void* stream, const double* S, int64_t n_d
                      double* C, const double* gram_diag, int max_modes, double tol_rel,
                      double* modes, double* evals, int* n_kept);
 
+/* podecm_pod_modes with the MGS pass optional (mgs = 0: modes = S v_i /
+ * sqrt(lambda_i) only).  The row-sharded POD runs it on each
+ * rank's dof rows S_k with the all-reduced Gram sum_k S_k^T S_k, gathers the
+ * rows and runs podecm_pod_mgs on the whole basis. */
+int podecm_pod_modes_ex(podecm_ctx* ctx, void* stream, const double* S, int64_t n_dof, int n_snap,
+                        double* C, const double* gram_diag, int max_modes, double tol_rel,
+                        double* modes, double* evals, int* n_kept, int mgs);
+/* mgs_pass (podkit.cpp:75-86) on k column-major modes (n_dof x k), in the
+ * diag(g) metric (gram_diag nullable = identity).  Synchronises the stream. */
+int podecm_pod_mgs(podecm_ctx* ctx, void* stream, double* modes, int64_t n_dof, int k, const double* gram_diag);
+
 /* EcmOpts (ecm.hpp:28-32) plus stop_at_count: configs 3/4 stop at
  * max_points selected points instead of throwing (documented deviation). */
 typedef struct podecm_ecm_opts {
@@ -349,6 +360,28 @@ int podecm_ecm_stress_snapshots(podecm_ctx* ctx, void* stream, podecm_rve* rve, 
 int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const double* H, int N,
                       const double* W, int64_t L, const podecm_ecm_opts* opts, int32_t* ids,
                       double* weights, int* n_sel, double* resid_rel, int* iterations);
+
+/* Candidate-sharded greedy (ecm.cpp:163-173): this rank holds
+ * the candidates [q0, q0 + nq_local) of the cell (H [nq_local][N][4], W
+ * [L][nq_local][4]); the exchanges run through caller-supplied host
+ * callbacks (e.g. torch.distributed / NCCL), each returning 0 on success:
+ *   allreduce_sum: in place elementwise sum over ranks of n host doubles;
+ *   argmax: in place (score, global index) -> the global best, larger score
+ *           then smaller index (index -1 = no positive score on that rank),
+ *           and the owning rank;
+ *   bcast: in place broadcast of n host doubles from rank root.
+ * Outputs as podecm_ecm_select (global ids), identical on every rank. */
+typedef struct podecm_ecm_comm {
+  void* user;
+  int64_t q0, nq_local;
+  int (*allreduce_sum)(void* user, double* host, int64_t n);
+  int (*argmax)(void* user, double* score, int64_t* index, int* owner);
+  int (*bcast)(void* user, double* host, int64_t n, int root);
+} podecm_ecm_comm;
+int podecm_ecm_select_sharded(podecm_ctx* ctx, void* stream, podecm_rve* rve, const double* H, int N,
+                              const double* W, int64_t L, const podecm_ecm_comm* comm,
+                              const podecm_ecm_opts* opts, int32_t* ids, double* weights, int* n_sel,
+                              double* resid_rel, int* iterations);
 
 /* ---- diagnostics ---------------------------------------------------------
  * FP64 roofline probes (mode 0: DFMA chain, mode 1: mma.sync m8n8k4 f64);

@@ -156,3 +156,91 @@ def ecm_select(H, W, wq, eps, volume_row=True, max_points=0, stop_at_count=False
     weights = x[order]
     rel = 0.0 if rhs_norm == 0.0 else np.linalg.norm(resid) / rhs_norm
     return ids, weights, rel, iters
+
+
+def ecm_select_sharded(H_loc, W_loc, wq, q0, eps, volume_row=True, max_points=0, stop_at_count=False):
+    """The candidate-sharded greedy of the device path (SURVEY §8(e);
+    podecm_ecm_select_sharded) restated for the host: this rank holds
+    candidates [q0, q0 + nq_local) (H_loc [nq_local, N, 4], W_loc
+    [L, nq_local, 4]; wq = all quadrature weights).  rhs = J w summed over the
+    shards, each iteration's local best (score, global index) reduced with
+    the strict-'>' first-index rule (ecm.cpp:164-173), the selected column
+    broadcast from its owner, refit / residual replicated.  Uses the
+    torch.distributed helpers of paper_2307_16894_b200.shard (gloo in the
+    CPU tests); with one rank it is ecm_select."""
+    from paper_2307_16894_b200 import shard
+    nql, N, _ = H_loc.shape
+    nq = wq.shape[0]
+    L = W_loc.shape[0]
+    vol = 1 if volume_row else 0
+    m = N * L + vol
+    part = np.ascontiguousarray(np.einsum("qic,sqc->is", H_loc * wq[q0:q0 + nql, None, None], W_loc).reshape(-1))
+    shard.allreduce_host(part)
+    rhs = np.concatenate([part, [wq.sum()]]) if vol else part
+    rhs_norm = np.linalg.norm(rhs)
+    row_tol = eps * rhs_norm / np.sqrt(float(m))
+    cap = max_points if max_points > 0 else nq
+    col_norm = np.sqrt((_J_cols(H_loc, W_loc, np.arange(nql), vol) ** 2).sum(0)) if nql else np.zeros(0)
+    selected, cols = [], []
+    unavailable = np.zeros(nql, bool)
+    x = np.zeros(0)
+    resid = rhs.copy()
+    iters = 0
+    Wf = W_loc.reshape(L, nql * 4)
+
+    def converged(r):
+        if rhs_norm == 0.0:
+            return True
+        return np.linalg.norm(r) <= eps * rhs_norm and np.abs(r).max() <= row_tol
+
+    while not converged(resid):
+        if len(selected) >= cap:
+            if stop_at_count:
+                break
+            raise RuntimeError("cubature did not reach the requested accuracy within the point budget")
+        loc_s, loc_i = 0.0, -1
+        if nql:
+            T = resid[: N * L].reshape(N, L) @ Wf
+            corr = np.einsum("iqc,qic->q", T.reshape(N, nql, 4), H_loc)
+            if vol:
+                corr = corr + resid[-1]
+            ok = (~unavailable) & (col_norm != 0.0)
+            v = np.where(ok, corr / np.where(col_norm != 0.0, col_norm, 1.0), -np.inf)
+            k = int(np.argmax(v))
+            if v[k] > 0.0:
+                loc_s, loc_i = float(v[k]), q0 + k
+        s, best, owner = shard.argmax_owner(loc_s, loc_i)
+        if best < 0:
+            raise RuntimeError("cubature stalled: no remaining point improves the residual")
+        col = np.zeros(m)
+        if q0 <= best < q0 + nql:
+            unavailable[best - q0] = True
+            col[:] = _J_cols(H_loc, W_loc, np.array([best - q0]), vol)[:, 0]
+        shard.bcast_host(col, owner)
+        selected.append(best)
+        cols.append(col)
+        x = np.concatenate([x, [0.0]])
+        while selected:  # restore_feasible (ecm.cpp:56-90), replicated
+            A = np.stack(cols, 1)
+            z = sla.lstsq(A, rhs, lapack_driver="gelsy")[0]
+            if z.min() > 0.0:
+                x = z
+                break
+            alpha = 1.0
+            for kk in range(len(z)):
+                if z[kk] <= 0.0:
+                    alpha = min(alpha, x[kk] / (x[kk] - z[kk]))
+            x = x + alpha * (z - x)
+            zero_tol = 1e-12 * max(np.abs(x).max(), 1e-30)
+            keep = x > zero_tol
+            selected = [s_ for s_, kp in zip(selected, keep) if kp]
+            cols = [c_ for c_, kp in zip(cols, keep) if kp]
+            x = x[keep]
+        iters += 1
+        resid = rhs.copy()
+        for kk in range(len(selected)):
+            resid -= x[kk] * cols[kk]
+    order = np.argsort(np.array(selected, dtype=np.int64), kind="stable")
+    ids = np.array(selected, dtype=np.int64)[order]
+    rel = 0.0 if rhs_norm == 0.0 else np.linalg.norm(resid) / rhs_norm
+    return ids, x[order], rel, iters

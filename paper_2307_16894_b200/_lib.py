@@ -28,6 +28,16 @@ class podecm_ecm_opts(C.Structure):
     _fields_ = [("eps", D), ("volume_row", I32), ("max_points", I32), ("stop_at_count", I32)]
 
 
+ECM_ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), I64)
+ECM_ARGMAX = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(I64), C.POINTER(C.c_int))
+ECM_BCAST = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), I64, C.c_int)
+
+
+class podecm_ecm_comm(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("q0", I64), ("nq_local", I64), ("allreduce_sum", ECM_ALLREDUCE),
+                ("argmax", ECM_ARGMAX), ("bcast", ECM_BCAST)]
+
+
 class podecm_newton(C.Structure):
     _fields_ = [("eps_rel", D), ("eps_abs", D), ("force_ref", D), ("max_iter", I32),
                 ("max_bisect", I32)]
@@ -65,6 +75,11 @@ _SIGS = {
     "podecm_rom_global_iterations": (I64, [P]),
     "podecm_pod_gram": (C.c_int, [P, P, P, I64, C.c_int, P, P]),
     "podecm_pod_modes": (C.c_int, [P, P, P, I64, C.c_int, P, P, C.c_int, D, P, P, C.POINTER(C.c_int)]),
+    "podecm_pod_modes_ex": (C.c_int, [P, P, P, I64, C.c_int, P, P, C.c_int, D, P, P, C.POINTER(C.c_int),
+                                       C.c_int]),
+    "podecm_pod_mgs": (C.c_int, [P, P, P, I64, C.c_int, P]),
+    "podecm_ecm_select_sharded": (C.c_int, [P, P, P, P, C.c_int, P, I64, P, C.POINTER(podecm_ecm_opts), P, P,
+                                            C.POINTER(C.c_int), C.POINTER(D), C.POINTER(C.c_int)]),
     "podecm_ecm_mode_grads": (C.c_int, [P, P, P, P, C.c_int, P]),
     "podecm_ecm_stress_snapshots": (C.c_int, [P, P, P, P, I64, P, P]),
     "podecm_ecm_select": (C.c_int, [P, P, P, P, C.c_int, P, I64, C.POINTER(podecm_ecm_opts), P, P,

@@ -370,6 +370,58 @@ def pod(S_cm: torch.Tensor, max_modes: int, tol_rel: float = 1e-10, gram_diag=No
     return modes[: kept.value], ev
 
 
+def pod_sharded(S_local: torch.Tensor, max_modes: int, tol_rel: float = 1e-10, ctx: Context | None = None):
+    """Row-sharded pod_diag: ``S_local`` [n_snap, n_local] holds
+    this rank's contiguous dof rows of the snapshot matrix (same layout as
+    pod()).  Local Gram S_k^T S_k on the device, one SUM all-reduce of the
+    n_snap^2 Gram (NCCL), the eigenproblem and S_k v / sqrt(lambda) on every
+    rank, an all-gather of the mode rows and the MGS pass (podkit.cpp:75-86)
+    on the whole basis.  Returns (modes^T [kept, n_dof], eigenvalues), the
+    same on every rank."""
+    import torch.distributed as dist
+    ctx = ctx or Context.default(S_local.device.index or 0)
+    n_snap, n_loc = S_local.shape
+    dev = S_local.device
+    C_ = torch.empty((n_snap, n_snap), dtype=torch.float64, device=dev)
+    rc = ctx.lib.podecm_pod_gram(ctx.h, ctx.stream(), _ptr(S_local), n_loc, n_snap, None, _ptr(C_))
+    _lib.raise_for(rc, ctx.h, "podecm_pod_gram")
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    if world > 1:
+        if "nccl" in str(dist.get_backend()):
+            dist.all_reduce(C_)
+        else:  # host backend (gloo): reduce a host copy
+            h = C_.cpu()
+            dist.all_reduce(h)
+            C_.copy_(h)
+    modes_l = torch.empty((max_modes, n_loc), dtype=torch.float64, device=dev)
+    ev = torch.empty(n_snap, dtype=torch.float64, device=dev)
+    kept = C.c_int()
+    rc = ctx.lib.podecm_pod_modes_ex(ctx.h, ctx.stream(), _ptr(S_local), n_loc, n_snap, _ptr(C_), None, max_modes,
+                                     tol_rel, _ptr(modes_l), _ptr(ev), C.byref(kept), 0)
+    _lib.raise_for(rc, ctx.h, "podecm_pod_modes_ex")
+    k = kept.value
+    if world > 1:
+        sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather_object(sizes, int(n_loc))
+        mx = max(sizes)
+        pad = torch.zeros((k, mx), dtype=torch.float64, device=dev)
+        pad[:, :n_loc] = modes_l[:k]
+        if "nccl" in str(dist.get_backend()):
+            parts = [torch.empty_like(pad) for _ in range(world)]
+            dist.all_gather(parts, pad)
+        else:
+            hp = pad.cpu()
+            hparts = [torch.empty_like(hp) for _ in range(world)]
+            dist.all_gather(hparts, hp)
+            parts = [p.to(dev) for p in hparts]
+        full = torch.cat([p[:, :n] for p, n in zip(parts, sizes)], dim=1).contiguous()
+    else:
+        full = modes_l[:k].contiguous()
+    rc = ctx.lib.podecm_pod_mgs(ctx.h, ctx.stream(), _ptr(full), full.shape[1], k, None)
+    _lib.raise_for(rc, ctx.h, "podecm_pod_mgs")
+    return full, ev
+
+
 @dataclass
 class EcmOpts:
     """EcmOpts (ecm.hpp:28-32) + stop_at_count (configs 3/4 stop at a count)."""
@@ -418,6 +470,32 @@ def ecm_select(rve: Rve, H: torch.Tensor, W: torch.Tensor, opts: EcmOpts):
                                    ids.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p),
                                    C.byref(n), C.byref(rr), C.byref(it))
     _lib.raise_for(rc, rve.ctx.h, "podecm_ecm_select")
+    return ids[: n.value].copy(), w[: n.value].copy(), rr.value, it.value
+
+
+def ecm_select_sharded(rve: Rve, H_local: torch.Tensor, W_local: torch.Tensor, q0: int, opts: EcmOpts):
+    """The greedy of ecm_select over this rank's candidate shard [q0, q0 +
+    nq_local) of the cell: H_local [nq_local, N, 4], W_local
+    [L, nq_local, 4].  The exchanges (rhs all-reduce, per-iteration (score,
+    index) argmax with the first-index rule, the selected column's
+    broadcast) run over torch.distributed; the refit is replicated.  Returns
+    ecm_select's tuple (global ids), the same on every rank."""
+    import numpy as np
+    from . import shard
+    nql, N = H_local.shape[0], H_local.shape[1]
+    L = W_local.shape[0]
+    cap = opts.max_points if opts.max_points > 0 else rve.n_qp
+    ids = np.empty(cap, np.int32)
+    w = np.empty(cap)
+    n = C.c_int()
+    rr = C.c_double()
+    it = C.c_int()
+    oc = opts.c()
+    comm = shard.ecm_comm(q0, nql)
+    rc = rve.lib.podecm_ecm_select_sharded(rve.ctx.h, rve.ctx.stream(), rve.h, _ptr(H_local), N, _ptr(W_local), L,
+                                           C.byref(comm), C.byref(oc), ids.ctypes.data_as(C.c_void_p),
+                                           w.ctypes.data_as(C.c_void_p), C.byref(n), C.byref(rr), C.byref(it))
+    _lib.raise_for(rc, rve.ctx.h, "podecm_ecm_select_sharded")
     return ids[: n.value].copy(), w[: n.value].copy(), rr.value, it.value
 
 

@@ -632,21 +632,43 @@ int podecm_ecm_stress_snapshots(podecm_ctx* ctx, void* stream, podecm_rve* rve, 
 int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const double* H, int N,
                       const double* W, int64_t L, const podecm_ecm_opts* opts, int32_t* ids,
                       double* weights, int* n_sel, double* resid_rel, int* iterations) {
+  return podecm_ecm_select_sharded(ctx, stream, rve, H, N, W, L, nullptr, opts, ids, weights, n_sel, resid_rel,
+                                   iterations);
+}
+
+// The greedy of ecm_select over this rank's candidate shard (comm != NULL;
+// SURVEY §8(e)): rhs = J w summed over the shards, each iteration's local
+// best (score, global index) reduced with the reference's strict-'>' first-
+// index rule, the selected column broadcast from its owner, the refit (QR +
+// restore_feasible) and the residual replicated on every rank.  Every rank
+// takes the same decisions, so the result equals the single-rank greedy's
+// up to the summation order of rhs.  Direct scoring (a J^T r pass over the
+// local candidates per iteration).
+int podecm_ecm_select_sharded(podecm_ctx* ctx, void* stream, podecm_rve* rve, const double* H, int N,
+                              const double* W, int64_t L, const podecm_ecm_comm* comm,
+                              const podecm_ecm_opts* opts, int32_t* ids, double* weights, int* n_sel,
+                              double* resid_rel, int* iterations) {
   if (!ctx || !rve || !H || !W || !opts || !ids || !weights || !n_sel) return PODECM_ECONFIG;
+  if (comm && (!comm->allreduce_sum || !comm->argmax || !comm->bcast || comm->q0 < 0 || comm->nq_local < 0 ||
+               comm->q0 + comm->nq_local > rve->n_qp))
+    return set_err(ctx, PODECM_ECONFIG, "ecm: invalid candidate shard / communicator");
+  const int64_t q0 = comm ? comm->q0 : 0;
   // scoring mode, read per call: Gram-updated (default) or PODECM_ECM_SCORE=
-  // direct (a J^T r DMMA pass every iteration)
+  // direct (a J^T r DMMA pass every iteration); the sharded greedy scores
+  // directly
   const bool gram_env = [] {
     const char* e = getenv("PODECM_ECM_SCORE");
     return !(e && !strcmp(e, "direct"));
-  }();
+  }() && !comm;
   if (N < 1 || N > (gram_env ? 1024 : 56))
     return set_err(ctx, PODECM_ECONFIG, gram_env ? "ecm: need 1 <= N <= 1024 displacement modes"
                                                  : "ecm: the direct scoring mode needs 1 <= N <= 56");
   auto s = static_cast<cudaStream_t>(stream);
-  const int nq = rve->n_qp;
+  const int nq = comm ? (int)comm->nq_local : rve->n_qp;  // candidates of this rank
+  const int nq_all = rve->n_qp;
   const int vol = opts->volume_row ? 1 : 0;
   const int64_t m = (int64_t)N * L + vol;
-  const int cap = opts->max_points > 0 ? std::min(opts->max_points, nq) : nq;
+  const int cap = opts->max_points > 0 ? std::min(opts->max_points, nq_all) : nq_all;
   // device workspaces (J_sel, Q: m x kq; R: kq^2) hold at most kMaxSel columns
   constexpr int kMaxSel = 1024;
   const int kq = std::min(cap, kMaxSel);
@@ -703,7 +725,7 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
   if (!rc) {
     cudaMemsetAsync(unav, 0, nq, s);
     // rhs = J w: Hw[i][(q,c)] = w_q H[q][i][c]; rhs[(i,s)] = sum_k Hw[i][k] W[s][k]
-    k_ecm_hw<<<grid_for((int64_t)nq * N * 4, 256), 256, 0, s>>>(nq, N, H, rve->d_w, Hw);
+    k_ecm_hw<<<grid_for((int64_t)nq * N * 4, 256), 256, 0, s>>>(nq, N, H, rve->d_w + q0, Hw);
     GemmArgs a{};
     a.M = N;
     a.N = L;
@@ -718,10 +740,20 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
     a.c_rs = L;  // rhs[i * L + s]
     a.c_cs = 1;
     dim3 grid((unsigned)((a.N + kGBN - 1) / kGBN), (unsigned)((a.M + kGBM - 1) / kGBM));
-    k_gemm_dmma<<<grid, 128, 0, s>>>(a);
+    if (nq > 0) k_gemm_dmma<<<grid, 128, 0, s>>>(a);
+    else cudaMemsetAsync(rhs, 0, sizeof(double) * N * L, s);
+    if (comm) {  // rhs = sum over the candidate shards
+      std::vector<double> hp((size_t)N * L);
+      cudaMemcpyAsync(hp.data(), rhs, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      if (comm->allreduce_sum(comm->user, hp.data(), (int64_t)hp.size()) != 0)
+        rc = fail(PODECM_ECUDA, "ecm: rhs all-reduce failed");
+      cudaMemcpyAsync(rhs, hp.data(), sizeof(double) * hp.size(), cudaMemcpyHostToDevice, s);
+      cudaStreamSynchronize(s);
+    }
     if (vol) {
       double wsum = 0.0;
-      for (int q = 0; q < nq; ++q) wsum += rve->w[q];
+      for (int q = 0; q < nq_all; ++q) wsum += rve->w[q];
       cudaMemcpyAsync(rhs + m - 1, &wsum, sizeof(double), cudaMemcpyHostToDevice, s);
     }
     k_ecm_colnorm<<<grid_for(nq, 128), 128, 0, s>>>(L, nq, N, H, W, vol, cn);
@@ -811,20 +843,47 @@ int podecm_ecm_select(podecm_ctx* ctx, void* stream, podecm_rve* rve, const doub
     ctx->launches += 2;
     cudaMemcpyAsync(pbest, best_i, sizeof(int), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
-    const int best = *pbest;
-    if (best < 0) {
+    int best = *pbest;  // local index
+    int owner = 0;
+    int64_t gbest = best < 0 ? -1 : q0 + best;
+    if (comm) {  // global best: larger score, then smaller global index
+      double sc = 0.0;
+      if (best >= 0) {
+        cudaMemcpyAsync(pm, best_b, sizeof(double), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        sc = *pm;
+      }
+      if (comm->argmax(comm->user, &sc, &gbest, &owner) != 0) {
+        rc = fail(PODECM_ECUDA, "ecm: argmax exchange failed");
+        break;
+      }
+      best = (gbest >= q0 && gbest < q0 + nq) ? (int)(gbest - q0) : -1;
+    }
+    if (gbest < 0) {
       rc = fail(PODECM_ESOLVE, "cubature stalled: no remaining point improves the residual");
       break;
     }
-    selected.push_back(best);
-    cudaMemcpyAsync(unav + best, pone, 1, cudaMemcpyHostToDevice, s);
+    selected.push_back((int)gbest);
+    if (best >= 0) cudaMemcpyAsync(unav + best, pone, 1, cudaMemcpyHostToDevice, s);
     x.push_back(0.0);
-    // materialise the new column and extend the QR
-    {
+    // materialise the new column (its owner; broadcast to the other shards)
+    // and extend the QR
+    if (best >= 0) {
       KTimer kt(ctx, s, "k_ecm_column");
       k_ecm_column<<<grid_for(m, 256), 256, 0, s>>>(L, nq, N, best, H, W, vol, Jsel + (int64_t)qr.k * m);
+      ctx->launches += 1;
     }
-    ctx->launches += 1;
+    if (comm) {
+      std::vector<double> col(m);
+      if (best >= 0) cudaMemcpyAsync(col.data(), Jsel + (int64_t)qr.k * m, sizeof(double) * m, cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      if (comm->bcast(comm->user, col.data(), m, owner) != 0) {
+        rc = fail(PODECM_ECUDA, "ecm: column broadcast failed");
+        break;
+      }
+      cudaMemcpyAsync(Jsel + (int64_t)qr.k * m, col.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s);
+      cudaStreamSynchronize(s);
+    }
     if (gram) {  // column (J^T J)[:, best] for the scores of the next iterations
       KTimer kt(ctx, s, "k_ecm_gram_col");
       k_ecm_gram_col<<<dim3(n_cta_g, kGramSplit), 256, 0, s>>>(L, nq, N, best, H, W, gpart);

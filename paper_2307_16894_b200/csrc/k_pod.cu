@@ -122,6 +122,29 @@ int podecm_pod_gram(podecm_ctx* ctx, void* stream, const double* S, int64_t n_do
 int podecm_pod_modes(podecm_ctx* ctx, void* stream, const double* S, int64_t n_dof, int n_snap,
                      double* C, const double* gram_diag, int max_modes, double tol_rel,
                      double* modes, double* evals, int* n_kept) {
+  return podecm_pod_modes_ex(ctx, stream, S, n_dof, n_snap, C, gram_diag, max_modes, tol_rel, modes, evals,
+                             n_kept, 1);
+}
+
+int podecm_pod_mgs(podecm_ctx* ctx, void* stream, double* modes, int64_t n_dof, int k, const double* gram_diag) {
+  if (!ctx || !modes || k < 0 || n_dof <= 0) return PODECM_ECONFIG;
+  if (k == 0) return PODECM_OK;
+  auto s = static_cast<cudaStream_t>(stream);
+  double* gm = nullptr;
+  if (gram_diag) PODECM_CUDA_TRY(ctx, cudaMalloc(&gm, sizeof(double) * n_dof * k));
+  {
+    KTimer kt(ctx, s, "k_mgs");
+    k_mgs<<<1, 1024, 0, s>>>(modes, gm, n_dof, k, gram_diag);
+  }
+  PODECM_LAUNCHED(ctx, 1);
+  cudaStreamSynchronize(s);
+  cudaFree(gm);
+  return PODECM_OK;
+}
+
+int podecm_pod_modes_ex(podecm_ctx* ctx, void* stream, const double* S, int64_t n_dof, int n_snap,
+                        double* C, const double* gram_diag, int max_modes, double tol_rel,
+                        double* modes, double* evals, int* n_kept, int mgs) {
   if (!ctx || !S || !C || !modes || !evals || !n_kept) return PODECM_ECONFIG;
   auto s = static_cast<cudaStream_t>(stream);
   cusolverDnHandle_t h = nullptr;
@@ -180,15 +203,9 @@ int podecm_pod_modes(podecm_ctx* ctx, void* stream, const double* S, int64_t n_d
       rc = gemm(ctx, s, a);
       if (!rc) {
         k_scale_cols<<<grid_for(n_dof * keep, 256), 256, 0, s>>>(modes, n_dof, keep, evals);
-        double* gm = nullptr;
-        if (gram_diag) cudaMalloc(&gm, sizeof(double) * n_dof * keep);
-        {
-          KTimer kt(ctx, s, "k_mgs");
-          k_mgs<<<1, 1024, 0, s>>>(modes, gm, n_dof, keep, gram_diag);
-        }
-        PODECM_LAUNCHED(ctx, 2);
+        PODECM_LAUNCHED(ctx, 1);
+        if (mgs) rc = podecm_pod_mgs(ctx, s, modes, n_dof, keep, gram_diag);
         cudaStreamSynchronize(s);
-        cudaFree(gm);
       }
     }
   }
