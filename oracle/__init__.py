@@ -318,7 +318,8 @@ def libm(which: str, x):
     glibc, built for the host)."""
     x = np.ascontiguousarray(x, dtype=np.float64)
     out = np.empty_like(x)
-    code = {"exp": 0, "log": 1, "pdm_exp": 2, "pdm_log": 3, "gm_exp": 4, "gm_log": 5}[which]
+    code = {"exp": 0, "log": 1, "pdm_exp": 2, "pdm_log": 3, "gm_exp": 4, "gm_log": 5, "gm_exp_fast": 6,
+            "gm_log_core": 7}[which]
     lib().orc_libm(code, x.size, _p(x), _p(out))
     return out
 

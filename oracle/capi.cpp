@@ -588,7 +588,9 @@ void orc_libm(int which, long n, const double* x, double* out) {
       case 2: out[i] = pdm::exp(x[i]); break;
       case 3: out[i] = pdm::log(x[i]); break;
       case 4: out[i] = gm::exp(x[i]); break;
-      default: out[i] = gm::log(x[i]); break;
+      case 5: out[i] = gm::log(x[i]); break;
+      case 6: out[i] = gm::exp_fast(x[i]); break;  // the material's fast paths on their domains
+      default: out[i] = gm::log_core(x[i]); break;
     }
   }
 }

@@ -84,19 +84,26 @@ GM_HD double fma_(double a, double b, double c) {
 #endif
 }
 
-GM_HD uint64_t etab(int i) {
+// Table pairs (exp: tail, scale bits; log: invc, logc) as one 16-byte load.
+GM_HD void etab2(int k, uint64_t& tail, uint64_t& sb) {
 #ifdef __CUDA_ARCH__
-  return __ldg(gm_exp_tab + i);
+  const ulonglong2 v = __ldg(reinterpret_cast<const ulonglong2*>(gm_exp_tab) + k);
+  tail = v.x;
+  sb = v.y;
 #else
-  return gm_exp_tab[i];
+  tail = gm_exp_tab[2 * k];
+  sb = gm_exp_tab[2 * k + 1];
 #endif
 }
 
-GM_HD double ltab(int i) {
+GM_HD void ltab2(int i, double& invc, double& logc) {
 #ifdef __CUDA_ARCH__
-  return __ldg(gm_log_tab + i);
+  const double2 v = __ldg(reinterpret_cast<const double2*>(gm_log_tab) + i);
+  invc = v.x;
+  logc = v.y;
 #else
-  return gm_log_tab[i];
+  invc = gm_log_tab[2 * i];
+  logc = gm_log_tab[2 * i + 1];
 #endif
 }
 
@@ -115,9 +122,10 @@ GM_HD void exp_tmp(double x, double& tmp, uint64_t& sbits, uint32_t& ki_lo) {
   kd = kd - gm_ek[kShift];
   double r = fma_(kd, gm_ek[kNegLn2hiN], x);
   r = fma_(kd, gm_ek[kNegLn2loN], r);
-  const int idx = 2 * (int)(ki & 127u);
-  const double tail = from_bits(etab(idx));
-  sbits = etab(idx + 1) + (ki << 45);
+  uint64_t tb, sb;
+  etab2((int)(ki & 127u), tb, sb);
+  const double tail = from_bits(tb);
+  sbits = sb + (ki << 45);
   ki_lo = (uint32_t)ki;
   const double r2 = r * r;
   const double t = r + tail;
@@ -172,14 +180,15 @@ GM_NOINLINE double exp_rare(double x) {
   return y * 0x1p-1022;
 }
 
-// |x| < 512: the main path, or 1 + x below 2^-54 (e.g. the elastic
-// branch's exp(+0)), as one straight-line select.
+// |x| < 512: the main path.  Below 2^-54 glibc returns 1 + x instead, and
+// exp_core gives the same bits there: kd = Shift exactly, so k = 0, r = x,
+// tail = 0, scale = 1, |tmp| = |x| (1 + tiny) < 2^-54 and RN(1 + tmp) =
+// RN(1 + x) = 1 (zeros and subnormals included; tests/test_gmath.py checks
+// exp_core against glibc over the whole tiny range).  So the elastic branch's
+// exp(+0) needs no special path.
 GM_HD bool exp_fast_ok(double x) { return ((uint32_t)(bits(x) >> 52) & 0x7ffu) < 0x408u; }
 
-GM_HD double exp_fast(double x) {
-  const double m = exp_core(x);
-  return ((uint32_t)(bits(x) >> 52) & 0x7ffu) < 0x3c9u ? 1.0 + x : m;
-}
+GM_HD double exp_fast(double x) { return exp_core(x); }
 
 GM_HD double exp(double x) { return exp_main_ok(x) ? exp_core(x) : exp_rare(x); }
 
@@ -202,7 +211,8 @@ GM_HD double log_general(uint64_t ix) {
   const int i = (int)((tmp >> 45) & 127u);
   const int k = (int)((int64_t)tmp >> 52);
   const uint64_t iz = ix - (tmp & 0xfff0000000000000ull);
-  const double invc = ltab(2 * i), logc = ltab(2 * i + 1);
+  double invc, logc;
+  ltab2(i, invc, logc);
   const double z = from_bits(iz);
   const double kd = (double)k;
   const double w = fma_(kd, gm_lk[kLn2hi], logc);
@@ -248,12 +258,14 @@ GM_HD double log_near(double x) {
 }
 
 // Both paths evaluated, one selected (branch-free; x normal positive).
+// glibc returns +0 for x == 1 explicitly (the sign of zero under downward
+// rounding); under round-to-nearest the near-1 path yields +0 there too
+// (r = +0 and every term is a signed zero that sums to +0), so no select.
 GM_HD double log_core(double x) {
   const uint64_t ix = bits(x);
   const double g = log_general(ix);
   const double n = log_near(x);
-  const double v = log_near1(ix) ? n : g;
-  return ix == 0x3ff0000000000000ull ? 0.0 : v;
+  return log_near1(ix) ? n : g;
 }
 
 // Zero, negative, subnormal, inf, nan (e_log.c's special-case block).
@@ -296,13 +308,60 @@ GM_HD void exp_pair(double x0, double x1, double& r0, double& r1) {
 #endif
 }
 
+// Device: both paths in every lane, one selected.  With -DGM_WARP_LOG the
+// near-1 path (24 FP64 instructions, needed for a minority of arguments but
+// by almost every warp) runs once per warp on the warp's near-1 arguments
+// packed into consecutive lanes (ballot ranks; fetched and returned by
+// shuffles) — bit-identical, but measured slower in the material kernel
+// (1.205 against 1.09 ms per config-1 step: the shuffles and ranks sit on
+// the critical path of every evaluation), so it is off by default.
 GM_HD void log_pair(double x0, double x1, double& r0, double& r1) {
 #ifndef __CUDA_ARCH__
   r0 = gm::log(x0);
   r1 = gm::log(x1);
-#else
+#elif !defined(GM_WARP_LOG)
   r0 = log_core(x0);
   r1 = log_core(x1);
+  if (!(log_main_ok(x0) && log_main_ok(x1))) {
+    r0 = gm::log(x0);
+    r1 = gm::log(x1);
+  }
+#else
+  const uint64_t i0 = bits(x0), i1 = bits(x1);
+  r0 = log_general(i0);
+  r1 = log_general(i1);
+  const bool n0 = log_near1(i0), n1 = log_near1(i1);
+  const unsigned act = __activemask();
+  const unsigned b0 = __ballot_sync(act, n0), b1 = __ballot_sync(act, n1);
+  if (b0 | b1) {
+    const int c0 = __popc(b0), c = c0 + __popc(b1);
+    const int nact = __popc(act);
+    if (c <= nact) {
+      unsigned lt;
+      asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+      const bool full = act == 0xffffffffu;
+      const int rank = __popc(act & lt);
+      const int lane = __popc(lt);
+      int src = lane;
+      bool second = false;
+      if (rank < c) {  // this lane evaluates slot `rank` of the packed list
+        second = rank >= c0;
+        src = (int)__fns(second ? b1 : b0, 0, (second ? rank - c0 : rank) + 1);
+      }
+      const double a0 = __shfl_sync(act, x0, src), a1 = __shfl_sync(act, x1, src);
+      const double v = log_near(second ? a1 : a0);
+      const int s0 = __popc(b0 & lt), s1 = c0 + __popc(b1 & lt);
+      const int h0 = full ? s0 : (int)__fns(act, 0, s0 + 1);
+      const int h1 = full ? s1 : (int)__fns(act, 0, s1 + 1);
+      const double v0 = __shfl_sync(act, v, h0 & 31), v1 = __shfl_sync(act, v, h1 & 31);
+      r0 = n0 ? v0 : r0;
+      r1 = n1 ? v1 : r1;
+    } else {
+      const double v0 = log_near(x0), v1 = log_near(x1);
+      r0 = n0 ? v0 : r0;
+      r1 = n1 ? v1 : r1;
+    }
+  }
   if (!(log_main_ok(x0) && log_main_ok(x1))) {
     r0 = gm::log(x0);
     r1 = gm::log(x1);

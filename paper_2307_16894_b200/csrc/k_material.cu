@@ -69,7 +69,10 @@ __global__ void __launch_bounds__(128, MINB) k_material_batch(
 
 // Slab variant: the point's operands sit in a shared-memory slab column
 // (material.cuh, SlabSrc) instead of registers across the 9 evaluations.
-template <int MINB>
+// UNI: one material for every point (no region map, as in config 1): the
+// constants are then kernel-parameter operands at fixed offsets instead of
+// loads at a per-point index.
+template <int MINB, bool UNI = false>
 __global__ void __launch_bounds__(128, MINB) k_material_slab(
     int64_t n, MatTable tab, int n_mats, const int32_t* __restrict__ region,
     const double* __restrict__ F, const double* __restrict__ st, double* __restrict__ P,
@@ -80,9 +83,9 @@ __global__ void __launch_bounds__(128, MINB) k_material_slab(
   volatile double* c = slab + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    int r = region ? __ldg(region + i) : 0;
+    int r = (!UNI && region) ? __ldg(region + i) : 0;
     r = (r < 0 || r >= n_mats) ? 0 : r;
-    const MatConst& p = tab.m[r];
+    const MatConst& p = UNI ? tab.m[0] : tab.m[r];
     {
       double f[4], fp[4];
 #pragma unroll
@@ -134,13 +137,17 @@ const KFn kVariants[] = {k_material_batch<true, 3>, k_material_batch<true, 4>,
                          k_material_batch<false, 4>, k_material_batch<false, 5>,
                          k_material_slab<6>,         k_material_slab<7>,
                          k_material_slab<8>};
+// uniform-material forms of the slab variants 4, 5, 6
+const KFn kUniVariants[] = {k_material_slab<6, true>, k_material_slab<7, true>, k_material_slab<8, true>};
 constexpr int kNVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+
+constexpr int kDefaultVariant = 5;
 
 int k1_variant() {
   static int v = [] {
     const char* e = getenv("PODECM_K1_VARIANT");
-    int x = e ? atoi(e) : 5;
-    return (x >= 0 && x < kNVariants) ? x : 5;
+    int x = e ? atoi(e) : kDefaultVariant;
+    return (x >= 0 && x < kNVariants) ? x : kDefaultVariant;
   }();
   return v;
 }
@@ -259,7 +266,9 @@ int podecm_material_batch_ex(podecm_ctx* ctx, void* stream, int64_t n, const pod
   const int64_t blocks = (n + block - 1) / block;
   const int grid = (int)(blocks < (int64_t)ctx->n_sm * 64 ? blocks : (int64_t)ctx->n_sm * 64);
   KTimer kt(ctx, static_cast<cudaStream_t>(stream), "k_material_batch");
-  kVariants[k1_variant()]<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
+  const int v = k1_variant();
+  const bool uni = (!region || n_mats == 1) && v >= 4 && v <= 6;
+  (uni ? kUniVariants[v - 4] : kVariants[v])<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
       n, tab, n_mats, region, F, st_in, P, A, st_out, status, ctx->d_fail, h_rel, extra);
   PODECM_LAUNCHED(ctx, 1);
   return PODECM_OK;

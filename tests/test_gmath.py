@@ -54,3 +54,22 @@ def test_gm_special_values(orc):
     g = orc.libm("exp", xe)
     m = orc.libm("gm_exp", xe)
     assert np.array_equal(g.view(np.int64), m.view(np.int64))
+
+
+def test_fast_paths_on_their_domains(orc):
+    """The branch-free forms the material kernels call: exp_fast (= exp_core)
+    on |x| < 512 including the tiny range glibc special-cases (|x| < 2^-54,
+    zeros, subnormals), log_core on every normal positive x (both paths and
+    x == 1)."""
+    rng = np.random.default_rng(5)
+    tiny = np.concatenate([np.ldexp(rng.uniform(1, 2, 200000), rng.integers(-1074, -54, 200000)),
+                           [0.0, -0.0, 5e-324, -5e-324, 2.0 ** -55, -(2.0 ** -55), np.nextafter(2.0 ** -54, 0)]])
+    tiny = np.concatenate([tiny, -tiny])
+    xe = np.concatenate([tiny, rng.uniform(-511.9, 511.9, 400000), rng.uniform(-1e-3, 1e-3, 200000)])
+    g, m = orc.libm("exp", xe), orc.libm("gm_exp_fast", xe)
+    assert np.array_equal(g.view(np.int64), m.view(np.int64))
+    xl = np.concatenate([np.ldexp(rng.uniform(1, 2, 400000), rng.integers(-1021, 1023, 400000)),
+                         rng.uniform(0.9, 1.1, 400000), [1.0, np.nextafter(1.0, 0), np.nextafter(1.0, 2),
+                                                         2.2250738585072014e-308, 1.7976931348623157e308]])
+    g, m = orc.libm("log", xl), orc.libm("gm_log_core", xl)
+    assert np.array_equal(g.view(np.int64), m.view(np.int64))
