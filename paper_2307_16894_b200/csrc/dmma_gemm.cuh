@@ -33,15 +33,27 @@ struct GemmArgs {
   int64_t c_rs, c_cs;
   const double* diag;  // nullable, length K
   int sym;
+  // split-K (gridDim.z slices): slice z covers k in [z kslice, (z+1) kslice)
+  // and writes its partial product at C + z zc (kslice 0: no split)
+  int64_t kslice, zc;
 };
 
 // 128 threads = 2x2 warps, warp tile 32x32 (4x4 DMMA tiles).  Internal
 // linkage: every translation unit that launches it gets its own copy.
-static __global__ void __launch_bounds__(128) k_gemm_dmma(GemmArgs g) {
+template <bool SPLIT>
+static __global__ void __launch_bounds__(128) k_gemm_dmma_t(GemmArgs g) {
   __shared__ double sA[2][kGBM][kGLD];
   __shared__ double sB[2][kGBN][kGLD];
   const int bi = blockIdx.y, bj = blockIdx.x;
   if (g.sym && bj < bi) return;
+  if (SPLIT) {  // this CTA's K slice
+    const int64_t k0 = (int64_t)blockIdx.z * g.kslice;
+    g.A += k0 * g.a_cs;
+    g.B += k0 * g.b_rs;
+    if (g.diag) g.diag += k0;
+    g.K = g.K - k0 < g.kslice ? g.K - k0 : g.kslice;
+    g.C += (int64_t)blockIdx.z * g.zc;
+  }
   const int64_t i0 = (int64_t)bi * kGBM, j0 = (int64_t)bj * kGBN;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wm = warp >> 1, wn = warp & 1, gid = lane >> 2, tig = lane & 3;
@@ -106,5 +118,9 @@ static __global__ void __launch_bounds__(128) k_gemm_dmma(GemmArgs g) {
         }
       }
 }
+
+// the plain GEMM and the split-K one (gridDim.z K slices, GemmArgs.kslice)
+#define k_gemm_dmma k_gemm_dmma_t<false>
+#define k_gemm_dmma_split k_gemm_dmma_t<true>
 
 }  // namespace podecm_dev

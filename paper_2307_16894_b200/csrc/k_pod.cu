@@ -5,8 +5,16 @@
 //   1. corr = S^T diag(g) S — symmetric DMMA GEMM (only the upper tile
 //      triangle is computed and mirrored; exactly symmetric, so the
 //      reference's 0.5 (corr + corr^T) is the identity on it);
-//   2. the dense symmetric eigendecomposition — cuSOLVER syevd (library
-//      call), eigenvalues reordered descending;
+//   2. the leading eigenpairs of corr by a hand-written block subspace
+//      iteration (k_pod_eig: DMMA products C X, CholQR2 orthonormalisation
+//      with a one-CTA Cholesky / triangular inverse, Rayleigh-Ritz with a
+//      one-CTA cyclic Jacobi eigensolver on the b x b projection, residual
+//      test ||C x_i - theta_i x_i|| <= 1e-13 lambda_0 on the kept pairs);
+//      block b = 128 for up to 64 requested modes.  Corr of order <= 128 is
+//      diagonalised directly by the Jacobi kernel.  Only the leading b
+//      eigenvalues are computed (evals[b..] = 0; the keep rule below never
+//      reaches them).  cuSOLVER syevd remains behind PODECM_POD_EIG=syevd
+//      as the reference point of tests/test_gpu_pod_ecm.py;
 //   3. keep while lambda > tol^2 lambda_0 and lambda > 0, <= max_modes;
 //      mode_i = S v_i / sqrt(lambda_i) — DMMA GEMM + column division;
 //   4. one modified Gram-Schmidt pass in the diag(g) metric, one CTA with
@@ -15,6 +23,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
@@ -80,6 +90,289 @@ __global__ void __launch_bounds__(1024) k_mgs(double* m, double* gm, int64_t row
   }
 }
 
+// ---- leading eigenpairs of a symmetric matrix (subspace iteration) ------
+constexpr int kEigB = 128;  // block size (SMEM Jacobi / Cholesky bound)
+
+// deterministic start block: X[i + j n] = hash(i, j) in [-1, 1)
+__global__ void k_eig_init(double* X, int64_t n, int b) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * b) return;
+  uint64_t z = 0x9e3779b97f4a7c15ull * (uint64_t)(t + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  X[t] = (double)(z >> 11) * 0x1p-52 - 1.0;
+}
+
+// Upper Cholesky factor R of the b x b Gram G (G = R^T R, column-major in)
+// and its inverse Rinv (upper, column-major out), one CTA of >= b threads,
+// both triangles packed in SMEM (element (i, j), i <= j, at j (j + 1) / 2 +
+// i).  Up-looking: step k, thread j forms G_kj - sum_{m<k} R_mk R_mj, then
+// row k is scaled by R_kk = sqrt(of the diagonal one).  A pivot below
+// 1e-26 max(diag) (a rank-deficient block) gets R = 1 and a zero row.  The
+// inverse runs row by row from the bottom, one thread per column.
+__global__ void __launch_bounds__(128) k_eig_cholinv(const double* G, double* Rinv, int b) {
+  extern __shared__ double sh[];
+  const int np = b * (b + 1) / 2;
+  double* R = sh;        // packed upper
+  double* I = sh + np;   // packed upper inverse
+  __shared__ double dmax;
+  auto ix = [](int i, int j) { return j * (j + 1) / 2 + i; };
+  for (int t = threadIdx.x; t < b * b; t += blockDim.x) {
+    const int i = t % b, j = t / b;
+    if (i <= j) R[ix(i, j)] = G[t];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int k = 0; k < b; ++k) m = fmax(m, R[ix(k, k)]);
+    dmax = m;
+  }
+  __syncthreads();
+  const int j = threadIdx.x;
+  const int cj = j * (j + 1) / 2;  // column j of the packed triangles
+  for (int k = 0; k < b; ++k) {
+    const int ck = k * (k + 1) / 2;
+    double v = 0.0;
+    if (j >= k && j < b) {
+      for (int m = 0; m < k; ++m) v = fma(R[ck + m], R[cj + m], v);
+      v = R[cj + k] - v;
+    }
+    __syncthreads();
+    const double akk = j == k ? v : 0.0;
+    if (j == k) R[ck + k] = akk;  // unscaled diagonal, read back below
+    __syncthreads();
+    const double dk = R[ck + k];
+    const bool ok = dk > 1e-26 * dmax;
+    const double d = ok ? sqrt(dk) : 1.0;
+    if (j > k && j < b) R[cj + k] = ok ? v / d : 0.0;
+    __syncthreads();
+    if (j == k) R[ck + k] = d;
+  }
+  __syncthreads();
+  for (int i = b - 1; i >= 0; --i) {  // row i of R^-1 from the rows below
+    if (j >= i && j < b) {
+      double v = i == j ? 1.0 : 0.0;
+      for (int m = i + 1; m <= j; ++m) v = fma(-R[ix(i, m)], I[cj + m], v);
+      I[cj + i] = v / R[ix(i, i)];
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < b * b; t += blockDim.x) {
+    const int i = t % b, jj = t / b;
+    Rinv[t] = i <= jj ? I[ix(i, jj)] : 0.0;
+  }
+}
+
+// Cyclic Jacobi on the symmetric b x b T (column-major, in SMEM), one CTA:
+// round-robin parallel ordering (b/2 disjoint rotations J_m per round).  A
+// round is one pass: every 2 x 2 block of T on the row pair of rotation m1
+// and the column pair of rotation m2 becomes J_m1^T B J_m2 (blocks are
+// disjoint, so they update in place without a second phase), and W's column
+// pairs rotate.  Sweeps until the off-diagonal Frobenius norm is <= 1e-15
+// ||T||_F (max 30).  Outputs theta [b] and the eigenvectors W [b][b]
+// (column-major) sorted by decreasing theta (ties: lower index first).
+__global__ void __launch_bounds__(1024) k_eig_jacobi(const double* Tin, int b, double* theta, double* W,
+                                                     double* Wtmp) {
+  extern __shared__ double sh[];
+  double* T = sh;                 // [b][b]
+  double* cs = sh + b * b;        // [bb/2][2] rotations of the round
+  int* pr = reinterpret_cast<int*>(cs + b + 2);  // [bb/2][2] pairs
+  __shared__ double red[32];
+  __shared__ double offn, totn;
+  const int bb = b + (b & 1);     // players (a dummy for odd b)
+  const int half = bb / 2;
+  for (int t = threadIdx.x; t < b * b; t += blockDim.x) {
+    T[t] = Tin[t];
+    Wtmp[t] = (t % b) == (t / b) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  auto block_sum2 = [&](double v) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    double s0 = 0.0;
+    for (int k = 0; k < nw; ++k) s0 += red[k];
+    __syncthreads();
+    return s0;
+  };
+  for (int sweep = 0; sweep < 30; ++sweep) {
+    double po = 0.0, pt = 0.0;
+    for (int t = threadIdx.x; t < b * b; t += blockDim.x) {
+      const double v = T[t] * T[t];
+      pt += v;
+      if (t % b != t / b) po += v;
+    }
+    const double so = block_sum2(po), st = block_sum2(pt);
+    if (threadIdx.x == 0) {
+      offn = so;
+      totn = st;
+    }
+    __syncthreads();
+    if (!(offn > 1e-30 * totn)) break;
+    for (int r = 0; r < bb - 1; ++r) {
+      // circle method: player 0 fixed, the others rotate
+      for (int m = threadIdx.x; m < half; m += blockDim.x) {
+        auto player = [&](int k) { return k == 0 ? 0 : 1 + (k - 1 + r) % (bb - 1); };
+        int p = player(m), q = player(bb - 1 - m);
+        if (p > q) {
+          const int x = p;
+          p = q;
+          q = x;
+        }
+        double c = 1.0, sn = 0.0;
+        if (q < b) {
+          const double apq = T[q * b + p];
+          if (apq != 0.0) {
+            const double tau = (T[q * b + q] - T[p * b + p]) / (2.0 * apq);
+            const double tt = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + tt * tt);
+            sn = tt * c;
+          }
+        } else {
+          q = p;  // the dummy's partner: no rotation
+        }
+        pr[2 * m] = p;
+        pr[2 * m + 1] = q;
+        cs[2 * m] = c;
+        cs[2 * m + 1] = sn;
+      }
+      __syncthreads();
+      // T <- J^T T J blockwise: rows (p1, q1) of m1, columns (p2, q2) of m2
+      for (int t = threadIdx.x; t < half * half; t += blockDim.x) {
+        const int m2 = t / half, m1 = t - m2 * half;  // consecutive threads: distinct rows (banks)
+        const int p1 = pr[2 * m1], q1 = pr[2 * m1 + 1], p2 = pr[2 * m2], q2 = pr[2 * m2 + 1];
+        const double c1 = cs[2 * m1], s1 = cs[2 * m1 + 1], c2 = cs[2 * m2], s2 = cs[2 * m2 + 1];
+        if (p1 == q1 && p2 == q2) continue;  // dummy x dummy
+        if (p1 == q1) {  // a single row (the dummy's partner): columns only
+          const double a = T[p2 * b + p1], d = T[q2 * b + p1];
+          T[p2 * b + p1] = c2 * a - s2 * d;
+          T[q2 * b + p1] = s2 * a + c2 * d;
+          continue;
+        }
+        if (p2 == q2) {  // a single column: rows only
+          const double a = T[p2 * b + p1], d = T[p2 * b + q1];
+          T[p2 * b + p1] = c1 * a - s1 * d;
+          T[p2 * b + q1] = s1 * a + c1 * d;
+          continue;
+        }
+        const double a = T[p2 * b + p1], bq = T[q2 * b + p1], cc = T[p2 * b + q1], d = T[q2 * b + q1];
+        // rows: [r_p; r_q] = [c1 -s1; s1 c1] [a bq; cc d]
+        const double ra = c1 * a - s1 * cc, rb = c1 * bq - s1 * d;
+        const double rc = s1 * a + c1 * cc, rd = s1 * bq + c1 * d;
+        // columns: [.. p, .. q] = [x_p x_q] [c2 s2; -s2 c2]
+        T[p2 * b + p1] = c2 * ra - s2 * rb;
+        T[q2 * b + p1] = s2 * ra + c2 * rb;
+        T[p2 * b + q1] = c2 * rc - s2 * rd;
+        T[q2 * b + q1] = s2 * rc + c2 * rd;
+      }
+      for (int t = threadIdx.x; t < half * b; t += blockDim.x) {
+        const int m = t / b, i = t - m * b;
+        const int p = pr[2 * m], q = pr[2 * m + 1];
+        if (p == q) continue;
+        const double c = cs[2 * m], sn = cs[2 * m + 1];
+        const double wp = Wtmp[p * b + i], wq = Wtmp[q * b + i];
+        Wtmp[p * b + i] = c * wp - sn * wq;
+        Wtmp[q * b + i] = sn * wp + c * wq;
+      }
+      __syncthreads();
+    }
+  }
+  // sort by decreasing eigenvalue (rank by counting; ties by index)
+  for (int j = threadIdx.x; j < b; j += blockDim.x) {
+    const double v = T[j * b + j];
+    int rank = 0;
+    for (int k = 0; k < b; ++k) {
+      const double u = T[k * b + k];
+      rank += (u > v || (u == v && k < j)) ? 1 : 0;
+    }
+    theta[rank] = v;
+    for (int i = 0; i < b; ++i) W[(size_t)rank * b + i] = Wtmp[(size_t)j * b + i];
+  }
+}
+
+// Split-K products: slice z of gridDim.z sums k in [z K/nz, (z+1) K/nz) into
+// its own output; k_sum_slices adds the slices in fixed order.
+__global__ void k_sum_slices(const double* part, int64_t m, int nz, double* out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  double v = part[t];
+  for (int z = 1; z < nz; ++z) v += part[(int64_t)z * m + t];
+  out[t] = v;
+}
+
+// column norms of R = Y W - X theta for the first k columns, per column
+// partial sums over row blocks (deterministic fixed-order reduction)
+__global__ void __launch_bounds__(256) k_eig_resid(const double* Y, const double* X, const double* theta,
+                                                   int64_t n, int k, double* out) {
+  __shared__ double red[8];
+  const int j = blockIdx.x;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double r = Y[(size_t)j * n + i] - theta[j] * X[(size_t)j * n + i];
+    s = fma(r, r, s);
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    out[j] = sqrt(t);
+  }
+}
+
+// Right-looking form of mgs_pass (podkit.cpp:75-86): at step j the column
+// m_j (all earlier projections already removed) is normalised in the diag(g)
+// metric and projected out of every later column — the same per-column
+// sequence of operations as the left-looking loop, with the dot products as
+// fixed-order two-stage reductions over row blocks on the whole GPU.
+constexpr int kMgsRB = 256;  // rows per partial-sum block
+__global__ void __launch_bounds__(256) k_mgs_dots(const double* m, const double* g, int64_t rows, int cols, int j,
+                                                  double* part) {
+  // part[(i - j) * nb + blk] = sum over block blk of (g m_j) . m_i, i = j..cols-1
+  __shared__ double red[8];
+  const int blk = blockIdx.x, nb = gridDim.x;
+  const int i = j + blockIdx.y;
+  const int64_t r = (int64_t)blk * kMgsRB + threadIdx.x;
+  double v = 0.0;
+  if (r < rows) {
+    const double mj = m[(int64_t)j * rows + r];
+    v = (g ? g[r] * mj : mj) * m[(int64_t)i * rows + r];
+  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[(int64_t)blockIdx.y * nb + blk] = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_mgs_update(double* m, int64_t rows, int cols, int j, const double* part,
+                                                    int nb) {
+  // one thread per (row, later column): c_i = <g m_j, m_i> / |m_j|, m_i -= c_i m_j / |m_j|
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nc = cols - j;
+  if (t >= rows * nc) return;
+  const int i = j + (int)(t / rows);
+  const int64_t r = t - (int64_t)(i - j) * rows;
+  double nn = 0.0;
+  for (int b = 0; b < nb; ++b) nn += part[b];
+  const double nrm = sqrt(nn);
+  const double mj = m[(int64_t)j * rows + r] / nrm;
+  if (i == j) {
+    m[(int64_t)j * rows + r] = mj;
+    return;
+  }
+  double c = 0.0;
+  for (int b = 0; b < nb; ++b) c += part[(int64_t)(i - j) * nb + b];
+  c = c / nrm;
+  m[(int64_t)i * rows + r] -= c * mj;
+}
+
 int gemm(podecm_ctx* ctx, cudaStream_t s, const GemmArgs& a) {
   dim3 grid((unsigned)((a.N + kGBN - 1) / kGBN), (unsigned)((a.M + kGBM - 1) / kGBM));
   {
@@ -130,63 +423,219 @@ int podecm_pod_mgs(podecm_ctx* ctx, void* stream, double* modes, int64_t n_dof, 
   if (!ctx || !modes || k < 0 || n_dof <= 0) return PODECM_ECONFIG;
   if (k == 0) return PODECM_OK;
   auto s = static_cast<cudaStream_t>(stream);
-  double* gm = nullptr;
-  if (gram_diag) PODECM_CUDA_TRY(ctx, cudaMalloc(&gm, sizeof(double) * n_dof * k));
+  const int nb = (int)((n_dof + kMgsRB - 1) / kMgsRB);
+  double* part = nullptr;
+  PODECM_CUDA_TRY(ctx, cudaMalloc(&part, sizeof(double) * (size_t)nb * k));
   {
     KTimer kt(ctx, s, "k_mgs");
-    k_mgs<<<1, 1024, 0, s>>>(modes, gm, n_dof, k, gram_diag);
+    for (int j = 0; j < k; ++j) {
+      k_mgs_dots<<<dim3(nb, k - j), 256, 0, s>>>(modes, gram_diag, n_dof, k, j, part);
+      k_mgs_update<<<grid_for(n_dof * (k - j), 256), 256, 0, s>>>(modes, n_dof, k, j, part, nb);
+    }
   }
-  PODECM_LAUNCHED(ctx, 1);
+  PODECM_LAUNCHED(ctx, 2 * k);
   cudaStreamSynchronize(s);
-  cudaFree(gm);
+  cudaFree(part);
   return PODECM_OK;
 }
 
-int podecm_pod_modes_ex(podecm_ctx* ctx, void* stream, const double* S, int64_t n_dof, int n_snap,
-                        double* C, const double* gram_diag, int max_modes, double tol_rel,
-                        double* modes, double* evals, int* n_kept, int mgs) {
-  if (!ctx || !S || !C || !modes || !evals || !n_kept) return PODECM_ECONFIG;
-  auto s = static_cast<cudaStream_t>(stream);
+namespace {
+
+// syevd (library) eigenpairs, descending: lam_desc [n], V_desc = C's columns
+// reversed (returned as B pointer/stride for the mode GEMM).
+int eig_syevd(podecm_ctx* ctx, cudaStream_t s, double* C, int n, std::vector<double>& desc) {
   cusolverDnHandle_t h = nullptr;
-  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS)
-    return set_err(ctx, PODECM_ECUDA, "cusolverDnCreate failed");
+  if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) return set_err(ctx, PODECM_ECUDA, "cusolverDnCreate failed");
   cusolverDnSetStream(h, s);
-  double* w = nullptr;
+  double *w = nullptr, *work = nullptr;
   int* info = nullptr;
-  double* work = nullptr;
-  int lwork = 0;
-  int rc = PODECM_OK;
-  PODECM_CUDA_TRY(ctx, cudaMalloc(&w, sizeof(double) * n_snap));
-  PODECM_CUDA_TRY(ctx, cudaMalloc(&info, sizeof(int)));
-  if (cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, n_snap, C,
-                                  n_snap, w, &lwork) != CUSOLVER_STATUS_SUCCESS)
+  int lwork = 0, rc = PODECM_OK;
+  if (cudaMalloc(&w, sizeof(double) * n) != cudaSuccess || cudaMalloc(&info, sizeof(int)) != cudaSuccess)
+    rc = set_err(ctx, PODECM_ECUDA, "syevd allocation");
+  if (!rc && cusolverDnDsyevd_bufferSize(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, n, C, n, w, &lwork) !=
+                 CUSOLVER_STATUS_SUCCESS)
     rc = set_err(ctx, PODECM_ECUDA, "syevd buffer query failed");
   if (!rc && cudaMalloc(&work, sizeof(double) * std::max(lwork, 1)) != cudaSuccess)
     rc = set_err(ctx, PODECM_ECUDA, "syevd workspace");
   if (!rc) {
     KTimer kt(ctx, s, "cusolver_syevd");
-    if (cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, n_snap, C, n_snap, w,
-                         work, lwork, info) != CUSOLVER_STATUS_SUCCESS)
+    if (cusolverDnDsyevd(h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_UPPER, n, C, n, w, work, lwork, info) !=
+        CUSOLVER_STATUS_SUCCESS)
       rc = set_err(ctx, PODECM_ECUDA, "syevd failed");
   }
   int hinfo = 0;
-  std::vector<double> lam(n_snap);
+  std::vector<double> lam(n);
   if (!rc) {
     cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, s);
-    cudaMemcpyAsync(lam.data(), w, sizeof(double) * n_snap, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(lam.data(), w, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     if (hinfo != 0) rc = set_err(ctx, PODECM_ESOLVE, "snapshot eigenproblem failed to converge");
   }
+  desc.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) desc[i] = lam[n - 1 - i];
+  cudaFree(w);
+  cudaFree(info);
+  cudaFree(work);
+  cusolverDnDestroy(h);
+  return rc;
+}
+
+// Leading b eigenpairs of the symmetric n x n C (column-major), hand-written
+// (see the header): V [n][b] column-major, theta [b] descending (host copy).
+int eig_subspace(podecm_ctx* ctx, cudaStream_t s, const double* C, int n, int k_need, double* V,
+                 std::vector<double>& theta, int& b_out) {
+  const int b = std::min(n, kEigB);
+  b_out = b;
+  const size_t smem_j = sizeof(double) * (size_t)b * b + sizeof(double) * b + sizeof(int) * b + 64;
+  const size_t smem_c = sizeof(double) * (size_t)b * (b + 1);
+  static bool attrs = [] {
+    cudaFuncSetAttribute(k_eig_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_eig_cholinv, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return true;
+  }();
+  (void)attrs;
+  int rc = PODECM_OK;
+  double *X = nullptr, *Y = nullptr, *T = nullptr, *W = nullptr, *Wt = nullptr, *th = nullptr, *rn = nullptr;
+  const size_t nb = (size_t)n * b;
+  if (cudaMalloc(&X, sizeof(double) * nb) != cudaSuccess || cudaMalloc(&Y, sizeof(double) * nb) != cudaSuccess ||
+      cudaMalloc(&T, sizeof(double) * b * b) != cudaSuccess || cudaMalloc(&W, sizeof(double) * b * b) != cudaSuccess ||
+      cudaMalloc(&Wt, sizeof(double) * b * b) != cudaSuccess || cudaMalloc(&th, sizeof(double) * b) != cudaSuccess ||
+      cudaMalloc(&rn, sizeof(double) * b) != cudaSuccess)
+    rc = set_err(ctx, PODECM_ECUDA, "pod eig: allocation failed");
+  // split-K partial products (fixed-order sum): enough CTAs for the SMs
+  double* part = nullptr;
+  const int kz_max = 32;
+  if (!rc && cudaMalloc(&part, sizeof(double) * (size_t)kz_max * std::max(nb, (size_t)b * b)) != cudaSuccess)
+    rc = set_err(ctx, PODECM_ECUDA, "pod eig: allocation failed");
+  auto mm = [&](int64_t M, int64_t N, int64_t K, const double* A, int64_t ars, int64_t acs, const double* B,
+                int64_t brs, int64_t bcs, double* Cc, int sym) {
+    KTimer kt(ctx, s, K == n && M == n ? "eig_gemm_CX" : (K == n ? "eig_gemm_XtY" : "eig_gemm_XW"));
+    GemmArgs a{};
+    a.M = M, a.N = N, a.K = K, a.A = A, a.a_rs = ars, a.a_cs = acs, a.B = B, a.b_rs = brs, a.b_cs = bcs;
+    a.C = Cc, a.c_rs = 1, a.c_cs = M, a.sym = sym;
+    const int64_t tiles = ((N + kGBN - 1) / kGBN) * ((M + kGBM - 1) / kGBM);
+    int nz = (int)std::min<int64_t>(kz_max, std::max<int64_t>(1, (4 * ctx->n_sm) / tiles));
+    nz = (int)std::min<int64_t>(nz, std::max<int64_t>(1, K / 128));
+    if (nz > 1) {
+      a.kslice = (K + nz - 1) / nz;
+      a.C = part;
+      a.zc = M * N;
+    }
+    dim3 grid((unsigned)((N + kGBN - 1) / kGBN), (unsigned)((M + kGBM - 1) / kGBM), (unsigned)nz);
+    if (nz > 1)
+      k_gemm_dmma_split<<<grid, 128, 0, s>>>(a);
+    else
+      k_gemm_dmma<<<grid, 128, 0, s>>>(a);
+    ctx->launches += 1;
+    if (nz > 1) {
+      k_sum_slices<<<grid_for(M * N, 256), 256, 0, s>>>(part, M * N, nz, Cc);
+      ctx->launches += 1;
+    }
+  };
+  auto jacobi = [&](const double* Tin) {
+    KTimer kt(ctx, s, "k_eig_jacobi");
+    k_eig_jacobi<<<1, 1024, smem_j, s>>>(Tin, b, th, W, Wt);
+    ctx->launches += 1;
+  };
+  if (!rc && n <= kEigB) {  // small: diagonalise C itself
+    jacobi(C);
+    cudaMemcpyAsync(V, W, sizeof(double) * nb, cudaMemcpyDeviceToDevice, s);
+  } else if (!rc) {
+    k_eig_init<<<grid_for((int64_t)nb, 256), 256, 0, s>>>(X, n, b);
+    ctx->launches += 1;
+    auto cholqr = [&](int passes) {  // X = orth(Y): CholQR (passes = 2: CholQR2)
+      for (int pass = 0; pass < passes; ++pass) {
+        const double* src = pass ? X : Y;
+        mm(b, b, n, src, n, 1, src, 1, n, T, 1);  // G = src^T src
+        {
+          KTimer kt(ctx, s, "k_eig_cholinv");
+          k_eig_cholinv<<<1, 128, smem_c, s>>>(T, W, b);
+        }
+        double* dst = pass ? Y : X;  // ping-pong: Y <- X Rinv on the second pass
+        mm(n, b, b, src, 1, n, W, 1, b, dst, 0);
+      }
+      if (passes == 2) std::swap(X, Y);  // the result of pass 2 sits in Y
+    };
+    // Rayleigh-Ritz (and the convergence test) first after 28 products, then
+    // every 4 (config 4 converges at 32); the basis is CholQR'd between products (cond(C X) <= lambda_0 /
+    // lambda_b, ~340 for config 4) and CholQR2'd right before a Ritz step
+    const int first_rr = 28, every = 4, max_it = 400;
+    bool done = false;
+    for (int it = 1; it <= max_it && !done && !rc; ++it) {
+      mm(n, b, n, C, 1, n, X, 1, n, Y, 0);  // Y = C X
+      if (it >= first_rr && (it - first_rr) % every == 0) {
+        // Rayleigh-Ritz: T = X^T C X (symmetric tiles mirrored), T = W diag(theta) W^T
+        mm(b, b, n, X, n, 1, Y, 1, n, T, 1);
+        jacobi(T);
+        mm(n, b, b, X, 1, n, W, 1, b, V, 0);   // Ritz vectors
+        mm(n, b, b, Y, 1, n, W, 1, b, X, 0);   // C times them
+        k_eig_resid<<<k_need, 256, 0, s>>>(X, V, th, n, k_need, rn);
+        ctx->launches += 1;
+        std::vector<double> hr(k_need), ht(b);
+        cudaMemcpyAsync(hr.data(), rn, sizeof(double) * k_need, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(ht.data(), th, sizeof(double) * b, cudaMemcpyDeviceToHost, s);
+        if (cudaStreamSynchronize(s) != cudaSuccess) rc = set_err(ctx, PODECM_ECUDA, "pod eig failed");
+        double rmax = 0.0;
+        for (double v : hr) rmax = std::max(rmax, v);
+        done = rmax <= 1e-13 * std::max(ht[0], 0.0);
+        if (getenv("PODECM_POD_DEBUG"))
+          fprintf(stderr, "pod eig: it %d  max residual / theta0 %.3e  theta0 %.6e theta[k-1] %.6e\n", it,
+                  rmax / ht[0], ht[0], ht[k_need - 1]);
+        cudaMemcpyAsync(X, V, sizeof(double) * nb, cudaMemcpyDeviceToDevice, s);  // restart from the Ritz basis
+      } else {
+        cholqr((it + 1 >= first_rr && (it + 1 - first_rr) % every == 0) ? 2 : 1);
+      }
+    }
+    if (!done && !rc) rc = set_err(ctx, PODECM_ESOLVE, "snapshot eigenproblem failed to converge");
+  }
+  theta.assign(b, 0.0);
+  if (!rc) {
+    cudaMemcpyAsync(theta.data(), th, sizeof(double) * b, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+  }
+  cudaFree(part);
+  cudaFree(X);
+  cudaFree(Y);
+  cudaFree(T);
+  cudaFree(W);
+  cudaFree(Wt);
+  cudaFree(th);
+  cudaFree(rn);
+  return rc;
+}
+
+}  // namespace
+
+int podecm_pod_modes_ex(podecm_ctx* ctx, void* stream, const double* S, int64_t n_dof, int n_snap,
+                        double* C, const double* gram_diag, int max_modes, double tol_rel,
+                        double* modes, double* evals, int* n_kept, int mgs) {
+  if (!ctx || !S || !C || !modes || !evals || !n_kept) return PODECM_ECONFIG;
+  if (n_snap <= 0 || max_modes < 0) return set_err(ctx, PODECM_ECONFIG, "pod_modes: bad sizes");
+  auto s = static_cast<cudaStream_t>(stream);
+  const bool use_syevd = [] {
+    const char* e = getenv("PODECM_POD_EIG");
+    return e && !strcmp(e, "syevd");
+  }() || (n_snap > kEigB && max_modes > kEigB / 2);  // wide bases: b = 128 is too narrow
+  std::vector<double> desc;
+  double* V = nullptr;  // eigenvectors, descending, column-major [n_snap][>= keep]
+  int64_t v_cs = n_snap;
+  int b = n_snap, rc = PODECM_OK;
+  if (use_syevd) {
+    rc = eig_syevd(ctx, s, C, n_snap, desc);
+  } else {
+    if (cudaMalloc(&V, sizeof(double) * (size_t)n_snap * std::min(n_snap, kEigB)) != cudaSuccess)
+      return set_err(ctx, PODECM_ECUDA, "pod eig: allocation failed");
+    rc = eig_subspace(ctx, s, C, n_snap, std::min(std::max(max_modes, 1), std::min(n_snap, kEigB)), V, desc, b);
+    desc.resize(n_snap, 0.0);  // only the leading b are computed
+  }
   int keep = 0;
   if (!rc) {
-    std::vector<double> desc(n_snap);
-    for (int i = 0; i < n_snap; ++i) desc[i] = lam[n_snap - 1 - i];
     const double lead = std::max(desc[0], 0.0);
     const double cut = tol_rel * tol_rel * lead;
-    while (keep < n_snap && keep < max_modes && desc[keep] > cut && desc[keep] > 0.0) ++keep;
+    while (keep < b && keep < max_modes && desc[keep] > cut && desc[keep] > 0.0) ++keep;
     cudaMemcpyAsync(evals, desc.data(), sizeof(double) * n_snap, cudaMemcpyHostToDevice, s);
     if (keep > 0) {
-      // modes = S * V_desc, V_desc(:, i) = C(:, n_snap-1-i)
+      // modes = S * V_desc
       GemmArgs a{};
       a.M = n_dof;
       a.N = keep;
@@ -194,9 +643,14 @@ int podecm_pod_modes_ex(podecm_ctx* ctx, void* stream, const double* S, int64_t 
       a.A = S;
       a.a_rs = 1;
       a.a_cs = n_dof;
-      a.B = C + (int64_t)(n_snap - 1) * n_snap;
+      if (use_syevd) {  // V_desc(:, i) = C(:, n_snap-1-i)
+        a.B = C + (int64_t)(n_snap - 1) * n_snap;
+        a.b_cs = -(int64_t)n_snap;
+      } else {
+        a.B = V;
+        a.b_cs = v_cs;
+      }
       a.b_rs = 1;
-      a.b_cs = -(int64_t)n_snap;
       a.C = modes;
       a.c_rs = 1;
       a.c_cs = n_dof;
@@ -209,11 +663,9 @@ int podecm_pod_modes_ex(podecm_ctx* ctx, void* stream, const double* S, int64_t 
       }
     }
   }
+  cudaStreamSynchronize(s);
+  cudaFree(V);
   *n_kept = keep;
-  cudaFree(w);
-  cudaFree(info);
-  cudaFree(work);
-  cusolverDnDestroy(h);
   return rc;
 }
 
