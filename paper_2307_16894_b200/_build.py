@@ -41,6 +41,7 @@ def nvcc_flags() -> list[str]:
         "-ccbin", HOST_CXX,
         "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
         "-Xptxas", "-v",
+        *os.environ.get("PODECM_NVCC_DEFS", "").split(),  # A/B builds, e.g. -DPODECM_Q2_UNI=0
     ]
 
 
