@@ -836,20 +836,37 @@ __device__ __forceinline__ void warp_lu_solve_rm(double* A, int N, double* rhs, 
     }
     __syncwarp();
     const double bk = rhs[k];
-    for (int j = k + 1 + lane; j < N; j += 32) {
-      const double u = A[k * N + j];
+    // rank-1 update, lanes over columns: a lane's columns j and j + 32 (the
+    // second exists while N - k > 33) in one pass over 8-row chunks, so up to
+    // 16 independent FMAs are in flight per chunk (same per-element FMA
+    // sequence, bit-identical to a column-by-column loop)
+    for (int j = k + 1 + lane; j < N; j += 64) {
+      const int j2 = j + 32;
+      const bool two = j2 < N;
+      const double u = A[k * N + j], u2 = two ? A[k * N + j2] : 0.0;
       int i = k + 1;
-      for (; i + 3 < N; i += 4) {
-        const double l0 = A[i * N + k], l1 = A[(i + 1) * N + k];
-        const double l2 = A[(i + 2) * N + k], l3 = A[(i + 3) * N + k];
-        const double a0 = A[i * N + j], a1 = A[(i + 1) * N + j];
-        const double a2 = A[(i + 2) * N + j], a3 = A[(i + 3) * N + j];
-        A[i * N + j] = fma(-l0, u, a0);
-        A[(i + 1) * N + j] = fma(-l1, u, a1);
-        A[(i + 2) * N + j] = fma(-l2, u, a2);
-        A[(i + 3) * N + j] = fma(-l3, u, a3);
+      for (; i + 7 < N; i += 8) {
+        double l[8], a[8], b[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) l[r] = A[(i + r) * N + k];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) a[r] = A[(i + r) * N + j];
+        if (two) {
+#pragma unroll
+          for (int r = 0; r < 8; ++r) b[r] = A[(i + r) * N + j2];
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) A[(i + r) * N + j] = fma(-l[r], u, a[r]);
+        if (two) {
+#pragma unroll
+          for (int r = 0; r < 8; ++r) A[(i + r) * N + j2] = fma(-l[r], u2, b[r]);
+        }
       }
-      for (; i < N; ++i) A[i * N + j] = fma(-A[i * N + k], u, A[i * N + j]);
+      for (; i < N; ++i) {
+        const double l = A[i * N + k];
+        A[i * N + j] = fma(-l, u, A[i * N + j]);
+        if (two) A[i * N + j2] = fma(-l, u2, A[i * N + j2]);
+      }
     }
     for (int i = k + 1 + lane; i < N; i += 32) rhs[i] = fma(-A[i * N + k], bk, rhs[i]);
     __syncwarp();
