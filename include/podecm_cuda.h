@@ -165,7 +165,12 @@ int64_t podecm_rom_global_iterations(const podecm_rom* rom);
  *   geom [n_inst][2]; sched [n_inst][K][4] macro F per increment;
  *   outputs pbar [n_inst][K][4] homogenised stress history,
  *   iters [n_inst][K] (nullable), resid [n_inst][K] (nullable),
- *   a_final [n_inst][N] (nullable), status [n_inst] (nullable). */
+ *   a_final [n_inst][N] (nullable), status [n_inst] (nullable).
+ * Default "lazy tangent" order: the FD tangent is not evaluated at an
+ * iterate that already meets the Newton tolerance (the reference computes
+ * and discards it, rom.cpp:132-141), so an FD failure there — which would
+ * make the reference bisect — goes unseen; environment PODECM_ROM_LAZY=0
+ * selects the strict order. */
 int podecm_rom_solve_batch(podecm_ctx* ctx, void* stream, podecm_rom* rom, int64_t n_inst,
                            const double* geom, const double* sched, int K,
                            const podecm_newton* opts, double* pbar, int32_t* iters, double* resid,

@@ -282,7 +282,16 @@ class Rom:
         """Batched rom_solve (rom.cpp:177-200): pbar [n, K, 4] history,
         iters [n, K], resid [n, K], a_final [n, N], status [n].  abar=True adds
         run_online's effective stiffness at the last increment
-        (pipeline.cpp:456-483): abar [n, 16], Tensor4 storage r + 4c."""
+        (pipeline.cpp:456-483): abar [n, 16], Tensor4 storage r + 4c.
+
+        Lazy tangent (default): the reference assembles K with the FD tangent
+        at every Newton check (rom.cpp:132), also at the iterate that then
+        meets the tolerance, and discards it there; this pipeline skips that
+        tangent.  The one observable difference: if an FD evaluation at such a
+        converged iterate hit a non-positive elastic stretch, the reference
+        would fail the attempt and bisect while this pipeline accepts the
+        step.  PODECM_ROM_LAZY=0 selects the strict order (every check with
+        its tangent); tests/test_gpu_rom.py runs the module both ways."""
         opts = opts or NewtonOpts()
         n, K = sched.shape[0], sched.shape[1]
         dev = sched.device

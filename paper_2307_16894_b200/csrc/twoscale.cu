@@ -468,17 +468,27 @@ int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* c
         }
       }
       for (int i = 0; i < n; ++i) res[i] = -res[i];
-      cudaMemcpyAsync(d_con, h_con, sizeof(double) * n_con, cudaMemcpyHostToDevice, s);
-      cudaMemsetAsync(d_K, 0, sizeof(double) * (size_t)n * n, s);
-      k_macro_gather<<<(n_ent + 255) / 256, 256, 0, s>>>(n_ent, d_ent, d_eptr, d_eidx, d_con, d_K);
-      ctx->launches += 1;
-      cudaMemcpyAsync(d_b, res.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s);
-      cusolverDnDgetrf(dn, n, n, d_K, n, d_work, d_piv, d_info);
-      cusolverDnDgetrs(dn, CUBLAS_OP_N, n, 1, d_K, n, d_piv, d_b, n, d_info);
+      // every copy, launch and factorisation is checked (an error ends the
+      // run with PODECM_ECUDA after the common cleanup)
+      auto cu = [&](cudaError_t e, const char* what) {
+        if (e != cudaSuccess && !rc) rc = cuda_err(ctx, e, what);
+      };
+      cu(cudaMemcpyAsync(d_con, h_con, sizeof(double) * n_con, cudaMemcpyHostToDevice, s), "macro contributions H2D");
+      cu(cudaMemsetAsync(d_K, 0, sizeof(double) * (size_t)n * n, s), "macro tangent clear");
+      if (n_ent > 0) {  // all dofs constrained: nothing to gather
+        k_macro_gather<<<(n_ent + 255) / 256, 256, 0, s>>>(n_ent, d_ent, d_eptr, d_eidx, d_con, d_K);
+        cu(cudaGetLastError(), "k_macro_gather launch");
+        ctx->launches += 1;
+      }
+      cu(cudaMemcpyAsync(d_b, res.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s), "macro residual H2D");
+      if (!rc && (cusolverDnDgetrf(dn, n, n, d_K, n, d_work, d_piv, d_info) != CUSOLVER_STATUS_SUCCESS ||
+                  cusolverDnDgetrs(dn, CUBLAS_OP_N, n, 1, d_K, n, d_piv, d_b, n, d_info) != CUSOLVER_STATUS_SUCCESS))
+        rc = set_err(ctx, PODECM_ECUDA, "macro tangent: cuSOLVER getrf/getrs failed");
       int info = 0;
-      cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, s);
-      cudaMemcpyAsync(res.data(), d_b, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
-      cudaStreamSynchronize(s);
+      cu(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, s), "macro info D2H");
+      cu(cudaMemcpyAsync(res.data(), d_b, sizeof(double) * n, cudaMemcpyDeviceToHost, s), "macro update D2H");
+      cu(cudaStreamSynchronize(s), "macro solve");
+      if (rc) break;
       if (info != 0) {
         rc = set_err(ctx, PODECM_ESOLVE, "macro tangent factorization failed at step " + std::to_string(step));
         break;
