@@ -51,6 +51,14 @@ struct AsmArgs {
   double* a_field;  // nullable [n][16][n_qp] (AssemblyOpts::store_tangent_field)
   const double* field;  // field-rows mode: [n][16][n_qp] tangent field, column `field_col`
   int field_col;
+  // tiled mode (k_asm_qp2t): tile tables (rve.cuh), local item outputs
+  const int32_t* t_elem;
+  const int32_t* t_lptr;
+  const int32_t* t_litem;
+  const uint64_t* t_lpack;
+  const int32_t* t_hpos;
+  double* kvals;
+  double* f;
 };
 
 // 4-lane butterfly over the quad of lanes holding the 4 qps of one element:
@@ -234,16 +242,29 @@ constexpr int kQPlanes = 29;
 // contracted each tangent column into element terms inside the FD loop.)
 constexpr int kQ2Thr = 128;
 
-template <int MINB>
+// TILED (k_asm_qp2t): the CTA is one 8 x 4 element tile (blockIdx.x) of one
+// instance (blockIdx.y); element sums also go to shared memory, and after the
+// element phase the CTA sums the tile's local items there (in the gather's
+// group order: the same bits) and stores them; only halo terms go to the
+// compact scratch.  Otherwise one thread per (instance, qp) in qp order.
+template <int MINB, bool TILED = false>
 __global__ void __launch_bounds__(kQ2Thr, MINB) k_asm_qp2(AsmArgs g, MatTable tab) {
   __shared__ double sq[kQPlanes * kQ2Thr];  // [plane][thread]
   const int lt = threadIdx.x;
-  const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t total = (int64_t)g.n_inst * g.n_qp;
-  const bool valid = tid0 < total;
-  const int64_t tid = valid ? tid0 : total - 1;  // whole quads stay converged
-  const int c = (int)(tid / g.n_qp);
-  const int q = (int)(tid - (int64_t)c * g.n_qp);
+  bool valid;
+  int c, q;
+  if constexpr (TILED) {
+    valid = true;
+    c = blockIdx.y;
+    q = 4 * __ldg(g.t_elem + (size_t)blockIdx.x * 32 + (lt >> 2)) + (lt & 3);
+  } else {
+    const int64_t tid0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)g.n_inst * g.n_qp;
+    valid = tid0 < total;
+    const int64_t tid = valid ? tid0 : total - 1;  // whole quads stay converged
+    c = (int)(tid / g.n_qp);
+    q = (int)(tid - (int64_t)c * g.n_qp);
+  }
   const int64_t inst = g.inst0 + c;
   const int e = q >> 2, k = q & 3;
   const int nq = g.n_qp;
@@ -348,8 +369,14 @@ __global__ void __launch_bounds__(kQ2Thr, MINB) k_asm_qp2(AsmArgs g, MatTable ta
 #pragma unroll
   for (int t = 0; t < 4; ++t) P[t] = sq[(16 + t) * kQ2Thr + lt];
   double* sc = g.scratch + (size_t)c * g.n_groups;
-  const int32_t* ps = g.pos + (size_t)e * 72;
+  const int32_t* ps = (TILED ? g.t_hpos : g.pos) + (size_t)e * 72;
   const int u0 = 4 * (k & 1) + 2 * ((k >> 1) & 1);
+  // TILED: this element's 72 sums in shared memory, [local element][72]
+  // TILED: the element sums stay in sq, each written over planes this pass
+  // has finished reading (rve_host.cu tile_smem_slot: f terms over the first
+  // stress planes, the K terms of trial component j over the tangent
+  // columns j and j + 2); __syncwarp orders the quad's reads before writes.
+  const int qb = lt & ~3;  // first lane of this element's quad
   {
     double v[8], o[2];
 #pragma unroll
@@ -361,6 +388,14 @@ __global__ void __launch_bounds__(kQ2Thr, MINB) k_asm_qp2(AsmArgs g, MatTable ta
       const int p0 = __ldg(ps + 64 + u0), p1 = __ldg(ps + 64 + u0 + 1);
       if (p0 >= 0) sc[p0] = o[0];
       if (p1 >= 0) sc[p1] = o[1];
+      if (TILED) {
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int u = u0 + h;
+          sq[(16 + (u >> 2)) * kQ2Thr + qb + (u & 3)] = o[h];
+        }
+      }
     }
   }
   if (g.tangent) {
@@ -371,6 +406,7 @@ __global__ void __launch_bounds__(kQ2Thr, MINB) k_asm_qp2(AsmArgs g, MatTable ta
       for (int dd = 0; dd < 2; ++dd)
 #pragma unroll
         for (int r = 0; r < 4; ++r) cd[dd][r] = sq[(r + 4 * (j + 2 * dd)) * kQ2Thr + lt];
+      if (TILED) __syncwarp();
       double T[2][2][4];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
@@ -391,8 +427,14 @@ __global__ void __launch_bounds__(kQ2Thr, MINB) k_asm_qp2(AsmArgs g, MatTable ta
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             const int u = u0 + h, b = u >> 1, i = u & 1;
-            const int pp = __ldg(ps + a * 16 + b * 4 + i * 2 + j);
+            const int tl = a * 16 + b * 4 + i * 2 + j;
+            const int pp = __ldg(ps + tl);
             if (pp >= 0) sc[pp] = o[h];
+            if (TILED) {
+              const int idx = a * 8 + b * 2 + i;
+              const int pl = (idx >> 2) < 4 ? 4 * j + (idx >> 2) : 8 + 4 * j + (idx >> 2) - 4;
+              sq[pl * kQ2Thr + qb + (idx & 3)] = o[h];
+            }
           }
         }
       }
@@ -401,6 +443,42 @@ __global__ void __launch_bounds__(kQ2Thr, MINB) k_asm_qp2(AsmArgs g, MatTable ta
   if (!ok && valid) {
     if (g.status) g.status[inst] = PODECM_ESOLVE;
     atomicAdd(g.fail, 1u);
+  }
+  if constexpr (TILED) {
+    // the tile's local items: the gather's sum (first group, then + in group
+    // order; residual rows start from 0.0 +) over the element sums in SMEM
+    __syncthreads();
+    const int l0 = __ldg(g.t_lptr + blockIdx.x), l1 = __ldg(g.t_lptr + blockIdx.x + 1);
+    const int64_t nnz = g.nnz;
+    constexpr int kU = 8;  // items per thread per round, all table loads issued first
+    for (int base = l0; base < l1; base += kU * kQ2Thr) {
+      int its[kU];
+      uint64_t pks[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int li = base + u * kQ2Thr + lt;
+        its[u] = li < l1 ? __ldg(g.t_litem + li) : -1;
+        pks[u] = li < l1 ? __ldg(g.t_lpack + li) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int it = its[u];
+        if (it < 0) continue;
+        const bool is_slot = it < nnz;
+        if (is_slot && !g.tangent) continue;
+        const uint64_t pk = pks[u];
+        const int n = (int)(pk >> 48);
+        double sm = sq[pk & 0xfff];
+        if (!is_slot) sm = 0.0 + sm;
+        if (n > 1) sm = sm + sq[(pk >> 12) & 0xfff];
+        if (n > 2) sm = sm + sq[(pk >> 24) & 0xfff];
+        if (n > 3) sm = sm + sq[(pk >> 36) & 0xfff];
+        if (is_slot)
+          __stcs(g.kvals + (size_t)inst * nnz + it, sm);
+        else
+          __stcs(g.f + (size_t)inst * g.n_red + (it - nnz), sm);
+      }
+    }
   }
 }
 
@@ -557,6 +635,37 @@ __global__ void __launch_bounds__(256) k_asm_gather_fused(GatherArgs g, const in
     g.f[(size_t)inst * g.n_red + (it - nnz)] = sm;
 }
 
+// Tiled mode: the halo items only (items [0, nnz) CSR slots, then residual
+// rows), each a contiguous run of the compact scratch, summed in group order.
+__global__ void __launch_bounds__(256) k_asm_gather_halo(GatherArgs g, const int32_t* __restrict__ hitem,
+                                                         const int32_t* __restrict__ hgptr, int n_halo,
+                                                         int64_t n_hgroups) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= n_halo) return;
+  const int it = __ldg(hitem + h);
+  const bool is_slot = it < g.nnz;
+  if (is_slot && !g.kvals) return;
+  const int c = blockIdx.y;
+  const int b0 = __ldg(hgptr + h), b1 = __ldg(hgptr + h + 1);
+  const double* sc = g.scratch + (size_t)c * n_hgroups;
+  const int n = b1 - b0;
+  const double v0 = n > 0 ? __ldcs(sc + b0) : 0.0;
+  const double v1 = n > 1 ? __ldcs(sc + b0 + 1) : 0.0;
+  const double v2 = n > 2 ? __ldcs(sc + b0 + 2) : 0.0;
+  const double v3 = n > 3 ? __ldcs(sc + b0 + 3) : 0.0;
+  double sm = v0;
+  if (!is_slot) sm = 0.0 + sm;
+  if (n > 1) sm = sm + v1;
+  if (n > 2) sm = sm + v2;
+  if (n > 3) sm = sm + v3;
+  for (int m = b0 + 4; m < b1; ++m) sm = sm + __ldcs(sc + m);
+  const int64_t inst = g.inst0 + c;
+  if (is_slot)
+    g.kvals[(size_t)inst * g.nnz + it] = sm;
+  else
+    g.f[(size_t)inst * g.n_red + (it - g.nnz)] = sm;
+}
+
 __global__ void k_morph(int64_t n_inst, int nq, double r0, const double* nodes, const int32_t* elems,
                         const double* grad, const double* geom, double* fmu_inv, double* det,
                         int32_t* status, unsigned int* fail) {
@@ -609,7 +718,14 @@ int assemble_impl(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst, 
     const char* e = getenv("PODECM_ASM_MINB");
     return e ? atoi(e) : 4;
   }();
-  const size_t per_inst = (exact ? (size_t)r->n_elems * 72 * 4 : (size_t)r->n_groups) * sizeof(double);
+  // tiled assembly (default where the cell divides into 8 x 4 element tiles;
+  // PODECM_ASM_TILED=0: the per-qp grid with every element sum gathered)
+  const bool tiled = !exact && !field && r->n_tiles > 0 && [] {
+    const char* e = getenv("PODECM_ASM_TILED");
+    return !(e && atoi(e) == 0);
+  }();
+  const size_t per_inst =
+      (exact ? (size_t)r->n_elems * 72 * 4 : (size_t)(tiled ? r->n_hgroups : r->n_groups)) * sizeof(double);
   // Chunk of instances per (qp kernel, gather) pair: the scratch budget
   // (PODECM_ASM_CHUNK_MB, default 768 MB; 81 instances of 128^2).  Large grids
   // beat L2 residency here: 48 MB chunks (5 instances, 3.5 waves of the qp
@@ -620,17 +736,39 @@ int assemble_impl(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst, 
   }();
   int64_t chunk = std::max<int64_t>(1, (chunk_mb << 20) / (int64_t)per_inst);
   chunk = std::min<int64_t>(chunk, n_inst);
+  // Two or more chunks (default mode): double-buffered scratch, the gather of
+  // chunk i on r->gather_s (low priority) overlapping the compute-bound qp
+  // kernel of chunk i+1 on s (PODECM_ASM_PIPE=0: one stream).
+  const bool pipe = !exact && !field && n_inst > chunk && [] {
+    const char* e = getenv("PODECM_ASM_PIPE");
+    return !(e && atoi(e) == 0);
+  }();
+  const int nbuf = pipe ? 2 : 1;
   // scratch_inst counts BYTES: the two modes have different per-instance
   // footprints and may alternate on one cell
-  if (r->scratch_inst < (int64_t)per_inst * chunk) {
+  if (r->scratch_inst < (int64_t)per_inst * chunk * nbuf) {
     cudaFree(r->d_scratch);
     r->d_scratch = nullptr;
-    PODECM_CUDA_TRY(ctx, cudaMalloc(&r->d_scratch, per_inst * chunk));
-    r->scratch_inst = (int64_t)per_inst * chunk;
+    PODECM_CUDA_TRY(ctx, cudaMalloc(&r->d_scratch, per_inst * chunk * nbuf));
+    r->scratch_inst = (int64_t)per_inst * chunk * nbuf;
   }
+  if (pipe && !r->gather_s) {
+    int lo = 0, hi = 0;
+    PODECM_CUDA_TRY(ctx, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    PODECM_CUDA_TRY(ctx, cudaStreamCreateWithPriority(&r->gather_s, cudaStreamNonBlocking, lo));
+    for (int k = 0; k < 2; ++k) {
+      PODECM_CUDA_TRY(ctx, cudaEventCreateWithFlags(&r->ev_qp[k], cudaEventDisableTiming));
+      PODECM_CUDA_TRY(ctx, cudaEventCreateWithFlags(&r->ev_g[k], cudaEventDisableTiming));
+    }
+  }
+  int chunk_no = 0;
   if (status && !field) PODECM_CUDA_TRY(ctx, cudaMemsetAsync(status, 0, n_inst * sizeof(int32_t), s));
-  for (int64_t i0 = 0; i0 < n_inst; i0 += chunk) {
+  for (int64_t i0 = 0; i0 < n_inst; i0 += chunk, ++chunk_no) {
     const int nc = (int)std::min<int64_t>(chunk, n_inst - i0);
+    const int buf = chunk_no & 1;
+    double* scratch = r->d_scratch + (pipe ? (size_t)buf * (per_inst / sizeof(double)) * chunk : 0);
+    if (pipe && chunk_no >= 2)  // the gather of chunk - 2 has released this half
+      PODECM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, r->ev_g[buf], 0));
     AsmArgs a;
     a.n_qp = r->n_qp;
     a.n_red = r->n_red;
@@ -651,7 +789,7 @@ int assemble_impl(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst, 
     a.st0 = st0;
     a.st1 = st1;
     a.p_field = p_field;
-    a.scratch = r->d_scratch;
+    a.scratch = scratch;
     a.pos = r->d_pos;
     a.n_groups = r->n_groups;
     a.status = status;
@@ -660,8 +798,22 @@ int assemble_impl(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst, 
     a.a_field = a_field;
     a.field = field;
     a.field_col = field_col;
+    a.t_elem = r->d_t_elem;
+    a.t_lptr = r->d_t_lptr;
+    a.t_litem = r->d_t_litem;
+    a.t_lpack = r->d_t_lpack;
+    a.t_hpos = r->d_t_hpos;
+    a.kvals = kvals;
+    a.f = f;
+    if (tiled) a.n_groups = r->n_hgroups;
     const int64_t nthr = (int64_t)nc * r->n_qp;
-    if (field) {
+    if (tiled) {
+      KTimer kt(ctx, s, "k_asm_qp2t");
+      if (minb == 5)
+        k_asm_qp2<5, true><<<dim3(r->n_tiles, nc), kQ2Thr, 0, s>>>(a, r->mats);
+      else
+        k_asm_qp2<4, true><<<dim3(r->n_tiles, nc), kQ2Thr, 0, s>>>(a, r->mats);
+    } else if (field) {
       KTimer kt(ctx, s, "k_asm_field_terms");
       k_asm_field_terms<<<grid_for(nthr, 256), 256, 0, s>>>(a);
     } else if (exact) {
@@ -684,19 +836,33 @@ int assemble_impl(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst, 
     gg.slot_grp = r->d_slot_grp;
     gg.frow_gptr = r->d_frow_gptr;
     gg.frow_grp = r->d_frow_grp;
-    gg.scratch = r->d_scratch;
+    gg.scratch = scratch;
     gg.f = f;
     gg.kvals = kvals;
     const int64_t nitems = ((kvals ? r->nnz : 0) + r->n_red) * nc;
+    cudaStream_t gs = s;
+    if (pipe) {
+      PODECM_CUDA_TRY(ctx, cudaEventRecord(r->ev_qp[buf], s));
+      PODECM_CUDA_TRY(ctx, cudaStreamWaitEvent(r->gather_s, r->ev_qp[buf], 0));
+      gs = r->gather_s;
+    }
     {
-      KTimer kt(ctx, s, "k_asm_gather");
-      if (exact)
-        k_asm_gather<<<grid_for(nitems, 256), 256, 0, s>>>(gg);
-      else
-        k_asm_gather_fused<<<dim3(grid_for(nitems / nc, 256), nc), 256, 0, s>>>(gg, r->d_gptr_all, r->n_groups);
+      KTimer kt(ctx, gs, "k_asm_gather");
+      if (tiled) {
+        const int nh = (int)r->t_hitem.size();
+        k_asm_gather_halo<<<dim3(grid_for(nh, 256), nc), 256, 0, gs>>>(gg, r->d_t_hitem, r->d_t_hgptr, nh,
+                                                                       r->n_hgroups);
+      } else if (exact) {
+        k_asm_gather<<<grid_for(nitems, 256), 256, 0, gs>>>(gg);
+      } else {
+        k_asm_gather_fused<<<dim3(grid_for(nitems / nc, 256), nc), 256, 0, gs>>>(gg, r->d_gptr_all, r->n_groups);
+      }
     }
     PODECM_LAUNCHED(ctx, 2);
+    if (pipe) PODECM_CUDA_TRY(ctx, cudaEventRecord(r->ev_g[buf], r->gather_s));
   }
+  if (pipe)  // the caller's stream sees the last gathers (stream-ordered results)
+    for (int k = 0; k < 2 && k < chunk_no; ++k) PODECM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, r->ev_g[k], 0));
   return PODECM_OK;
 }
 

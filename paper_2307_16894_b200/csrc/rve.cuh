@@ -27,7 +27,20 @@ struct podecm_rve {
   // (slot groups, then residual-row groups); -1 = unused (anchor dofs).
   std::vector<int32_t> pos, gptr_all;
   int64_t n_groups = 0;
+  // tiled assembly (k_asm_qp2t): CTA = one 8 x 4 element tile; an item (CSR
+  // slot or residual row) whose element sums all come from one tile is summed
+  // there from shared memory (same group order as the gather); the others
+  // ("halo") go through a compact scratch and the halo gather.
+  int n_tiles = 0;                            // 0: not tiled (mesh not divisible)
+  std::vector<int32_t> t_elem;                // [n_tiles * 32] element of (tile, local element)
+  std::vector<int32_t> t_lptr, t_litem;       // per tile: local items
+  std::vector<uint64_t> t_lpack;              // their <= 4 SMEM offsets (le * 72 + term), 12 bits each, + count
+  std::vector<int32_t> t_hitem, t_hgptr, t_hpos;  // halo items, their compact groups, positions
+  int64_t n_hgroups = 0;
   // device tables
+  int32_t *d_t_elem = nullptr, *d_t_lptr = nullptr, *d_t_litem = nullptr;
+  uint64_t* d_t_lpack = nullptr;
+  int32_t *d_t_hitem = nullptr, *d_t_hgptr = nullptr, *d_t_hpos = nullptr;
   double *d_nodes = nullptr, *d_grad = nullptr, *d_w = nullptr;
   int32_t *d_elems = nullptr, *d_regions = nullptr, *d_node_dof = nullptr;
   int32_t *d_slot_gptr = nullptr, *d_slot_grp = nullptr, *d_frow_gptr = nullptr,
@@ -35,6 +48,11 @@ struct podecm_rve {
   // assembly scratch (per-qp K and f terms of a chunk of instances)
   double* d_scratch = nullptr;
   int64_t scratch_inst = 0;  // bytes of d_scratch
+  // chunk pipeline (default mode): the gather of chunk i runs on gather_s
+  // while the qp kernel of chunk i+1 runs on the caller's stream, with two
+  // scratch halves; events order reuse (created on first use)
+  cudaStream_t gather_s = nullptr;
+  cudaEvent_t ev_qp[2] = {nullptr, nullptr}, ev_g[2] = {nullptr, nullptr};
 };
 
 namespace podecm_dev {

@@ -223,6 +223,95 @@ void build_pattern(podecm_rve& r) {
   for (size_t k = 1; k < r.frow_gptr.size(); ++k) r.gptr_all.push_back((int32_t)(ns + r.frow_gptr[k]));
 }
 
+// Where k_asm_qp2t leaves element sum `term` of local element le in its
+// [29][128] shared planes (k_assemble.cu): the K terms of trial component j
+// over the 8 tangent-column planes that term's pass has finished reading,
+// the f terms over the 2 first stress planes; 4 lanes per element.
+int tile_smem_slot(int le, int term) {
+  static const int planes[2][8] = {{0, 1, 2, 3, 8, 9, 10, 11}, {4, 5, 6, 7, 12, 13, 14, 15}};
+  if (term >= 64) {
+    const int u = term - 64;
+    return (16 + (u >> 2)) * 128 + 4 * le + (u & 3);
+  }
+  const int a = term >> 4, b = (term >> 2) & 3, i = (term >> 1) & 1, j = term & 1;
+  const int idx = a * 8 + b * 2 + i;
+  return planes[j][idx >> 2] * 128 + 4 * le + (idx & 3);
+}
+
+// Tiles of 8 x 4 elements (row-major element ids e = iy n + ix) and the
+// local / halo split of the items (CSR slots, then residual rows) over them.
+void build_tiles(podecm_rve& r) {
+  const int n = r.n_cells, TX = 8, TY = 4;
+  r.n_tiles = 0;
+  if (n % TX != 0 || n % TY != 0 || r.n_elems % 32 != 0) return;
+  r.n_tiles = r.n_elems / 32;
+  const int ntx = n / TX;
+  r.t_elem.assign((size_t)r.n_tiles * 32, 0);
+  std::vector<int32_t> tile_of(r.n_elems), local_of(r.n_elems);
+  for (int t = 0; t < r.n_tiles; ++t)
+    for (int le = 0; le < 32; ++le) {
+      const int tx = t % ntx, ty = t / ntx, lx = le % TX, ly = le / TX;
+      const int e = (ty * TY + ly) * n + tx * TX + lx;
+      r.t_elem[(size_t)t * 32 + le] = e;
+      tile_of[e] = t;
+      local_of[e] = le;
+    }
+  const int64_t ns = (int64_t)r.slot_grp.size();
+  const int64_t n_items = r.nnz + r.n_red;
+  auto group = [&](int64_t g, int& e, int& term) {
+    if (g < ns) {
+      const int grp = r.slot_grp[g];
+      e = grp >> 6;
+      term = grp & 63;
+    } else {
+      const int grp = r.frow_grp[g - ns];
+      e = grp >> 3;
+      term = 64 + (grp & 7);
+    }
+  };
+  std::vector<std::vector<int32_t>> litems(r.n_tiles);
+  std::vector<std::vector<uint64_t>> lpacks(r.n_tiles);
+  r.t_hitem.clear();
+  r.t_hgptr.assign(1, 0);
+  r.t_hpos.assign((size_t)r.n_elems * 72, -1);
+  int64_t nh = 0;
+  for (int64_t it = 0; it < n_items; ++it) {
+    const int g0 = r.gptr_all[it], g1 = r.gptr_all[it + 1];
+    int e, term, tile = -1;
+    bool local = g1 > g0 && g1 - g0 <= 4;
+    for (int g = g0; g < g1; ++g) {
+      group(g, e, term);
+      if (tile < 0) tile = tile_of[e];
+      local = local && tile_of[e] == tile;
+    }
+    if (local) {
+      uint64_t pk = (uint64_t)(g1 - g0) << 48;
+      for (int g = g0; g < g1; ++g) {
+        group(g, e, term);
+        pk |= (uint64_t)tile_smem_slot(local_of[e], term) << (12 * (g - g0));
+      }
+      litems[tile].push_back((int32_t)it);
+      lpacks[tile].push_back(pk);
+    } else {
+      r.t_hitem.push_back((int32_t)it);
+      for (int g = g0; g < g1; ++g) {
+        group(g, e, term);
+        r.t_hpos[(size_t)e * 72 + term] = (int32_t)nh++;
+      }
+      r.t_hgptr.push_back((int32_t)nh);
+    }
+  }
+  r.n_hgroups = nh;
+  r.t_lptr.assign(1, 0);
+  r.t_litem.clear();
+  r.t_lpack.clear();
+  for (int t = 0; t < r.n_tiles; ++t) {
+    r.t_litem.insert(r.t_litem.end(), litems[t].begin(), litems[t].end());
+    r.t_lpack.insert(r.t_lpack.end(), lpacks[t].begin(), lpacks[t].end());
+    r.t_lptr.push_back((int32_t)r.t_litem.size());
+  }
+}
+
 template <class T>
 int upload(podecm_ctx* ctx, T** d, const std::vector<T>& h) {
   PODECM_CUDA_TRY(ctx, cudaMalloc(d, std::max<size_t>(1, h.size()) * sizeof(T)));
@@ -243,7 +332,19 @@ void free_rve(podecm_rve* r) {
   cudaFree(r->d_frow_grp);
   cudaFree(r->d_pos);
   cudaFree(r->d_gptr_all);
+  cudaFree(r->d_t_elem);
+  cudaFree(r->d_t_lptr);
+  cudaFree(r->d_t_litem);
+  cudaFree(r->d_t_lpack);
+  cudaFree(r->d_t_hitem);
+  cudaFree(r->d_t_hgptr);
+  cudaFree(r->d_t_hpos);
   cudaFree(r->d_scratch);
+  for (int k = 0; k < 2; ++k) {
+    if (r->ev_qp[k]) cudaEventDestroy(r->ev_qp[k]);
+    if (r->ev_g[k]) cudaEventDestroy(r->ev_g[k]);
+  }
+  if (r->gather_s) cudaStreamDestroy(r->gather_s);
 }
 
 }  // namespace
@@ -275,6 +376,7 @@ int podecm_rve_create_q4_regions(podecm_ctx* ctx, int n_cells, double r0, const 
     build_cache(*r);
     build_dofs(*r);
     build_pattern(*r);
+    build_tiles(*r);
     for (int reg : r->regions)
       if (reg < 0 || reg >= n_mats) {  // RveProblem::build, microfem.cpp:17-21
         delete r;
@@ -297,6 +399,15 @@ int podecm_rve_create_q4_regions(podecm_ctx* ctx, int n_cells, double r0, const 
   if (!rc) rc = upload(ctx, &r->d_frow_grp, r->frow_grp);
   if (!rc) rc = upload(ctx, &r->d_pos, r->pos);
   if (!rc) rc = upload(ctx, &r->d_gptr_all, r->gptr_all);
+  if (!rc && r->n_tiles) {
+    rc = upload(ctx, &r->d_t_elem, r->t_elem);
+    if (!rc) rc = upload(ctx, &r->d_t_lptr, r->t_lptr);
+    if (!rc) rc = upload(ctx, &r->d_t_litem, r->t_litem);
+    if (!rc) rc = upload(ctx, &r->d_t_lpack, r->t_lpack);
+    if (!rc) rc = upload(ctx, &r->d_t_hitem, r->t_hitem);
+    if (!rc) rc = upload(ctx, &r->d_t_hgptr, r->t_hgptr);
+    if (!rc) rc = upload(ctx, &r->d_t_hpos, r->t_hpos);
+  }
   if (rc) {
     free_rve(r);
     delete r;
