@@ -736,39 +736,18 @@ int assemble_impl(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst, 
   }();
   int64_t chunk = std::max<int64_t>(1, (chunk_mb << 20) / (int64_t)per_inst);
   chunk = std::min<int64_t>(chunk, n_inst);
-  // Two or more chunks (default mode): double-buffered scratch, the gather of
-  // chunk i on r->gather_s (low priority) overlapping the compute-bound qp
-  // kernel of chunk i+1 on s (PODECM_ASM_PIPE=0: one stream).
-  const bool pipe = !exact && !field && n_inst > chunk && [] {
-    const char* e = getenv("PODECM_ASM_PIPE");
-    return !(e && atoi(e) == 0);
-  }();
-  const int nbuf = pipe ? 2 : 1;
-  // scratch_inst counts BYTES: the two modes have different per-instance
+  // scratch_inst counts BYTES: the modes have different per-instance
   // footprints and may alternate on one cell
-  if (r->scratch_inst < (int64_t)per_inst * chunk * nbuf) {
+  if (r->scratch_inst < (int64_t)per_inst * chunk) {
     cudaFree(r->d_scratch);
     r->d_scratch = nullptr;
-    PODECM_CUDA_TRY(ctx, cudaMalloc(&r->d_scratch, per_inst * chunk * nbuf));
-    r->scratch_inst = (int64_t)per_inst * chunk * nbuf;
+    PODECM_CUDA_TRY(ctx, cudaMalloc(&r->d_scratch, per_inst * chunk));
+    r->scratch_inst = (int64_t)per_inst * chunk;
   }
-  if (pipe && !r->gather_s) {
-    int lo = 0, hi = 0;
-    PODECM_CUDA_TRY(ctx, cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    PODECM_CUDA_TRY(ctx, cudaStreamCreateWithPriority(&r->gather_s, cudaStreamNonBlocking, lo));
-    for (int k = 0; k < 2; ++k) {
-      PODECM_CUDA_TRY(ctx, cudaEventCreateWithFlags(&r->ev_qp[k], cudaEventDisableTiming));
-      PODECM_CUDA_TRY(ctx, cudaEventCreateWithFlags(&r->ev_g[k], cudaEventDisableTiming));
-    }
-  }
-  int chunk_no = 0;
   if (status && !field) PODECM_CUDA_TRY(ctx, cudaMemsetAsync(status, 0, n_inst * sizeof(int32_t), s));
-  for (int64_t i0 = 0; i0 < n_inst; i0 += chunk, ++chunk_no) {
+  for (int64_t i0 = 0; i0 < n_inst; i0 += chunk) {
     const int nc = (int)std::min<int64_t>(chunk, n_inst - i0);
-    const int buf = chunk_no & 1;
-    double* scratch = r->d_scratch + (pipe ? (size_t)buf * (per_inst / sizeof(double)) * chunk : 0);
-    if (pipe && chunk_no >= 2)  // the gather of chunk - 2 has released this half
-      PODECM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, r->ev_g[buf], 0));
+    double* scratch = r->d_scratch;
     AsmArgs a;
     a.n_qp = r->n_qp;
     a.n_red = r->n_red;
@@ -841,11 +820,6 @@ int assemble_impl(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst, 
     gg.kvals = kvals;
     const int64_t nitems = ((kvals ? r->nnz : 0) + r->n_red) * nc;
     cudaStream_t gs = s;
-    if (pipe) {
-      PODECM_CUDA_TRY(ctx, cudaEventRecord(r->ev_qp[buf], s));
-      PODECM_CUDA_TRY(ctx, cudaStreamWaitEvent(r->gather_s, r->ev_qp[buf], 0));
-      gs = r->gather_s;
-    }
     {
       KTimer kt(ctx, gs, "k_asm_gather");
       if (tiled) {
@@ -859,10 +833,7 @@ int assemble_impl(podecm_ctx* ctx, void* stream, podecm_rve* r, int64_t n_inst, 
       }
     }
     PODECM_LAUNCHED(ctx, 2);
-    if (pipe) PODECM_CUDA_TRY(ctx, cudaEventRecord(r->ev_g[buf], r->gather_s));
   }
-  if (pipe)  // the caller's stream sees the last gathers (stream-ordered results)
-    for (int k = 0; k < 2 && k < chunk_no; ++k) PODECM_CUDA_TRY(ctx, cudaStreamWaitEvent(s, r->ev_g[k], 0));
   return PODECM_OK;
 }
 

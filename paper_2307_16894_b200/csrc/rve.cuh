@@ -48,11 +48,6 @@ struct podecm_rve {
   // assembly scratch (per-qp K and f terms of a chunk of instances)
   double* d_scratch = nullptr;
   int64_t scratch_inst = 0;  // bytes of d_scratch
-  // chunk pipeline (default mode): the gather of chunk i runs on gather_s
-  // while the qp kernel of chunk i+1 runs on the caller's stream, with two
-  // scratch halves; events order reuse (created on first use)
-  cudaStream_t gather_s = nullptr;
-  cudaEvent_t ev_qp[2] = {nullptr, nullptr}, ev_g[2] = {nullptr, nullptr};
 };
 
 namespace podecm_dev {

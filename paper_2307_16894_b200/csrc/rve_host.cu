@@ -340,11 +340,6 @@ void free_rve(podecm_rve* r) {
   cudaFree(r->d_t_hgptr);
   cudaFree(r->d_t_hpos);
   cudaFree(r->d_scratch);
-  for (int k = 0; k < 2; ++k) {
-    if (r->ev_qp[k]) cudaEventDestroy(r->ev_qp[k]);
-    if (r->ev_g[k]) cudaEventDestroy(r->ev_g[k]);
-  }
-  if (r->gather_s) cudaStreamDestroy(r->gather_s);
 }
 
 }  // namespace
