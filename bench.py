@@ -79,7 +79,7 @@ def _fp64_issue_roofline(points_per_s: float, clk):
     return {"bound": "fp64-pipe", "achieved": round(ach / 1e12, 3), "peak": round(peak / 1e12, 3),
             "unit": "T FP64 thread-instructions/s", "frac": round(ach / peak, 4),
             "fp64_inst_per_point": per_pt, "sm_mhz": mhz,
-            "note": "DMUL and DADD occupy the FP64 pipe like DFMA; cf. ncu sm__pipe_fp64_cycles_active 69.0 % (profiles/r1_ncu_summary_v7.md)"}
+            "note": "DMUL and DADD occupy the FP64 pipe like DFMA; cf. ncu sm__pipe_fp64_cycles_active 72.0 % (profiles/r2_ncu_summary.md)"}
 
 
 class ClockSampler:
@@ -438,13 +438,22 @@ def run_rve(args, ws, rank, local, ctx, n_cells, n_inst, hm, geom_range, steps, 
            "launches_per_step": launches / steps,
            "kernels_ms_per_step": {k: round(v[0] / steps, 4) for k, v in tk.items()},
            "algorithmic_bytes_per_instance": bytes_inst}
-    kq = (tk.get("k_asm_qp2", (0, 1))[0] + tk.get("k_asm_qp", (0, 1))[0]) / steps
     kall = sum(v[0] for v in tk.values()) / steps
     peak, src = _hbm_peak()
     ach = bytes_inst * n_inst / (kall * 1e-3) / 1e9
+    traffic = None
+    try:  # committed ncu capture: DRAM bytes per instance of the qp kernel + halo gather
+        t = json.loads((ROOT / "profiles" / "ncu_traffic.json").read_text())
+        traffic = sum((t[k]["dram_bytes_read"] + t[k]["dram_bytes_write"]) / t[k]["instances_per_launch"]
+                      for k in ("k_asm_qp2t", "k_asm_gather_halo"))
+    except Exception:
+        pass
+    kq = (tk.get("k_asm_qp2", (0, 1))[0] + tk.get("k_asm_qp2t", (0, 1))[0] + tk.get("k_asm_qp", (0, 1))[0]) / steps
     res["roofline"] = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                        "frac": round(ach / peak, 4), "peak_source": src,
-                       "note": "k_asm_qp2 (material + element sums, FP64-issue bound) is "
+                       "traffic_per_instance": round(traffic) if traffic else None,
+                       "traffic_over_algorithmic": round(traffic / bytes_inst, 3) if traffic else None,
+                       "note": "the qp kernel (material + element sums, FP64-issue bound) is "
                                f"{100 * kq / max(kall, 1e-9):.0f}% of the step"}
     if rank == 0 and ws == 1 and not args.no_cpu and cpu_sample > 0:
         import oracle
