@@ -184,8 +184,15 @@ def dist_setup(cpu_only: bool = False):
             dist.init_process_group("gloo")
         else:
             import torch
-            torch.cuda.set_device(local)
-            dist.init_process_group("cuda:nccl,cpu:gloo")
+            # PODECM_BENCH_SAME_GPU=1 (tests on a one-GPU box only): every rank on
+            # cuda:0 with gloo exchanges, since NCCL refuses two ranks per GPU
+            if os.environ.get("PODECM_BENCH_SAME_GPU") == "1":
+                local = 0
+                torch.cuda.set_device(0)
+                dist.init_process_group("gloo")
+            else:
+                torch.cuda.set_device(local)
+                dist.init_process_group("cuda:nccl,cpu:gloo")
     return ws, rank, local
 
 
@@ -229,7 +236,8 @@ def max_over_ranks(ws, x: float) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if "nccl" in str(dist.get_backend()) else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -704,6 +712,10 @@ def run_c4(args, ws, rank, local, ctx, steps, warmup, fp64):
                         "ecm_score_tflops": round(score_flop * ks[1] / steps / (ks[0] / steps * 1e-3) / 1e12, 2) if ks[0] else None,
                         "peak": fp64.get("dmma"), "unit": "TFLOP/s",
                         "peak_source": "DMMA probe measured in this run"}}
+    gp = ROOT / "tests" / "golden" / "c4_ecm_golden.npz"
+    if gp.exists():  # the CPU oracle's full-size selection (tests/golden/make_c4_golden.py)
+        out["ids_equal_golden"] = bool(np.array_equal(
+            res["ids"].cpu().numpy() if hasattr(res["ids"], "cpu") else np.asarray(res["ids"]), np.load(gp)["ids"]))
     kgc = tk.get("k_ecm_gram_col", (0.0, 0))
     if kgc[1]:
         hbm, src = _hbm_peak()

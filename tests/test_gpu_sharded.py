@@ -108,3 +108,24 @@ def test_two_rank_split_config4(monkeypatch):
             print(f"rank {r}: ids equal {np.array_equal(got[0], want[0])}, iters {got[3]} vs {want[3]}")
             assert np.array_equal(got[0], want[0]) and got[3] == want[3]
             assert np.abs(got[1] - want[1]).max() <= 1e-9 * np.abs(want[1]).max()
+
+
+def test_bench_two_rank_config4_full_size():
+    """bench.py's own N=2 path at the full config-4 size (4000 snapshots,
+    65,536 candidates, 400 points): re-executed under torch.distributed.run,
+    both ranks on cuda:0 with gloo exchanges (PODECM_BENCH_SAME_GPU=1, the
+    one-GPU stand-in for the NCCL launch); the selected ids equal the CPU
+    oracle's full-size golden selection."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, PODECM_BENCH_SAME_GPU="1")
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--config", "c4", "--steps", "1",
+                        "--warmup", "3", "--no-cpu"], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    c4 = line["also"]["c4"]
+    assert line["n_gpus"] == 2 and c4["selected"] == 400
+    assert c4["ids_equal_golden"] is True
