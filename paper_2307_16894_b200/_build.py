@@ -90,6 +90,17 @@ def build_oracle(force: bool = False) -> Path:
     r = subprocess.run(args, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"oracle build failed:\n{r.stdout}\n{r.stderr}")
+    # oracle/_ref: the reference's own sources compiled unchanged (only where
+    # /root/reference exists, i.e. in the build container; the GPU box uses the
+    # prebuilt .so files that travel with the snapshot)
+    ref_src = Path(os.environ.get("PODECM_REF", "/root/reference/proj"))
+    if (ref_src / "src" / "material.cpp").exists():
+        rargs = ["make", "-C", str(ORACLE_DIR / "ref"), "-s", f"REF={ref_src}"]
+        if force:
+            subprocess.run(["make", "-C", str(ORACLE_DIR / "ref"), "clean", "-s"], check=True)
+        r = subprocess.run(rargs, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"oracle/_ref build failed:\n{r.stdout}\n{r.stderr}")
     return ORACLE_LIB
 
 
