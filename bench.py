@@ -357,12 +357,13 @@ def run_c1(args, ws, rank, local, ctx, clk):
     if rank == 0 and ws == 1 and not args.no_cpu:
         import oracle
         nt = oracle.max_threads()
+        kind, run_cpu, what = _c1_cpu_impl(oracle, mats)
         t0 = time.perf_counter()
-        oracle.material_batch(F_np, st_np, mats, nthreads=nt)
+        run_cpu(F_np, st_np, nt)
         dt = time.perf_counter() - t0
-        res["cpu"] = {"value": n / dt, "unit": "points/s", "cores": nt, "kind": "port",
+        res["cpu"] = {"value": n / dt, "unit": "points/s", "cores": nt, "kind": kind,
                       "sample": f"the full config-1 batch ({n} points: P + FD tangent + history) once, "
-                                f"{dt:.2f} s wall on {nt} host threads (oracle/ C++ restatement, -O2, no FMA)"}
+                                f"{dt:.2f} s wall on {nt} host threads ({what})"}
     del F, st, out, dF, dS, dout
     torch.cuda.empty_cache()
     return res
@@ -758,6 +759,20 @@ def run_c4(args, ws, rank, local, ctx, steps, warmup, fp64):
 
 
 # --------------------------------------------------------------------------
+def _c1_cpu_impl(oracle, mats):
+    """The reference's own CPU material path for config 1: oracle/_ref (the
+    reference's material.cpp compiled unchanged, OpenMP over the points) when
+    it was built, else the oracle restatement."""
+    if oracle.ref_available():
+        return ("reference",
+                lambda F, st, nt: oracle.ref_material_batch(F, st, mats[0], nthreads=nt),
+                "oracle/_ref: the reference's large_strain_update + large_strain_tangent, "
+                "material.cpp compiled unchanged, -O3, no FMA")
+    return ("port",
+            lambda F, st, nt: oracle.material_batch(F, st, mats, nthreads=nt),
+            "oracle/ C++ restatement of material.cpp, -O2, no FMA")
+
+
 def reference_arm(args, ws, rank, base):
     """--impl reference: the reference's CPU algorithm (oracle/ restatement)
     on all host threads, same metric/config; each step a bounded sample."""
@@ -768,20 +783,21 @@ def reference_arm(args, ws, rank, base):
     nt = oracle.max_threads()
     F_np, st_np = synth.config1_points(args.points, 2027)
     mats = [api.matrix_params()]
+    kind, run_cpu, what = _c1_cpu_impl(oracle, mats)
     for _ in range(args.warmup):
-        oracle.material_batch(F_np[:, :4096], st_np[:, :4096], mats, nthreads=nt)
+        run_cpu(F_np[:, :4096], st_np[:, :4096], nt)
     sample = args.points  # the whole config-1 batch every step (same workload as the GPU arm)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.material_batch(F_np[:, :sample], st_np[:, :sample], mats, nthreads=nt)
+        run_cpu(F_np[:, :sample], st_np[:, :sample], nt)
     dt = (time.perf_counter() - t0) / args.steps
     v = sample / dt
     line = dict(base, impl="reference", value=v, ms_per_step=dt * 1e3 * args.points / sample,
                 config={"workload": base["config"]["workload"], "points": args.points,
                         "sample_points_per_step": sample},
-                cpu_baseline={"value": v, "unit": "points/s", "cores": nt, "kind": "port",
+                cpu_baseline={"value": v, "unit": "points/s", "cores": nt, "kind": kind,
                               "sample": f"{sample} of the {args.points} config-1 points per step on "
-                                        f"{nt} host threads (oracle/ C++ restatement of material.cpp)"},
+                                        f"{nt} host threads ({what})"},
                 e2e={"value": v, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
     print(json.dumps(line))
 

@@ -230,13 +230,15 @@ class Matrix {
     return m;
   }
 
-  Index rows() const { return rows_; }
-  Index cols() const { return cols_; }
-  Index size() const { return rows_ * cols_; }
+  // fixed dimensions are compile-time constants (lets the compiler unroll
+  // the coefficient loops of the 2x2 / 4-vector hot path as Eigen does)
+  Index rows() const { return R > 0 ? R : rows_; }
+  Index cols() const { return C > 0 ? C : cols_; }
+  Index size() const { return rows() * cols(); }
   T* data() { return s_.p(); }
   const T* data() const { return s_.p(); }
-  T& operator()(Index i, Index j) { return s_.p()[i + rows_ * j]; }
-  const T& operator()(Index i, Index j) const { return s_.p()[i + rows_ * j]; }
+  T& operator()(Index i, Index j) { return s_.p()[i + rows() * j]; }
+  const T& operator()(Index i, Index j) const { return s_.p()[i + rows() * j]; }
   T& operator()(Index k) { return s_.p()[k]; }
   const T& operator()(Index k) const { return s_.p()[k]; }
   T& coeffRef(Index i, Index j) { return (*this)(i, j); }
