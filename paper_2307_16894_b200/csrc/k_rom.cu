@@ -1215,6 +1215,153 @@ __global__ void __launch_bounds__(32) k_rom_solve(NewtonArgs g) {
     rom_update(g, c, s, lane, Ks, rhs, c->it);
 }
 
+// The same Newton update with [K | -f] resident in registers (compile-time N):
+// lane l holds the physical rows l + 32 t (t < R) and row exchanges are
+// virtual — every row carries its current position, so "swap rows k and p"
+// is a swap of two position tags and no data moves.  Per elimination step:
+// the pivot is the active row (position >= k) of max |a_rk|, ties to the
+// smaller position (a total order, so the warp's xor-tree gives the same row
+// as warp_lu_solve_rm's scan); its owner publishes the pivot row through
+// shared memory; every lane updates its rows below the pivot.  Each element
+// sees exactly warp_lu_solve_rm's operations in the same order (same
+// multipliers, same FMAs, same back substitution), so da is bit-identical —
+// at ~1/4 of the warp instructions, with no shared-memory round trip on the
+// critical path of the rank-1 updates.
+template <int N>
+__global__ void __launch_bounds__(32) k_rom_solve_reg(NewtonArgs g) {
+  constexpr int R = (N + 31) / 32;  // rows per lane
+  constexpr int W = N + 1;          // columns: K and the right-hand side
+  constexpr int kNone = 1 << 20;    // position tag of an empty slot
+  __shared__ __align__(16) double piv[W + 1];
+  __shared__ double xs[N];
+  const int lane = threadIdx.x;
+  const int j = blockIdx.x;
+  if (j >= *g.count) return;
+  const int64_t s = g.list[j];
+  RomCtl* c = g.ctl + s;
+  if (c->asm_fail != 0) {
+    rom_failed(g, c, s, lane);
+    return;
+  }
+  const int it = c->it;
+  double a[R][W];
+  int pos[R];
+  const double* src = g.Kg + (size_t)s * N * N;
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    const int row = lane + 32 * t;
+    const bool ok = row < N;
+    pos[t] = ok ? row : kNone;
+    const double* rp = src + (size_t)(ok ? row : 0) * N;
+    if constexpr ((N & 1) == 0) {
+#pragma unroll
+      for (int q = 0; q < N; q += 2) {
+        const double2 v = ok ? __ldcs(reinterpret_cast<const double2*>(rp + q)) : make_double2(0.0, 0.0);
+        a[t][q] = v.x;
+        a[t][q + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < N; ++q) a[t][q] = ok ? __ldcs(rp + q) : 0.0;
+    }
+    a[t][N] = ok ? -g.f[(size_t)s * N + row] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    // pivot: max |a_rk| over active rows, ties to the smaller position
+    double bv = -1.0;
+    int bp = kNone;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const double v = fabs(a[t][k]);
+      const bool act = pos[t] >= k && pos[t] < N;
+      if (act && (v > bv || (v == bv && pos[t] < bp))) {
+        bv = v;
+        bp = pos[t];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+      if (ov > bv || (ov == bv && op < bp)) {
+        bv = ov;
+        bp = op;
+      }
+    }
+    const int p = bp < N ? bp : k;  // all-NaN column: no exchange (the result is NaN anyway)
+    // the pivot row's owner publishes columns k .. N (pairs from an even
+    // column; constant loop bounds so every register index is static once
+    // the k loop is unrolled)
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      if (pos[t] == p) {
+#pragma unroll
+        for (int q = 0; q < W; q += 2) {
+          if (q + 1 >= k) {
+            if (q + 1 < W)
+              *reinterpret_cast<double2*>(piv + q) = make_double2(a[t][q], a[t][q + 1]);
+            else
+              piv[q] = a[t][q];
+          }
+        }
+      }
+    }
+    // exchange the position tags of rows k and p
+#pragma unroll
+    for (int t = 0; t < R; ++t) pos[t] = pos[t] == k ? p : (pos[t] == p ? k : pos[t]);
+    __syncwarp();
+    const double d = piv[k];
+    const double rd = __drcp_rn(d);
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      if (pos[t] > k && pos[t] < N) {
+        const double l = bv != 0.0 ? div_rcp(a[t][k], d, rd) : a[t][k];
+        a[t][k] = l;
+#pragma unroll
+        for (int q = 0; q < W; ++q)
+          if (q > k) a[t][q] = fma(-l, piv[q], a[t][q]);
+      }
+    }
+    __syncwarp();
+  }
+  // back substitution with U (positions descending)
+#pragma unroll
+  for (int k = N - 1; k >= 0; --k) {
+    double uk = 0.0, bk = 0.0;
+    bool own = false;
+#pragma unroll
+    for (int t = 0; t < R; ++t)
+      if (pos[t] == k) {
+        own = true;
+        uk = a[t][k];
+        bk = a[t][N];
+      }
+    const unsigned m = __ballot_sync(0xffffffffu, own);
+    const int owner = __ffs(m) - 1;
+    const double xo = div_rcp(bk, uk, __drcp_rn(uk));
+    const double x = __shfl_sync(0xffffffffu, xo, owner);
+    if (lane == 0) xs[k] = x;
+#pragma unroll
+    for (int t = 0; t < R; ++t)
+      if (pos[t] < k) a[t][N] = fma(-a[t][k], x, a[t][N]);
+  }
+  __syncwarp();
+  for (int i = lane; i < N; i += 32) g.a[(size_t)s * N + i] += xs[i];
+  if (lane == 0) c->it = it + 1;
+}
+
+// Newton update kernel of the lazy pipeline: the register-resident LU for the
+// mode counts it is instantiated for, the shared-memory LU otherwise
+// (PODECM_ROM_LU=smem forces the latter, for A/B comparisons).
+bool rom_lu_reg() {
+  static bool v = [] {
+    const char* e = getenv("PODECM_ROM_LU");
+    return !(e && std::strcmp(e, "smem") == 0);
+  }();
+  return v;
+}
+
 
 // ---- effective stiffness (rom_effective_stiffness, rom.cpp:202-241) -------
 // Per instance: K (k_rom_contract at the frozen history), then for the four
@@ -1860,7 +2007,10 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
       launch_contract(ctx, s, r, cr);
       {
         KTimer kt(ctx, s, "k_rom_solve");
-        k_rom_solve<<<(int)n_run, 32, (size_t)((size_t)N * (N + 1) + 2 * N) * sizeof(double), s>>>(na);
+        if (N == 50 && rom_lu_reg())
+          k_rom_solve_reg<50><<<(int)n_run, 32, 0, s>>>(na);
+        else
+          k_rom_solve<<<(int)n_run, 32, (size_t)((size_t)N * (N + 1) + 2 * N) * sizeof(double), s>>>(na);
       }
       PODECM_LAUNCHED(ctx, 6);
       r->last_global_iters = it + 1;
