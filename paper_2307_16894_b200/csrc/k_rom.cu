@@ -330,6 +330,108 @@ __global__ void __launch_bounds__(256) k_rom_F(PointArgs g) {
   }
 }
 
+// D += A B on one m8n8k4 f64 tile (mma.sync: DMMA; tcgen05 has no f64 kind)
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// The same F by FP64 tensor cores: U = A Gm^T with A the (instances x modes)
+// reduced coordinates and Gm the (4Q x N) mode-gradient stack (d_G, zero
+// padded), one DMMA GEMM tile per CTA (32 instances x 32 points = 128 point
+// rows, K = N rounded up to the k-step of 4), then F = Fbar + R(fmi)^T u per
+// (instance, point) from shared memory.  Same F formula as k_rom_F; u is
+// summed in the tensor cores' order instead of k_rom_F's sequential FMA chain
+// (agreement to rounding, well inside the ROM tolerance).
+constexpr int kFMI = 32;  // instances per CTA
+constexpr int kFMP = 32;  // points per CTA
+constexpr int kFUP = kFMP + 1;  // sU pitch per (instance, r): conflict-free lane = point reads
+
+__host__ __device__ inline int fmma_ld(int N) {
+  const int kp = (N + 3) & ~3;
+  return (kp & 7) == 4 ? kp : kp + 4;  // == 4 mod 8: conflict-free m8n8k4 fragment loads
+}
+__host__ __device__ inline size_t fmma_smem_doubles(int N) {
+  const int ld = fmma_ld(N);
+  const size_t b = (size_t)kFMP * 4 * ld, u = (size_t)kFMI * 4 * kFUP;
+  return (size_t)kFMI * ld + (b > u ? b : u);
+}
+
+__global__ void __launch_bounds__(256) k_rom_F_mma(PointArgs g, const double* __restrict__ G, int NP) {
+  extern __shared__ double sm[];
+  const int N = g.N, KP = (N + 3) & ~3, LD = fmma_ld(N);
+  double* sA = sm;                       // [kFMI][LD]   reduced coordinates
+  double* sB = sm + (size_t)kFMI * LD;   // [4 kFMP][LD] mode-gradient rows (p, r)
+  double* sU = sB;                       // [kFMI][4][kFUP] after the MMA
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int p0 = blockIdx.x * kFMP;
+  const int64_t s0 = (int64_t)blockIdx.y * kFMI;
+  {  // whole CTA idle (finished / failed instances): skip
+    __shared__ int any_active;
+    if (tid == 0) any_active = 0;
+    __syncthreads();
+    if (tid < kFMI && s0 + tid < g.n && g.ctl[inst_of(g.alist, s0 + tid)].active) any_active = 1;
+    __syncthreads();
+    if (!any_active) return;
+  }
+  for (int t = tid; t < kFMI * KP; t += 256) {
+    const int si = t / KP, k = t - si * KP;
+    double v = 0.0;
+    if (k < N && s0 + si < g.n) v = g.a[(size_t)inst_of(g.alist, s0 + si) * N + k];
+    sA[si * LD + k] = v;
+  }
+  const int R0 = p0 * 4, RQ = g.Qpad * 4;
+  for (int t = tid; t < kFMP * 4 * KP; t += 256) {
+    const int rr = t / KP, k = t - rr * KP;
+    sB[rr * LD + k] = R0 + rr < RQ ? __ldg(G + (size_t)(R0 + rr) * NP + k) : 0.0;
+  }
+  __syncthreads();
+  const int mt = warp & 3, nt0 = (warp >> 2) * 8;
+  double acc[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int ks = 0; ks < KP; ks += 4) {
+    const double afr = sA[(mt * 8 + gid) * LD + ks + tig];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dmma(acc[j][0], acc[j][1], afr, sB[((nt0 + j) * 8 + gid) * LD + ks + tig]);
+  }
+  __syncthreads();  // sB is reused as sU
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int row = (nt0 + j) * 8 + 2 * tig + h;  // point-row (pl, r) of the tile
+      sU[((mt * 8 + gid) * 4 + (row & 3)) * kFUP + (row >> 2)] = acc[j][h];
+    }
+  __syncthreads();
+  const int p = p0 + lane;
+  if (p >= g.Q) return;
+#pragma unroll
+  for (int q = 0; q < kFMI / 8; ++q) {
+    const int si = warp + 8 * q;
+    if (s0 + si >= g.n) break;
+    const int64_t s = inst_of(g.alist, s0 + si);
+    const RomCtl* c = g.ctl + s;
+    if (!c->active) continue;
+    double u[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) u[r] = sU[(si * 4 + r) * kFUP + lane];
+    const double* mo = g.morph + (size_t)s * 5 * g.Q;
+    double m[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) m[t] = mo[(size_t)t * g.Q + p];
+    const int top = c->sp - 1;
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+      for (int l = 0; l < 2; ++l)
+        g.Fb[((size_t)s * 4 + ii + 2 * l) * g.Q + p] =
+            c->fstack[top][4 + ii + 2 * l] + (u[ii] * m[2 * l] + u[ii + 2] * m[1 + 2 * l]);
+  }
+}
+
 // Material at every ECM point (one thread per point, C1-style register
 // budget): P, FD tangent, trial history, then the mapped operators
 // At = c R A R^T and Pt = c R P.  ABAR (rom_effective_stiffness,
@@ -463,11 +565,6 @@ struct ContractArgs {
   const int* count;
 };
 
-__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
 
 // Software-pipelined over chunks of kPC points: while the warps run the DMMA
 // k-steps of chunk c they also build Y for chunk c+1 (independent SMEM
@@ -1730,6 +1827,7 @@ void set_attrs() {
   std::lock_guard<std::mutex> lock(mu);
   if (dev < 64 && (done >> dev) & 1u) return;
   cudaFuncSetAttribute(k_rom_F, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_rom_F_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   set_contract_attrs<false>(std::make_integer_sequence<int, kMaxNT + 1>{});
   set_contract_attrs<true>(std::make_integer_sequence<int, kMaxNT + 1>{});
   cudaFuncSetAttribute(k_rom_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1782,8 +1880,23 @@ ContractArgs contract_args(podecm_rom* r, int64_t n) {
   return ca;
 }
 
+// F at the ECM points: the DMMA form by default; PODECM_ROM_F=fma selects the
+// DFMA kernel (k_rom_F) for A/B comparisons.
+bool rom_F_mma() {
+  static bool v = [] {
+    const char* e = getenv("PODECM_ROM_F");
+    return !(e && std::strcmp(e, "fma") == 0);
+  }();
+  return v;
+}
+
 void launch_F(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, const PointArgs& pa) {
   KTimer kt(ctx, s, "k_rom_F");
+  if (rom_F_mma()) {
+    const dim3 g((r->Q + kFMP - 1) / kFMP, (unsigned)((pa.n + kFMI - 1) / kFMI));
+    k_rom_F_mma<<<g, 256, fmma_smem_doubles(r->N) * sizeof(double), s>>>(pa, r->d_G, r->NP);
+    return;
+  }
   const dim3 gpt((r->Q + kPtsTile - 1) / kPtsTile, (unsigned)((pa.n + kFInst - 1) / kFInst));
   const size_t smem_pt = ((size_t)r->N * 4 * kPtsTile + (size_t)kFInst * r->N) * sizeof(double);
   k_rom_F<<<gpt, 256, smem_pt, s>>>(pa);
