@@ -369,36 +369,4 @@ GM_HD void log_pair(double x0, double x1, double& r0, double& r1) {
 #endif
 }
 
-// Warp-uniform form: each path runs only if some active lane of the warp
-// needs it (a vote per path), so a warp whose arguments all take the same
-// path evaluates that path alone.  Results are log_pair's bit for bit (the
-// same path functions, the same selection).  Pays off where the caller has
-// grouped its arguments by path (k_material_sorted: points partitioned by
-// the near-1 class of their trial eigenvalues); in a mixed warp it costs the
-// four votes on top of log_pair.
-GM_HD void log_pair_warp(double x0, double x1, double& r0, double& r1) {
-#ifndef __CUDA_ARCH__
-  r0 = gm::log(x0);
-  r1 = gm::log(x1);
-#else
-  const uint64_t i0 = bits(x0), i1 = bits(x1);
-  const bool n0 = log_near1(i0), n1 = log_near1(i1);
-  const unsigned m = __activemask();
-  double g0 = 0.0, g1 = 0.0, v0 = 0.0, v1 = 0.0;
-  if (__any_sync(m, !n0)) g0 = log_general(i0);
-  if (__any_sync(m, !n1)) g1 = log_general(i1);
-  if (__any_sync(m, n0)) v0 = log_near(x0);
-  if (__any_sync(m, n1)) v1 = log_near(x1);
-  r0 = n0 ? v0 : g0;
-  r1 = n1 ? v1 : g1;
-  if (!(log_main_ok(x0) && log_main_ok(x1))) {
-    r0 = gm::log(x0);
-    r1 = gm::log(x1);
-  }
-#endif
-}
-
-// near-1 class of an argument (the path log / log_pair take for it)
-GM_HD bool log_is_near1(double x) { return log_near1(bits(x)); }
-
 }  // namespace gm
