@@ -376,16 +376,40 @@ __global__ void __launch_bounds__(256) k_rom_F_mma(PointArgs g, const double* __
     __syncthreads();
     if (!any_active) return;
   }
-  for (int t = tid; t < kFMI * KP; t += 256) {
-    const int si = t / KP, k = t - si * KP;
-    double v = 0.0;
-    if (k < N && s0 + si < g.n) v = g.a[(size_t)inst_of(g.alist, s0 + si) * N + k];
-    sA[si * LD + k] = v;
+  // staging: each thread's loads are all issued before its shared-memory
+  // stores (kFB in flight), so the tile arrives at memory-level parallelism
+  // rather than one dependent round trip per element
+  constexpr int kFB = 8;
+  for (int t0 = 0; t0 < kFMI * KP; t0 += 256 * kFB) {
+    double v[kFB];
+#pragma unroll
+    for (int u = 0; u < kFB; ++u) {
+      const int t = t0 + u * 256 + tid;
+      const int si = t / KP, k = t - si * KP;
+      v[u] = (t < kFMI * KP && k < N && s0 + si < g.n) ? g.a[(size_t)inst_of(g.alist, s0 + si) * N + k] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kFB; ++u) {
+      const int t = t0 + u * 256 + tid;
+      const int si = t / KP, k = t - si * KP;
+      if (t < kFMI * KP) sA[si * LD + k] = v[u];
+    }
   }
   const int R0 = p0 * 4, RQ = g.Qpad * 4;
-  for (int t = tid; t < kFMP * 4 * KP; t += 256) {
-    const int rr = t / KP, k = t - rr * KP;
-    sB[rr * LD + k] = R0 + rr < RQ ? __ldg(G + (size_t)(R0 + rr) * NP + k) : 0.0;
+  for (int t0 = 0; t0 < kFMP * 4 * KP; t0 += 256 * kFB) {
+    double v[kFB];
+#pragma unroll
+    for (int u = 0; u < kFB; ++u) {
+      const int t = t0 + u * 256 + tid;
+      const int rr = t / KP, k = t - rr * KP;
+      v[u] = (t < kFMP * 4 * KP && R0 + rr < RQ) ? __ldg(G + (size_t)(R0 + rr) * NP + k) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kFB; ++u) {
+      const int t = t0 + u * 256 + tid;
+      const int rr = t / KP, k = t - rr * KP;
+      if (t < kFMP * 4 * KP) sB[rr * LD + k] = v[u];
+    }
   }
   __syncthreads();
   const int mt = warp & 3, nt0 = (warp >> 2) * 8;
@@ -408,27 +432,36 @@ __global__ void __launch_bounds__(256) k_rom_F_mma(PointArgs g, const double* __
   __syncthreads();
   const int p = p0 + lane;
   if (p >= g.Q) return;
+  // the warp's instances: control words and morph loads issued up front
+  int64_t sq[kFMI / 8];
+  bool act[kFMI / 8];
+  int top[kFMI / 8];
+  double m[kFMI / 8][4];
 #pragma unroll
   for (int q = 0; q < kFMI / 8; ++q) {
     const int si = warp + 8 * q;
-    if (s0 + si >= g.n) break;
-    const int64_t s = inst_of(g.alist, s0 + si);
+    sq[q] = s0 + si < g.n ? inst_of(g.alist, s0 + si) : -1;
+    act[q] = sq[q] >= 0 && g.ctl[sq[q]].active;
+    top[q] = act[q] ? g.ctl[sq[q]].sp - 1 : 0;
+    const double* mo = g.morph + (size_t)(act[q] ? sq[q] : 0) * 5 * g.Q;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) m[q][t] = act[q] ? mo[(size_t)t * g.Q + p] : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < kFMI / 8; ++q) {
+    const int si = warp + 8 * q;
+    if (!act[q]) continue;
+    const int64_t s = sq[q];
     const RomCtl* c = g.ctl + s;
-    if (!c->active) continue;
     double u[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) u[r] = sU[(si * 4 + r) * kFUP + lane];
-    const double* mo = g.morph + (size_t)s * 5 * g.Q;
-    double m[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) m[t] = mo[(size_t)t * g.Q + p];
-    const int top = c->sp - 1;
 #pragma unroll
     for (int ii = 0; ii < 2; ++ii)
 #pragma unroll
       for (int l = 0; l < 2; ++l)
         g.Fb[((size_t)s * 4 + ii + 2 * l) * g.Q + p] =
-            c->fstack[top][4 + ii + 2 * l] + (u[ii] * m[2 * l] + u[ii + 2] * m[1 + 2 * l]);
+            c->fstack[top[q]][4 + ii + 2 * l] + (u[ii] * m[q][2 * l] + u[ii + 2] * m[q][1 + 2 * l]);
   }
 }
 

@@ -19,7 +19,7 @@
     }                                                              \
   } while (0)
 
-int main() {
+int main(int argc, char** argv) {
   podecm_ctx* ctx = nullptr;
   if (podecm_ctx_create(0, &ctx)) {
     std::printf("FAIL ctx\n");
@@ -85,6 +85,15 @@ int main() {
   const bool ok2 = finite && kn > 0 && fn > 0;  // heterogeneous cell: nonzero residual
   std::printf("assembly: n_red %lld nnz %lld |f| %.6e |K| %.6e %s\n", (long long)nr, (long long)nnz,
               std::sqrt(fn), std::sqrt(kn), ok2 ? "ok" : "FAIL");
+  if (argc > 1) {  // the caller (tests/test_gpu_capi_cpp.py) checks f and K against the oracle
+    if (FILE* fo = std::fopen(argv[1], "wb")) {
+      const int64_t hdr[2] = {nr, nnz};
+      std::fwrite(hdr, sizeof(int64_t), 2, fo);
+      std::fwrite(hf.data(), sizeof(double), hf.size(), fo);
+      std::fwrite(hK.data(), sizeof(double), hK.size(), fo);
+      std::fclose(fo);
+    }
+  }
   std::printf("launches: %lld\n", (long long)podecm_launch_count(ctx));
   podecm_rve_destroy(rve);
   podecm_ctx_destroy(ctx);
