@@ -2,13 +2,16 @@
 // run_twoscale (/root/reference/proj/src/twoscale.cpp:131-242) on the
 // structured Quad8 plate of MacroConfig (twoscale.hpp:82-94).
 //
-// Per macro Newton iteration the deformation gradients of all macro Gauss
-// points go to the batched RomMicroEngine in ONE respond call (GPU: reduced
-// Newton + effective stiffness of every point), the macro residual and
-// tangent are assembled on the host from (Pbar, Abar) in the reference's
-// loop order, and the macro system (a few thousand dofs) is solved by a
-// dense LU on the device (cuSOLVER getrf/getrs standing in for
-// Eigen::SparseLU).  The mesh pieces restate structured_quad8
+// Per macro Newton iteration everything stays on the device: F at all macro
+// Gauss points (k_macro_F), ONE batched RomMicroEngine respond (reduced Newton
+// + effective stiffness of every point), the macro residual and its norm
+// (k_macro_res, k_macro_norm) and, when Newton goes on, the tangent
+// contributions (k_macro_con) summed into the dense K (k_macro_gather), each
+// in the reference loop's operation order, and the macro system (a few
+// thousand dofs) solved by a dense LU (cuSOLVER getrf/getrs standing in for
+// Eigen::SparseLU).  The host reads back two scalars per iteration (the
+// residual norm for the convergence test, the first failed engine) and the
+// displacement once per load step (compliance).  The mesh pieces restate structured_quad8
 // (meshgen.cpp:72-113), the Quad8 shape functions and 2x2 rule
 // (mesh.cpp:24-83), build_quad_cache (mesh.cpp:412-451),
 // dirichlet_dof_map (mesh.cpp:374-386), boundary_edges (mesh.cpp:118-136),
@@ -19,6 +22,7 @@
 #include <array>
 #include <cmath>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -229,6 +233,119 @@ __global__ void k_macro_gather(int n_ent, const int64_t* ent, const int32_t* ptr
   K[ent[e]] = v;
 }
 
+// ---- the macro assembly on the device (twoscale.cpp:150-204) ---------------
+// Each kernel keeps the reference loop's operation order per output value, so
+// the macro residual, its norm and the tangent contributions are the values
+// the host loop computes.
+
+// F = I + h at every macro Gauss point, h(i, j) = sum_a u(node_a, i) g_a(j)
+// over the element's 8 nodes in order (constrained nodes contribute u = 0).
+__global__ void k_macro_F(int nq, const int32_t* __restrict__ qdof, const double* __restrict__ grad,
+                          const double* __restrict__ u, double* __restrict__ F) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  double h[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int a = 0; a < 8; ++a) {
+    const int d = qdof[8 * q + a];
+    const double ua[2] = {d >= 0 ? u[d] : 0.0, d >= 0 ? u[d + 1] : 0.0};
+    const double* g = grad + ((size_t)q * 8 + a) * 2;
+    for (int i = 0; i < 2; ++i)
+      for (int j = 0; j < 2; ++j) h[i][j] += ua[i] * g[j];
+  }
+  F[4 * (size_t)q + 0] = 1.0 + h[0][0];
+  F[4 * (size_t)q + 1] = 0.0 + h[1][0];
+  F[4 * (size_t)q + 2] = 0.0 + h[0][1];
+  F[4 * (size_t)q + 3] = 1.0 + h[1][1];
+}
+
+// LinearElasticEngine (twoscale.cpp:17-20): pbar = D : (F - I), abar = D.
+struct Dlin {
+  double d[16];
+};
+__global__ void k_macro_linear(int nq, Dlin D, const double* __restrict__ F, double* __restrict__ P,
+                               double* __restrict__ A) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  const double* f = F + 4 * (size_t)q;
+  const double dfl[4] = {f[0] - 1.0, f[1] - 0.0, f[2] - 0.0, f[3] - 1.0};
+  for (int r = 0; r < 4; ++r) {
+    double v = 0.0;
+    for (int t = 0; t < 4; ++t) v += D.d[r + 4 * t] * dfl[t];
+    P[4 * (size_t)q + r] = v;
+  }
+  for (int t = 0; t < 16; ++t) A[16 * (size_t)q + t] = D.d[t];
+}
+
+// Residual of every free node: fint summed over its (q, a) incidences in the
+// host loop's order (increasing q, from 0), minus factor fext; b = -res is the
+// right-hand side of the Newton solve.
+__global__ void k_macro_res(int n_free, const int32_t* __restrict__ fnode_dof, const int32_t* __restrict__ nptr,
+                            const int32_t* __restrict__ nitem, const double* __restrict__ grad,
+                            const double* __restrict__ w, const double* __restrict__ P,
+                            const double* __restrict__ fext, double factor, double* __restrict__ res,
+                            double* __restrict__ b) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_free) return;
+  double f0 = 0.0, f1 = 0.0;
+  for (int k = nptr[i]; k < nptr[i + 1]; ++k) {
+    const int it = nitem[k], q = it >> 3;
+    const double* pb = P + 4 * (size_t)q;
+    const double* ga = grad + (size_t)it * 2;
+    const double wq = w[q];
+    f0 += wq * (pb[0] * ga[0] + pb[2] * ga[1]);
+    f1 += wq * (pb[1] * ga[0] + pb[3] * ga[1]);
+  }
+  const int d = fnode_dof[i];
+  const double r0 = f0 - factor * fext[d], r1 = f1 - factor * fext[d + 1];
+  res[d] = r0;
+  res[d + 1] = r1;
+  b[d] = -r0;
+  b[d + 1] = -r1;
+}
+
+// ||res|| (sequential sum in dof order, as the host loop) and the first failed
+// engine (-1 if none): one thread.
+__global__ void k_macro_norm(int n, const double* __restrict__ res, int nq, const int32_t* __restrict__ st,
+                             double* __restrict__ out_rn, int* __restrict__ out_fail) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double rn = 0.0;
+  for (int i = 0; i < n; ++i) rn += res[i] * res[i];
+  *out_rn = sqrt(rn);
+  int f = -1;
+  if (st)
+    for (int q = 0; q < nq; ++q)
+      if (st[q]) {
+        f = q;
+        break;
+      }
+  *out_fail = f;
+}
+
+// Tangent contributions w (g_a^T A g_b)(r, sc) of every (q, a, b) with both
+// dofs free, in the host loop's (q, a, b, r, sc) order.
+__global__ void k_macro_con(int n_pairs, const int32_t* __restrict__ pairs, const double* __restrict__ grad,
+                            const double* __restrict__ w, const double* __restrict__ A, double* __restrict__ con) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_pairs) return;
+  const int pk = pairs[t], q = pk >> 6, a = (pk >> 3) & 7, bb = pk & 7;
+  const double* ab = A + 16 * (size_t)q;
+  const double* ga = grad + ((size_t)q * 8 + a) * 2;
+  const double* gb = grad + ((size_t)q * 8 + bb) * 2;
+  const double wq = w[q];
+  for (int r = 0; r < 2; ++r)
+    for (int sc = 0; sc < 2; ++sc) {
+      double v = 0.0;
+      for (int c = 0; c < 2; ++c)
+        for (int d = 0; d < 2; ++d) v += ga[c] * ab[(r + 2 * c) + 4 * (sc + 2 * d)] * gb[d];
+      con[4 * (size_t)t + 2 * r + sc] = wq * v;
+    }
+}
+
+__global__ void k_macro_update(int n, double* __restrict__ u, const double* __restrict__ du) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) u[i] += du[i];
+}
+
 }  // namespace
 
 extern "C" {
@@ -321,13 +438,12 @@ int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* c
   const int n_ent = (int)ent.size();
   int64_t* d_ent = nullptr;
   int32_t *d_eptr = nullptr, *d_eidx = nullptr;
-  double *d_con = nullptr, *h_con = nullptr;
+  double* d_con = nullptr;
   {
     cudaError_t e2 = cudaMalloc(&d_ent, sizeof(int64_t) * std::max(n_ent, 1));
     if (!e2) e2 = cudaMalloc(&d_eptr, sizeof(int32_t) * (n_ent + 1));
     if (!e2) e2 = cudaMalloc(&d_eidx, sizeof(int32_t) * std::max<int64_t>(n_con, 1));
     if (!e2) e2 = cudaMalloc(&d_con, sizeof(double) * std::max<int64_t>(n_con, 1));
-    if (!e2) e2 = cudaMallocHost(&h_con, sizeof(double) * std::max<int64_t>(n_con, 1));
     if (!e2 && n_ent) e2 = cudaMemcpy(d_ent, ent.data(), sizeof(int64_t) * n_ent, cudaMemcpyHostToDevice);
     if (!e2) e2 = cudaMemcpy(d_eptr, eptr.data(), sizeof(int32_t) * (n_ent + 1), cudaMemcpyHostToDevice);
     if (!e2 && n_con) e2 = cudaMemcpy(d_eidx, order.data(), sizeof(int32_t) * n_con, cudaMemcpyHostToDevice);
@@ -336,7 +452,6 @@ int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* c
       cudaFree(d_eptr);
       cudaFree(d_eidx);
       cudaFree(d_con);
-      cudaFreeHost(h_con);
       cleanup();
       return cuda_err(ctx, e2, "twoscale: macro gather map");
     }
@@ -346,11 +461,70 @@ int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* c
     cudaFree(d_eptr);
     cudaFree(d_eidx);
     cudaFree(d_con);
-    cudaFreeHost(h_con);
   };
-  std::vector<double> u(n, 0.0), ufull(2 * (size_t)m.n_nodes), F(4 * (size_t)nq), P(4 * (size_t)nq),
-      A(16 * (size_t)nq), fint(2 * (size_t)m.n_nodes), res(n);
-  std::vector<int32_t> st(nq);
+  // ---- device-resident macro state and the maps of the device assembly
+  std::vector<int32_t> qdof((size_t)nq * 8);
+  for (int q = 0; q < nq; ++q)
+    for (int a = 0; a < 8; ++a) qdof[8 * (size_t)q + a] = m.node_dof[m.elems[8 * m.elem_of[q] + a]];
+  std::vector<int32_t> fnode_dof, nptr(1, 0), nitem;  // free nodes: incidences (q, a) in q order
+  {
+    std::vector<std::vector<int32_t>> inc(m.n_nodes);
+    for (int q = 0; q < nq; ++q)
+      for (int a = 0; a < 8; ++a) inc[m.elems[8 * m.elem_of[q] + a]].push_back(8 * q + a);
+    for (int i = 0; i < m.n_nodes; ++i) {
+      if (m.node_dof[i] < 0) continue;
+      fnode_dof.push_back(m.node_dof[i]);
+      nitem.insert(nitem.end(), inc[i].begin(), inc[i].end());
+      nptr.push_back((int32_t)nitem.size());
+    }
+  }
+  std::vector<int32_t> pairs;  // (q, a, b) with both dofs free, host loop order
+  for (int q = 0; q < nq; ++q)
+    for (int a = 0; a < 8; ++a) {
+      if (qdof[8 * (size_t)q + a] < 0) continue;
+      for (int b = 0; b < 8; ++b)
+        if (qdof[8 * (size_t)q + b] >= 0) pairs.push_back((q << 6) | (a << 3) | b);
+    }
+  const int n_free = (int)fnode_dof.size(), n_pairs = (int)pairs.size();
+  int32_t *d_qdof = nullptr, *d_fnd = nullptr, *d_nptr = nullptr, *d_nitem = nullptr, *d_pairs = nullptr;
+  double *d_grad = nullptr, *d_w = nullptr, *d_fext = nullptr, *d_u = nullptr, *d_res = nullptr,
+         *d_scal = nullptr, *h_scal = nullptr;
+  auto cleanup_dev = [&]() {
+    for (void* p : {(void*)d_qdof, (void*)d_fnd, (void*)d_nptr, (void*)d_nitem, (void*)d_pairs, (void*)d_grad,
+                    (void*)d_w, (void*)d_fext, (void*)d_u, (void*)d_res, (void*)d_scal})
+      cudaFree(p);
+    cudaFreeHost(h_scal);
+  };
+  {
+    auto upl = [&](auto** d, const auto& h) -> cudaError_t {
+      using T = std::remove_reference_t<decltype(h[0])>;
+      cudaError_t e = cudaMalloc(d, std::max<size_t>(1, h.size()) * sizeof(T));
+      if (!e && !h.empty()) e = cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+      return e;
+    };
+    cudaError_t e2 = upl(&d_qdof, qdof);
+    if (!e2) e2 = upl(&d_fnd, fnode_dof);
+    if (!e2) e2 = upl(&d_nptr, nptr);
+    if (!e2) e2 = upl(&d_nitem, nitem);
+    if (!e2) e2 = upl(&d_pairs, pairs);
+    if (!e2) e2 = upl(&d_grad, m.grad);
+    if (!e2) e2 = upl(&d_w, m.w);
+    if (!e2) e2 = upl(&d_fext, fext);
+    if (!e2) e2 = cudaMalloc(&d_u, sizeof(double) * std::max(n, 1));
+    if (!e2) e2 = cudaMemset(d_u, 0, sizeof(double) * std::max(n, 1));
+    if (!e2) e2 = cudaMalloc(&d_res, sizeof(double) * std::max(n, 1));
+    if (!e2) e2 = cudaMalloc(&d_scal, sizeof(double) * 2);
+    if (!e2) e2 = cudaMallocHost(&h_scal, sizeof(double) * 2);
+    if (e2) {
+      cleanup_dev();
+      cleanup_map();
+      cleanup();
+      return cuda_err(ctx, e2, "twoscale: device macro maps");
+    }
+  }
+  Dlin dl;
+  std::copy(dlin, dlin + 16, dl.d);
+  std::vector<double> u(n, 0.0), ufull(2 * (size_t)m.n_nodes);
   int64_t evals = 0;
   const int up = steps / 2;
   auto expand = [&]() {
@@ -361,76 +535,46 @@ int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* c
         ufull[2 * (size_t)i + 1] = u[m.node_dof[i] + 1];
       }
   };
+  // every copy, launch and factorisation is checked (an error ends the run
+  // with PODECM_ECUDA after the common cleanup)
+  auto cu = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && !rc) rc = cuda_err(ctx, e, what);
+  };
+  const int gq = (nq + 127) / 128;
   for (int step = 0; rc == PODECM_OK && step < steps; ++step) {
     const double factor = step < up ? (double)(step + 1) / up : (double)(steps - 1 - step) / (steps - up);
     double tol = cfg->newton.eps_abs;
     int it_done = 0;
     for (int it = 0;; ++it) {
-      expand();
-      // F = I + h at every macro Gauss point, h(i, j) = sum_a u(node_a, i) g_a(j)
-      for (int q = 0; q < nq; ++q) {
-        const int e = m.elem_of[q];
-        double h[2][2] = {{0, 0}, {0, 0}};
-        for (int a = 0; a < 8; ++a) {
-          const int nd = m.elems[8 * e + a];
-          for (int i = 0; i < 2; ++i)
-            for (int j = 0; j < 2; ++j) h[i][j] += ufull[2 * (size_t)nd + i] * m.grad[((size_t)q * 8 + a) * 2 + j];
-        }
-        F[4 * (size_t)q + 0] = 1.0 + h[0][0];
-        F[4 * (size_t)q + 1] = 0.0 + h[1][0];
-        F[4 * (size_t)q + 2] = 0.0 + h[0][1];
-        F[4 * (size_t)q + 3] = 1.0 + h[1][1];
-      }
-      // MicroEngine::respond for every macro Gauss point at once
+      // F at every macro Gauss point, then MicroEngine::respond for all of them at once
+      k_macro_F<<<gq, 128, 0, s>>>(nq, d_qdof, d_grad, d_u, d_F);
+      cu(cudaGetLastError(), "k_macro_F launch");
       if (eng) {
-        cudaMemcpyAsync(d_F, F.data(), sizeof(double) * 4 * nq, cudaMemcpyHostToDevice, s);
-        rc = podecm_rom_engines_respond(ctx, stream, eng, d_F, micro_opts, d_P, d_A, nullptr, d_st);
-        if (rc) break;
-        cudaMemcpyAsync(P.data(), d_P, sizeof(double) * 4 * nq, cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(A.data(), d_A, sizeof(double) * 16 * nq, cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(st.data(), d_st, sizeof(int32_t) * nq, cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
-        for (int q = 0; q < nq; ++q)
-          if (st[q]) {
-            rc = set_err(ctx, PODECM_ESOLVE, "twoscale: micro engine " + std::to_string(q) + " failed");
-            break;
-          }
-        if (rc) break;
-      } else {  // LinearElasticEngine (twoscale.cpp:17-20): pbar = D : (F - I), abar = D
-        for (int q = 0; q < nq; ++q) {
-          double dfl[4] = {F[4 * (size_t)q] - 1.0, F[4 * (size_t)q + 1] - 0.0, F[4 * (size_t)q + 2] - 0.0,
-                           F[4 * (size_t)q + 3] - 1.0};
-          for (int r = 0; r < 4; ++r) {
-            double v = 0.0;
-            for (int t = 0; t < 4; ++t) v += dlin[r + 4 * t] * dfl[t];
-            P[4 * (size_t)q + r] = v;
-          }
-          std::copy(dlin, dlin + 16, &A[16 * (size_t)q]);
-        }
+        if (!rc) rc = podecm_rom_engines_respond(ctx, stream, eng, d_F, micro_opts, d_P, d_A, nullptr, d_st);
+      } else {
+        k_macro_linear<<<gq, 128, 0, s>>>(nq, dl, d_F, d_P, d_A);
+        cu(cudaGetLastError(), "k_macro_linear launch");
       }
+      if (rc) break;
       evals += nq;
-      // macro residual (twoscale.cpp:171-204); the tangent only if Newton goes on
-      std::fill(fint.begin(), fint.end(), 0.0);
-      for (int q = 0; q < nq; ++q) {
-        const int e = m.elem_of[q];
-        const double w = m.w[q];
-        const double* pb = &P[4 * (size_t)q];
-        for (int a = 0; a < 8; ++a) {
-          const int na = m.elems[8 * e + a];
-          const double* ga = &m.grad[((size_t)q * 8 + a) * 2];
-          fint[2 * (size_t)na] += w * (pb[0] * ga[0] + pb[2] * ga[1]);
-          fint[2 * (size_t)na + 1] += w * (pb[1] * ga[0] + pb[3] * ga[1]);
-        }
+      // macro residual (twoscale.cpp:171-204) and its norm; the tangent only if Newton goes on
+      if (n_free > 0) {
+        k_macro_res<<<(n_free + 127) / 128, 128, 0, s>>>(n_free, d_fnd, d_nptr, d_nitem, d_grad, d_w, d_P, d_fext,
+                                                         factor, d_res, d_b);
+        cu(cudaGetLastError(), "k_macro_res launch");
       }
-      double rn = 0.0;
-      for (int i = 0; i < m.n_nodes; ++i)
-        if (m.node_dof[i] >= 0)
-          for (int c = 0; c < 2; ++c) {
-            const int d = m.node_dof[i] + c;
-            res[d] = fint[2 * (size_t)i + c] - factor * fext[d];
-          }
-      for (int i = 0; i < n; ++i) rn += res[i] * res[i];
-      rn = std::sqrt(rn);
+      k_macro_norm<<<1, 32, 0, s>>>(n, d_res, nq, eng ? d_st : nullptr, d_scal, reinterpret_cast<int*>(d_scal + 1));
+      cu(cudaGetLastError(), "k_macro_norm launch");
+      cu(cudaMemcpyAsync(h_scal, d_scal, sizeof(double) * 2, cudaMemcpyDeviceToHost, s), "macro norm D2H");
+      cu(cudaStreamSynchronize(s), "macro residual");
+      ctx->launches += 4;
+      if (rc) break;
+      const int failed = *reinterpret_cast<const int*>(h_scal + 1);
+      if (failed >= 0) {
+        rc = set_err(ctx, PODECM_ESOLVE, "twoscale: micro engine " + std::to_string(failed) + " failed");
+        break;
+      }
+      const double rn = h_scal[0];
       if (it == 0) tol = std::max(cfg->newton.eps_rel * rn, cfg->newton.eps_abs);
       if (rn <= tol) {
         it_done = it;
@@ -440,63 +584,37 @@ int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* c
         rc = set_err(ctx, PODECM_ESOLVE, "macro Newton did not converge at step " + std::to_string(step));
         break;
       }
-      // dense K (column-major): contributions w v in the host loop order,
-      // summed per entry on the device in that order
-      {
-        int64_t t = 0;
-        for (int q = 0; q < nq; ++q) {
-          const int e = m.elem_of[q];
-          const double w = m.w[q];
-          const double* ab = &A[16 * (size_t)q];
-          for (int a = 0; a < 8; ++a) {
-            const int da = m.node_dof[m.elems[8 * e + a]];
-            if (da < 0) continue;
-            const double* ga = &m.grad[((size_t)q * 8 + a) * 2];
-            for (int b = 0; b < 8; ++b) {
-              const int db = m.node_dof[m.elems[8 * e + b]];
-              if (db < 0) continue;
-              const double* gb = &m.grad[((size_t)q * 8 + b) * 2];
-              for (int r = 0; r < 2; ++r)
-                for (int sc = 0; sc < 2; ++sc) {
-                  double v = 0.0;
-                  for (int c = 0; c < 2; ++c)
-                    for (int d = 0; d < 2; ++d) v += ga[c] * ab[(r + 2 * c) + 4 * (sc + 2 * d)] * gb[d];
-                  h_con[t++] = w * v;
-                }
-            }
-          }
-        }
+      // dense K (column-major): the contributions of the host loop order, summed
+      // per entry in that order (k_macro_gather), then K du = -res, u += du
+      if (n_pairs > 0) {
+        k_macro_con<<<(n_pairs + 127) / 128, 128, 0, s>>>(n_pairs, d_pairs, d_grad, d_w, d_A, d_con);
+        cu(cudaGetLastError(), "k_macro_con launch");
       }
-      for (int i = 0; i < n; ++i) res[i] = -res[i];
-      // every copy, launch and factorisation is checked (an error ends the
-      // run with PODECM_ECUDA after the common cleanup)
-      auto cu = [&](cudaError_t e, const char* what) {
-        if (e != cudaSuccess && !rc) rc = cuda_err(ctx, e, what);
-      };
-      cu(cudaMemcpyAsync(d_con, h_con, sizeof(double) * n_con, cudaMemcpyHostToDevice, s), "macro contributions H2D");
       cu(cudaMemsetAsync(d_K, 0, sizeof(double) * (size_t)n * n, s), "macro tangent clear");
       if (n_ent > 0) {  // all dofs constrained: nothing to gather
         k_macro_gather<<<(n_ent + 255) / 256, 256, 0, s>>>(n_ent, d_ent, d_eptr, d_eidx, d_con, d_K);
         cu(cudaGetLastError(), "k_macro_gather launch");
-        ctx->launches += 1;
       }
-      cu(cudaMemcpyAsync(d_b, res.data(), sizeof(double) * n, cudaMemcpyHostToDevice, s), "macro residual H2D");
       if (!rc && (cusolverDnDgetrf(dn, n, n, d_K, n, d_work, d_piv, d_info) != CUSOLVER_STATUS_SUCCESS ||
                   cusolverDnDgetrs(dn, CUBLAS_OP_N, n, 1, d_K, n, d_piv, d_b, n, d_info) != CUSOLVER_STATUS_SUCCESS))
         rc = set_err(ctx, PODECM_ECUDA, "macro tangent: cuSOLVER getrf/getrs failed");
+      k_macro_update<<<(n + 255) / 256, 256, 0, s>>>(n, d_u, d_b);
+      cu(cudaGetLastError(), "k_macro_update launch");
       int info = 0;
       cu(cudaMemcpyAsync(&info, d_info, sizeof(int), cudaMemcpyDeviceToHost, s), "macro info D2H");
-      cu(cudaMemcpyAsync(res.data(), d_b, sizeof(double) * n, cudaMemcpyDeviceToHost, s), "macro update D2H");
       cu(cudaStreamSynchronize(s), "macro solve");
+      ctx->launches += 3;
       if (rc) break;
       if (info != 0) {
         rc = set_err(ctx, PODECM_ESOLVE, "macro tangent factorization failed at step " + std::to_string(step));
         break;
       }
-      for (int i = 0; i < n; ++i) u[i] += res[i];
     }
     if (rc) break;
     if (eng) rc = podecm_rom_engines_commit(ctx, stream, eng);
+    cu(cudaMemcpyAsync(u.data(), d_u, sizeof(double) * n, cudaMemcpyDeviceToHost, s), "macro u D2H");
+    cu(cudaStreamSynchronize(s), "macro step");
+    if (rc) break;
     expand();
     double comp = 0.0;
     for (size_t i = 0; i < ufull.size(); ++i) comp += fext_full[i] * ufull[i];
@@ -513,6 +631,7 @@ int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* c
     if (micro_evals) *micro_evals = evals;
   }
   cudaStreamSynchronize(s);
+  cleanup_dev();
   cleanup_map();
   cleanup();
   return rc;
