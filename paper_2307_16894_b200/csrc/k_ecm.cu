@@ -23,6 +23,8 @@
 #include <algorithm>
 #include <cmath>
 #include <numeric>
+#include <unordered_map>
+#include <utility>
 #include <vector>
 
 #include "rve.cuh"
@@ -230,44 +232,106 @@ __global__ void __launch_bounds__(224) k_ecm_score(int64_t L, int nq, int N, con
 // instead of the N L 4 n_qp DMMA GEMM of a direct J^T r pass.
 constexpr int kGramSplit = 4;  // L-range splits (partials summed in fixed order)
 
-__global__ void __launch_bounds__(256) k_ecm_gram_col(int64_t L, int nq, int N, int sel, const double* H,
-                                                      const double* W, double* gpart) {
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= nq) return;
+// Gram columns (J^T J)[:, sel_c] for C <= kGramCols selected / speculative
+// points in ONE pass over W, on the FP64 tensor cores.  For a block of 64
+// candidates the 4x4 blocks mw(q, c) = sum_l W_q[l] W_sel_c[l]^T are one
+// DMMA GEMM: rows (q, c') of W^T (the W stream, each element loaded once,
+// 64 B runs), columns (c, d) of the staged selected rows, K = the snapshots
+// of this split.  An m8n8k4 f64 DMMA accumulates every element as the
+// sequential FMA chain over k, so mw is bit-identical to the scalar
+// fma(W_q[c'], W_sel[d], .) loop in snapshot order; mh (over the modes) and
+// g = sum_t fma(mh[t], mw[t], .) are then formed per (candidate, column)
+// exactly as in the single-column form.  Each column is therefore the value
+// a one-column pass produces.
+constexpr int kGramCols = 4;
+constexpr int kGramLC = 32;  // snapshots staged per round (multiple of 4)
+template <int C>
+__global__ void __launch_bounds__(256) k_ecm_gram_cols(int64_t L, int nq, int N, const int* __restrict__ sels,
+                                                       const double* H, const double* W, double* gpart) {
+  constexpr int NT = (C + 1) / 2;  // n-tiles: 2 columns x 4 components each
+  constexpr int MT = 4;            // m-tiles per warp: 4 x 8 rows = 8 candidates
+  __shared__ double sw[kGramLC][NT * 8 + 1];  // staged W_sel rows, column n = 4 c + d
+  __shared__ double se[64][C][17];            // mw of every (candidate, column)
+  __shared__ int ssel[C];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int q0 = blockIdx.x * 64;
   const int sp = blockIdx.y;
   const int64_t l0 = L * sp / kGramSplit, l1 = L * (sp + 1) / kGramSplit;
-  double mw[16];
+  if (threadIdx.x < C) ssel[threadIdx.x] = sels[threadIdx.x];
+  double acc[MT][NT][2];
 #pragma unroll
-  for (int t = 0; t < 16; ++t) mw[t] = 0.0;
-  const double2* Wq = reinterpret_cast<const double2*>(W) + 2 * (int64_t)q;
-  const double2* Ws = reinterpret_cast<const double2*>(W) + 2 * (int64_t)sel;
-#pragma unroll 4
-  for (int64_t l = l0; l < l1; ++l) {
-    const double2 a0 = __ldcs(Wq + 2 * l * nq), a1 = __ldcs(Wq + 2 * l * nq + 1);
-    const double2 b0 = __ldg(Ws + 2 * l * nq), b1 = __ldg(Ws + 2 * l * nq + 1);
-    const double av[4] = {a0.x, a0.y, a1.x, a1.y}, bv[4] = {b0.x, b0.y, b1.x, b1.y};
+  for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+  // A fragment rows: (q, c') = row r of the warp's 32 rows; W^T[(q, c')][l] = W[l][q][c']
+  const int64_t rowbase = (int64_t)(q0 + warp * 8) * 4;  // first (q, c') row of the warp
+  const int64_t nrow = (int64_t)nq * 4;
+  for (int64_t lb = l0; lb < l1; lb += kGramLC) {
+    const int nl = (int)((l1 - lb) < kGramLC ? (l1 - lb) : kGramLC);
+    __syncthreads();
+    for (int t = threadIdx.x; t < kGramLC * NT * 8; t += 256) {
+      const int lc = t / (NT * 8), n = t - lc * (NT * 8), c = n >> 2, d = n & 3;
+      sw[lc][n] = (lc < nl && c < C) ? __ldg(W + ((lb + lc) * nq + ssel[c]) * 4 + d) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int k0 = 0; k0 < nl; k0 += 4) {
+      const int lk = k0 + tig;  // this thread's k (snapshot) of the step
+      const bool kin = lk < nl;
+      double a[MT], b[NT];
 #pragma unroll
-      for (int d = 0; d < 4; ++d) mw[c * 4 + d] = fma(av[c], bv[d], mw[c * 4 + d]);
+      for (int mt = 0; mt < MT; ++mt) {
+        const int64_t row = rowbase + mt * 8 + gid;
+        a[mt] = (kin && row < nrow) ? __ldcs(W + (lb + lk) * nrow + row) : 0.0;
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) b[nt] = sw[lk < kGramLC ? lk : 0][nt * 8 + gid];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], kin ? b[nt] : 0.0);
+    }
   }
-  double mh[16];
+  // acc[mt][nt][h]: row (q, c') = warp*32 + mt*8 + gid, column n = nt*8 + 2 tig + h = 4 c + d
 #pragma unroll
-  for (int t = 0; t < 16; ++t) mh[t] = 0.0;
-  for (int i = 0; i < N; ++i) {
-    const double* hq = H + ((int64_t)q * N + i) * 4;
-    const double* hs = H + ((int64_t)sel * N + i) * 4;
-    const double av[4] = {hq[0], hq[1], hq[2], hq[3]};
-    const double bv[4] = {__ldg(hs), __ldg(hs + 1), __ldg(hs + 2), __ldg(hs + 3)};
+  for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
+    for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int d = 0; d < 4; ++d) mh[c * 4 + d] = fma(av[c], bv[d], mh[c * 4 + d]);
+      for (int h = 0; h < 2; ++h) {
+        const int r = warp * 32 + mt * 8 + gid, n = nt * 8 + 2 * tig + h, c = n >> 2, d = n & 3;
+        if (c < C) se[r >> 2][c][(r & 3) * 4 + d] = acc[mt][nt][h];
+      }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 64 * C; t += 256) {
+    const int ql = t / C, c = t - ql * C, q = q0 + ql;
+    if (q >= nq) continue;
+    const int sel = ssel[c];
+    double mh[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) mh[u] = 0.0;
+    for (int i = 0; i < N; ++i) {
+      const double* hq = H + ((int64_t)q * N + i) * 4;
+      const double* hs = H + ((int64_t)sel * N + i) * 4;
+      const double av[4] = {hq[0], hq[1], hq[2], hq[3]};
+      const double bv[4] = {__ldg(hs), __ldg(hs + 1), __ldg(hs + 2), __ldg(hs + 3)};
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+        for (int d = 0; d < 4; ++d) mh[cc * 4 + d] = fma(av[cc], bv[d], mh[cc * 4 + d]);
+    }
+    double g = 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) g = fma(mh[u], se[ql][c][u], g);
+    gpart[((int64_t)c * kGramSplit + sp) * nq + q] = g;
   }
-  double g = 0.0;
-#pragma unroll
-  for (int t = 0; t < 16; ++t) g = fma(mh[t], mw[t], g);
-  gpart[(int64_t)sp * nq + q] = g;
+}
+
+template <int... I>
+void launch_gram_cols(int C, dim3 grid, cudaStream_t s, int64_t L, int nq, int N, const int* sels, const double* H,
+                      const double* W, double* gpart, std::integer_sequence<int, I...>) {
+  (..., (C == I + 1 ? (void)k_ecm_gram_cols<I + 1><<<grid, 256, 0, s>>>(L, nq, N, sels, H, W, gpart) : (void)0));
 }
 
 // G[k][q] = sum of the split partials (+ vol)
@@ -316,6 +380,49 @@ __global__ void __launch_bounds__(256) k_ecm_score_gram(int nq, int k, const dou
     cta_best[blockIdx.x] = sb[0];
     cta_idx[blockIdx.x] = si[0];
   }
+}
+
+// Speculation set for the Gram columns: out[0] = the selected point, out[1..T]
+// = the next best CTA winners of the same scoring pass (larger score, then
+// smaller index; -1 where there is none).  Candidates only: whether they are
+// selected later is decided by the exact scores of their own iteration.
+__global__ void k_ecm_runners(int n, const double* best, const int* idx, const int* best_i, int T, int* out) {
+  __shared__ double sb[1024];
+  __shared__ int si[1024];
+  __shared__ int picked[16];
+  if (threadIdx.x == 0) picked[0] = *best_i;
+  __syncthreads();
+  for (int r = 1; r <= T; ++r) {
+    double b = 0.0;
+    int i = -1;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const int oi = idx[k];
+      bool skip = oi < 0;
+      for (int u = 0; u < r; ++u) skip = skip || oi == picked[u];
+      const double ob = best[k];
+      if (!skip && (i < 0 || ob > b || (ob == b && oi < i))) {
+        b = ob;
+        i = oi;
+      }
+    }
+    sb[threadIdx.x] = b;
+    si[threadIdx.x] = i;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) {
+        const double ob = sb[threadIdx.x + o];
+        const int oi = si[threadIdx.x + o];
+        if (oi >= 0 && (si[threadIdx.x] < 0 || ob > sb[threadIdx.x] || (ob == sb[threadIdx.x] && oi < si[threadIdx.x]))) {
+          sb[threadIdx.x] = ob;
+          si[threadIdx.x] = oi;
+        }
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) picked[r] = si[0];
+    __syncthreads();
+  }
+  if (threadIdx.x <= T) out[threadIdx.x] = picked[threadIdx.x];
 }
 
 __global__ void k_ecm_argmax(int n, const double* best, const int* idx, double* out_b, int* out_i) {
@@ -709,10 +816,37 @@ int podecm_ecm_select_sharded(podecm_ctx* ctx, void* stream, podecm_rve* rve, co
   const bool gram = gram_env;
   double *c0 = nullptr, *Gsel = nullptr, *gpart = nullptr;
   const int n_cta_g = grid_for(nq, 256);
+  // speculative Gram columns (Gram mode): every pass over W also computes the
+  // columns of up to kSpec runner-up candidates into a column cache, so a
+  // later selection of one of them costs a 8 nq-byte copy instead of a pass
+  // over the whole W (PODECM_ECM_SPEC=0 turns it off; the ids, weights and
+  // every score are the same either way)
+  const int kSpec = [] {
+    const char* e = getenv("PODECM_ECM_SPEC");
+    const int v = e ? atoi(e) : 3;
+    return v < 0 ? 0 : (v > kGramCols - 1 ? kGramCols - 1 : v);
+  }();
+  int *spec_dev = nullptr, *sels_dev = nullptr, *pspec = nullptr, *psels = nullptr;
+  double* pool = nullptr;
+  int pool_cap = 0, pool_used = 0;
+  std::unordered_map<int, int> cached;  // candidate -> pool column
   if (gram) {
     alloc(&c0, nq);
     alloc(&Gsel, (size_t)kq * nq);
-    alloc(&gpart, (size_t)kGramSplit * nq);
+    alloc(&gpart, (size_t)(kSpec + 1) * kGramSplit * nq);
+    alloc(&spec_dev, kSpec + 1);
+    alloc(&sels_dev, kSpec + 1);
+    if (!rc && cudaMallocHost(&pspec, 2 * (kSpec + 1) * sizeof(int)) != cudaSuccess)
+      rc = fail(PODECM_ECUDA, "ecm: pinned allocation failed");
+    psels = pspec ? pspec + kSpec + 1 : nullptr;
+    if (kSpec > 0 && nq > 0) {
+      pool_cap = (int)std::min<int64_t>((int64_t)kSpec * kq, (int64_t(1) << 30) / ((int64_t)nq * 8));
+      if (pool_cap > 0 && cudaMalloc(&pool, (size_t)pool_cap * nq * sizeof(double)) != cudaSuccess) {
+        cudaGetLastError();  // no room for the cache: run without speculation
+        pool = nullptr;
+        pool_cap = 0;
+      }
+    }
   }
   double* cta_bg = nullptr;
   int* cta_ig = nullptr;
@@ -816,6 +950,9 @@ int podecm_ecm_select_sharded(podecm_ctx* ctx, void* stream, podecm_rve* rve, co
       break;
     }
     // corr = J^T r ; argmax of corr / ||J_q|| over available columns
+    int w_n = n_cta_g;  // the per-CTA winners the argmax reduced (for the speculation set)
+    const double* w_b = cta_bg;
+    const int* w_i = cta_ig;
     if (gram && iters > 0) {
       {
         KTimer kt(ctx, s, "k_ecm_score_gram");
@@ -828,6 +965,9 @@ int podecm_ecm_select_sharded(podecm_ctx* ctx, void* stream, podecm_rve* rve, co
         k_ecm_score<<<n_cta, 224, 0, s>>>(L, nq, N, r, vol ? r + m - 1 : nullptr, H, W, cn, unav, cta_b, cta_i,
                                           gram ? c0 : nullptr, N, 0);  // first pass: r = rhs, keep J^T rhs
         k_ecm_argmax<<<1, 1024, 0, s>>>(n_cta, cta_b, cta_i, best_b, best_i);
+        w_n = n_cta;
+        w_b = cta_b;
+        w_i = cta_i;
       } else {  // wide basis (Gram mode only): c0 = J^T rhs in row blocks of 56 modes, then score it
         KTimer kt(ctx, s, "k_ecm_score");
         for (int i0 = 0; i0 < N; i0 += 56) {
@@ -841,9 +981,16 @@ int podecm_ecm_select_sharded(podecm_ctx* ctx, void* stream, podecm_rve* rve, co
       }
     }
     ctx->launches += 2;
-    cudaMemcpyAsync(pbest, best_i, sizeof(int), cudaMemcpyDeviceToHost, s);
+    const bool spec = gram && pool_cap > 0;
+    if (spec) {  // the selected point and its runners-up in one read-back
+      k_ecm_runners<<<1, 1024, 0, s>>>(w_n, w_b, w_i, best_i, kSpec, spec_dev);
+      ctx->launches += 1;
+      cudaMemcpyAsync(pspec, spec_dev, sizeof(int) * (kSpec + 1), cudaMemcpyDeviceToHost, s);
+    } else {
+      cudaMemcpyAsync(pbest, best_i, sizeof(int), cudaMemcpyDeviceToHost, s);
+    }
     cudaStreamSynchronize(s);
-    int best = *pbest;  // local index
+    int best = spec ? pspec[0] : *pbest;  // local index
     int owner = 0;
     int64_t gbest = best < 0 ? -1 : q0 + best;
     if (comm) {  // global best: larger score, then smaller global index
@@ -885,10 +1032,30 @@ int podecm_ecm_select_sharded(podecm_ctx* ctx, void* stream, podecm_rve* rve, co
       cudaStreamSynchronize(s);
     }
     if (gram) {  // column (J^T J)[:, best] for the scores of the next iterations
-      KTimer kt(ctx, s, "k_ecm_gram_col");
-      k_ecm_gram_col<<<dim3(n_cta_g, kGramSplit), 256, 0, s>>>(L, nq, N, best, H, W, gpart);
-      k_ecm_gram_finish<<<n_cta_g, 256, 0, s>>>(nq, gpart, vol, Gsel + (int64_t)qr.k * nq);
-      ctx->launches += 2;
+      double* gdst = Gsel + (int64_t)qr.k * nq;
+      const auto hit = cached.find(best);
+      if (hit != cached.end()) {  // computed speculatively by an earlier pass
+        cudaMemcpyAsync(gdst, pool + (int64_t)hit->second * nq, sizeof(double) * nq, cudaMemcpyDeviceToDevice, s);
+        cached.erase(hit);
+      } else {
+        int C = 1;
+        psels[0] = best;
+        for (int k = 1; spec && k <= kSpec; ++k) {
+          const int c = pspec[k];
+          if (c >= 0 && c != best && !cached.count(c) && pool_used + C <= pool_cap) psels[C++] = c;
+        }
+        cudaMemcpyAsync(sels_dev, psels, sizeof(int) * C, cudaMemcpyHostToDevice, s);
+        KTimer kt(ctx, s, "k_ecm_gram_col");
+        launch_gram_cols(C, dim3(grid_for(nq, 64), kGramSplit), s, L, nq, N, sels_dev, H, W, gpart,
+                         std::make_integer_sequence<int, kGramCols>{});
+        k_ecm_gram_finish<<<n_cta_g, 256, 0, s>>>(nq, gpart, vol, gdst);
+        for (int k = 1; k < C; ++k) {
+          k_ecm_gram_finish<<<n_cta_g, 256, 0, s>>>(nq, gpart + (int64_t)k * kGramSplit * nq, vol,
+                                                    pool + (int64_t)pool_used * nq);
+          cached[psels[k]] = pool_used++;
+        }
+        ctx->launches += 1 + C;
+      }
     }
     qr.append();
     // restore_feasible (ecm.cpp:56-90)
@@ -990,6 +1157,10 @@ int podecm_ecm_select_sharded(podecm_ctx* ctx, void* stream, podecm_rve* rve, co
   cudaFree(c0);
   cudaFree(Gsel);
   cudaFree(gpart);
+  cudaFree(spec_dev);
+  cudaFree(sels_dev);
+  cudaFree(pool);
+  cudaFreeHost(pspec);
   cudaFree(cta_bg);
   cudaFree(cta_ig);
   return rc;

@@ -129,3 +129,24 @@ def test_ecm_wide_basis_ids_bit_exact(case):
     print(f"N=80: ids equal {np.array_equal(ids_g, ids_o)}; resid {rel_g:.6e} vs {rel_o:.6e}")
     assert np.array_equal(ids_g, ids_o) and it_g == it_o
     assert np.abs(w_g - w_o).max() <= 1e-8 * np.abs(w_o).max()
+
+
+@pytest.mark.parametrize("spec", [0, 1, 3])
+def test_ecm_speculative_gram_columns_change_nothing(case, monkeypatch, spec):
+    """The Gram-column cache (k_ecm.cu: each pass over W also computes the
+    columns of the scoring pass's runner-up candidates, on the DMMA path) only
+    changes how often W is streamed: ids, weights, residual and iteration
+    count are bit-identical to the uncached greedy, which computes one column
+    per pass."""
+    import torch
+    from paper_2307_16894_b200 import api
+    g, o, t, U, modes, lam, W, H = case
+    Hd, Wd = torch.from_numpy(H).cuda(), torch.from_numpy(W).cuda()
+    opts = api.EcmOpts(eps=1e-8, max_points=60, stop_at_count=True)
+    monkeypatch.setenv("PODECM_ECM_SPEC", "0")
+    ref = api.ecm_select(g, Hd, Wd, opts)
+    monkeypatch.setenv("PODECM_ECM_SPEC", str(spec))
+    got = api.ecm_select(g, Hd, Wd, opts)
+    assert np.array_equal(got[0], ref[0])
+    assert np.array_equal(np.asarray(got[1]).view(np.int64), np.asarray(ref[1]).view(np.int64))
+    assert got[2] == ref[2] and got[3] == ref[3]
