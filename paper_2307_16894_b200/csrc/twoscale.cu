@@ -595,9 +595,12 @@ int podecm_twoscale_run(podecm_ctx* ctx, void* stream, const podecm_macro_cfg* c
         k_macro_gather<<<(n_ent + 255) / 256, 256, 0, s>>>(n_ent, d_ent, d_eptr, d_eidx, d_con, d_K);
         cu(cudaGetLastError(), "k_macro_gather launch");
       }
-      if (!rc && (cusolverDnDgetrf(dn, n, n, d_K, n, d_work, d_piv, d_info) != CUSOLVER_STATUS_SUCCESS ||
-                  cusolverDnDgetrs(dn, CUBLAS_OP_N, n, 1, d_K, n, d_piv, d_b, n, d_info) != CUSOLVER_STATUS_SUCCESS))
-        rc = set_err(ctx, PODECM_ECUDA, "macro tangent: cuSOLVER getrf/getrs failed");
+      {
+        KTimer kt(ctx, s, "macro_lu");
+        if (!rc && (cusolverDnDgetrf(dn, n, n, d_K, n, d_work, d_piv, d_info) != CUSOLVER_STATUS_SUCCESS ||
+                    cusolverDnDgetrs(dn, CUBLAS_OP_N, n, 1, d_K, n, d_piv, d_b, n, d_info) != CUSOLVER_STATUS_SUCCESS))
+          rc = set_err(ctx, PODECM_ECUDA, "macro tangent: cuSOLVER getrf/getrs failed");
+      }
       k_macro_update<<<(n + 255) / 256, 256, 0, s>>>(n, d_u, d_b);
       cu(cudaGetLastError(), "k_macro_update launch");
       int info = 0;
