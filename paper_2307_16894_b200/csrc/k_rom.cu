@@ -1484,12 +1484,9 @@ __global__ void __launch_bounds__(32) k_rom_solve_reg(NewtonArgs g) {
 // Newton update kernel of the lazy pipeline: the register-resident LU for the
 // mode counts it is instantiated for, the shared-memory LU otherwise
 // (PODECM_ROM_LU=smem forces the latter, for A/B comparisons).
-bool rom_lu_reg() {
-  static bool v = [] {
-    const char* e = getenv("PODECM_ROM_LU");
-    return !(e && std::strcmp(e, "smem") == 0);
-  }();
-  return v;
+bool rom_lu_reg() {  // read per call (tests flip it)
+  const char* e = getenv("PODECM_ROM_LU");
+  return !(e && std::strcmp(e, "smem") == 0);
 }
 
 
@@ -1915,12 +1912,9 @@ ContractArgs contract_args(podecm_rom* r, int64_t n) {
 
 // F at the ECM points: the DMMA form by default; PODECM_ROM_F=fma selects the
 // DFMA kernel (k_rom_F) for A/B comparisons.
-bool rom_F_mma() {
-  static bool v = [] {
-    const char* e = getenv("PODECM_ROM_F");
-    return !(e && std::strcmp(e, "fma") == 0);
-  }();
-  return v;
+bool rom_F_mma() {  // read per call (tests flip it)
+  const char* e = getenv("PODECM_ROM_F");
+  return !(e && std::strcmp(e, "fma") == 0);
 }
 
 void launch_F(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, const PointArgs& pa) {

@@ -167,3 +167,25 @@ def test_fused_pipeline_variant():
                         "-k", "not fused_pipeline_variant", "-p", "no:cacheprovider"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("var,val", [("PODECM_ROM_LU", "smem"), ("PODECM_ROM_F", "fma")])
+def test_kernel_variants_bit_identical(setup, monkeypatch, var, val):
+    """The register-resident LU (k_rom_solve_reg<50>) against the shared-memory
+    LU, and the DMMA F kernel (k_rom_F_mma) against the DFMA one: same
+    pivots, same per-element FMA sequence (a DMMA accumulates as the
+    sequential FMA chain), so a whole solve — with bisections — must agree
+    byte for byte (pbar, iteration counts, status)."""
+    import torch
+    from paper_2307_16894_b200 import api
+    g, o, model, rom = setup
+    geom, sched = synth.rom_instances(96, 2, 77, 0.2)  # two big increments
+    T = lambda a: torch.from_numpy(a).cuda()
+    opts = api.NewtonOpts(eps_rel=1e-10, eps_abs=1e-12, max_iter=3, max_bisect=5)  # increments bisect
+    monkeypatch.delenv(var, raising=False)
+    a = {k: v.cpu().numpy() for k, v in rom.solve(T(geom), T(sched), opts).items()}
+    monkeypatch.setenv(var, val)
+    b = {k: v.cpu().numpy() for k, v in rom.solve(T(geom), T(sched), opts).items()}
+    assert (a["iters"] > 3).any(), "no increment bisected"
+    for k in ("pbar", "iters", "status"):
+        assert np.array_equal(np.ascontiguousarray(a[k]).view(np.uint8), np.ascontiguousarray(b[k]).view(np.uint8)), k
