@@ -556,6 +556,32 @@ def run_c3(args, ws, rank, local, ctx, n_inst, steps, warmup, fp64):
                         "share_of_step": {"contract": round(kc[0] / tot, 3), "material": round(k_mat / tot, 3),
                                           "newton_lu": round(k_lu / tot, 3),
                                           "residual_check": round(k_chk / tot, 3)} if tot > 0 else None}}
+    # Whole-step FP64 roofline: every part of the step on the one FP64 datapath
+    # (DMMA and DFMA share it), as useful FMA-slots at the measured
+    # DMMA rate.  Contraction: N^2 4Q + Y build 4Q N 4 per contraction;
+    # material: the FP64 thread-instructions of config 1's kernel
+    # (profiles/ncu_traffic.json), 8/9 of a point's for an FD-tangent point
+    # and 1/9 for a P-only point; LU 2N^3/3 + N^2; F and the residual check
+    # 4Q N each per assembly.
+    try:
+        c1i = json.load(open(ROOT / "profiles" / "ncu_traffic.json"))["k_material_batch"]["fp64_thread_inst_per_point"]
+        c1_fp64 = float(c1i["dfma"] + c1i["dmul"] + c1i["dadd"])
+    except Exception:  # noqa: BLE001
+        c1_fp64 = None
+    if c1_fp64 and fp64 and fp64.get("dmma"):
+        per_inst = {"contraction": contractions * (N * N * 4 * Q + 4 * Q * N * 4),
+                    "material_fd_tangent": contractions * Q * c1_fp64 * 8 / 9,
+                    "material_p_only": assemblies * Q * c1_fp64 / 9,
+                    "lu": contractions * (2 * N ** 3 / 3 + N * N),
+                    "F_and_check": assemblies * 2 * 4 * Q * N}
+        rate = fp64["dmma"] * 1e12 / 2  # FMA-slots per second
+        floor_ms = {k: v * n_inst * steps / rate * 1e3 / steps for k, v in per_inst.items()}
+        fl = sum(floor_ms.values())
+        res["whole_step_fp64"] = {"floor_ms": round(fl, 1), "ms_per_step": round(ms / steps, 1),
+                                  "frac": round(fl / (ms / steps), 4),
+                                  "floor_ms_by_part": {k: round(v, 1) for k, v in floor_ms.items()},
+                                  "peak": "DMMA probe measured in this run (FMA-slots = TFLOP/s / 2)",
+                                  "model": "useful FMA / FP64 instruction slots of each part at the FP64 datapath rate"}
     # §8(f) row 1: rom_effective_stiffness for every instance at its final
     # (Fbar_K, a_final) from a virgin history (one reduced assembly + LU with
     # 4 right-hand sides per instance), outside the headline step.
@@ -951,6 +977,8 @@ def main():
             c3 = also["c3"]
             bm["rom_rve_solves_per_s"] = c3["rve_solves_per_s"]
             bm["c3_contract_dmma_frac"] = c3["roofline"]["frac"]
+            if "whole_step_fp64" in c3:
+                bm["c3_whole_step_fp64_frac"] = c3["whole_step_fp64"]["frac"]
             bm["c3_ms_per_step"] = round(c3["ms_per_step"], 1)
         if "c2" in also_ok:
             bm["c2_qp_per_s"] = also["c2"]["qp_per_s"]
