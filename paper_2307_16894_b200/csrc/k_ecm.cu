@@ -244,7 +244,7 @@ constexpr int kGramSplit = 4;  // L-range splits (partials summed in fixed order
 // exactly as in the single-column form.  Each column is therefore the value
 // a one-column pass produces.
 constexpr int kGramCols = 4;
-constexpr int kGramLC = 32;  // snapshots staged per round (multiple of 4)
+constexpr int kGramLC = 64;  // snapshots staged per round (multiple of 4)
 template <int C>
 __global__ void __launch_bounds__(256) k_ecm_gram_cols(int64_t L, int nq, int N, const int* __restrict__ sels,
                                                        const double* H, const double* W, double* gpart) {
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(256) k_ecm_gram_cols(int64_t L, int nq, int N,
       sw[lc][n] = (lc < nl && c < C) ? __ldg(W + ((lb + lc) * nq + ssel[c]) * 4 + d) : 0.0;
     }
     __syncthreads();
-#pragma unroll 2
+#pragma unroll 4
     for (int k0 = 0; k0 < nl; k0 += 4) {
       const int lk = k0 + tig;  // this thread's k (snapshot) of the step
       const bool kin = lk < nl;
