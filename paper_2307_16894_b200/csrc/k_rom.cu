@@ -511,7 +511,10 @@ __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable t
   Frozen z;
   freeze(fp, s0p[(size_t)4 * g.Q + p], s0p[(size_t)5 * g.Q + p], z);
   const double cw = g.w[p] * det;  // rom.cpp:56
-  double* at = g.At + ((size_t)s * g.Qpad + p) * 20;
+  // Ã_p and P̃_p as planes [s][20][Qpad] (entry t at at[t * Qpad]): a warp's
+  // stores of one entry are one contiguous run of points
+  double* at = g.At + (size_t)s * 20 * g.Qpad + p;
+  const size_t aqs = (size_t)g.Qpad;
   bool ok = true;
   constexpr bool kSlab = SLAB && MODE != 1;
   volatile double* sc = slab + threadIdx.x;
@@ -543,7 +546,7 @@ __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable t
       *reinterpret_cast<double4*>(g.Pt + ((size_t)s * g.Qpad + p) * 4) = make_double4(pt[0], pt[1], pt[2], pt[3]);
     else
 #pragma unroll
-      for (int r = 0; r < 4; ++r) at[16 + r] = pt[r];
+      for (int r = 0; r < 4; ++r) at[(16 + r) * aqs] = pt[r];
   }
   if (ok && MODE != 1) {
     // At = c R A R^T streamed per column pair: columns e = (s&1) + 2l' arrive
@@ -573,7 +576,7 @@ __global__ void __launch_bounds__(128, MINB) k_rom_point(PointArgs g, MatTable t
       for (int h = 0; h < 2; ++h) {
         const int sc = sb + 2 * h, js = sc >> 1;
 #pragma unroll
-        for (int r = 0; r < 4; ++r) at[r + 4 * sc] = cw * fma(Tc[r], m[js + 2], T0[r] * m[js]);
+        for (int r = 0; r < 4; ++r) at[(r + 4 * sc) * aqs] = cw * fma(Tc[r], m[js + 2], T0[r] * m[js]);
       }
     };
     if constexpr (kSlab) {
@@ -681,15 +684,16 @@ __global__ void __launch_bounds__(32 * NT * IPC, (contract_minb<NT, IPC>())) k_r
       rA[k] = 0.0;
       if (t < kIPC * kPC * 20) {
         const int q = t / (kPC * 20), rem = t - q * kPC * 20;
+        const int tp = rem / kPC, pl = rem - tp * kPC;  // At planes [s][20][Qpad], points fastest
         if constexpr (LIST) {
           int64_t sq = sid[0];
 #pragma unroll
           for (int u = 1; u < kIPC; ++u)
             if (q == u) sq = sid[u];
-          if (sq >= 0) rA[k] = g.At[((size_t)sq * g.Qpad + (size_t)c * kPC) * 20 + rem];
+          if (sq >= 0) rA[k] = g.At[((size_t)sq * 20 + tp) * g.Qpad + (size_t)c * kPC + pl];
         } else {
           const int64_t sq = sbase + q;
-          if (sq < g.n) rA[k] = g.At[((size_t)sq * g.Qpad + (size_t)c * kPC) * 20 + rem];
+          if (sq < g.n) rA[k] = g.At[((size_t)sq * 20 + tp) * g.Qpad + (size_t)c * kPC + pl];
         }
       }
     }
@@ -703,7 +707,11 @@ __global__ void __launch_bounds__(32 * NT * IPC, (contract_minb<NT, IPC>())) k_r
 #pragma unroll
     for (int k = 0; k < APT; ++k) {
       const int t = tid + k * NTHR;
-      if (t < kIPC * kPC * 20) sAt[buf * kIPC * kPC * 20 + t] = rA[k];
+      if (t < kIPC * kPC * 20) {  // back to the [instance][point][20] shared layout of build_y
+        const int q = t / (kPC * 20), rem = t - q * kPC * 20;
+        const int tp = rem / kPC, pl = rem - tp * kPC;
+        sAt[buf * kIPC * kPC * 20 + q * kPC * 20 + pl * 20 + tp] = rA[k];
+      }
     }
   };
   // Y[(p,r)][j] = sum_t At_p[r][t] Gm[(p,t)][j] (j < N); Y[.][N] = Pt; else 0.
