@@ -728,8 +728,10 @@ def run_c4(args, ws, rank, local, ctx, steps, warmup, fp64):
     ks = tk.get("k_ecm_score", (0.0, 1))
     score_flop = 2.0 * 56 * L * 4 * rve.n_qp  # padded tile rows x L x 4 nqp per iteration
     out = {"n_dof": n_dof, "snapshots": L, "modes": N, "candidates": rve.n_qp, "selected": int(len(res["ids"])),
-           "split": (f"{ws} ranks: dof rows of S (Gram all-reduce) and candidates (argmax exchange + column "
-                     "broadcast); strong scaling of one reduction") if ws > 1 else "single GPU",
+           "split": (f"{ws} ranks: dof rows of S (the DMMA Gram GEMM fused with its reduce-scatter: peer-memory "
+                     "stores into the row owners' slots over CUDA IPC, rank-order sums, peer all-gather) and "
+                     "candidates (argmax exchange + column broadcast); strong scaling of one reduction")
+                    if ws > 1 else "single GPU",
            "ms_per_step": ms / steps, "pod_stage_s": round(res["pod_s"], 4), "ecm_greedy_s": round(res["ecm_s"], 4),
            "ecm_iterations": res["it"], "ecm_residual_rel": res["rel"],
            "kernels_ms_per_step": {k: round(v[0] / steps, 3) for k, v in tk.items()},

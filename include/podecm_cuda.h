@@ -338,6 +338,34 @@ int podecm_pod_modes_ex(podecm_ctx* ctx, void* stream, const double* S, int64_t 
  * diag(g) metric (gram_diag nullable = identity).  Synchronises the stream. */
 int podecm_pod_mgs(podecm_ctx* ctx, void* stream, double* modes, int64_t n_dof, int k, const double* gram_diag);
 
+/* Row-sharded Gram fused with its reduce-scatter over peer memory (SURVEY
+ * 8(e), the multi-GPU split of podkit.cpp:46): this rank's partial
+ * S_k^T diag(g) S_k (S_k = its dof rows, column-major n_dof x n_snap) is
+ * computed by the symmetric DMMA GEMM, whose epilogue stores every element
+ * (i, j) straight into the receive slot of the rank owning Gram row i:
+ * recv[o] + (rank * (row0[o+1] - row0[o]) + i - row0[o]) * n_snap + j, with
+ * recv[o] rank o's receive buffer ([world][rows of o][n_snap]) mapped into
+ * this process (podecm_ipc_open; NVLink peer stores across GPUs).  No local
+ * partial is materialised and no collective library call is made.  world <=
+ * 8; row0 [world + 1] (host) partitions the n_snap Gram rows. */
+int podecm_pod_gram_peer(podecm_ctx* ctx, void* stream, const double* S, int64_t n_dof, int n_snap,
+                         const double* gram_diag, double* const* recv, int rank, int world, const int64_t* row0);
+/* The owner's side of the reduce-scatter once every rank's GEMM has
+ * finished: G_rows = sum over k of recv[k] (rows x n_snap), in rank order. */
+int podecm_pod_gram_reduce(podecm_ctx* ctx, void* stream, const double* recv, int world, int64_t rows, int n_snap,
+                           double* G_rows);
+/* count doubles from src to dst (either may be a peer mapping): the
+ * all-gather of the reduced Gram rows. */
+int podecm_peer_copy(podecm_ctx* ctx, void* stream, double* dst, const double* src, int64_t count);
+/* Device buffers that can be exported to other processes (cudaMalloc'ed, so
+ * an IPC handle maps exactly them), their CUDA IPC handles (64 bytes) and
+ * the mapping of a peer's handle into this process. */
+int podecm_dev_alloc(podecm_ctx* ctx, int64_t bytes, void** out);
+void podecm_dev_free(void* p);
+int podecm_ipc_handle(podecm_ctx* ctx, void* p, unsigned char handle[64]);
+int podecm_ipc_open(podecm_ctx* ctx, const unsigned char handle[64], void** out);
+void podecm_ipc_close(void* p);
+
 /* EcmOpts (ecm.hpp:28-32) plus stop_at_count: configs 3/4 stop at
  * max_points selected points instead of throwing (documented deviation). */
 typedef struct podecm_ecm_opts {

@@ -78,6 +78,14 @@ _SIGS = {
     "podecm_pod_modes_ex": (C.c_int, [P, P, P, I64, C.c_int, P, P, C.c_int, D, P, P, C.POINTER(C.c_int),
                                        C.c_int]),
     "podecm_pod_mgs": (C.c_int, [P, P, P, I64, C.c_int, P]),
+    "podecm_pod_gram_peer": (C.c_int, [P, P, P, I64, C.c_int, P, P, C.c_int, C.c_int, P]),
+    "podecm_pod_gram_reduce": (C.c_int, [P, P, P, C.c_int, I64, C.c_int, P]),
+    "podecm_peer_copy": (C.c_int, [P, P, P, P, I64]),
+    "podecm_dev_alloc": (C.c_int, [P, I64, C.POINTER(P)]),
+    "podecm_dev_free": (None, [P]),
+    "podecm_ipc_handle": (C.c_int, [P, P, P]),
+    "podecm_ipc_open": (C.c_int, [P, P, C.POINTER(P)]),
+    "podecm_ipc_close": (None, [P]),
     "podecm_ecm_select_sharded": (C.c_int, [P, P, P, P, C.c_int, P, I64, P, C.POINTER(podecm_ecm_opts), P, P,
                                             C.POINTER(C.c_int), C.POINTER(D), C.POINTER(C.c_int)]),
     "podecm_ecm_mode_grads": (C.c_int, [P, P, P, P, C.c_int, P]),

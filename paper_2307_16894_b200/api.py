@@ -379,23 +379,101 @@ def pod(S_cm: torch.Tensor, max_modes: int, tol_rel: float = 1e-10, gram_diag=No
     return modes[: kept.value], ev
 
 
-def pod_sharded(S_local: torch.Tensor, max_modes: int, tol_rel: float = 1e-10, ctx: Context | None = None):
+def _gram_peer(ctx: "Context", S_local: torch.Tensor, n_snap: int, world: int, rank: int) -> torch.Tensor:
+    """The summed Gram sum_k S_k^T S_k by the peer-memory path: each rank's
+    DMMA GEMM stores its partial straight into the row owners' receive slots
+    (podecm_pod_gram_peer, CUDA IPC mappings: NVLink stores across GPUs), the
+    owner sums its slots in rank order (podecm_pod_gram_reduce) and every rank
+    pulls the reduced rows of the other owners (podecm_peer_copy).  Host-side
+    barriers separate the phases, so no kernel ever waits on another rank's.
+    Returns the full n_snap^2 Gram on this rank's device."""
+    import torch.distributed as dist
+    n_loc = S_local.shape[1]
+    row0 = [n_snap * o // world for o in range(world + 1)]
+    rows = row0[rank + 1] - row0[rank]
+    L = ctx.lib
+
+    def alloc(nbytes):
+        p = C.c_void_p()
+        _lib.raise_for(L.podecm_dev_alloc(ctx.h, nbytes, C.byref(p)), ctx.h, "podecm_dev_alloc")
+        return p
+
+    def share(p):
+        h = (C.c_ubyte * 64)()
+        _lib.raise_for(L.podecm_ipc_handle(ctx.h, p, C.cast(h, C.c_void_p)), ctx.h, "podecm_ipc_handle")
+        hs = [None] * world
+        dist.all_gather_object(hs, bytes(h))
+        out = []
+        for o in range(world):
+            if o == rank:
+                out.append(p)
+                continue
+            q = C.c_void_p()
+            hb = (C.c_ubyte * 64).from_buffer_copy(hs[o])
+            _lib.raise_for(L.podecm_ipc_open(ctx.h, C.cast(hb, C.c_void_p), C.byref(q)), ctx.h, "podecm_ipc_open")
+            out.append(q)
+        return out
+
+    recv = alloc(world * rows * n_snap * 8)  # [world][rows][n_snap]: the partials of this rank's rows
+    gfull = alloc(n_snap * n_snap * 8)
+    recv_all, g_all = share(recv), share(gfull)
+    try:
+        ptrs = (C.c_void_p * world)(*[p.value for p in recv_all])
+        r0 = (C.c_int64 * (world + 1))(*row0)
+        rc = L.podecm_pod_gram_peer(ctx.h, ctx.stream(), _ptr(S_local), n_loc, n_snap, None,
+                                    C.cast(ptrs, C.c_void_p), rank, world, C.cast(r0, C.c_void_p))
+        _lib.raise_for(rc, ctx.h, "podecm_pod_gram_peer")
+        torch.cuda.synchronize(S_local.device)
+        dist.barrier()  # every partial has landed in its owner's slots
+        rc = L.podecm_pod_gram_reduce(ctx.h, ctx.stream(), recv, world, rows, n_snap,
+                                      C.c_void_p(gfull.value + row0[rank] * n_snap * 8))
+        _lib.raise_for(rc, ctx.h, "podecm_pod_gram_reduce")
+        torch.cuda.synchronize(S_local.device)
+        dist.barrier()  # every owner's rows are reduced
+        for o in range(world):
+            if o != rank:
+                off = row0[o] * n_snap * 8
+                rc = L.podecm_peer_copy(ctx.h, ctx.stream(), C.c_void_p(gfull.value + off),
+                                        C.c_void_p(g_all[o].value + off), (row0[o + 1] - row0[o]) * n_snap)
+                _lib.raise_for(rc, ctx.h, "podecm_peer_copy")
+        G = torch.empty((n_snap, n_snap), dtype=torch.float64, device=S_local.device)
+        rc = L.podecm_peer_copy(ctx.h, ctx.stream(), _ptr(G), gfull, n_snap * n_snap)
+        _lib.raise_for(rc, ctx.h, "podecm_peer_copy")
+        torch.cuda.synchronize(S_local.device)
+        dist.barrier()  # nobody reads a peer buffer any more
+    finally:
+        for o in range(world):
+            if o != rank:
+                L.podecm_ipc_close(recv_all[o])
+                L.podecm_ipc_close(g_all[o])
+        L.podecm_dev_free(recv)
+        L.podecm_dev_free(gfull)
+    return G
+
+
+def pod_sharded(S_local: torch.Tensor, max_modes: int, tol_rel: float = 1e-10, ctx: Context | None = None,
+                exchange: str = "peer"):
     """Row-sharded pod_diag: ``S_local`` [n_snap, n_local] holds
     this rank's contiguous dof rows of the snapshot matrix (same layout as
-    pod()).  Local Gram S_k^T S_k on the device, one SUM all-reduce of the
-    n_snap^2 Gram (NCCL), the eigenproblem and S_k v / sqrt(lambda) on every
-    rank, an all-gather of the mode rows and the MGS pass (podkit.cpp:75-86)
-    on the whole basis.  Returns (modes^T [kept, n_dof], eigenvalues), the
-    same on every rank."""
+    pod()).  The summed Gram sum_k S_k^T S_k: ``exchange="peer"`` (default) by
+    the GEMM fused with its reduce-scatter over peer memory (_gram_peer), or
+    ``"collective"`` by a local Gram and one SUM all-reduce (NCCL, or gloo on a
+    host copy).  Then the eigenproblem and S_k v / sqrt(lambda) on every rank,
+    an all-gather of the mode rows and the MGS pass (podkit.cpp:75-86) on the
+    whole basis.  Returns (modes^T [kept, n_dof], eigenvalues), the same on
+    every rank."""
     import torch.distributed as dist
     ctx = ctx or Context.default(S_local.device.index or 0)
     n_snap, n_loc = S_local.shape
     dev = S_local.device
-    C_ = torch.empty((n_snap, n_snap), dtype=torch.float64, device=dev)
-    rc = ctx.lib.podecm_pod_gram(ctx.h, ctx.stream(), _ptr(S_local), n_loc, n_snap, None, _ptr(C_))
-    _lib.raise_for(rc, ctx.h, "podecm_pod_gram")
     world = dist.get_world_size() if dist.is_initialized() else 1
-    if world > 1:
+    if world > 1 and exchange == "peer":
+        C_ = _gram_peer(ctx, S_local, n_snap, world, dist.get_rank())
+    else:
+        C_ = torch.empty((n_snap, n_snap), dtype=torch.float64, device=dev)
+        rc = ctx.lib.podecm_pod_gram(ctx.h, ctx.stream(), _ptr(S_local), n_loc, n_snap, None, _ptr(C_))
+        _lib.raise_for(rc, ctx.h, "podecm_pod_gram")
+    if world > 1 and exchange != "peer":
         if "nccl" in str(dist.get_backend()):
             dist.all_reduce(C_)
         else:  # host backend (gloo): reduce a host copy

@@ -16,6 +16,7 @@
 namespace podecm_dev {
 
 constexpr int kGBM = 64, kGBN = 64, kGBK = 16, kGLD = kGBK + 4;
+constexpr int kMaxPeers = 8;  // ranks of a fused peer epilogue (one NVLink domain)
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -36,6 +37,14 @@ struct GemmArgs {
   // split-K (gridDim.z slices): slice z covers k in [z kslice, (z+1) kslice)
   // and writes its partial product at C + z zc (kslice 0: no split)
   int64_t kslice, zc;
+  // peer epilogue (peer_world > 0): element (i, j) goes to the receive slot
+  // of the rank owning row i (rows [row0[o], row0[o+1]) belong to rank o):
+  // peer[o] + (peer_rank * (row0[o+1] - row0[o]) + i - row0[o]) * c_rs + j,
+  // a store into that rank's memory (CUDA IPC / peer mapping, NVLink) — the
+  // reduce-scatter of a row-sharded Gram fused into the GEMM that produces it
+  int peer_world, peer_rank;
+  double* peer[kMaxPeers];
+  int64_t row0[kMaxPeers + 1];
 };
 
 // 128 threads = 2x2 warps, warp tile 32x32 (4x4 DMMA tiles).  Internal
@@ -113,8 +122,19 @@ static __global__ void __launch_bounds__(128) k_gemm_dmma_t(GemmArgs g) {
         const int64_t i = i0 + wm * 32 + a * 8 + gid;
         const int64_t j = j0 + wn * 32 + b * 8 + 2 * tig + h;
         if (i < g.M && j < g.N) {
-          g.C[i * g.c_rs + j * g.c_cs] = acc[a][b][h];
-          if (g.sym && bj != bi) g.C[j * g.c_rs + i * g.c_cs] = acc[a][b][h];
+          if (g.peer_world > 0) {  // symmetric Gram partial: row i and (mirrored) row j to their owners
+            auto put = [&](int64_t r, int64_t c, double v) {
+              int o = 0;
+              while (o + 1 < g.peer_world && r >= g.row0[o + 1]) ++o;
+              const int64_t rows = g.row0[o + 1] - g.row0[o];
+              g.peer[o][((int64_t)g.peer_rank * rows + r - g.row0[o]) * g.c_rs + c] = v;
+            };
+            put(i, j, acc[a][b][h]);
+            if (g.sym && bj != bi) put(j, i, acc[a][b][h]);
+          } else {
+            g.C[i * g.c_rs + j * g.c_cs] = acc[a][b][h];
+            if (g.sym && bj != bi) g.C[j * g.c_rs + i * g.c_cs] = acc[a][b][h];
+          }
         }
       }
 }

@@ -409,6 +409,108 @@ int podecm_pod_gram(podecm_ctx* ctx, void* stream, const double* S, int64_t n_do
   return gemm(ctx, static_cast<cudaStream_t>(stream), a);
 }
 
+// ---- row-sharded Gram with its reduce-scatter fused over peer memory -------
+// (the C4 Gram sum_k S_k^T S_k over the ranks' dof-row shards)
+
+int podecm_pod_gram_peer(podecm_ctx* ctx, void* stream, const double* S, int64_t n_dof, int n_snap,
+                         const double* gram_diag, double* const* recv, int rank, int world, const int64_t* row0) {
+  if (!ctx || !S || !recv || !row0) return PODECM_ECONFIG;
+  if (n_dof <= 0 || n_snap <= 0) return set_err(ctx, PODECM_ECONFIG, "pod_gram_peer: empty snapshot matrix");
+  if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world)
+    return set_err(ctx, PODECM_ECONFIG, "pod_gram_peer: need 1 <= world <= 8 and 0 <= rank < world");
+  if (row0[0] != 0 || row0[world] != n_snap) return set_err(ctx, PODECM_ECONFIG, "pod_gram_peer: bad row partition");
+  GemmArgs a{};
+  a.M = n_snap;
+  a.N = n_snap;
+  a.K = n_dof;
+  a.A = S;
+  a.a_rs = n_dof;
+  a.a_cs = 1;
+  a.B = S;
+  a.b_rs = 1;
+  a.b_cs = n_dof;
+  a.C = nullptr;
+  a.c_rs = n_snap;
+  a.c_cs = 1;
+  a.diag = gram_diag;
+  a.sym = 1;
+  a.peer_world = world;
+  a.peer_rank = rank;
+  for (int o = 0; o < world; ++o) {
+    if (!recv[o] || row0[o + 1] < row0[o]) return set_err(ctx, PODECM_ECONFIG, "pod_gram_peer: bad receive slot");
+    a.peer[o] = recv[o];
+    a.row0[o] = row0[o];
+  }
+  a.row0[world] = row0[world];
+  return gemm(ctx, static_cast<cudaStream_t>(stream), a);
+}
+
+}  // extern "C"
+
+namespace {
+// G[r][c] = recv[0][r][c] + recv[1][r][c] + ... in rank order (deterministic)
+__global__ void k_gram_reduce(int world, int64_t cnt, const double* __restrict__ recv, double* __restrict__ G) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  double v = recv[t];
+  for (int k = 1; k < world; ++k) v += recv[(int64_t)k * cnt + t];
+  G[t] = v;
+}
+}  // namespace
+
+extern "C" {
+
+int podecm_pod_gram_reduce(podecm_ctx* ctx, void* stream, const double* recv, int world, int64_t rows, int n_snap,
+                           double* G_rows) {
+  if (!ctx || !recv || !G_rows || world < 1 || rows < 0) return PODECM_ECONFIG;
+  const int64_t cnt = rows * (int64_t)n_snap;
+  if (cnt == 0) return PODECM_OK;
+  auto s = static_cast<cudaStream_t>(stream);
+  {
+    KTimer kt(ctx, s, "k_gram_reduce");
+    k_gram_reduce<<<grid_for(cnt, 256), 256, 0, s>>>(world, cnt, recv, G_rows);
+  }
+  PODECM_LAUNCHED(ctx, 1);
+  return PODECM_OK;
+}
+
+int podecm_peer_copy(podecm_ctx* ctx, void* stream, double* dst, const double* src, int64_t count) {
+  if (!ctx || (count > 0 && (!dst || !src))) return PODECM_ECONFIG;
+  if (count <= 0) return PODECM_OK;
+  PODECM_CUDA_TRY(ctx, cudaMemcpyAsync(dst, src, sizeof(double) * count, cudaMemcpyDefault,
+                                       static_cast<cudaStream_t>(stream)));
+  return PODECM_OK;
+}
+
+int podecm_dev_alloc(podecm_ctx* ctx, int64_t bytes, void** out) {
+  if (!ctx || !out || bytes < 0) return PODECM_ECONFIG;
+  *out = nullptr;
+  PODECM_CUDA_TRY(ctx, cudaMalloc(out, (size_t)std::max<int64_t>(bytes, 8)));
+  return PODECM_OK;
+}
+
+void podecm_dev_free(void* p) { cudaFree(p); }
+
+int podecm_ipc_handle(podecm_ctx* ctx, void* p, unsigned char handle[64]) {
+  if (!ctx || !p || !handle) return PODECM_ECONFIG;
+  cudaIpcMemHandle_t h;
+  PODECM_CUDA_TRY(ctx, cudaIpcGetMemHandle(&h, p));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(handle, &h, 64);
+  return PODECM_OK;
+}
+
+int podecm_ipc_open(podecm_ctx* ctx, const unsigned char handle[64], void** out) {
+  if (!ctx || !handle || !out) return PODECM_ECONFIG;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  *out = nullptr;
+  PODECM_CUDA_TRY(ctx, cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  return PODECM_OK;
+}
+
+void podecm_ipc_close(void* p) { cudaIpcCloseMemHandle(p); }
+
 // C (n_snap x n_snap, overwritten by eigenvectors).  Outputs modes
 // [max_modes][n_dof] (column-major n_dof x keep), evals [n_snap]
 // descending (device), *n_kept (host).  Synchronises the stream.

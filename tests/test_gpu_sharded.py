@@ -1,8 +1,9 @@
 """The split config-4 path of SURVEY §8(e) on the device: two processes (one
 CUDA context each, both on cuda:0 here — the box has one GPU; their kernels
 never wait on each other, every exchange is a host-side gloo collective)
-run the row-sharded POD (api.pod_sharded: local DMMA Gram, all-reduce,
-gathered MGS) and the candidate-sharded greedy (api.ecm_select_sharded ->
+run the row-sharded POD (api.pod_sharded: the DMMA Gram fused with its
+reduce-scatter over CUDA-IPC peer memory — bitwise equal to the local-Gram +
+all-reduce path — gathered MGS) and the candidate-sharded greedy (api.ecm_select_sharded ->
 podecm_ecm_select_sharded).  Eigenvalues within 1e-12 of the single-process
 POD, modes within 1e-10 up to sign, and the selected ids, iteration count and
 weights equal to the single-process greedy (direct scoring), on a reduced
@@ -51,7 +52,8 @@ def _worker(rank, world, port, q):
         rve = api.Rve(32, _mats())
         U = _inputs(api, rve, torch)
         d0, d1 = shard.shard_range(U.shape[1], rank, world)
-        modes, ev = api.pod_sharded(U[:, d0:d1].contiguous(), 12)
+        modes, ev = api.pod_sharded(U[:, d0:d1].contiguous(), 12)  # peer-memory Gram exchange
+        modes_c, ev_c = api.pod_sharded(U[:, d0:d1].contiguous(), 12, exchange="collective")
         W, _ = api.ecm_stress_snapshots(rve, U)
         H = api.ecm_mode_grads(rve, modes)
         q0, q1 = shard.shard_range(rve.n_qp, rank, world)
@@ -63,7 +65,8 @@ def _worker(rank, world, port, q):
         T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
         r2 = api.ecm_select_sharded(g, T(Hd[a0:a1]), T(Wd[:, a0:a1]), a0,
                                     api.EcmOpts(eps=1e-6, max_points=60, stop_at_count=True))
-        q.put((rank, {"modes": modes.cpu().numpy(), "ev": ev.cpu().numpy(), "ecm": r1, "drop": r2}))
+        q.put((rank, {"modes": modes.cpu().numpy(), "ev": ev.cpu().numpy(), "ecm": r1, "drop": r2,
+                      "modes_c": modes_c.cpu().numpy(), "ev_c": ev_c.cpu().numpy()}))
     except Exception as e:  # surface it in the parent
         q.put((rank, {"error": repr(e)}))
     finally:
@@ -101,6 +104,10 @@ def test_two_rank_split_config4(monkeypatch):
     m0 = modes.cpu().numpy()
     for r in range(2):
         d = res[r]
+        # the peer-memory Gram exchange (GEMM fused with its reduce-scatter,
+        # rank-order sums) gives the collective all-reduce's bits at 2 ranks
+        assert np.array_equal(d["ev"].view(np.int64), d["ev_c"].view(np.int64))
+        assert np.array_equal(d["modes"].view(np.int64), d["modes_c"].view(np.int64))
         assert np.abs(d["ev"][:12] - ev).max() <= 1e-12 * ev[0]
         sgn = np.sign((d["modes"] * m0).sum(1))
         assert np.abs(d["modes"] * sgn[:, None] - m0).max() <= 1e-10 * np.abs(m0).max()
