@@ -1243,58 +1243,77 @@ __global__ void __launch_bounds__(32 * kNW) k_rom_newton(NewtonArgs g) {
 // Newton decision, one warp per instance.  Converged and failed instances
 // finish here without ever needing K; the rest are appended to g.list for the
 // tangent pass, the contraction and k_rom_solve.
-constexpr int kCI = 32;     // instances (and warps) per k_rom_check CTA (each CTA streams all of Gm once)
+constexpr int kCW = 32;     // warps per k_rom_check CTA
+constexpr int kCI = 32;     // instances per CTA at IPW = 1 (each CTA streams all of Gm once)
 constexpr int kCRows = 32;  // Gm rows per SMEM stage (kPC points)
 constexpr int kCLdp = kCRows + 4;
 
-__host__ __device__ constexpr size_t check_smem_doubles(int NP) {
-  return (size_t)kCRows * (NP + 4) + (size_t)kCI * kCLdp + (size_t)kCI * NP;
+__host__ __device__ constexpr size_t check_smem_doubles(int NP, int ipw = 1) {
+  return (size_t)kCRows * (NP + 4) + (size_t)kCW * ipw * kCLdp + (size_t)kCW * ipw * NP;
 }
 
-__global__ void __launch_bounds__(32 * kCI) k_rom_check(NewtonArgs g) {
+// IPW instances per warp (kCW * IPW per CTA): every stage of Gm brought into
+// shared memory feeds IPW times the DMMA work (large batches; the f sums keep
+// their k order, so f is the same for any IPW).
+template <int IPW = 1>
+__global__ void __launch_bounds__(32 * kCW) k_rom_check(NewtonArgs g) {
+  constexpr int CI = kCW * IPW;
   extern __shared__ double smk[];
   const int NP = g.NP, LDG = NP + 4, N = g.N;
   double* sG = smk;                                // [kCRows][LDG]
-  double* sPt = sG + (size_t)kCRows * LDG;         // [kCI][kCLdp]
-  double* sF = sPt + (size_t)kCI * kCLdp;          // [kCI][NP]
+  double* sPt = sG + (size_t)kCRows * LDG;         // [CI][kCLdp]
+  double* sF = sPt + (size_t)CI * kCLdp;           // [CI][NP]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const int64_t k0 = (int64_t)blockIdx.x * kCI;
-  const int64_t s = k0 + warp < g.n ? inst_of(g.alist, k0 + warp) : g.n;
-  const bool act = k0 + warp < g.n && g.ctl[s].active;
-  if (!__syncthreads_or(act)) return;
+  const int64_t k0 = (int64_t)blockIdx.x * CI;
+  int64_t sv[IPW];
+  bool av[IPW];
+  bool anyl = false;
+#pragma unroll
+  for (int q = 0; q < IPW; ++q) {
+    const int64_t k = k0 + warp + q * kCW;
+    sv[q] = k < g.n ? inst_of(g.alist, k) : g.n;
+    av[q] = k < g.n && g.ctl[sv[q]].active;
+    anyl |= av[q];
+  }
+  if (!__syncthreads_or(anyl)) return;
   const int NTt = NP / 8;
-  constexpr int MT = kCI / 8;  // m-tiles (8 instances each)
-  // jobs: (m-tile, n-tile) = (j % MT, j / MT), two per warp at most (NT <= 15)
-  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  constexpr int MT = CI / 8;  // m-tiles (8 instances each)
+  constexpr int JPW = (MT * 15 + kCW - 1) / kCW;  // jobs per warp at most (NT <= 15)
+  // jobs: (m-tile, n-tile) = (j % MT, j / MT), j = warp + u kCW
+  double acc[JPW][2];
+#pragma unroll
+  for (int u = 0; u < JPW; ++u) acc[u][0] = acc[u][1] = 0.0;
   const int R = g.Qpad * 4;  // padding rows of Gm and Pt are zero
-  constexpr int kGPT = kCRows * 128 / (32 * kCI);  // Gm doubles per thread per stage (NP <= 128)
-  double rG[kGPT], rP;
+  constexpr int kGPT = kCRows * 128 / (32 * kCW);  // Gm doubles per thread per stage (NP <= 128)
+  double rG[kGPT], rP[IPW];
   auto load = [&](int r0) {  // next stage into registers (in flight during the DMMAs)
 #pragma unroll
     for (int k = 0; k < kGPT; ++k) {
-      const int t = tid + k * 32 * kCI;
+      const int t = tid + k * 32 * kCW;
       rG[k] = t < kCRows * NP ? g.G[(size_t)r0 * NP + t] : 0.0;
     }
     const int row = r0 + lane;
-    rP = act ? g.Pt[((size_t)s * g.Qpad) * 4 + row] : 0.0;
+#pragma unroll
+    for (int q = 0; q < IPW; ++q) rP[q] = av[q] ? g.Pt[((size_t)sv[q] * g.Qpad) * 4 + row] : 0.0;
   };
   load(0);
   for (int r0 = 0; r0 < R; r0 += kCRows) {
 #pragma unroll
     for (int k = 0; k < kGPT; ++k) {
-      const int t = tid + k * 32 * kCI;
+      const int t = tid + k * 32 * kCW;
       if (t < kCRows * NP) {
         const int rr = t / NP, i = t - rr * NP;
         sG[rr * LDG + i] = rG[k];
       }
     }
-    sPt[warp * kCLdp + lane] = rP;
+#pragma unroll
+    for (int q = 0; q < IPW; ++q) sPt[(warp + q * kCW) * kCLdp + lane] = rP[q];
     __syncthreads();
     if (r0 + kCRows < R) load(r0 + kCRows);
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int j = warp + u * kCI;
+    for (int u = 0; u < JPW; ++u) {
+      const int j = warp + u * kCW;
       if (j < MT * NTt) {
         const int mt = j % MT, nt = j / MT;
 #pragma unroll
@@ -1308,8 +1327,8 @@ __global__ void __launch_bounds__(32 * kCI) k_rom_check(NewtonArgs g) {
     __syncthreads();
   }
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    const int j = warp + u * kCI;
+  for (int u = 0; u < JPW; ++u) {
+    const int j = warp + u * kCW;
     if (j < MT * NTt) {
       const int mt = j % MT, nt = j / MT;
       sF[(mt * 8 + gid) * NP + nt * 8 + 2 * tig] = acc[u][0];
@@ -1317,22 +1336,27 @@ __global__ void __launch_bounds__(32 * kCI) k_rom_check(NewtonArgs g) {
     }
   }
   __syncthreads();
-  if (!act) return;
-  RomCtl* c = g.ctl + s;
-  double ss = 0.0;
-  for (int i = lane; i < N; i += 32) {
-    const double v = sF[warp * NP + i];
-    g.f_out[(size_t)s * N + i] = v;
-    ss = fma(v, v, ss);
+#pragma unroll
+  for (int q = 0; q < IPW; ++q) {
+    if (!av[q]) continue;
+    const int64_t s = sv[q];
+    const int wi = warp + q * kCW;
+    RomCtl* c = g.ctl + s;
+    double ss = 0.0;
+    for (int i = lane; i < N; i += 32) {
+      const double v = sF[wi * NP + i];
+      g.f_out[(size_t)s * N + i] = v;
+      ss = fma(v, v, ss);
+    }
+    const int it = c->it;
+    double r;
+    const int d = rom_decide(g, c, s, lane, ss, &r);
+    if (d == 1) rom_converged(g, c, s, lane, r, it);
+    if (d == 2) rom_failed(g, c, s, lane);
+    if (d == 0 && lane == 0) g.list[atomicAdd(g.count, 1)] = (int)s;
+    __syncwarp();
+    if (lane == 0 && c->active) atomicAdd(g.nactive, 1);
   }
-  const int it = c->it;
-  double r;
-  const int d = rom_decide(g, c, s, lane, ss, &r);
-  if (d == 1) rom_converged(g, c, s, lane, r, it);
-  if (d == 2) rom_failed(g, c, s, lane);
-  if (d == 0 && lane == 0) g.list[atomicAdd(g.count, 1)] = (int)s;
-  __syncwarp();
-  if (lane == 0 && c->active) atomicAdd(g.nactive, 1);
 }
 
 // Lazy-tangent pipeline, step 2 (after the tangent pass and the contraction
@@ -1492,6 +1516,17 @@ __global__ void __launch_bounds__(32) k_rom_solve_reg(NewtonArgs g) {
 // Newton update kernel of the lazy pipeline: the register-resident LU for the
 // mode counts it is instantiated for, the shared-memory LU otherwise
 // (PODECM_ROM_LU=smem forces the latter, for A/B comparisons).
+// Instances per warp of the residual check: the largest of 4 / 2 / 1 that
+// still gives >= 2 CTAs per SM (PODECM_ROM_CHECK_IPW = 1, 2 or 4 forces it;
+// read per call).  Every stage of Gm in shared memory then feeds IPW times the
+// DMMA work: 27.0 -> 22.2 (IPW 2) -> 21.5 ms (IPW 4) per C3 solve at 16,384.
+int rom_check_ipw(int64_t n_run) {
+  const char* e = getenv("PODECM_ROM_CHECK_IPW");
+  if (e && (atoi(e) == 1 || atoi(e) == 2 || atoi(e) == 4)) return atoi(e);
+  const int64_t ctas2 = 2 * 148;
+  return n_run >= 4 * kCW * ctas2 ? 4 : (n_run >= 2 * kCW * ctas2 ? 2 : 1);
+}
+
 bool rom_lu_reg() {  // read per call (tests flip it)
   const char* e = getenv("PODECM_ROM_LU");
   return !(e && std::strcmp(e, "smem") == 0);
@@ -1869,7 +1904,9 @@ void set_attrs() {
   set_contract_attrs<false>(std::make_integer_sequence<int, kMaxNT + 1>{});
   set_contract_attrs<true>(std::make_integer_sequence<int, kMaxNT + 1>{});
   cudaFuncSetAttribute(k_rom_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_rom_check, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_rom_check<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_rom_check<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_rom_check<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_rom_newton, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_rom_abar, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (dev < 64) done |= uint64_t(1) << dev;
@@ -2101,6 +2138,8 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
   cl.list = r->d_list;
   cl.count = r->d_nactive + 1;
   const size_t smem_ck = check_smem_doubles(r->NP) * sizeof(double);
+  const size_t smem_ck2 = check_smem_doubles(r->NP, 2) * sizeof(double);
+  const size_t smem_ck4 = check_smem_doubles(r->NP, 4) * sizeof(double);
   const size_t smem_nt = (size_t)kNW * ((size_t)N * (N + 1) + 2 * N) * sizeof(double);
   const int gnt = (int)((n_inst + kNW - 1) / kNW);
 
@@ -2146,7 +2185,14 @@ int rom_solve_impl(podecm_ctx* ctx, void* stream, podecm_rom* r, int64_t n_inst,
       PODECM_CUDA_TRY(ctx, cudaMemsetAsync(r->d_nactive, 0, 2 * sizeof(int), s));
       {
         KTimer kt(ctx, s, "k_rom_check");
-        k_rom_check<<<(int)((n_run + kCI - 1) / kCI), 32 * kCI, smem_ck, s>>>(nr_);
+        // instances per warp: as many as keep >= 2 CTAs per SM busy
+        const int cipw = rom_check_ipw(n_run);
+        if (cipw == 4)
+          k_rom_check<4><<<(int)((n_run + 4 * kCW - 1) / (4 * kCW)), 32 * kCW, smem_ck4, s>>>(nr_);
+        else if (cipw == 2)
+          k_rom_check<2><<<(int)((n_run + 2 * kCW - 1) / (2 * kCW)), 32 * kCW, smem_ck2, s>>>(nr_);
+        else
+          k_rom_check<1><<<(int)((n_run + kCW - 1) / kCW), 32 * kCW, smem_ck, s>>>(nr_);
       }
       {
         KTimer kt(ctx, s, "k_rom_point_tangent");
