@@ -1516,15 +1516,15 @@ __global__ void __launch_bounds__(32) k_rom_solve_reg(NewtonArgs g) {
 // Newton update kernel of the lazy pipeline: the register-resident LU for the
 // mode counts it is instantiated for, the shared-memory LU otherwise
 // (PODECM_ROM_LU=smem forces the latter, for A/B comparisons).
-// Instances per warp of the residual check: the largest of 4 / 2 / 1 that
-// still gives >= 2 CTAs per SM (PODECM_ROM_CHECK_IPW = 1, 2 or 4 forces it;
-// read per call).  Every stage of Gm in shared memory then feeds IPW times the
-// DMMA work: 27.0 -> 22.2 (IPW 2) -> 21.5 ms (IPW 4) per C3 solve at 16,384.
+// Instances per warp of the residual check (PODECM_ROM_CHECK_IPW = 1, 2 or 4
+// forces it; read per call).  Every stage of Gm in shared memory feeds IPW
+// times the DMMA work: 27.0 -> 22.2 (IPW 2) -> 21.5 ms (IPW 4) per C3 solve at
+// 16,384 instances, fewer but fuller CTAs winning even below one per SM;
+// small batches (the FE2 engines) keep one instance per warp.
 int rom_check_ipw(int64_t n_run) {
   const char* e = getenv("PODECM_ROM_CHECK_IPW");
   if (e && (atoi(e) == 1 || atoi(e) == 2 || atoi(e) == 4)) return atoi(e);
-  const int64_t ctas2 = 2 * 148;
-  return n_run >= 4 * kCW * ctas2 ? 4 : (n_run >= 2 * kCW * ctas2 ? 2 : 1);
+  return n_run >= 4096 ? 4 : (n_run >= 2048 ? 2 : 1);
 }
 
 bool rom_lu_reg() {  // read per call (tests flip it)
