@@ -800,6 +800,228 @@ __global__ void __launch_bounds__(32 * NT * IPC, (contract_minb<NT, IPC>())) k_r
     }
 }
 
+// ---- remainder-packed contraction (lazy pipeline, N = 8 NTM + 1 or 2) --------
+// For N = 50 the 56-wide tiling above spends 13 of its 49 DMMA tiles per
+// k-step on the two remainder rows and columns.  Here the NTM x NTM block of
+// full tiles runs as above (NTM warps per instance, NTM column tiles each),
+// and the remainder of BOTH instances of the CTA is one 8-column B tile for
+// one extra warp: with Zc = Gm[:, 8 NTM ..] (the last 1-2 mode columns),
+//   K[:, 8NTM + m]  = Gm^T (D Zc)      (the usual Y columns)        m < 2
+//   K[8NTM + m, :]^T = Gm^T (D^T Zc)   (the rows, through the transposed At)
+// so B = [D Zc | D^T Zc] of instance 0, then of instance 1: NTM + 1 tiles per
+// k-step for the pair.  Per pair and k-step 2 NTM^2 + NTM + 1 DMMAs instead of
+// 2 (NTM + 1)^2: 79 against 98 for N = 50.  The remainder rows are summed over
+// D^T Zc instead of Y, so they differ from the 56-wide kernel's by rounding;
+// every other entry is the same sum in the same order.
+template <int NTM>
+constexpr size_t contract_rp_smem_bytes() {
+  return sizeof(double) * (2 * (kPC * 4) * contract_ld<NTM + 1>() + 2 * 2 * (kPC * 4) * (NTM * 8 + 4) +
+                           2 * (kPC * 4) * 12 + 2 * 2 * kPC * 20);
+}
+
+// Warps own a 2 x 3 block of tiles (row-tile pair x column-tile triple: 5
+// fragment loads per 6 DMMAs instead of 7; the kernel is bound by the
+// shared-memory data pipe and by warp balance, not by the DMMA pipe).  The
+// remainder tile's NTM + 1 row tiles ride on four of the warps, one per SM
+// sub-partition (warp w runs on sub-partition w % 4): warps 0, 9, 10 add the
+// two row tiles of their own A fragments, warp 3 the last (padded) row tile,
+// so every sub-partition issues 38-40 DMMAs per k-step.
+template <int NTM>
+__global__ void __launch_bounds__(32 * 2 * NTM, 2) k_rom_contract_rp(ContractArgs g) {
+  static_assert(NTM == 6, "warp roles below are laid out for 6 x 6 full tiles");
+  constexpr int NT = NTM + 1;
+  constexpr int NP = NT * 8;     // columns of the global Gm rows
+  constexpr int NM = NTM * 8;    // modes in full tiles
+  constexpr int LDG = contract_ld<NT>();
+  constexpr int LDY = NM + 4;    // = 4 mod 16: conflict-free fragment loads
+  constexpr int LDR = 12;        // 8 remainder columns + 4
+  constexpr int KR = kPC * 4;
+  constexpr int NW = 2 * NTM;
+  constexpr int NTHR = 32 * NW;
+  constexpr int NB = NM + 2;     // Y columns built per point: full tiles + D Zc (2)
+  constexpr int NITEM = 2 * kPC * NB;
+  constexpr int GPT = (KR * NP + NTHR - 1) / NTHR;
+  constexpr int APT = (2 * kPC * 16 + NTHR - 1) / NTHR;
+  constexpr int CB = NTM / 3;    // column-triple blocks per instance
+  static_assert(LDY % 16 == 4 || LDY % 16 == 12, "Y row stride");
+  static_assert(NITEM - 2 * NTHR == 32, "two full rounds of Y items + one warp's worth");
+  extern __shared__ double smc[];
+  double* sGm = smc;                      // [2][KR][LDG]
+  double* sY = sGm + 2 * KR * LDG;        // [2][2][KR][LDY]
+  double* sR = sY + 2 * 2 * KR * LDY;     // [2][KR][LDR]
+  double* sAt = sR + 2 * KR * LDR;        // [2][2][kPC][20]: At[r][t] at 4 r + t
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int si = warp / NTM, wb = warp - si * NTM;
+  const int rb = wb / CB, cb = wb - rb * CB;  // row tiles 2 rb, 2 rb + 1; column tiles 3 cb ..
+  const bool rem2 = warp == 0 || warp == 9 || warp == 10;  // rb = 0, 1, 2: remainder row tiles 2 rb, 2 rb + 1
+  const bool rem7 = warp == 3;                             // remainder row tile NTM
+  const int64_t sbase = (int64_t)blockIdx.x * 2;
+  const int64_t lim = *g.count;
+  int64_t sid[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) sid[q] = sbase + q < lim ? (int64_t)g.list[sbase + q] : -1;
+  if (sid[0] < 0 && sid[1] < 0) return;
+  const int gid = lane >> 2, tig = lane & 3;
+  double acc[6][2];   // tile (h, c) of the block at acc[3 h + c]
+  double accr[2][2];  // remainder row tiles of this warp (rem2: 2 rb + h; rem7: NTM at [0])
+#pragma unroll
+  for (int ct = 0; ct < 6; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
+  accr[0][0] = accr[0][1] = accr[1][0] = accr[1][1] = 0.0;
+  const int nch = g.Qpad / kPC;
+  double rG[GPT], rA[APT];
+
+  auto gload = [&](int c) {
+    const double* gsrc = g.G + (size_t)c * kPC * 4 * NP;
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+      const int t = tid + k * NTHR;
+      rG[k] = t < KR * NP ? gsrc[t] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+      const int t = tid + k * NTHR;
+      rA[k] = 0.0;
+      if (t < 2 * kPC * 16) {
+        const int q = t / (kPC * 16), rm = t - q * kPC * 16;
+        const int tp = rm / kPC, pl = rm - tp * kPC;  // At planes [s][20][Qpad], points fastest
+        const int64_t sq = q ? sid[1] : sid[0];
+        if (sq >= 0) rA[k] = g.At[((size_t)sq * 20 + tp) * g.Qpad + (size_t)c * kPC + pl];
+      }
+    }
+  };
+  auto gstore = [&](int buf) {
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+      const int t = tid + k * NTHR;
+      if (t < KR * NP) sGm[buf * KR * LDG + (t / NP) * LDG + t % NP] = rG[k];
+    }
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+      const int t = tid + k * NTHR;
+      if (t < 2 * kPC * 16) {
+        const int q = t / (kPC * 16), rm = t - q * kPC * 16;
+        const int tp = rm / kPC, pl = rm - tp * kPC;  // plane tp = r + 4 t holds At[r][t]
+        sAt[buf * 2 * kPC * 20 + q * kPC * 20 + pl * 20 + 4 * (tp & 3) + (tp >> 2)] = rA[k];
+      }
+    }
+  };
+  // Item t = (instance q, point, column j < NM + 2): the 4 rows of Y column j
+  // (j >= NM: into the remainder tile, columns 4 q + j - NM), row r from At's
+  // row r (one 32-byte load) in the 56-wide kernel's FMA order.
+  auto y_item = [&](const double* G0, int buf, int t) {
+    const int q = t / (kPC * NB), rm = t - q * kPC * NB;
+    const int pl = rm / NB, j = rm - pl * NB;
+    const double* at = sAt + (buf * 2 + q) * kPC * 20 + pl * 20;
+    const double g0 = G0[(pl * 4) * LDG + j], g1 = G0[(pl * 4 + 1) * LDG + j];
+    const double g2 = G0[(pl * 4 + 2) * LDG + j], g3 = G0[(pl * 4 + 3) * LDG + j];
+    double* y = j < NM ? sY + (buf * 2 + q) * KR * LDY + (pl * 4) * LDY + j
+                       : sR + buf * KR * LDR + (pl * 4) * LDR + q * 4 + (j - NM);
+    const int ld = j < NM ? LDY : LDR;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const double4 ar = *reinterpret_cast<const double4*>(at + 4 * r);  // At[r][0..3]
+      y[r * ld] = fma(ar.w, g3, fma(ar.z, g2, fma(ar.y, g1, ar.x * g0)));
+    }
+  };
+  // two items per thread; the last 32 items go to warp 7 and the 32
+  // (instance, point, m) columns of D^T Zc to warp 11 (both on the
+  // sub-partition with the fewest remainder DMMAs)
+  auto build_tail = [&](const double* G0, int buf) {
+    if (warp == 7) y_item(G0, buf, 2 * NTHR + lane);
+    if (warp == 11) {  // (D^T Zc)[4p + t] = sum_r At[r][t] Zc[4p + r]
+      static_assert(2 * kPC * 2 == 32, "one lane per (instance, point, m)");
+      const int q = lane >> 4, pl = (lane >> 1) & (kPC - 1), m = lane & 1;
+      const double* at = sAt + (buf * 2 + q) * kPC * 20 + pl * 20;
+      const double g0 = G0[(pl * 4) * LDG + NM + m], g1 = G0[(pl * 4 + 1) * LDG + NM + m];
+      const double g2 = G0[(pl * 4 + 2) * LDG + NM + m], g3 = G0[(pl * 4 + 3) * LDG + NM + m];
+      double* y = sR + buf * KR * LDR + (pl * 4) * LDR + q * 4 + 2 + m;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) y[t * LDR] = fma(at[12 + t], g3, fma(at[8 + t], g2, fma(at[4 + t], g1, at[t] * g0)));
+    }
+  };
+  auto build_y = [&](int buf) {
+    const double* G0 = sGm + buf * KR * LDG;
+    y_item(G0, buf, tid);
+    y_item(G0, buf, tid + NTHR);
+    build_tail(G0, buf);
+  };
+  auto mma = [&](int buf) {
+    const double* G0 = sGm + buf * KR * LDG;
+    const double* Y0 = sY + (buf * 2 + si) * KR * LDY + cb * 24 + gid;
+    const double* A0 = G0 + rb * 16 + gid;
+    const double* R0 = sR + buf * KR * LDR + gid;
+#pragma unroll
+    for (int ks = 0; ks < KR / 4; ++ks) {
+      const double a0 = A0[(ks * 4 + tig) * LDG], a1 = A0[(ks * 4 + tig) * LDG + 8];  // (Gm^T)[i][k]
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double b = Y0[(ks * 4 + tig) * LDY + c * 8];
+        dmma(acc[c][0], acc[c][1], a0, b);
+        dmma(acc[3 + c][0], acc[3 + c][1], a1, b);
+      }
+      if (rem2) {
+        const double br = R0[(ks * 4 + tig) * LDR];
+        dmma(accr[0][0], accr[0][1], a0, br);
+        dmma(accr[1][0], accr[1][1], a1, br);
+      } else if (rem7) {
+        dmma(accr[0][0], accr[0][1], G0[(ks * 4 + tig) * LDG + NM + gid], R0[(ks * 4 + tig) * LDR]);
+      }
+    }
+  };
+
+  gload(0);
+  gstore(0);
+  __syncthreads();
+  build_y(0);
+  if (nch > 1) {
+    gload(1);
+    gstore(1);
+  }
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    const int cur = c & 1, nxt = cur ^ 1;
+    if (c + 2 < nch) gload(c + 2);
+    if (c + 1 < nch) build_y(nxt);
+    mma(cur);
+    __syncthreads();
+    if (c + 2 < nch) gstore(cur);
+    __syncthreads();
+  }
+  {
+    const int64_t s = si ? sid[1] : sid[0];
+    if (s >= 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = (2 * rb + h) * 8 + gid;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            g.K[((size_t)s * g.N + i) * g.N + (3 * cb + c) * 8 + 2 * tig + e] = acc[3 * h + c][e];
+      }
+    }
+  }
+  if (!rem2 && !rem7) return;
+  // remainder tile columns n = 2 tig + e: instance n >> 2, item m = n & 3
+  const int64_t s = (tig >> 1) ? sid[1] : sid[0];
+  if (s < 0) return;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (rem7 && h) break;
+    const int i = (rem7 ? NTM : 2 * rb + h) * 8 + gid;
+    if (i >= g.N) continue;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int m = 2 * (tig & 1) + e;
+      if (m < 2) {
+        if (NM + m < g.N) g.K[((size_t)s * g.N + i) * g.N + NM + m] = accr[h][e];
+      } else if (NM + m - 2 < g.N && i < NM) {
+        g.K[((size_t)s * g.N + NM + m - 2) * g.N + i] = accr[h][e];
+      }
+    }
+  }
+}
+
 // ---- Newton / bisection state machine + LU --------------------------------
 struct NewtonArgs {
   int64_t n;
@@ -1903,6 +2125,8 @@ void set_attrs() {
   cudaFuncSetAttribute(k_rom_F_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   set_contract_attrs<false>(std::make_integer_sequence<int, kMaxNT + 1>{});
   set_contract_attrs<true>(std::make_integer_sequence<int, kMaxNT + 1>{});
+  cudaFuncSetAttribute(k_rom_contract_rp<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)contract_rp_smem_bytes<6>());
   cudaFuncSetAttribute(k_rom_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_rom_check<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_rom_check<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1997,8 +2221,22 @@ void launch_contract_sw(int nt, cudaStream_t s, const ContractArgs& ca, std::int
     (..., (nt == I + 1 ? launch_contract_nt<I + 1, false>(s, ca) : (void)0));
 }
 
+// Remainder-packed form: lazy pipeline (list), N = 49 or 50, large batches
+// (PODECM_ROM_CONTRACT=std: the 56-wide kernel, =rp: any batch size; read per
+// call, tests flip it).
+bool contract_rp_on(int64_t n) {
+  const char* e = getenv("PODECM_ROM_CONTRACT");
+  if (e && std::strcmp(e, "std") == 0) return false;
+  if (e && std::strcmp(e, "rp") == 0) return true;  // any batch size (tests)
+  return n >= kSmallBatch;
+}
+
 void launch_contract(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, const ContractArgs& ca) {
   KTimer kt(ctx, s, "k_rom_contract");
+  if (ca.list && r->NT == 7 && r->N > 48 && r->N <= 50 && contract_rp_on(ca.n)) {
+    k_rom_contract_rp<6><<<(int)((ca.n + 1) / 2), 32 * 12, contract_rp_smem_bytes<6>(), s>>>(ca);
+    return;
+  }
   launch_contract_sw(r->NT, s, ca, std::make_integer_sequence<int, kMaxNT>{});
 }
 

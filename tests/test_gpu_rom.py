@@ -189,3 +189,31 @@ def test_kernel_variants_bit_identical(setup, monkeypatch, var, val):
     assert (a["iters"] > 3).any(), "no increment bisected"
     for k in ("pbar", "iters", "status"):
         assert np.array_equal(np.ascontiguousarray(a[k]).view(np.uint8), np.ascontiguousarray(b[k]).view(np.uint8)), k
+
+
+def test_remainder_packed_contraction(setup, monkeypatch):
+    """k_rom_contract_rp (N = 50: the 48 x 48 block of full DMMA tiles per
+    instance, the two remainder rows and columns of both instances of a CTA
+    packed into one 8-column tile) against the 56-wide kernel: the remainder
+    rows are summed through the transposed tangent, so K differs by rounding
+    there and nowhere else; whole solves — odd instance count, with
+    bisections — agree to 1e-11 in pbar with equal iteration counts, and the
+    packed form holds the oracle tolerance on its own."""
+    import torch
+    from paper_2307_16894_b200 import api
+    g, o, model, rom = setup
+    geom, sched = synth.rom_instances(97, 2, 78, 0.2)
+    T = lambda a: torch.from_numpy(a).cuda()
+    opts = api.NewtonOpts(eps_rel=1e-10, eps_abs=1e-12, max_iter=4, max_bisect=5)
+    res = {}
+    for mode in ("std", "rp"):
+        monkeypatch.setenv("PODECM_ROM_CONTRACT", mode)
+        res[mode] = {k: v.cpu().numpy() for k, v in rom.solve(T(geom), T(sched), opts).items()}
+    a, b = res["std"], res["rp"]
+    assert np.array_equal(a["status"], b["status"]) and np.array_equal(a["iters"], b["iters"])
+    rel = np.abs(a["pbar"] - b["pbar"]).max() / np.abs(a["pbar"]).max()
+    print(f"rp vs std: pbar max rel {rel:.2e}; bitwise equal: {np.array_equal(a['pbar'], b['pbar'])}")
+    assert 0 < rel <= 1e-11 or np.array_equal(a["pbar"], b["pbar"])
+    ro = o.rom_solve(model["ids"], model["weights"], model["mode_grads"], geom, sched, eps_rel=opts.eps_rel,
+                     eps_abs=opts.eps_abs, max_iter=opts.max_iter, max_bisect=opts.max_bisect)
+    _check(b, ro)
