@@ -624,6 +624,11 @@ def run_c3(args, ws, rank, local, ctx, n_inst, steps, warmup, fp64):
 # --------------------------------------------------------------- config 4 --
 
 # ------------------------------------------------------------ FE2 (paper) --
+# peak traction of the FE2 plate (the synthetic ROM's engines exhaust their bisections at some
+# values, on the CPU oracle too: DESIGN.md section 5); dev override for probing
+FE2_PEAK_TRACTION = float(os.environ.get("PODECM_FE2_TRACTION", "0.075"))
+
+
 def run_fe2(args, ws, rank, local, ctx):
     """The paper's headline workload at its Example-2 sizes:
     FE2 plate of 200 Quad8 / 800 macro Gauss points, 50 load steps, a ROM micro
@@ -642,7 +647,7 @@ def run_fe2(args, ws, rank, local, ctx):
     micro = api.NewtonOpts(eps_rel=1e-10, eps_abs=1e-12, max_iter=25)
 
     def run(steps):
-        cfg = api.MacroConfig(nx=20, ny=10, steps=steps, peak_traction=0.07, newton=macro_newton)
+        cfg = api.MacroConfig(nx=20, ny=10, steps=steps, peak_traction=FE2_PEAK_TRACTION, newton=macro_newton)
         x = cfg.qp_positions()  # graded inclusion geometry over the plate (cf. graded_pore_params)
         geom = np.stack([0.2 + 0.1 * (1 - x[:, 0] / cfg.width) ** 2, 0.2 + 0.1 * (1 - x[:, 1] / cfg.height)], 1)
         eng = api.RomEngines(rom, torch.from_numpy(geom).to(dev))

@@ -283,6 +283,8 @@ def lib(libm: str = "glibc"):
         l.orc_rve_morph.argtypes = [P, D, D, P, P]
         l.orc_rve_assemble.restype = L
         l.orc_rve_assemble.argtypes = [P, L, P, P, P, P, P, P, P, P, P, I]
+        l.orc_rom_set_init_resid.restype = None
+        l.orc_rom_set_init_resid.argtypes = [P]
         l.orc_rom_solve.restype = L
         l.orc_rom_solve.argtypes = [P, I, I, P, P, P, L, P, P, I, D, D, I, I, P, P, P, P, P, P, I]
         l.orc_rom_effective_stiffness.restype = L
@@ -437,10 +439,15 @@ class Rve:
         af = np.empty((n, N))
         status = np.empty(n, np.int32)
         ab = np.zeros((n, 16)) if abar else None
-        self.L.orc_rom_solve(self.h, N, Q, _p(ids), _p(weights), _p(mg), n, _p(geom), _p(sched), K,
-                            eps_rel, eps_abs, max_iter, max_bisect, _p(pbar), _p(iters), _p(resid),
-                            _p(af), _p(status), _p(ab) if abar else None, nthreads)
-        out = {"pbar": pbar, "iters": iters, "resid": resid, "a_final": af, "status": status}
+        r0 = np.zeros((n, K))  # initial residual per increment (tolerance = max(eps_rel r0, eps_abs))
+        self.L.orc_rom_set_init_resid(_p(r0))
+        try:
+            self.L.orc_rom_solve(self.h, N, Q, _p(ids), _p(weights), _p(mg), n, _p(geom), _p(sched), K,
+                                eps_rel, eps_abs, max_iter, max_bisect, _p(pbar), _p(iters), _p(resid),
+                                _p(af), _p(status), _p(ab) if abar else None, nthreads)
+        finally:
+            self.L.orc_rom_set_init_resid(None)
+        out = {"pbar": pbar, "iters": iters, "resid": resid, "a_final": af, "status": status, "init_resid": r0}
         if abar:
             out["abar"] = ab
         return out

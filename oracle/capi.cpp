@@ -219,6 +219,12 @@ long orc_rve_assemble(void* hp, long n_inst, const double* geom, const double* f
 // iters[n_inst][K], resid[n_inst][K], a_final[n_inst][N]; status 0/3;
 // abar[n_inst][16] (nullable): rom_effective_stiffness at the last increment
 // the way run_online requests it (pipeline.cpp:456-483).
+// Optional extra output of orc_rom_solve: init_resid[n_inst][K], the initial
+// residual of every increment (its Newton tolerance is max(eps_rel * that,
+// eps_abs)); set before the call, nullptr to stop.
+static double* g_rom_init_resid = nullptr;
+void orc_rom_set_init_resid(double* buf) { g_rom_init_resid = buf; }
+
 long orc_rom_solve(void* hp, int N, int Q, const int* ids, const double* weights,
                    const double* mode_grads, long n_inst, const double* geom, const double* sched,
                    int K, double eps_rel, double eps_abs, int max_iter, int max_bisect, double* pbar,
@@ -259,6 +265,7 @@ long orc_rom_solve(void* hp, int N, int Q, const int* ids, const double* weights
         for (int c = 0; c < 4; ++c) pbar[((size_t)s * K + k) * 4 + c] = recs[k].pbar.a[c];
         if (iters) iters[(size_t)s * K + k] = recs[k].iters;
         if (resid) resid[(size_t)s * K + k] = recs[k].residual;
+        if (g_rom_init_resid) g_rom_init_resid[(size_t)s * K + k] = recs[k].initial_residual;
       }
       if (a_final) std::memcpy(a_final + (size_t)s * N, af.data(), N * sizeof(double));
       if (status) status[s] = 0;

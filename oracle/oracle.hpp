@@ -189,6 +189,7 @@ struct RomStepRecord {
   Mat2 pbar;
   int iters = 0;
   double residual = 0;
+  double initial_residual = 0;  // RomStepResult::initial_residual (sets the increment's tolerance)
 };
 // rom.cpp:177-200 with rom_solve_step_adaptive (rom.cpp:152-175).
 // fmu_inv/det are the morph slice at the ECM ids.  Throws SolveError.

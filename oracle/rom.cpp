@@ -201,6 +201,7 @@ std::vector<RomStepRecord> rom_solve(const RveProblem& prob, const RomModel& mod
     r.pbar = st.pbar;
     r.iters = st.iters;
     r.residual = st.residual;
+    r.initial_residual = st.initial_residual;
     recs.push_back(r);
   }
   if (a_final) *a_final = a;

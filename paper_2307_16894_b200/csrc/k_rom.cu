@@ -813,22 +813,28 @@ __global__ void __launch_bounds__(32 * NT * IPC, (contract_minb<NT, IPC>())) k_r
 // 2 (NTM + 1)^2: 79 against 98 for N = 50.  The remainder rows are summed over
 // D^T Zc instead of Y, so they differ from the 56-wide kernel's by rounding;
 // every other entry is the same sum in the same order.
-template <int NTM>
+template <int NTM, int IPC>
 constexpr size_t contract_rp_smem_bytes() {
-  return sizeof(double) * (2 * (kPC * 4) * contract_ld<NTM + 1>() + 2 * 2 * (kPC * 4) * (NTM * 8 + 4) +
-                           2 * (kPC * 4) * 12 + 2 * 2 * kPC * 20);
+  return sizeof(double) * (2 * (kPC * 4) * contract_ld<NTM + 1>() + 2 * IPC * (kPC * 4) * (NTM * 8 + 4) +
+                           2 * (kPC * 4) * 12 + 2 * IPC * kPC * 20);
 }
 
 // Warps own a 2 x 3 block of tiles (row-tile pair x column-tile triple: 5
 // fragment loads per 6 DMMAs instead of 7; the kernel is bound by the
 // shared-memory data pipe and by warp balance, not by the DMMA pipe).  The
-// remainder tile's NTM + 1 row tiles ride on four of the warps, one per SM
-// sub-partition (warp w runs on sub-partition w % 4): warps 0, 9, 10 add the
-// two row tiles of their own A fragments, warp 3 the last (padded) row tile,
-// so every sub-partition issues 38-40 DMMAs per k-step.
-template <int NTM>
-__global__ void __launch_bounds__(32 * 2 * NTM, 2) k_rom_contract_rp(ContractArgs g) {
-  static_assert(NTM == 6, "warp roles below are laid out for 6 x 6 full tiles");
+// remainder tile's NTM + 1 row tiles ride on four of the warps, on different
+// SM sub-partitions (warp w runs on sub-partition w % 4): three add the two
+// row tiles of their own A fragments, one the last (padded) row tile; with
+// two instances per CTA every sub-partition issues 38-40 DMMAs per k-step.
+// IPC = 1 (small batches: twice the CTAs) leaves half of the remainder tile
+// empty and gives its row tiles to two extra warps (4 + 3 tiles: 12, 12, 10, 9
+// DMMAs per k-step on the four sub-partitions); an instance's K has the same
+// bits either way (its columns of the tile do not depend on the other
+// instance's, and every tile is the same k-ordered DMMA chain).
+template <int NTM, int IPC>
+__global__ void __launch_bounds__(32 * (IPC * NTM + (IPC == 1 ? 2 : 0)), (IPC == 2 ? 2 : 3))
+    k_rom_contract_rp(ContractArgs g) {
+  static_assert(NTM == 6 && (IPC == 1 || IPC == 2), "warp roles below are laid out for 6 x 6 full tiles");
   constexpr int NT = NTM + 1;
   constexpr int NP = NT * 8;     // columns of the global Gm rows
   constexpr int NM = NTM * 8;    // modes in full tiles
@@ -836,37 +842,46 @@ __global__ void __launch_bounds__(32 * 2 * NTM, 2) k_rom_contract_rp(ContractArg
   constexpr int LDY = NM + 4;    // = 4 mod 16: conflict-free fragment loads
   constexpr int LDR = 12;        // 8 remainder columns + 4
   constexpr int KR = kPC * 4;
-  constexpr int NW = 2 * NTM;
+  constexpr int NWM = IPC * NTM;            // warps with a 2 x 3 block of full tiles
+  constexpr int NW = NWM + (IPC == 1 ? 2 : 0);
   constexpr int NTHR = 32 * NW;
-  constexpr int NB = NM + 2;     // Y columns built per point: full tiles + D Zc (2)
-  constexpr int NITEM = 2 * kPC * NB;
   constexpr int GPT = (KR * NP + NTHR - 1) / NTHR;
-  constexpr int APT = (2 * kPC * 16 + NTHR - 1) / NTHR;
+  constexpr int APT = (IPC * kPC * 16 + NTHR - 1) / NTHR;
   constexpr int CB = NTM / 3;    // column-triple blocks per instance
+  constexpr int NRA = IPC == 1 ? 4 : 2;     // remainder accumulator tiles per warp
   static_assert(LDY % 16 == 4 || LDY % 16 == 12, "Y row stride");
-  static_assert(NITEM - 2 * NTHR == 32, "two full rounds of Y items + one warp's worth");
   extern __shared__ double smc[];
-  double* sGm = smc;                      // [2][KR][LDG]
-  double* sY = sGm + 2 * KR * LDG;        // [2][2][KR][LDY]
-  double* sR = sY + 2 * 2 * KR * LDY;     // [2][KR][LDR]
-  double* sAt = sR + 2 * KR * LDR;        // [2][2][kPC][20]: At[r][t] at 4 r + t
+  double* sGm = smc;                        // [2][KR][LDG]
+  double* sY = sGm + 2 * KR * LDG;          // [2][IPC][KR][LDY]
+  double* sR = sY + 2 * IPC * KR * LDY;     // [2][KR][LDR]
+  double* sAt = sR + 2 * KR * LDR;          // [2][IPC][kPC][20]: At[r][t] at 4 r + t
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int si = warp / NTM, wb = warp - si * NTM;
+  const bool mainw = warp < NWM;
+  const int si = mainw ? warp / NTM : 0, wb = mainw ? warp - si * NTM : 0;
   const int rb = wb / CB, cb = wb - rb * CB;  // row tiles 2 rb, 2 rb + 1; column tiles 3 cb ..
-  const bool rem2 = warp == 0 || warp == 9 || warp == 10;  // rb = 0, 1, 2: remainder row tiles 2 rb, 2 rb + 1
-  const bool rem7 = warp == 3;                             // remainder row tile NTM
-  const int64_t sbase = (int64_t)blockIdx.x * 2;
+  // IPC 2: remainder row tiles 2 rb, 2 rb + 1 (rb = 0, 1, 2) / row tile NTM ride on main warps
+  const bool rem2 = IPC == 2 && (warp == 0 || warp == 9 || warp == 10);
+  const bool rem7 = IPC == 2 && warp == 3;
+  // IPC 1: warp NWM owns remainder row tiles 0..3, warp NWM + 1 tiles 4..NTM
+  const int rt0 = warp == NWM ? 0 : 4, rtn = warp == NWM ? 4 : NT - 4;
+  constexpr int kTailA = IPC == 2 ? 7 : 7, kTailB = IPC == 2 ? 11 : 7;  // warps building D Zc / D^T Zc
+  const int64_t sbase = (int64_t)blockIdx.x * IPC;
   const int64_t lim = *g.count;
-  int64_t sid[2];
+  int64_t sid[IPC];
+  bool any = false;
 #pragma unroll
-  for (int q = 0; q < 2; ++q) sid[q] = sbase + q < lim ? (int64_t)g.list[sbase + q] : -1;
-  if (sid[0] < 0 && sid[1] < 0) return;
+  for (int q = 0; q < IPC; ++q) {
+    sid[q] = sbase + q < lim ? (int64_t)g.list[sbase + q] : -1;
+    any = any || sid[q] >= 0;
+  }
+  if (!any) return;
   const int gid = lane >> 2, tig = lane & 3;
   double acc[6][2];   // tile (h, c) of the block at acc[3 h + c]
-  double accr[2][2];  // remainder row tiles of this warp (rem2: 2 rb + h; rem7: NTM at [0])
+  double accr[NRA][2];  // remainder row tiles of this warp (rem2: 2 rb + h; rem7: NTM at [0]; IPC 1: rt0 + h)
 #pragma unroll
   for (int ct = 0; ct < 6; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
-  accr[0][0] = accr[0][1] = accr[1][0] = accr[1][1] = 0.0;
+#pragma unroll
+  for (int ct = 0; ct < NRA; ++ct) accr[ct][0] = accr[ct][1] = 0.0;
   const int nch = g.Qpad / kPC;
   double rG[GPT], rA[APT];
 
@@ -881,10 +896,10 @@ __global__ void __launch_bounds__(32 * 2 * NTM, 2) k_rom_contract_rp(ContractArg
     for (int k = 0; k < APT; ++k) {
       const int t = tid + k * NTHR;
       rA[k] = 0.0;
-      if (t < 2 * kPC * 16) {
+      if (t < IPC * kPC * 16) {
         const int q = t / (kPC * 16), rm = t - q * kPC * 16;
         const int tp = rm / kPC, pl = rm - tp * kPC;  // At planes [s][20][Qpad], points fastest
-        const int64_t sq = q ? sid[1] : sid[0];
+        const int64_t sq = (IPC == 2 && q) ? sid[IPC - 1] : sid[0];
         if (sq >= 0) rA[k] = g.At[((size_t)sq * 20 + tp) * g.Qpad + (size_t)c * kPC + pl];
       }
     }
@@ -898,23 +913,21 @@ __global__ void __launch_bounds__(32 * 2 * NTM, 2) k_rom_contract_rp(ContractArg
 #pragma unroll
     for (int k = 0; k < APT; ++k) {
       const int t = tid + k * NTHR;
-      if (t < 2 * kPC * 16) {
+      if (t < IPC * kPC * 16) {
         const int q = t / (kPC * 16), rm = t - q * kPC * 16;
         const int tp = rm / kPC, pl = rm - tp * kPC;  // plane tp = r + 4 t holds At[r][t]
-        sAt[buf * 2 * kPC * 20 + q * kPC * 20 + pl * 20 + 4 * (tp & 3) + (tp >> 2)] = rA[k];
+        sAt[buf * IPC * kPC * 20 + q * kPC * 20 + pl * 20 + 4 * (tp & 3) + (tp >> 2)] = rA[k];
       }
     }
   };
-  // Item t = (instance q, point, column j < NM + 2): the 4 rows of Y column j
-  // (j >= NM: into the remainder tile, columns 4 q + j - NM), row r from At's
-  // row r (one 32-byte load) in the 56-wide kernel's FMA order.
-  auto y_item = [&](const double* G0, int buf, int t) {
-    const int q = t / (kPC * NB), rm = t - q * kPC * NB;
-    const int pl = rm / NB, j = rm - pl * NB;
-    const double* at = sAt + (buf * 2 + q) * kPC * 20 + pl * 20;
+  // Item (instance q, point pl, column j): the 4 rows of Y column j (j >= NM:
+  // into the remainder tile, columns 4 q + j - NM), row r from At's row r (one
+  // 32-byte load) in the 56-wide kernel's FMA order.
+  auto y_item = [&](const double* G0, int buf, int q, int pl, int j) {
+    const double* at = sAt + (buf * IPC + q) * kPC * 20 + pl * 20;
     const double g0 = G0[(pl * 4) * LDG + j], g1 = G0[(pl * 4 + 1) * LDG + j];
     const double g2 = G0[(pl * 4 + 2) * LDG + j], g3 = G0[(pl * 4 + 3) * LDG + j];
-    double* y = j < NM ? sY + (buf * 2 + q) * KR * LDY + (pl * 4) * LDY + j
+    double* y = j < NM ? sY + (buf * IPC + q) * KR * LDY + (pl * 4) * LDY + j
                        : sR + buf * KR * LDR + (pl * 4) * LDR + q * 4 + (j - NM);
     const int ld = j < NM ? LDY : LDR;
 #pragma unroll
@@ -923,15 +936,29 @@ __global__ void __launch_bounds__(32 * 2 * NTM, 2) k_rom_contract_rp(ContractArg
       y[r * ld] = fma(ar.w, g3, fma(ar.z, g2, fma(ar.y, g1, ar.x * g0)));
     }
   };
-  // two items per thread; the last 32 items go to warp 7 and the 32
-  // (instance, point, m) columns of D^T Zc to warp 11 (both on the
-  // sub-partition with the fewest remainder DMMAs)
-  auto build_tail = [&](const double* G0, int buf) {
-    if (warp == 7) y_item(G0, buf, 2 * NTHR + lane);
-    if (warp == 11) {  // (D^T Zc)[4p + t] = sum_r At[r][t] Zc[4p + r]
-      static_assert(2 * kPC * 2 == 32, "one lane per (instance, point, m)");
-      const int q = lane >> 4, pl = (lane >> 1) & (kPC - 1), m = lane & 1;
-      const double* at = sAt + (buf * 2 + q) * kPC * 20 + pl * 20;
+  // Two items per thread over the IPC x kPC x NM full-tile columns (a
+  // half-warp = 16 consecutive columns of one point: conflict-free stores).
+  // The IPC x kPC x 2 remainder columns D Zc and as many of D^T Zc go to the
+  // tail warp(s), on the sub-partition with the fewest remainder DMMAs.
+  static_assert(IPC * kPC * NM <= 2 * NTHR && NTHR % 16 == 0, "at most two full-tile columns per thread");
+  auto build_y = [&](int buf) {
+    const double* G0 = sGm + buf * KR * LDG;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int u = tid + h * NTHR;
+      if (u >= IPC * kPC * NM) break;
+      const int q = u / (kPC * NM), rm = u - q * kPC * NM;
+      y_item(G0, buf, q, rm / NM, rm % NM);
+    }
+    if (warp != kTailA && warp != kTailB) return;
+    // lane -> (instance or kind, point, m)
+    const int hi = lane >> 4, pl = (lane >> 1) & (kPC - 1), m = lane & 1;
+    const int q = IPC == 2 ? hi : 0;
+    const bool tr = IPC == 2 ? warp == kTailB : hi == 1;
+    if (!tr) {
+      y_item(G0, buf, q, pl, NM + m);
+    } else {  // (D^T Zc)[4p + t] = sum_r At[r][t] Zc[4p + r]
+      const double* at = sAt + (buf * IPC + q) * kPC * 20 + pl * 20;
       const double g0 = G0[(pl * 4) * LDG + NM + m], g1 = G0[(pl * 4 + 1) * LDG + NM + m];
       const double g2 = G0[(pl * 4 + 2) * LDG + NM + m], g3 = G0[(pl * 4 + 3) * LDG + NM + m];
       double* y = sR + buf * KR * LDR + (pl * 4) * LDR + q * 4 + 2 + m;
@@ -939,17 +966,22 @@ __global__ void __launch_bounds__(32 * 2 * NTM, 2) k_rom_contract_rp(ContractArg
       for (int t = 0; t < 4; ++t) y[t * LDR] = fma(at[12 + t], g3, fma(at[8 + t], g2, fma(at[4 + t], g1, at[t] * g0)));
     }
   };
-  auto build_y = [&](int buf) {
-    const double* G0 = sGm + buf * KR * LDG;
-    y_item(G0, buf, tid);
-    y_item(G0, buf, tid + NTHR);
-    build_tail(G0, buf);
-  };
   auto mma = [&](int buf) {
     const double* G0 = sGm + buf * KR * LDG;
-    const double* Y0 = sY + (buf * 2 + si) * KR * LDY + cb * 24 + gid;
+    const double* Y0 = sY + (buf * IPC + si) * KR * LDY + cb * 24 + gid;
     const double* A0 = G0 + rb * 16 + gid;
     const double* R0 = sR + buf * KR * LDR + gid;
+    if (IPC == 1 && !mainw) {  // remainder-only warp: its row tiles against the remainder B tile
+      const double* Ar = G0 + rt0 * 8 + gid;
+#pragma unroll
+      for (int ks = 0; ks < KR / 4; ++ks) {
+        const double br = R0[(ks * 4 + tig) * LDR];
+#pragma unroll
+        for (int t = 0; t < NRA; ++t)
+          if (t < rtn) dmma(accr[t][0], accr[t][1], Ar[(ks * 4 + tig) * LDG + t * 8], br);
+      }
+      return;
+    }
 #pragma unroll
     for (int ks = 0; ks < KR / 4; ++ks) {
       const double a0 = A0[(ks * 4 + tig) * LDG], a1 = A0[(ks * 4 + tig) * LDG + 8];  // (Gm^T)[i][k]
@@ -969,6 +1001,9 @@ __global__ void __launch_bounds__(32 * 2 * NTM, 2) k_rom_contract_rp(ContractArg
     }
   };
 
+  if constexpr (IPC == 1) {  // the unused half of the remainder tile stays zero
+    for (int t = tid; t < 2 * KR * LDR; t += NTHR) sR[t] = 0.0;
+  }
   gload(0);
   gstore(0);
   __syncthreads();
@@ -987,8 +1022,8 @@ __global__ void __launch_bounds__(32 * 2 * NTM, 2) k_rom_contract_rp(ContractArg
     if (c + 2 < nch) gstore(cur);
     __syncthreads();
   }
-  {
-    const int64_t s = si ? sid[1] : sid[0];
+  if (mainw) {
+    const int64_t s = sid[IPC == 2 ? si : 0];
     if (s >= 0) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -1001,14 +1036,15 @@ __global__ void __launch_bounds__(32 * 2 * NTM, 2) k_rom_contract_rp(ContractArg
       }
     }
   }
-  if (!rem2 && !rem7) return;
+  if (IPC == 2 ? (!rem2 && !rem7) : mainw) return;
   // remainder tile columns n = 2 tig + e: instance n >> 2, item m = n & 3
-  const int64_t s = (tig >> 1) ? sid[1] : sid[0];
+  if (IPC == 1 && (tig >> 1)) return;
+  const int64_t s = sid[IPC == 2 ? (tig >> 1) : 0];
   if (s < 0) return;
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    if (rem7 && h) break;
-    const int i = (rem7 ? NTM : 2 * rb + h) * 8 + gid;
+  for (int h = 0; h < NRA; ++h) {
+    if (IPC == 2 ? (rem7 && h) : h >= rtn) break;
+    const int i = (IPC == 2 ? (rem7 ? NTM : 2 * rb + h) : rt0 + h) * 8 + gid;
     if (i >= g.N) continue;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -2125,8 +2161,10 @@ void set_attrs() {
   cudaFuncSetAttribute(k_rom_F_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   set_contract_attrs<false>(std::make_integer_sequence<int, kMaxNT + 1>{});
   set_contract_attrs<true>(std::make_integer_sequence<int, kMaxNT + 1>{});
-  cudaFuncSetAttribute(k_rom_contract_rp<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)contract_rp_smem_bytes<6>());
+  cudaFuncSetAttribute(k_rom_contract_rp<6, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)contract_rp_smem_bytes<6, 1>());
+  cudaFuncSetAttribute(k_rom_contract_rp<6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)contract_rp_smem_bytes<6, 2>());
   cudaFuncSetAttribute(k_rom_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_rom_check<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_rom_check<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -2221,20 +2259,20 @@ void launch_contract_sw(int nt, cudaStream_t s, const ContractArgs& ca, std::int
     (..., (nt == I + 1 ? launch_contract_nt<I + 1, false>(s, ca) : (void)0));
 }
 
-// Remainder-packed form: lazy pipeline (list), N = 49 or 50, large batches
-// (PODECM_ROM_CONTRACT=std: the 56-wide kernel, =rp: any batch size; read per
-// call, tests flip it).
-bool contract_rp_on(int64_t n) {
+// Remainder-packed form: lazy pipeline (list), N = 49 or 50 (PODECM_ROM_CONTRACT=std:
+// the 56-wide kernel; read per call, tests flip it).
+bool contract_rp_on() {
   const char* e = getenv("PODECM_ROM_CONTRACT");
-  if (e && std::strcmp(e, "std") == 0) return false;
-  if (e && std::strcmp(e, "rp") == 0) return true;  // any batch size (tests)
-  return n >= kSmallBatch;
+  return !(e && std::strcmp(e, "std") == 0);
 }
 
 void launch_contract(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, const ContractArgs& ca) {
   KTimer kt(ctx, s, "k_rom_contract");
-  if (ca.list && r->NT == 7 && r->N > 48 && r->N <= 50 && contract_rp_on(ca.n)) {
-    k_rom_contract_rp<6><<<(int)((ca.n + 1) / 2), 32 * 12, contract_rp_smem_bytes<6>(), s>>>(ca);
+  if (ca.list && r->NT == 7 && r->N > 48 && r->N <= 50 && contract_rp_on()) {
+    if (ca.n < kSmallBatch)  // one instance per CTA: twice the CTAs, the same bits
+      k_rom_contract_rp<6, 1><<<(int)ca.n, 32 * 8, contract_rp_smem_bytes<6, 1>(), s>>>(ca);
+    else
+      k_rom_contract_rp<6, 2><<<(int)((ca.n + 1) / 2), 32 * 12, contract_rp_smem_bytes<6, 2>(), s>>>(ca);
     return;
   }
   launch_contract_sw(r->NT, s, ca, std::make_integer_sequence<int, kMaxNT>{});
