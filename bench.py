@@ -315,14 +315,14 @@ def run_c1(args, ws, rank, local, ctx, clk):
 
     # e2e through the public API with pinned host buffers; H2D and D2H of every
     # step's inputs / results inside the timed region, pipelined over 3 streams
-    n_chunks = int(os.environ.get("PODECM_E2E_CHUNKS", "8"))
+    n_chunks = int(os.environ.get("PODECM_E2E_CHUNKS", "16"))
     cs = n // n_chunks
     hF = [torch.from_numpy(np.ascontiguousarray(F_np[:, c * cs:(c + 1) * cs])).pin_memory() for c in range(n_chunks)]
     hS = [torch.from_numpy(np.ascontiguousarray(st_np[:, c * cs:(c + 1) * cs])).pin_memory() for c in range(n_chunks)]
     oP = [torch.empty((4, cs), dtype=torch.float64).pin_memory() for _ in range(n_chunks)]
     oA = [torch.empty((16, cs), dtype=torch.float64).pin_memory() for _ in range(n_chunks)]
     oS = [torch.empty((6, cs), dtype=torch.float64).pin_memory() for _ in range(n_chunks)]
-    streams = [torch.cuda.Stream(dev) for _ in range(int(os.environ.get("PODECM_E2E_STREAMS", "3")))]
+    streams = [torch.cuda.Stream(dev) for _ in range(int(os.environ.get("PODECM_E2E_STREAMS", "4")))]
     dF = [torch.empty((4, cs), dtype=torch.float64, device=dev) for _ in streams]
     dS = [torch.empty((6, cs), dtype=torch.float64, device=dev) for _ in streams]
     dout = [{"P": torch.empty((4, cs), dtype=torch.float64, device=dev),
@@ -351,8 +351,28 @@ def run_c1(args, ws, rank, local, ctx, clk):
     e2e_steps = max(3, min(args.steps, 10))
     e2e_ms = timed(torch, ws, e2e_steps, e2e_step) / e2e_steps
     same = bool(torch.equal(oP[0], out["P"][:, :cs].cpu())) and bool(torch.equal(oA[-1], out["A"][:, -cs:].cpu()))
+
+    # the link floor of that step: the same result bytes device -> pinned host and input bytes
+    # host -> device as bare concurrent copies (no kernel), timed the same way
+    def link_step():
+        for s in streams:
+            s.wait_stream(main)
+        with torch.cuda.stream(streams[0]):
+            for c in range(n_chunks):
+                oA[c].copy_(dout[0]["A"], non_blocking=True)
+                oP[c].copy_(dout[0]["P"], non_blocking=True)
+                oS[c].copy_(dout[0]["st"], non_blocking=True)
+        with torch.cuda.stream(streams[1 % len(streams)]):
+            for c in range(n_chunks):
+                dF[1 % len(streams)].copy_(hF[c], non_blocking=True)
+                dS[1 % len(streams)].copy_(hS[c], non_blocking=True)
+        for s in streams:
+            main.wait_stream(s)
+
+    link_step()
+    link_ms = timed(torch, ws, 3, link_step) / 3
     ctx.check()
-    res = {"ms": ms, "kern_ms": kern_ms, "launches": launches, "e2e_ms": e2e_ms, "e2e_same": same,
+    res = {"ms": ms, "kern_ms": kern_ms, "launches": launches, "e2e_ms": e2e_ms, "e2e_same": same, "link_ms": link_ms,
            "h2d": (4 + 6) * 8 * n, "d2h": (4 + 16 + 6) * 8 * n, "plastic_frac": plastic}
     if rank == 0 and ws == 1 and not args.no_cpu:
         import oracle
@@ -901,7 +921,11 @@ def main():
                 "e2e": {"value": ws * n / (r["e2e_ms"] * 1e-3), "unit": "points/s",
                         "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
                         "matches_resident_path": r["e2e_same"],
-                        "how": "public API (api.material_batch) on pinned host buffers, 8 chunks x 3 streams"},
+                        "ms_per_step": round(r["e2e_ms"], 3),
+                        "link_floor_ms": round(r["link_ms"], 3),
+                        "link_frac": round(r["link_ms"] / r["e2e_ms"], 4),
+                        "how": "public API (api.material_batch) on pinned host buffers, 16 chunks x 4 streams; "
+                               "link_floor_ms = the same H2D + D2H bytes as bare concurrent copies (PCIe bound)"},
                 "gpu_launches": r["launches"],
             })
             if "cpu" in r:
