@@ -127,11 +127,13 @@ def test_folding_morph_fails_only_its_instance(setup):
         rom.ctx.check()
 
 
-@pytest.mark.parametrize("N", [80, 119])
+@pytest.mark.parametrize("N", [48, 49, 51, 80, 119])
 def test_wide_bases(orc, N):
-    """Bases wider than the one-CTA-pair tile (N + 1 > 56 columns): the
-    contraction runs one instance per CTA with up to 15 column tiles; the warp
-    LU, the effective stiffness and the Newton logic are generic in N."""
+    """Bases other than N = 50.  N + 1 > 56 columns: the contraction runs one
+    instance per CTA with up to 15 column tiles; N = 49 takes the
+    remainder-packed kernel with ONE remainder row / column, N = 48 and 51 the
+    column-tiled kernel next to it; the warp LU, the effective stiffness and
+    the Newton logic are generic in N."""
     import torch
     from paper_2307_16894_b200 import api
     g = api.Rve(16, _mats())
