@@ -264,7 +264,14 @@ int podecm_material_batch_ex(podecm_ctx* ctx, void* stream, int64_t n, const pod
   const MatTable tab = make_table(mats, n_mats);
   const int block = 128;
   const int64_t blocks = (n + block - 1) / block;
-  const int grid = (int)(blocks < (int64_t)ctx->n_sm * 64 ? blocks : (int64_t)ctx->n_sm * 64);
+  // CTAs per SM of the grid-stride loop: 224 = 32 waves of 7 resident CTAs, so
+  // config 1 (32,768 blocks) runs one point per thread and the last partial
+  // wave is short (64 gave 3-or-4-point CTAs: 1.065 vs 1.053 ms per step)
+  static const int64_t gmult = [] {
+    const char* e = getenv("PODECM_K1_GRID_MULT");
+    return (int64_t)(e ? std::max(1, atoi(e)) : 224);
+  }();
+  const int grid = (int)(blocks < (int64_t)ctx->n_sm * gmult ? blocks : (int64_t)ctx->n_sm * gmult);
   KTimer kt(ctx, static_cast<cudaStream_t>(stream), "k_material_batch");
   const int v = k1_variant();
   const bool uni = (!region || n_mats == 1) && v >= 4 && v <= 6;
