@@ -445,40 +445,51 @@ __global__ void __launch_bounds__(kQ2Thr, MINB) k_asm_qp2(AsmArgs g, MatTable ta
     atomicAdd(g.fail, 1u);
   }
   if constexpr (TILED) {
-    // the tile's local items: the gather's sum (first group, then + in group
-    // order; residual rows start from 0.0 +) over the element sums in SMEM
-    __syncthreads();
-    const int l0 = __ldg(g.t_lptr + blockIdx.x), l1 = __ldg(g.t_lptr + blockIdx.x + 1);
+    // The tile's local items: the gather's sum (first group, then + in group
+    // order; residual rows start from 0.0 +) over the element sums in SMEM.
+    // Items fed by one element row (= this warp's 8 elements: two thirds of
+    // them) are summed by the warp right after its own element phase, so a
+    // warp that is ahead works instead of idling at the CTA barrier; the items
+    // spanning two rows follow after the barrier.
+    const int32_t* lp = g.t_lptr + (size_t)blockIdx.x * 5;
     const int64_t nnz = g.nnz;
-    constexpr int kU = 8;  // items per thread per round, all table loads issued first
-    for (int base = l0; base < l1; base += kU * kQ2Thr) {
-      int its[kU];
-      uint64_t pks[kU];
+    constexpr int kU = 4;  // items per thread per round, all table loads issued first
+    auto sum_items = [&](int l0, int l1, int first, int stride) {
+      for (int base = l0; base < l1; base += kU * stride) {
+        int its[kU];
+        uint64_t pks[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int li = base + u * kQ2Thr + lt;
-        its[u] = li < l1 ? __ldg(g.t_litem + li) : -1;
-        pks[u] = li < l1 ? __ldg(g.t_lpack + li) : 0ull;
-      }
+        for (int u = 0; u < kU; ++u) {
+          const int li = base + u * stride + first;
+          its[u] = li < l1 ? __ldg(g.t_litem + li) : -1;
+          pks[u] = li < l1 ? __ldg(g.t_lpack + li) : 0ull;
+        }
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int it = its[u];
-        if (it < 0) continue;
-        const bool is_slot = it < nnz;
-        if (is_slot && !g.tangent) continue;
-        const uint64_t pk = pks[u];
-        const int n = (int)(pk >> 48);
-        double sm = sq[pk & 0xfff];
-        if (!is_slot) sm = 0.0 + sm;
-        if (n > 1) sm = sm + sq[(pk >> 12) & 0xfff];
-        if (n > 2) sm = sm + sq[(pk >> 24) & 0xfff];
-        if (n > 3) sm = sm + sq[(pk >> 36) & 0xfff];
-        if (is_slot)
-          __stcs(g.kvals + (size_t)inst * nnz + it, sm);
-        else
-          __stcs(g.f + (size_t)inst * g.n_red + (it - nnz), sm);
+        for (int u = 0; u < kU; ++u) {
+          const int it = its[u];
+          if (it < 0) continue;
+          const bool is_slot = it < nnz;
+          if (is_slot && !g.tangent) continue;
+          const uint64_t pk = pks[u];
+          const int n = (int)(pk >> 48);
+          double sm = sq[pk & 0xfff];
+          if (!is_slot) sm = 0.0 + sm;
+          if (n > 1) sm = sm + sq[(pk >> 12) & 0xfff];
+          if (n > 2) sm = sm + sq[(pk >> 24) & 0xfff];
+          if (n > 3) sm = sm + sq[(pk >> 36) & 0xfff];
+          if (is_slot)
+            __stcs(g.kvals + (size_t)inst * nnz + it, sm);
+          else
+            __stcs(g.f + (size_t)inst * g.n_red + (it - nnz), sm);
+        }
       }
-    }
+    };
+    const int w = lt >> 5;
+    const int r0 = __ldg(lp + w), r1 = __ldg(lp + w + 1), c0 = __ldg(lp + 4), c1 = __ldg(lp + 5);
+    __syncwarp();
+    sum_items(r0, r1, lt & 31, 32);
+    __syncthreads();
+    sum_items(c0, c1, lt, kQ2Thr);
   }
 }
 

@@ -269,8 +269,11 @@ void build_tiles(podecm_rve& r) {
       term = 64 + (grp & 7);
     }
   };
-  std::vector<std::vector<int32_t>> litems(r.n_tiles);
-  std::vector<std::vector<uint64_t>> lpacks(r.n_tiles);
+  // per tile 5 segments: items fed by one element row ly (a warp of the qp
+  // kernel: it sums them right after its own element phase), then the items
+  // spanning two rows (summed after the CTA barrier)
+  std::vector<std::vector<int32_t>> litems((size_t)r.n_tiles * 5);
+  std::vector<std::vector<uint64_t>> lpacks((size_t)r.n_tiles * 5);
   r.t_hitem.clear();
   r.t_hgptr.assign(1, 0);
   r.t_hpos.assign((size_t)r.n_elems * 72, -1);
@@ -286,12 +289,15 @@ void build_tiles(podecm_rve& r) {
     }
     if (local) {
       uint64_t pk = (uint64_t)(g1 - g0) << 48;
+      int row = -1;
       for (int g = g0; g < g1; ++g) {
         group(g, e, term);
         pk |= (uint64_t)tile_smem_slot(local_of[e], term) << (12 * (g - g0));
+        const int ly = local_of[e] / TX;
+        row = (g == g0 || row == ly) ? ly : 4;
       }
-      litems[tile].push_back((int32_t)it);
-      lpacks[tile].push_back(pk);
+      litems[(size_t)tile * 5 + row].push_back((int32_t)it);
+      lpacks[(size_t)tile * 5 + row].push_back(pk);
     } else {
       r.t_hitem.push_back((int32_t)it);
       for (int g = g0; g < g1; ++g) {
@@ -305,7 +311,7 @@ void build_tiles(podecm_rve& r) {
   r.t_lptr.assign(1, 0);
   r.t_litem.clear();
   r.t_lpack.clear();
-  for (int t = 0; t < r.n_tiles; ++t) {
+  for (size_t t = 0; t < (size_t)r.n_tiles * 5; ++t) {  // t_lptr: [n_tiles][5] segment starts + end
     r.t_litem.insert(r.t_litem.end(), litems[t].begin(), litems[t].end());
     r.t_lpack.insert(r.t_lpack.end(), lpacks[t].begin(), lpacks[t].end());
     r.t_lptr.push_back((int32_t)r.t_litem.size());
