@@ -1058,6 +1058,251 @@ __global__ void __launch_bounds__(32 * (IPC * NTM + (IPC == 1 ? 2 : 0)), (IPC ==
   }
 }
 
+// The large-batch form: four warps per instance, each a 3 x 3 block of tiles (6
+// fragment loads per 9 DMMAs; 8 warps per two-instance CTA at 128 registers, no
+// spills; fewer, fatter warps: barrier stalls 4.0 -> 1.5 per issue, DMMA pipe 62 ->
+// 65 % against the 12-warp 2 x 3 form, 365.1 -> 353.0 ms at 16,384 instances).  The
+// remainder row tiles ride on warps 0-3 (one per SM sub-partition: 20 / 20 / 20 / 19
+// DMMAs per k-step).  Every tile is the same k-ordered DMMA chain as in
+// k_rom_contract_rp, so K has the same bits.  Notes of the 2 x 3 form follow: warps
+// own a 2 x 3 block of tiles (row-tile pair x column-tile triple: 5
+// fragment loads per 6 DMMAs instead of 7; the kernel is bound by the
+// shared-memory data pipe and by warp balance, not by the DMMA pipe).  The
+// remainder tile's NTM + 1 row tiles ride on four of the warps, on different
+// SM sub-partitions (warp w runs on sub-partition w % 4): three add the two
+// row tiles of their own A fragments, one the last (padded) row tile; with
+// two instances per CTA every sub-partition issues 38-40 DMMAs per k-step.
+// IPC = 1 (small batches: twice the CTAs) leaves half of the remainder tile
+// empty and gives its row tiles to two extra warps (4 + 3 tiles: 12, 12, 10, 9
+// DMMAs per k-step on the four sub-partitions); an instance's K has the same
+// bits either way (its columns of the tile do not depend on the other
+// instance's, and every tile is the same k-ordered DMMA chain).
+template <int NTM, int IPC>
+__global__ void __launch_bounds__(128 * IPC, (IPC == 2 ? 2 : 3)) k_rom_contract_rp3(ContractArgs g) {
+  static_assert(IPC == 1 || IPC == 2, "3 x 3 blocks: four warps per instance");
+  static_assert(NTM == 6 && (IPC == 1 || IPC == 2), "warp roles below are laid out for 6 x 6 full tiles");
+  constexpr int NT = NTM + 1;
+  constexpr int NP = NT * 8;     // columns of the global Gm rows
+  constexpr int NM = NTM * 8;    // modes in full tiles
+  constexpr int LDG = contract_ld<NT>();
+  constexpr int LDY = NM + 4;    // = 4 mod 16: conflict-free fragment loads
+  constexpr int LDR = 12;        // 8 remainder columns + 4
+  constexpr int KR = kPC * 4;
+  constexpr int NWM = 4 * IPC;              // warps with a 3 x 3 block of full tiles
+  constexpr int NW = NWM;
+  constexpr int NTHR = 32 * NW;
+  constexpr int GPT = (KR * NP + NTHR - 1) / NTHR;
+  constexpr int APT = (IPC * kPC * 16 + NTHR - 1) / NTHR;
+  constexpr int CB = 2;          // column-triple blocks per instance
+  constexpr int NRA = IPC == 1 ? 4 : 2;     // remainder accumulator tiles per warp
+  static_assert(LDY % 16 == 4 || LDY % 16 == 12, "Y row stride");
+  extern __shared__ double smc[];
+  double* sGm = smc;                        // [2][KR][LDG]
+  double* sY = sGm + 2 * KR * LDG;          // [2][IPC][KR][LDY]
+  double* sR = sY + 2 * IPC * KR * LDY;     // [2][KR][LDR]
+  double* sAt = sR + 2 * KR * LDR;          // [2][IPC][kPC][20]: At[r][t] at 4 r + t
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool mainw = warp < NWM;
+  const int si = warp >> 2, wb = warp & 3;
+  const int rb = wb / CB, cb = wb - rb * CB;  // row tiles 3 rb .. 3 rb + 2; column tiles 3 cb ..
+  // IPC 2: remainder row tiles 2 rb, 2 rb + 1 (rb = 0, 1, 2) / row tile NTM ride on main warps
+  // remainder row tiles: warp 0: 0, 1 (its A fragments 0, 1); warp 1: 2 (A fragment 2) and NTM (extra
+  // load); warp 2: 3, 4; warp 3: 5 -- one warp per SM sub-partition, 20 / 20 / 20 / 19 DMMAs per k-step
+  const bool rem2 = warp == 0 || warp == 2;
+  const bool rem7 = warp == 1;
+  const bool rem1 = warp == 3;
+  // IPC 1: warp NWM owns remainder row tiles 0..3, warp NWM + 1 tiles 4..NTM
+  const int rt0 = warp == NWM ? 0 : 4, rtn = warp == NWM ? 4 : NT - 4;
+  constexpr int kTailA = IPC == 2 ? 5 : 3, kTailB = IPC == 2 ? 7 : 3;  // warps building D Zc / D^T Zc
+  const int64_t sbase = (int64_t)blockIdx.x * IPC;
+  const int64_t lim = *g.count;
+  int64_t sid[IPC];
+  bool any = false;
+#pragma unroll
+  for (int q = 0; q < IPC; ++q) {
+    sid[q] = sbase + q < lim ? (int64_t)g.list[sbase + q] : -1;
+    any = any || sid[q] >= 0;
+  }
+  if (!any) return;
+  const int gid = lane >> 2, tig = lane & 3;
+  double acc[9][2];   // tile (h, c) of the block at acc[3 h + c]
+  double accr[NRA][2];  // remainder row tiles of this warp (rem2: 2 rb + h; rem7: NTM at [0]; IPC 1: rt0 + h)
+#pragma unroll
+  for (int ct = 0; ct < 9; ++ct) acc[ct][0] = acc[ct][1] = 0.0;
+#pragma unroll
+  for (int ct = 0; ct < NRA; ++ct) accr[ct][0] = accr[ct][1] = 0.0;
+  const int nch = g.Qpad / kPC;
+  double rG[GPT], rA[APT];
+
+  auto gload = [&](int c) {
+    const double* gsrc = g.G + (size_t)c * kPC * 4 * NP;
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+      const int t = tid + k * NTHR;
+      rG[k] = t < KR * NP ? gsrc[t] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+      const int t = tid + k * NTHR;
+      rA[k] = 0.0;
+      if (t < IPC * kPC * 16) {
+        const int q = t / (kPC * 16), rm = t - q * kPC * 16;
+        const int tp = rm / kPC, pl = rm - tp * kPC;  // At planes [s][20][Qpad], points fastest
+        const int64_t sq = (IPC == 2 && q) ? sid[IPC - 1] : sid[0];
+        if (sq >= 0) rA[k] = g.At[((size_t)sq * 20 + tp) * g.Qpad + (size_t)c * kPC + pl];
+      }
+    }
+  };
+  auto gstore = [&](int buf) {
+#pragma unroll
+    for (int k = 0; k < GPT; ++k) {
+      const int t = tid + k * NTHR;
+      if (t < KR * NP) sGm[buf * KR * LDG + (t / NP) * LDG + t % NP] = rG[k];
+    }
+#pragma unroll
+    for (int k = 0; k < APT; ++k) {
+      const int t = tid + k * NTHR;
+      if (t < IPC * kPC * 16) {
+        const int q = t / (kPC * 16), rm = t - q * kPC * 16;
+        const int tp = rm / kPC, pl = rm - tp * kPC;  // plane tp = r + 4 t holds At[r][t]
+        sAt[buf * IPC * kPC * 20 + q * kPC * 20 + pl * 20 + 4 * (tp & 3) + (tp >> 2)] = rA[k];
+      }
+    }
+  };
+  // Item (instance q, point pl, column j): the 4 rows of Y column j (j >= NM:
+  // into the remainder tile, columns 4 q + j - NM), row r from At's row r (one
+  // 32-byte load) in the 56-wide kernel's FMA order.
+  auto y_item = [&](const double* G0, int buf, int q, int pl, int j) {
+    const double* at = sAt + (buf * IPC + q) * kPC * 20 + pl * 20;
+    const double g0 = G0[(pl * 4) * LDG + j], g1 = G0[(pl * 4 + 1) * LDG + j];
+    const double g2 = G0[(pl * 4 + 2) * LDG + j], g3 = G0[(pl * 4 + 3) * LDG + j];
+    double* y = j < NM ? sY + (buf * IPC + q) * KR * LDY + (pl * 4) * LDY + j
+                       : sR + buf * KR * LDR + (pl * 4) * LDR + q * 4 + (j - NM);
+    const int ld = j < NM ? LDY : LDR;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const double4 ar = *reinterpret_cast<const double4*>(at + 4 * r);  // At[r][0..3]
+      y[r * ld] = fma(ar.w, g3, fma(ar.z, g2, fma(ar.y, g1, ar.x * g0)));
+    }
+  };
+  // Two items per thread over the IPC x kPC x NM full-tile columns (a
+  // half-warp = 16 consecutive columns of one point: conflict-free stores).
+  // The IPC x kPC x 2 remainder columns D Zc and as many of D^T Zc go to the
+  // tail warp(s), on the sub-partition with the fewest remainder DMMAs.
+  static_assert(IPC * kPC * NM == 3 * NTHR && NTHR % 16 == 0, "three full-tile columns per thread");
+  auto build_y = [&](int buf) {
+    const double* G0 = sGm + buf * KR * LDG;
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+      const int u = tid + h * NTHR;
+      const int q = u / (kPC * NM), rm = u - q * kPC * NM;
+      y_item(G0, buf, q, rm / NM, rm % NM);
+    }
+    if (warp != kTailA && warp != kTailB) return;
+    // lane -> (instance or kind, point, m)
+    const int hi = lane >> 4, pl = (lane >> 1) & (kPC - 1), m = lane & 1;
+    const int q = IPC == 2 ? hi : 0;
+    const bool tr = IPC == 2 ? warp == kTailB : hi == 1;
+    if (!tr) {
+      y_item(G0, buf, q, pl, NM + m);
+    } else {  // (D^T Zc)[4p + t] = sum_r At[r][t] Zc[4p + r]
+      const double* at = sAt + (buf * IPC + q) * kPC * 20 + pl * 20;
+      const double g0 = G0[(pl * 4) * LDG + NM + m], g1 = G0[(pl * 4 + 1) * LDG + NM + m];
+      const double g2 = G0[(pl * 4 + 2) * LDG + NM + m], g3 = G0[(pl * 4 + 3) * LDG + NM + m];
+      double* y = sR + buf * KR * LDR + (pl * 4) * LDR + q * 4 + 2 + m;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) y[t * LDR] = fma(at[12 + t], g3, fma(at[8 + t], g2, fma(at[4 + t], g1, at[t] * g0)));
+    }
+  };
+  auto mma = [&](int buf) {
+    const double* G0 = sGm + buf * KR * LDG;
+    const double* Y0 = sY + (buf * IPC + si) * KR * LDY + cb * 24 + gid;
+    const double* A0 = G0 + rb * 24 + gid;
+    const double* R0 = sR + buf * KR * LDR + gid;
+#pragma unroll
+    for (int ks = 0; ks < KR / 4; ++ks) {
+      double av[3];
+#pragma unroll
+      for (int h = 0; h < 3; ++h) av[h] = A0[(ks * 4 + tig) * LDG + h * 8];  // (Gm^T)[i][k]
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const double b = Y0[(ks * 4 + tig) * LDY + c * 8];
+#pragma unroll
+        for (int h = 0; h < 3; ++h) dmma(acc[3 * h + c][0], acc[3 * h + c][1], av[h], b);
+      }
+      if (rem2) {
+        const double br = R0[(ks * 4 + tig) * LDR];
+        dmma(accr[0][0], accr[0][1], av[0], br);
+        dmma(accr[1][0], accr[1][1], av[1], br);
+      } else if (rem7) {
+        const double br = R0[(ks * 4 + tig) * LDR];
+        dmma(accr[0][0], accr[0][1], av[2], br);
+        dmma(accr[1][0], accr[1][1], G0[(ks * 4 + tig) * LDG + NM + gid], br);
+      } else if (rem1) {
+        dmma(accr[0][0], accr[0][1], av[2], R0[(ks * 4 + tig) * LDR]);
+      }
+    }
+  };
+
+  if constexpr (IPC == 1) {  // the unused half of the remainder tile stays zero
+    for (int t = tid; t < 2 * KR * LDR; t += NTHR) sR[t] = 0.0;
+  }
+  gload(0);
+  gstore(0);
+  __syncthreads();
+  build_y(0);
+  if (nch > 1) {
+    gload(1);
+    gstore(1);
+  }
+  __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    const int cur = c & 1, nxt = cur ^ 1;
+    if (c + 2 < nch) gload(c + 2);
+    if (c + 1 < nch) build_y(nxt);
+    mma(cur);
+    __syncthreads();
+    if (c + 2 < nch) gstore(cur);
+    __syncthreads();
+  }
+  {
+    const int64_t s = sid[IPC == 2 ? si : 0];
+    if (s >= 0) {
+#pragma unroll
+      for (int h = 0; h < 3; ++h) {
+        const int i = (3 * rb + h) * 8 + gid;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            g.K[((size_t)s * g.N + i) * g.N + (3 * cb + c) * 8 + 2 * tig + e] = acc[3 * h + c][e];
+      }
+    }
+  }
+  if (!rem2 && !rem7 && !rem1) return;
+  // remainder tile columns n = 2 tig + e: instance n >> 2, item m = n & 3
+  if (IPC == 1 && (tig >> 1)) return;
+  const int64_t s = sid[IPC == 2 ? (tig >> 1) : 0];
+  if (s < 0) return;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (rem1 && h) break;
+    // row tile of accr[h]: warp 0: h; warp 2: 3 + h; warp 1: 2, NTM; warp 3: 5
+    const int rt = rem2 ? 3 * rb + h : (rem7 ? (h ? NTM : 2) : 5);
+    const int i = rt * 8 + gid;
+    if (i >= g.N) continue;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int m = 2 * (tig & 1) + e;
+      if (m < 2) {
+        if (NM + m < g.N) g.K[((size_t)s * g.N + i) * g.N + NM + m] = accr[h][e];
+      } else if (NM + m - 2 < g.N && i < NM) {
+        g.K[((size_t)s * g.N + NM + m - 2) * g.N + i] = accr[h][e];
+      }
+    }
+  }
+}
+
 // ---- Newton / bisection state machine + LU --------------------------------
 struct NewtonArgs {
   int64_t n;
@@ -2165,6 +2410,8 @@ void set_attrs() {
                        (int)contract_rp_smem_bytes<6, 1>());
   cudaFuncSetAttribute(k_rom_contract_rp<6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)contract_rp_smem_bytes<6, 2>());
+  cudaFuncSetAttribute(k_rom_contract_rp3<6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)contract_rp_smem_bytes<6, 2>());
   cudaFuncSetAttribute(k_rom_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_rom_check<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_rom_check<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -2260,7 +2507,8 @@ void launch_contract_sw(int nt, cudaStream_t s, const ContractArgs& ca, std::int
 }
 
 // Remainder-packed form: lazy pipeline (list), N = 49 or 50 (PODECM_ROM_CONTRACT=std:
-// the 56-wide kernel; read per call, tests flip it).
+// the 56-wide kernel, =rp23: the 12-warp 2 x 3-block form for large batches; read per
+// call, tests flip it).
 bool contract_rp_on() {
   const char* e = getenv("PODECM_ROM_CONTRACT");
   return !(e && std::strcmp(e, "std") == 0);
@@ -2269,10 +2517,13 @@ bool contract_rp_on() {
 void launch_contract(podecm_ctx* ctx, cudaStream_t s, podecm_rom* r, const ContractArgs& ca) {
   KTimer kt(ctx, s, "k_rom_contract");
   if (ca.list && r->NT == 7 && r->N > 48 && r->N <= 50 && contract_rp_on()) {
+    const char* e = getenv("PODECM_ROM_CONTRACT");
     if (ca.n < kSmallBatch)  // one instance per CTA: twice the CTAs, the same bits
       k_rom_contract_rp<6, 1><<<(int)ca.n, 32 * 8, contract_rp_smem_bytes<6, 1>(), s>>>(ca);
-    else
+    else if (e && std::strcmp(e, "rp23") == 0)  // 12 warps with 2 x 3 tile blocks (A/B)
       k_rom_contract_rp<6, 2><<<(int)((ca.n + 1) / 2), 32 * 12, contract_rp_smem_bytes<6, 2>(), s>>>(ca);
+    else  // 8 warps with 3 x 3 tile blocks
+      k_rom_contract_rp3<6, 2><<<(int)((ca.n + 1) / 2), 256, contract_rp_smem_bytes<6, 2>(), s>>>(ca);
     return;
   }
   launch_contract_sw(r->NT, s, ca, std::make_integer_sequence<int, kMaxNT>{});

@@ -212,6 +212,18 @@ def test_remainder_packed_contraction(setup, monkeypatch):
         monkeypatch.setenv("PODECM_ROM_CONTRACT", mode)
         res[mode] = {k: v.cpu().numpy() for k, v in rom.solve(T(geom), T(sched), opts).items()}
     a, b = res["std"], res["rp"]
+    # the large-batch forms (two instances per CTA: 8 warps with 3 x 3 tile blocks by default, 12 warps
+    # with 2 x 3 blocks under rp23) give every instance the bits of the one-instance form used above
+    gl, sl = synth.rom_instances(4097, 1, 79, 0.2)
+    big = {}
+    for mode in ("rp", "rp23"):
+        monkeypatch.setenv("PODECM_ROM_CONTRACT", mode)
+        big[mode] = {k: v.cpu().numpy() for k, v in rom.solve(T(gl), T(sl), opts).items()}
+    monkeypatch.setenv("PODECM_ROM_CONTRACT", "rp")
+    small = {k: v.cpu().numpy() for k, v in rom.solve(T(gl[:33]), T(sl[:33]), opts).items()}
+    for k in ("pbar", "iters", "status"):
+        assert np.array_equal(big["rp"][k], big["rp23"][k]), k
+        assert np.array_equal(big["rp"][k][:33], small[k]), k
     assert np.array_equal(a["status"], b["status"]) and np.array_equal(a["iters"], b["iters"])
     rel = np.abs(a["pbar"] - b["pbar"]).max() / np.abs(a["pbar"]).max()
     print(f"rp vs std: pbar max rel {rel:.2e}; bitwise equal: {np.array_equal(a['pbar'], b['pbar'])}")
