@@ -952,7 +952,7 @@ def main():
         if args.config in ("all", "c2"):
             also["c2"] = guarded(run_rve, args, ws, rank, local, ctx, 128, args.c2_inst, 0.2, (0.15, 0.35),
                                  steps=5 if args.config == "all" else args.steps,
-                                 warmup=args.warmup, seed=2028, cpu_sample=8)
+                                 warmup=args.warmup, seed=2028, cpu_sample=256)
         if args.config in ("all", "c3"):
             also["c3"] = guarded(run_c3, args, ws, rank, local, ctx, args.c3_inst,
                                 steps=2 if args.config == "all" else args.steps,
