@@ -231,3 +231,29 @@ def test_remainder_packed_contraction(setup, monkeypatch):
     ro = o.rom_solve(model["ids"], model["weights"], model["mode_grads"], geom, sched, eps_rel=opts.eps_rel,
                      eps_abs=opts.eps_abs, max_iter=opts.max_iter, max_bisect=opts.max_bisect)
     _check(b, ro)
+
+
+@pytest.mark.parametrize("N", [49, 50])
+def test_packed_contraction_large_batch_small_cell(orc, N):
+    """The two-instance packed contraction (3 x 3 tile blocks) at N = 49 (one
+    remainder row / column) and N = 50 on a 16 x 16 cell, 4,097 instances (an
+    odd count: the last CTA holds one instance): every instance has the bits
+    of the one-instance form that a 33-instance sub-batch runs, and a spread
+    sample meets the oracle tolerance with equal Newton counts."""
+    import torch
+    from paper_2307_16894_b200 import api
+    g = api.Rve(16, _mats())
+    o = orc.Rve(16, _mats())
+    model = synth.rom_model(g.export(), g.n_red, N=N, Q=56, seed=2050 + N)
+    rom = api.Rom(g, model["ids"], model["weights"], model["mode_grads"])
+    geom, sched = synth.rom_instances(4097, 2, 2051, 0.12)
+    opts = api.NewtonOpts(eps_rel=1e-10, eps_abs=1e-12)
+    T = lambda a: torch.from_numpy(a).cuda()
+    big = {k: v.cpu().numpy() for k, v in rom.solve(T(geom), T(sched), opts).items()}
+    pick = np.unique(np.linspace(0, 4096, 33).astype(np.int64))
+    small = {k: v.cpu().numpy() for k, v in rom.solve(T(geom[pick]), T(sched[pick]), opts).items()}
+    for k in ("pbar", "iters", "status"):
+        assert np.array_equal(big[k][pick], small[k]), k
+    ro = o.rom_solve(model["ids"], model["weights"], model["mode_grads"], geom[pick], sched[pick], eps_rel=1e-10,
+                     eps_abs=1e-12)
+    _check(small, ro)
